@@ -1,0 +1,431 @@
+#!/usr/bin/env python
+"""Benchmark: decoded Gbps of batched Min-Sum LDPC decoding on B200 (BASELINE.json "metric").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (one process per GPU, NCCL)
+
+A step is one pass of the whole hot path (ingested H; stage-in, check-node / bit-node sweeps with
+fused syndrome and per-frame early stop, stage-out and counters) over this rank's batch: config C2 =
+2^20 frames of a random (3,6)-regular 504x1008 code split into 7 contiguous Eb/N0 blocks
+1.0..4.0 dB, max_iter 50, one ldpc_decode per Eb/N0 block.  Frames are keyed by global frame
+index, so rank r of N decodes its own 2^20 frames (weak scaling); the only collectives are the
+barrier, the MAX of the elapsed time and the SUM of the 8 counters.
+
+value = (frames decoded by all ranks) * n / (max-over-ranks device time), in Gbit/s.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from gen import channel, codes  # noqa: E402
+
+METRIC = "decoded Gbps (1/2/4/8 B200) at fixed max_iter; % of HBM roofline"
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS_PATH) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+def describe(cfg_name, cfg, code):
+    return (f"{cfg_name}: {code.name} ({code.m}x{code.n}, nnz {code.nnz}), {cfg['frames']} frames per GPU over "
+            f"Eb/N0 {cfg['ebn0']} dB, max_iter {cfg['max_iter']}, BPSK/AWGN all-zero codeword")
+
+
+# ------------------------------------------------------------------ distributed plumbing -------
+def dist_setup(n_gpus):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def reduce_max(x: float, world: int, dev) -> float:
+    if world == 1:
+        return x
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def reduce_sum_(t, world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return t
+
+
+# ------------------------------------------------------------------ clocks -------------------
+class ClockSampler:
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={','.join(self.FIELDS)}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, v in zip(self.NAMES, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ workload -----------------
+def build_workload(cfg_name, rank, dev):
+    cfg = codes.CONFIGS[cfg_name]
+    code = cfg["code"]()
+    if isinstance(code, list):
+        code = code[0]
+    F = cfg["frames"]
+    pts = codes.point_ranges(F, len(cfg["ebn0"]))
+    llr = torch.empty((F, code.n), dtype=torch.float32, device=dev)
+    for p, (lo, hi) in enumerate(pts):
+        # global frame index of this rank's frames: rank * F + local (weak scaling)
+        channel.bpsk_awgn(code.n, code.rate, cfg["ebn0"][p], cfg["seed"], p, rank * F + lo, hi - lo, device=dev,
+                          out=llr[lo:hi])
+    return cfg, code, llr, pts
+
+
+def algorithmic_bytes(code, iters: np.ndarray, L: int, early: bool):
+    """Bytes the method must move with its state in HBM:
+    check node: gather s (4n) + read/write the compressed row state (9m + E/8 each way; body 1 has
+    no old state); bit node: read row state (9m + E/8) + r (4n) + write s (4n)."""
+    n, m, E = code.n, code.m, code.nnz
+    state = 9 * m + E / 8
+    k = iters.astype(np.int64)
+    if early:
+        cn_units = np.minimum(k + 1, L) if L > 0 else np.zeros_like(k)  # CN bodies that touch frame f
+        bn_units = k  # BN bodies that update frame f
+    else:
+        cn_units = np.full_like(k, L)
+        bn_units = np.full_like(k, L)
+    F = len(k)
+    cn = float(cn_units.sum()) * (4 * n + 2 * state) - (F * state if L > 0 else 0.0)  # body 1 reads no state
+    bn = float(bn_units.sum()) * (8 * n + state)
+    return cn, bn
+
+
+# ------------------------------------------------------------------ our arm ------------------
+def run_ours(args):
+    import paper_2507_10424_b200 as P
+
+    rank, world, local = dist_setup(args.gpus)
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    cfg, code, llr, pts = build_workload(args.config, rank, dev)
+    F, n, L = cfg["frames"], code.n, cfg["max_iter"]
+    rr, cc = code.coo()
+    h = P.Handle.from_coo(torch.from_numpy(rr).to(dev), torch.from_numpy(cc).to(dev), code.m, code.n,
+                          flags=args.flags)
+    out = P.DecodeResult(torch.empty((F, n), dtype=torch.uint8, device=dev),
+                         torch.empty(F, dtype=torch.int32, device=dev),
+                         torch.empty(F, dtype=torch.uint8, device=dev),
+                         torch.empty((F, n), dtype=torch.float32, device=dev))
+    stats = torch.zeros((len(pts), 8), dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        for p, (lo, hi) in enumerate(pts):
+            sub = P.DecodeResult(out.bits[lo:hi], out.iters[lo:hi], out.converged[lo:hi], out.posterior[lo:hi])
+            h.decode(llr[lo:hi], L, posterior=True, stats=stats[p], out=sub, stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    stats.zero_()
+    h.profile(True)
+    h.profile_reset()
+    launches0 = h.launch_count
+    barrier(world)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    launches = h.launch_count - launches0
+    ms_local = e0.elapsed_time(e1)
+    prof = h.profile_read()
+    h.profile(False)
+    ms = reduce_max(ms_local, world, dev)
+    tot_stats = reduce_sum_(stats.sum(dim=0).clone(), world).cpu().numpy()
+    per_point = stats.cpu().numpy()
+
+    # ---- roofline of the dominant kernel (per-launch algorithmic bytes / per-launch device time)
+    iters_np = out.iters.cpu().numpy()
+    early = not (args.flags & P.FLAG_NO_EARLY_STOP)
+    cn_b, bn_b = algorithmic_bytes(code, iters_np, L, early)
+    peak, peak_src = hbm_peak()
+    kern = {"check_node": cn_b, "bit_node": bn_b}
+    dom = max(kern, key=lambda c: prof[c][1])
+    n_launch, kms = prof[dom]
+    roof = None
+    if n_launch and kms > 0:
+        per_launch_bytes = kern[dom] * args.steps / n_launch
+        per_launch_s = kms / 1e3 / n_launch
+        achieved = per_launch_bytes / per_launch_s / 1e9
+        roof = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic_from_profiles(args.config, dom),
+                "algorithmic_bytes_per_launch": round(per_launch_bytes), "avg_launch_us": round(per_launch_s * 1e6, 2),
+                "share_of_step": round(kms / (ms_local * 1.0), 4), "peak_source": peak_src,
+                "kernel_ms": {k: round(v[1], 3) for k, v in prof.items() if v[0]},
+                "kernel_launches": {k: v[0] for k, v in prof.items() if v[0]}}
+    total_bits = float(world) * F * n * args.steps
+    value = total_bits / (ms / 1e3) / 1e9
+
+    # ---- end to end through the host-buffer C-ABI call (copies inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(h, llr, pts, L, args, world, dev)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, code, args)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 4), "unit": "Gbit/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": describe(args.config, cfg, code), "global_batch": world * F,
+                       "frames_per_gpu": F, "m": code.m, "n": code.n, "nnz": code.nnz, "max_iter": L,
+                       "ebn0_db": cfg["ebn0"], "schedule": h.schedule, "flags": args.flags,
+                       "parallelism": f"dp{world} (frame shards, no data-path collective)",
+                       "l2": f"inputs {F * n * 4 / 1e9:.2f} GB per GPU > 126 MB L2 (no flush needed)"},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "stats": {k: int(v) for k, v in zip(P.STATS_FIELDS, tot_stats)},
+            "per_point": [{"ebn0_db": cfg["ebn0"][p], "frames": int(s[0]), "fer": s[2] / max(1, s[0]),
+                           "ber": s[1] / max(1, s[0] * n), "raw_ber": s[7] / max(1, s[0] * n),
+                           "avg_iters": s[4] / max(1, s[0]), "near_zero_frames": int(s[6])}
+                          for p, s in enumerate(per_point)],
+        }
+        print(json.dumps(line), flush=True)
+    h.close()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def traffic_from_profiles(cfg_name, kernel):
+    """Per-launch DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of the kernel from the
+    committed ncu --set full summary, if one exists for this config."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d[cfg_name][kernel]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+def run_e2e(h, llr_dev, pts, L, args, world, dev):
+    F, n = llr_dev.shape
+    host_llr = llr_dev.cpu().pin_memory()
+    import paper_2507_10424_b200 as P
+
+    outs = P.DecodeResult(torch.empty((F, n), dtype=torch.uint8).pin_memory(),
+                          torch.empty(F, dtype=torch.int32).pin_memory(),
+                          torch.empty(F, dtype=torch.uint8).pin_memory(),
+                          torch.empty((F, n), dtype=torch.float32).pin_memory())
+    st = torch.zeros(8, dtype=torch.int64)
+
+    def step():
+        for lo, hi in pts:
+            sub = P.DecodeResult(outs.bits[lo:hi], outs.iters[lo:hi], outs.converged[lo:hi], outs.posterior[lo:hi])
+            h.decode_host(host_llr[lo:hi], L, posterior=True, stats=st, out=sub)
+
+    step()  # warm (pipeline buffers)
+    barrier(world)
+    torch.cuda.synchronize()
+    steps = max(1, min(args.steps, 3))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    t1 = time.perf_counter()
+    secs = reduce_max(t1 - t0, world, dev)
+    bits = float(world) * F * n * steps
+    return {"value": round(bits / secs / 1e9, 4), "unit": "Gbit/s", "steps": steps,
+            "h2d_bytes_per_step": int(F * n * 4), "d2h_bytes_per_step": int(F * n + F * n * 4 + F * 4 + F),
+            "api": "ldpc_decode_host (pinned host buffers, chunked H2D/decode/D2H overlap)"}
+
+
+# ------------------------------------------------------------------ CPU oracle ---------------
+def cpu_baseline(cfg, code, args, budget_s: float = 15.0):
+    import oracle
+
+    oracle.build()
+    threads = oracle.max_threads()
+    F = cfg["frames"]
+    pts = codes.point_ranges(F, len(cfg["ebn0"]))
+
+    def sample(per_point):
+        parts = []
+        for p, (lo, hi) in enumerate(pts):
+            idx = np.linspace(lo, hi - 1, per_point).astype(np.int64)
+            for i in idx:
+                parts.append(channel.bpsk_awgn(code.n, code.rate, cfg["ebn0"][p], cfg["seed"], p, int(i), 1).numpy())
+        return np.concatenate(parts)
+
+    # calibrate on a small sample, then size the timed sample for ~budget_s of CPU work
+    cal = sample(max(1, threads // len(pts) + 1))
+    t0 = time.perf_counter()
+    oracle.decode(code.oracle_h(), cal, cfg["max_iter"], threads=threads)
+    t_cal = time.perf_counter() - t0
+    per_frame = t_cal / len(cal)
+    per_point = int(max(1, min(5000, budget_s / max(per_frame, 1e-6) / len(pts))))
+    llr = sample(per_point)
+    t0 = time.perf_counter()
+    oracle.decode(code.oracle_h(), llr, cfg["max_iter"], threads=threads)
+    secs = time.perf_counter() - t0
+    gbps = len(llr) * code.n / secs / 1e9
+    return {"value": round(gbps, 6), "unit": "Gbit/s", "cores": threads, "kind": "oracle",
+            "sample": f"{per_point} frames per Eb/N0 block x {len(pts)} blocks = {len(llr)} frames, evenly "
+                      f"spaced over the {F}-frame batch; {secs:.1f} s on {threads} threads"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle (the only reference this tier has) on the same workload."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = codes.CONFIGS[args.config]
+    code = cfg["code"]()
+    if isinstance(code, list):
+        code = code[0]
+    import oracle
+
+    oracle.build()
+    threads = oracle.max_threads()
+    F = cfg["frames"]
+    pts = codes.point_ranges(F, len(cfg["ebn0"]))
+    per_point = max(1, int(os.environ.get("REF_FRAMES_PER_POINT", "24")))
+
+    def sample(step_idx):
+        parts = []
+        for p, (lo, hi) in enumerate(pts):
+            idx = lo + (np.arange(per_point) * ((hi - lo) // per_point) + step_idx) % (hi - lo)
+            for i in idx:
+                parts.append(channel.bpsk_awgn(code.n, code.rate, cfg["ebn0"][p], cfg["seed"], p, int(i), 1).numpy())
+        return np.concatenate(parts)
+
+    for w in range(args.warmup):
+        oracle.decode(code.oracle_h(), sample(1000 + w), cfg["max_iter"], threads=threads)
+    tot_t, tot_frames = 0.0, 0
+    for s in range(args.steps):
+        llr = sample(s)
+        t0 = time.perf_counter()
+        oracle.decode(code.oracle_h(), llr, cfg["max_iter"], threads=threads)
+        tot_t += time.perf_counter() - t0
+        tot_frames += len(llr)
+    value = tot_frames * code.n / tot_t / 1e9
+    desc = (f"{per_point} frames per Eb/N0 block x {len(pts)} blocks per step (every "
+            f"{F // len(pts) // per_point}-th frame of each block of the {F}-frame batch)")
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "Gbit/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot_t / args.steps * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": describe(args.config, cfg, code), "global_batch": F, "max_iter": cfg["max_iter"],
+                       "ebn0_db": cfg["ebn0"], "parallelism": "host threads over frames"},
+            "cpu_baseline": {"value": round(value, 6), "unit": "Gbit/s", "cores": threads, "kind": "oracle",
+                             "sample": desc},
+            "e2e": {"value": round(value, 6), "unit": "Gbit/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=sorted(codes.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--flags", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: the timing rules require --warmup >= 3", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

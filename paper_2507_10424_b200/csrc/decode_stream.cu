@@ -1,0 +1,450 @@
+// decode_stream.cu -- the HBM-streaming schedule of the Min-Sum hot path (steps a2-a7).
+//
+// One loop body of Alg. 1 over a chunk of frames is two sweeps:
+//   k_cn  check-node update, Eq. eta_update through Observations 1 and 2:
+//         per row and frame, lambda_e = s_j - eta^prev_e is formed in registers, reduced to
+//         (min0, min0Location, min1, sign parity) -- the paper's "four vectors of size m"
+//          -- and the sign bit of every lambda_e.  That state IS eta (Eq. etaCalculation,
+//         P:327-336, with the delta placement of Obs. 1, reading A2); no per-edge message is stored.
+//         Fused: the syndrome of b = slice(s) over the same gathered s.
+//   k_bn  bit-node update, Eq. lambda_j / sCalculation: eta_{i,j} rebuilt
+//         from the row state, summed over M_j in ascending row order from +0.0, then + r_j (A14).
+// The syndrome computed by k_cn at body k is the stopping test of body k-1; k_bn then
+// freezes stopped frames and records k-1.  No host round trip anywhere.
+//
+// Layout: frames are interleaved in tiles of 128 ([tile][row-or-column][128 frames]); lane l of a
+// warp owns frames 4l..4l+3 of the tile, so every gather of s, r or row state is one 512-byte
+// contiguous float4 access per warp, and per-frame bits of 128 frames are four ballot words.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "ldpc_internal.cuh"
+
+namespace ldpc {
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+template <typename T>
+struct Vec4;
+template <>
+struct Vec4<uint8_t> {
+    using type = uchar4;
+};
+template <>
+struct Vec4<uint16_t> {
+    using type = ushort4;
+};
+
+__device__ __forceinline__ float comp(const float4 &a, int v) { return v == 0 ? a.x : v == 1 ? a.y : v == 2 ? a.z : a.w; }
+__device__ __forceinline__ unsigned comp(const uint4 &a, int v) { return v == 0 ? a.x : v == 1 ? a.y : v == 2 ? a.z : a.w; }
+template <typename V>
+__device__ __forceinline__ int compl4(const V &a, int v) {
+    return v == 0 ? (int)a.x : v == 1 ? (int)a.y : v == 2 ? (int)a.z : (int)a.w;
+}
+
+__device__ __forceinline__ float4 ldg4(const float *p) { return __ldg(reinterpret_cast<const float4 *>(p)); }
+__device__ __forceinline__ float4 ld4(const float *p) { return *reinterpret_cast<const float4 *>(p); }
+__device__ __forceinline__ void st4(float *p, float4 v) { *reinterpret_cast<float4 *>(p) = v; }
+__device__ __forceinline__ uint4 ldu4(const uint32_t *p) { return *reinterpret_cast<const uint4 *>(p); }
+
+// ------------------------------------------------------------------------------------------------
+// a2: stage-in.  llr [F][n] -> r, s [T][n][128] (s = r), init per-tile flags.
+// ------------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(CTA) k_stage_in(const float *__restrict__ llr, int64_t frames, int n, int T,
+                                                  float *__restrict__ r, float *__restrict__ s,
+                                                  uint32_t *__restrict__ unsat, uint32_t *__restrict__ done,
+                                                  int *__restrict__ fbe, int *__restrict__ fraw, int *__restrict__ fnz) {
+    __shared__ float tile[32][TILE + 1];
+    const int t = blockIdx.y, j0 = blockIdx.x * 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t f0 = (int64_t)t * TILE;
+    for (int fl = warp; fl < TILE; fl += CTA / 32) {
+        int64_t f = f0 + fl;
+        int j = j0 + lane;
+        tile[lane][fl] = (f < frames && j < n) ? __ldg(llr + f * n + j) : -1.0f;
+    }
+    __syncthreads();
+    for (int jl = warp; jl < 32; jl += CTA / 32) {
+        int j = j0 + jl;
+        if (j >= n) break;
+        size_t base = ((size_t)t * n + j) * TILE;
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            float v = tile[jl][lane + 32 * q];
+            r[base + lane + 32 * q] = v;
+            s[base + lane + 32 * q] = v;
+        }
+    }
+    if (blockIdx.x == 0) {
+        int tid = threadIdx.x;
+        if (tid < 4) {
+            // frame 4*lane+v of the tile is bit `lane` of word v; padding frames start "done"
+            uint32_t pad = 0;
+            for (int l = 0; l < 32; l++)
+                if (f0 + 4 * l + tid >= frames) pad |= 1u << l;
+            done[(size_t)t * 4 + tid] = pad;
+            unsat[(size_t)t * 4 + tid] = 0;
+            unsat[((size_t)T + t) * 4 + tid] = 0;
+        }
+        if (tid < TILE) {
+            fbe[(size_t)t * TILE + tid] = 0;
+            fraw[(size_t)t * TILE + tid] = 0;
+            fnz[(size_t)t * TILE + tid] = 0;
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// a3/a4/a6: check-node sweep of loop body k (k = 1..L), fused syndrome of b^(k-1).
+// FIRST: eta^prev = 0, so no old state is read.
+// ------------------------------------------------------------------------------------------------
+template <typename LocT, bool FIRST, bool EARLY>
+__global__ void __launch_bounds__(CTA) k_cn(Graph g, StreamState w, int k, int rows_per_cta, int literal) {
+    using L4 = typename Vec4<LocT>::type;
+    const int t = blockIdx.y;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __shared__ uint32_t s_u[4];
+    if (EARLY) {
+        const uint4 dw = ldu4(w.done + (size_t)t * 4);
+        if ((dw.x & dw.y & dw.z & dw.w) == FULL) return;  // every frame of the tile has stopped
+        if (threadIdx.x < 4) s_u[threadIdx.x] = 0;
+        __syncthreads();
+    }
+    const int m = g.m, n = g.n, E = g.E;
+    const size_t tm = (size_t)t * m, tn = (size_t)t * n, tE = (size_t)t * E;
+    const int i0 = blockIdx.x * rows_per_cta, i1 = min(m, i0 + rows_per_cta);
+    uint32_t u0 = 0, u1 = 0, u2 = 0, u3 = 0;
+    for (int i = i0 + warp; i < i1; i += CTA / 32) {
+        const int a = __ldg(g.row_ptr + i), d = __ldg(g.row_ptr + i + 1) - a;
+        const unsigned corr = (unsigned)(d & 1) & (unsigned)(!literal);  // (-1)^{d_i}, reading A1
+        const size_t st = (tm + i) * TILE + 4 * lane;
+        float4 om0 = make_float4(0.f, 0.f, 0.f, 0.f), om1 = om0;
+        L4 olc{};
+        if (!FIRST) {
+            om0 = ld4(w.min0 + st);
+            om1 = ld4(w.min1 + st);
+            olc = *reinterpret_cast<const L4 *>(reinterpret_cast<const LocT *>(w.loc) + st);
+        }
+        float nm0[4], nm1[4];
+        int nloc[4];
+        unsigned npar = 0, syn = 0;
+#pragma unroll
+        for (int v = 0; v < 4; v++) {
+            nm0[v] = __int_as_float(0x7f800000);
+            nm1[v] = __int_as_float(0x7f800000);
+            nloc[v] = 0;
+        }
+        for (int p = 0; p < d; p++) {
+            const int e = a + p;
+            const int j = __ldg(g.col_idx + e);
+            const float4 sv = ld4(w.s + (tn + j) * TILE + 4 * lane);
+            uint4 sw = make_uint4(0, 0, 0, 0);
+            if (!FIRST) sw = ldu4(w.sgn + (tE + e) * 4);
+            unsigned nw[4];
+#pragma unroll
+            for (int v = 0; v < 4; v++) {
+                const float sj = comp(sv, v);
+                float x = sj;
+                if (!FIRST) {
+                    const float m0v = comp(om0, v);
+                    const float mag = (p == compl4(olc, v)) ? comp(om1, v) : fabsf(m0v);
+                    const unsigned neg_eta = ((comp(sw, v) >> lane) & 1u) ^ (__float_as_uint(m0v) >> 31) ^ corr;
+                    x = sj - (neg_eta ? -mag : mag);  // lambda_k - eta^prev_{i,k}
+                }
+                const float ax = fabsf(x);
+                const bool lt = ax < nm0[v];  // first strict minimum (A13)
+                nm1[v] = lt ? nm0[v] : fminf(nm1[v], ax);
+                nm0[v] = lt ? ax : nm0[v];
+                nloc[v] = lt ? p : nloc[v];
+                const bool neg = x < 0.f;  // sign(0) = +1
+                npar ^= (unsigned)neg << v;
+                if (EARLY) syn ^= (unsigned)(sj > 0.f) << v;  // b_j = slice(s_j)
+                nw[v] = __ballot_sync(FULL, neg);
+            }
+            if (lane == 0) *reinterpret_cast<uint4 *>(w.sgn + (tE + e) * 4) = make_uint4(nw[0], nw[1], nw[2], nw[3]);
+        }
+        float4 o0, o1;
+        o0.x = __uint_as_float(__float_as_uint(nm0[0]) | ((npar & 1u) << 31));
+        o0.y = __uint_as_float(__float_as_uint(nm0[1]) | (((npar >> 1) & 1u) << 31));
+        o0.z = __uint_as_float(__float_as_uint(nm0[2]) | (((npar >> 2) & 1u) << 31));
+        o0.w = __uint_as_float(__float_as_uint(nm0[3]) | (((npar >> 3) & 1u) << 31));
+        o1 = make_float4(nm1[0], nm1[1], nm1[2], nm1[3]);
+        st4(w.min0 + st, o0);
+        st4(w.min1 + st, o1);
+        L4 nl;
+        nl.x = (LocT)nloc[0];
+        nl.y = (LocT)nloc[1];
+        nl.z = (LocT)nloc[2];
+        nl.w = (LocT)nloc[3];
+        *reinterpret_cast<L4 *>(reinterpret_cast<LocT *>(w.loc) + st) = nl;
+        if (EARLY) {
+            u0 |= __ballot_sync(FULL, syn & 1u);
+            u1 |= __ballot_sync(FULL, syn & 2u);
+            u2 |= __ballot_sync(FULL, syn & 4u);
+            u3 |= __ballot_sync(FULL, syn & 8u);
+        }
+    }
+    if (EARLY) {
+        if (lane == 0) {
+            if (u0) atomicOr(&s_u[0], u0);
+            if (u1) atomicOr(&s_u[1], u1);
+            if (u2) atomicOr(&s_u[2], u2);
+            if (u3) atomicOr(&s_u[3], u3);
+        }
+        __syncthreads();
+        if (threadIdx.x < 4 && s_u[threadIdx.x])
+            atomicOr(w.unsat + ((size_t)(k & 1) * w.T + t) * 4 + threadIdx.x, s_u[threadIdx.x]);
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// a5/a6: bit-node sweep of loop body k; stops frames whose b^(k-1) satisfied every check.
+// ------------------------------------------------------------------------------------------------
+template <typename LocT, bool EARLY>
+__global__ void __launch_bounds__(CTA) k_bn(Graph g, StreamState w, int k, int cols_per_cta, int literal) {
+    using L4 = typename Vec4<LocT>::type;
+    const int t = blockIdx.y;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int T = w.T;
+    uint4 act = make_uint4(FULL, FULL, FULL, FULL);
+    if (EARLY) {
+        const uint4 ua = ldu4(w.unsat + ((size_t)(k & 1) * T + t) * 4);
+        const uint4 dw = ldu4(w.done + (size_t)t * 4);
+        const uint4 newly = make_uint4(~ua.x & ~dw.x, ~ua.y & ~dw.y, ~ua.z & ~dw.z, ~ua.w & ~dw.w);
+        act = make_uint4(ua.x & ~dw.x, ua.y & ~dw.y, ua.z & ~dw.z, ua.w & ~dw.w);
+        if (blockIdx.x == 0) {
+            const int tid = threadIdx.x;
+            if (tid < 4) {
+                w.done[(size_t)t * 4 + tid] = comp(dw, tid) | comp(newly, tid);
+                w.unsat[((size_t)((k + 1) & 1) * T + t) * 4 + tid] = 0;  // buffer of body k+1
+            }
+            if (tid < TILE && ((comp(newly, tid & 3) >> (tid >> 2)) & 1u))
+                w.iters[(size_t)t * TILE + tid] = k - 1;  // stopped after k-1 bodies
+        }
+        if ((act.x | act.y | act.z | act.w) == 0) return;
+    }
+    const unsigned mine = ((act.x >> lane) & 1u) | (((act.y >> lane) & 1u) << 1) | (((act.z >> lane) & 1u) << 2) |
+                          (((act.w >> lane) & 1u) << 3);
+    const int m = g.m, n = g.n, E = g.E;
+    const size_t tm = (size_t)t * m, tn = (size_t)t * n, tE = (size_t)t * E;
+    const int j0 = blockIdx.x * cols_per_cta, j1 = min(n, j0 + cols_per_cta);
+    for (int j = j0 + warp; j < j1; j += CTA / 32) {
+        const int c0 = __ldg(g.col_ptr + j), dv = __ldg(g.col_ptr + j + 1) - c0;
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int q = 0; q < dv; q++) {
+            const int4 ed = __ldg(g.bn_edge + c0 + q);  // {e, i, p, d_i & 1}, ascending i
+            const size_t st = (tm + ed.y) * TILE + 4 * lane;
+            const float4 m0 = ld4(w.min0 + st);
+            const float4 m1 = ld4(w.min1 + st);
+            const L4 lc = *reinterpret_cast<const L4 *>(reinterpret_cast<const LocT *>(w.loc) + st);
+            const uint4 sw = ldu4(w.sgn + (tE + ed.x) * 4);
+            const unsigned corr = (unsigned)ed.w & (unsigned)(!literal);
+#pragma unroll
+            for (int v = 0; v < 4; v++) {
+                const float m0v = comp(m0, v);
+                const float mag = (ed.z == compl4(lc, v)) ? comp(m1, v) : fabsf(m0v);  // Obs. 1
+                const unsigned neg = ((comp(sw, v) >> lane) & 1u) ^ (__float_as_uint(m0v) >> 31) ^ corr;  // Obs. 2
+                acc[v] = acc[v] + (neg ? -mag : mag);
+            }
+        }
+        const size_t sj = (tn + j) * TILE + 4 * lane;
+        const float4 rv = ld4(w.r + sj);
+        float4 out = make_float4(acc[0] + rv.x, acc[1] + rv.y, acc[2] + rv.z, acc[3] + rv.w);
+        if (mine == 0xFu) {
+            st4(w.s + sj, out);
+        } else if (mine) {
+            const float4 old = ld4(w.s + sj);
+            out.x = (mine & 1u) ? out.x : old.x;
+            out.y = (mine & 2u) ? out.y : old.y;
+            out.z = (mine & 4u) ? out.z : old.z;
+            out.w = (mine & 8u) ? out.w : old.w;
+            st4(w.s + sj, out);
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// a6: syndrome of b^(L) (the test after the last body), into unsat[slot].
+// ------------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(CTA) k_syndrome(Graph g, StreamState w, int slot, int rows_per_cta) {
+    const int t = blockIdx.y;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __shared__ uint32_t s_u[4];
+    const uint4 dw = ldu4(w.done + (size_t)t * 4);
+    if ((dw.x & dw.y & dw.z & dw.w) == FULL) return;
+    if (threadIdx.x < 4) s_u[threadIdx.x] = 0;
+    __syncthreads();
+    const size_t tn = (size_t)t * g.n;
+    const int i0 = blockIdx.x * rows_per_cta, i1 = min(g.m, i0 + rows_per_cta);
+    uint32_t u[4] = {0, 0, 0, 0};
+    for (int i = i0 + warp; i < i1; i += CTA / 32) {
+        const int a = __ldg(g.row_ptr + i), d = __ldg(g.row_ptr + i + 1) - a;
+        unsigned syn = 0;
+        for (int p = 0; p < d; p++) {
+            const int j = __ldg(g.col_idx + a + p);
+            const float4 sv = ld4(w.s + (tn + j) * TILE + 4 * lane);
+            syn ^= (unsigned)(sv.x > 0.f) | ((unsigned)(sv.y > 0.f) << 1) | ((unsigned)(sv.z > 0.f) << 2) |
+                   ((unsigned)(sv.w > 0.f) << 3);
+        }
+#pragma unroll
+        for (int v = 0; v < 4; v++) u[v] |= __ballot_sync(FULL, (syn >> v) & 1u);
+    }
+    if (lane == 0)
+#pragma unroll
+        for (int v = 0; v < 4; v++)
+            if (u[v]) atomicOr(&s_u[v], u[v]);
+    __syncthreads();
+    if (threadIdx.x < 4 && s_u[threadIdx.x])
+        atomicOr(w.unsat + ((size_t)slot * w.T + t) * 4 + threadIdx.x, s_u[threadIdx.x]);
+}
+
+// ------------------------------------------------------------------------------------------------
+// a7: stage-out.  s [T][n][128] -> posterior [F][n], bits = slice(s) [F][n]; per-frame counters.
+// ------------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(CTA) k_finalize(StreamState w, int n, int64_t frames, float *__restrict__ post,
+                                                  uint8_t *__restrict__ bits) {
+    __shared__ float ts[32][TILE + 1];
+    __shared__ float tr[32][TILE + 1];
+    const int t = blockIdx.y, j0 = blockIdx.x * 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int jl = warp; jl < 32; jl += CTA / 32) {
+        const int j = j0 + jl;
+        if (j >= n) break;
+        const size_t base = ((size_t)t * n + j) * TILE;
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            ts[jl][lane + 32 * q] = w.s[base + lane + 32 * q];
+            tr[jl][lane + 32 * q] = w.r[base + lane + 32 * q];
+        }
+    }
+    __syncthreads();
+    const int j = j0 + lane;
+    const bool jv = j < n;
+    for (int fl = warp; fl < TILE; fl += CTA / 32) {
+        const int64_t f = (int64_t)t * TILE + fl;
+        if (f >= frames) break;
+        const float sv = ts[lane][fl];
+        const bool b = jv && sv > 0.f;  // Eq. slice
+        if (jv) {
+            if (post) post[f * n + j] = sv;
+            if (bits) bits[f * n + j] = (uint8_t)b;
+        }
+        const int be = __popc(__ballot_sync(FULL, b));
+        const int raw = __popc(__ballot_sync(FULL, jv && tr[lane][fl] > 0.f));
+        const bool nz = __any_sync(FULL, jv && fabsf(sv) <= 1e-4f);
+        if (lane == 0) {
+            if (be) atomicAdd(w.fbe + (size_t)t * TILE + fl, be);
+            if (raw) atomicAdd(w.fraw + (size_t)t * TILE + fl, raw);
+            if (nz) w.fnz[(size_t)t * TILE + fl] = 1;
+        }
+    }
+}
+
+// per-frame k, isCodeword and the 8 accumulated counters
+__global__ void __launch_bounds__(CTA) k_frame_stats(StreamState w, int64_t frames, int L, int early, int slot,
+                                                     int32_t *__restrict__ iters_out, uint8_t *__restrict__ conv_out,
+                                                     unsigned long long *__restrict__ stats) {
+    __shared__ unsigned long long s_acc[8];
+    if (threadIdx.x < 8) s_acc[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t f = blockIdx.x * (int64_t)CTA + threadIdx.x;
+    unsigned long long c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (f < frames) {
+        const int64_t t = f / TILE;
+        const int fl = (int)(f % TILE), ln = fl >> 2, v = fl & 3;
+        int it = L, conv;
+        const bool stopped = early && ((w.done[t * 4 + v] >> ln) & 1u);
+        if (stopped) {
+            it = w.iters[f];
+            conv = 1;
+        } else {
+            conv = !((w.unsat[((int64_t)slot * w.T + t) * 4 + v] >> ln) & 1u);
+        }
+        if (iters_out) iters_out[f] = it;
+        if (conv_out) conv_out[f] = (uint8_t)conv;
+        const int be = w.fbe[f];
+        c[0] = 1;
+        c[1] = (unsigned long long)be;
+        c[2] = be > 0;
+        c[3] = (be > 0) && conv;
+        c[4] = (unsigned long long)it;
+        c[5] = conv;
+        c[6] = w.fnz[f] != 0;
+        c[7] = (unsigned long long)w.fraw[f];
+    }
+    if (stats) {
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            unsigned long long x = c[q];
+            for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
+            if ((threadIdx.x & 31) == 0 && x) atomicAdd(&s_acc[q], x);
+        }
+        __syncthreads();
+        if (threadIdx.x < 8 && s_acc[threadIdx.x]) atomicAdd(stats + threadIdx.x, s_acc[threadIdx.x]);
+    }
+}
+
+inline dim3 grid2(int64_t x, int y) { return dim3((unsigned)std::max<int64_t>(1, x), (unsigned)y); }
+
+}  // namespace
+
+int launch_stage_in(const Graph &g, const StreamState &w, const float *llr, int64_t frames, cudaStream_t st) {
+    k_stage_in<<<grid2((g.n + 31) / 32, w.T), CTA, 0, st>>>(llr, frames, g.n, w.T, w.r, w.s, w.unsat, w.done, w.fbe,
+                                                           w.fraw, w.fnz);
+    return 1;
+}
+
+int launch_check_node(const Graph &g, const StreamState &w, int k, bool first, bool early, bool literal, bool loc16,
+                      const StreamLaunch &cfg, cudaStream_t st) {
+    const dim3 grid = grid2((g.m + cfg.rows_per_cta - 1) / cfg.rows_per_cta, w.T);
+    const int lit = literal ? 1 : 0;
+#define CN_CASE(LT, F, EA) k_cn<LT, F, EA><<<grid, CTA, 0, st>>>(g, w, k, cfg.rows_per_cta, lit)
+    if (loc16) {
+        if (first) { if (early) CN_CASE(uint16_t, true, true); else CN_CASE(uint16_t, true, false); }
+        else { if (early) CN_CASE(uint16_t, false, true); else CN_CASE(uint16_t, false, false); }
+    } else {
+        if (first) { if (early) CN_CASE(uint8_t, true, true); else CN_CASE(uint8_t, true, false); }
+        else { if (early) CN_CASE(uint8_t, false, true); else CN_CASE(uint8_t, false, false); }
+    }
+#undef CN_CASE
+    return 1;
+}
+
+int launch_bit_node(const Graph &g, const StreamState &w, int k, bool early, bool literal, bool loc16,
+                    const StreamLaunch &cfg, cudaStream_t st) {
+    const dim3 grid = grid2((g.n + cfg.cols_per_cta - 1) / cfg.cols_per_cta, w.T);
+    const int lit = literal ? 1 : 0;
+    if (loc16) {
+        if (early) k_bn<uint16_t, true><<<grid, CTA, 0, st>>>(g, w, k, cfg.cols_per_cta, lit);
+        else k_bn<uint16_t, false><<<grid, CTA, 0, st>>>(g, w, k, cfg.cols_per_cta, lit);
+    } else {
+        if (early) k_bn<uint8_t, true><<<grid, CTA, 0, st>>>(g, w, k, cfg.cols_per_cta, lit);
+        else k_bn<uint8_t, false><<<grid, CTA, 0, st>>>(g, w, k, cfg.cols_per_cta, lit);
+    }
+    return 1;
+}
+
+int launch_syndrome(const Graph &g, const StreamState &w, int slot, const StreamLaunch &cfg, cudaStream_t st) {
+    k_syndrome<<<grid2((g.m + cfg.rows_per_cta - 1) / cfg.rows_per_cta, w.T), CTA, 0, st>>>(g, w, slot,
+                                                                                             cfg.rows_per_cta);
+    return 1;
+}
+
+int launch_finalize(const Graph &g, const StreamState &w, int64_t frames, float *posterior, uint8_t *bits,
+                    cudaStream_t st) {
+    k_finalize<<<grid2((g.n + 31) / 32, w.T), CTA, 0, st>>>(w, g.n, frames, posterior, bits);
+    return 1;
+}
+
+int launch_frame_stats(const Graph &g, const StreamState &w, int64_t frames, int L, bool early, int final_slot,
+                       int32_t *iters_out, uint8_t *conv_out, unsigned long long *stats, cudaStream_t st) {
+    (void)g;
+    k_frame_stats<<<(unsigned)std::max<int64_t>(1, (frames + CTA - 1) / CTA), CTA, 0, st>>>(
+        w, frames, L, early ? 1 : 0, final_slot, iters_out, conv_out, stats);
+    return 1;
+}
+
+}  // namespace ldpc

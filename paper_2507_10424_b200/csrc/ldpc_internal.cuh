@@ -1,0 +1,90 @@
+// ldpc_internal.cuh -- internal declarations of libldpc (not part of the C-ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+#include "../../include/ldpc.h"
+
+namespace ldpc {
+
+// Frames are processed in tiles of 128 (one warp = 32 lanes x 4 frames, float4 per lane).
+constexpr int TILE = 128;
+constexpr int CTA = 256;  // threads per CTA of the streaming kernels (8 warps)
+
+// Error bits raised by the ingest kernels.
+enum : int { ERRB_NOT_BINARY = 1, ERRB_ROW_DEGREE = 2, ERRB_DUPLICATE = 4, ERRB_RANGE = 8 };
+
+// Device view of the ingested Tanner graph.
+struct Graph {
+    int m, n, E;
+    const int *row_ptr;  // [m+1]   N_i = col_idx[row_ptr[i] .. row_ptr[i+1])
+    const int *col_idx;  // [E]     ascending within a row
+    const int *col_ptr;  // [n+1]   M_j = bn_edge[col_ptr[j] .. col_ptr[j+1])
+    const int4 *bn_edge; // [E]     {edge id e (row-list position), row i, position p in N_i, d_i & 1}
+};
+
+// Per-chunk decode state of the streaming schedule, frame-interleaved in tiles of 128:
+//   r, s   [T][n][128] fp32          channel values and current soft vector (Eq. sCalculation)
+//   min0   [T][m][128] fp32          |lambda| minimum of the row; SIGN BIT = row sign parity (Obs. 2)
+//   min1   [T][m][128] fp32          second minimum (Obs. 1)
+//   loc    [T][m][128] u8 / u16      min0Location as the position inside N_i
+//   sgn    [T][E][4]   u32           sign bit of lambda_e per frame (bit `lane` of word v = frame 4*lane+v)
+//   unsat  [2][T][4]   u32           per-frame "some check unsatisfied" bits (double-buffered by iteration)
+//   done   [T][4]      u32           per-frame "stopped" bits
+//   iters  [T*128]     i32           k at which a frame stopped (early stop)
+//   fbe/fraw/fnz [T*128] i32         per-frame bit errors, raw errors, near-zero flag
+struct StreamState {
+    int T;
+    float *r, *s, *min0, *min1;
+    void *loc;
+    uint32_t *sgn, *unsat, *done;
+    int *iters, *fbe, *fraw, *fnz;
+};
+
+// ---- ingest (ingest.cu) ----
+int ingest_dense(const uint8_t *H, int m, int n, cudaStream_t st, struct HostGraph *hg);
+int ingest_coo(const int32_t *rows, const int32_t *cols, int64_t nnz, int m, int n, cudaStream_t st,
+               struct HostGraph *hg);
+
+struct HostGraph {  // device allocations owned by the plan
+    int m = 0, n = 0, E = 0, max_row_deg = 0, max_col_deg = 0;
+    int *row_ptr = nullptr, *col_idx = nullptr, *col_ptr = nullptr, *col_edge = nullptr;
+    int4 *bn_edge = nullptr;
+    int64_t launches = 0;
+    Graph view() const { return Graph{m, n, E, row_ptr, col_idx, col_ptr, bn_edge}; }
+    void free_all();
+};
+
+// ---- streaming schedule (decode_stream.cu) ----
+struct StreamLaunch {
+    int rows_per_cta = 32;
+    int cols_per_cta = 32;
+};
+// Launch helpers; each returns the number of kernels launched.
+int launch_stage_in(const Graph &g, const StreamState &w, const float *llr, int64_t frames, cudaStream_t st);
+int launch_check_node(const Graph &g, const StreamState &w, int k, bool first, bool early, bool literal, bool loc16,
+                      const StreamLaunch &cfg, cudaStream_t st);
+int launch_bit_node(const Graph &g, const StreamState &w, int k, bool early, bool literal, bool loc16,
+                    const StreamLaunch &cfg, cudaStream_t st);
+int launch_syndrome(const Graph &g, const StreamState &w, int slot, const StreamLaunch &cfg, cudaStream_t st);
+int launch_finalize(const Graph &g, const StreamState &w, int64_t frames, float *posterior, uint8_t *bits,
+                    cudaStream_t st);
+int launch_frame_stats(const Graph &g, const StreamState &w, int64_t frames, int L, bool early, int final_slot,
+                       int32_t *iters_out, uint8_t *conv_out, unsigned long long *stats, cudaStream_t st);
+
+// ---- resident schedule (decode_resident.cu) ----
+struct ResidentPlan {
+    bool ok = false;
+    int slots = 0;       // frame slots per CTA
+    int threads = 0;     // threads per CTA
+    size_t smem = 0;     // dynamic shared memory bytes
+    int ctas = 0;        // persistent grid size
+};
+ResidentPlan plan_resident(const HostGraph &g, bool loc16, int device);
+int launch_resident(const Graph &g, const ResidentPlan &rp, const float *llr, int64_t frames, int L, bool early,
+                    bool literal, bool loc16, float *posterior, uint8_t *bits, int32_t *iters_out,
+                    uint8_t *conv_out, unsigned long long *stats, int *work_counter, cudaStream_t st);
+
+}  // namespace ldpc

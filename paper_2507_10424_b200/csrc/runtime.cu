@@ -1,0 +1,488 @@
+// runtime.cu -- host runtime behind the C-ABI of include/ldpc.h: handle, workspace, schedule choice,
+// the stream-ordered loop over chunks and loop bodies, the host-buffer pipeline and kernel accounting.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "ldpc_internal.cuh"
+
+using namespace ldpc;
+
+struct ldpc_plan {
+    HostGraph g;
+    uint32_t flags = 0;
+    int device = 0;
+    bool poisoned = false;
+    // streaming workspace
+    void *ws = nullptr;
+    size_t ws_bytes = 0;
+    int ws_tiles = 0;
+    int64_t chunk_cap = 0;  // frames per chunk, 0 = automatic
+    StreamLaunch cfg;
+    // resident schedule
+    ResidentPlan rp;
+    int *work_counter = nullptr;
+    // accounting
+    int64_t launches = 0;
+    bool prof = false;
+    struct Ev {
+        int cls;
+        cudaEvent_t a, b;
+    };
+    std::vector<Ev> evs;
+    std::vector<cudaEvent_t> pool;
+    int64_t prof_launches[LDPC_K_NUM_CLASSES] = {};
+    double prof_ms[LDPC_K_NUM_CLASSES] = {};
+    // host pipeline
+    cudaStream_t hs[3] = {nullptr, nullptr, nullptr};
+    void *hbuf[2] = {nullptr, nullptr};
+    size_t hbuf_bytes = 0;
+};
+
+namespace {
+
+int status_of(cudaError_t e) {
+    if (e == cudaSuccess) return LDPC_OK;
+    if (e == cudaErrorMemoryAllocation) return LDPC_ERR_OOM;
+    return LDPC_ERR_CUDA;
+}
+
+cudaEvent_t get_event(ldpc_plan *h) {
+    if (!h->pool.empty()) {
+        cudaEvent_t e = h->pool.back();
+        h->pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// Launch one kernel (or a fixed group) of class `cls`, bracketed by events when profiling.
+template <typename F>
+void launch(ldpc_plan *h, int cls, cudaStream_t st, F &&fn) {
+    if (h->prof) {
+        cudaEvent_t a = get_event(h), b = get_event(h);
+        cudaEventRecord(a, st);
+        int nl = fn();
+        cudaEventRecord(b, st);
+        h->evs.push_back({cls, a, b});
+        h->launches += nl;
+        h->prof_launches[cls] += nl;
+    } else {
+        h->launches += fn();
+    }
+}
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+size_t tile_bytes(const HostGraph &g, bool loc16) {
+    const size_t m = g.m, n = g.n, E = g.E;
+    size_t b = 0;
+    b += 2 * align256(n * TILE * 4);                 // r, s
+    b += 2 * align256(m * TILE * 4);                 // min0, min1
+    b += align256(m * TILE * (loc16 ? 2 : 1));       // loc
+    b += align256(E * 16);                           // sgn
+    b += 3 * 256;                                    // unsat x2, done
+    b += 4 * align256(TILE * 4);                     // iters, fbe, fraw, fnz
+    return b;
+}
+
+// carve the workspace into per-array regions of T tiles each
+StreamState carve(void *base, int T, const HostGraph &g, bool loc16) {
+    const size_t m = g.m, n = g.n, E = g.E;
+    char *p = static_cast<char *>(base);
+    auto take = [&](size_t bytes) {
+        char *q = p;
+        p += align256(bytes);
+        return q;
+    };
+    StreamState w;
+    w.T = T;
+    w.r = reinterpret_cast<float *>(take((size_t)T * n * TILE * 4));
+    w.s = reinterpret_cast<float *>(take((size_t)T * n * TILE * 4));
+    w.min0 = reinterpret_cast<float *>(take((size_t)T * m * TILE * 4));
+    w.min1 = reinterpret_cast<float *>(take((size_t)T * m * TILE * 4));
+    w.loc = take((size_t)T * m * TILE * (loc16 ? 2 : 1));
+    w.sgn = reinterpret_cast<uint32_t *>(take((size_t)T * E * 16));
+    w.unsat = reinterpret_cast<uint32_t *>(take((size_t)2 * T * 16));
+    w.done = reinterpret_cast<uint32_t *>(take((size_t)T * 16));
+    w.iters = reinterpret_cast<int *>(take((size_t)T * TILE * 4));
+    w.fbe = reinterpret_cast<int *>(take((size_t)T * TILE * 4));
+    w.fraw = reinterpret_cast<int *>(take((size_t)T * TILE * 4));
+    w.fnz = reinterpret_cast<int *>(take((size_t)T * TILE * 4));
+    return w;
+}
+
+int64_t auto_chunk_tiles(ldpc_plan *h, bool loc16) {
+    size_t freeb = 0, total = 0;
+    cudaMemGetInfo(&freeb, &total);
+    size_t budget = std::min<size_t>(freeb / 2 + h->ws_bytes / 2, (size_t)32 << 30);
+    int64_t tiles = (int64_t)(budget / tile_bytes(h->g, loc16));
+    return std::max<int64_t>(1, std::min<int64_t>(tiles, 65535));
+}
+
+int ensure_ws(ldpc_plan *h, int T, bool loc16) {
+    // size for the full per-array layout of T tiles
+    size_t need = 0;
+    {
+        const size_t m = h->g.m, n = h->g.n, E = h->g.E;
+        need = 2 * align256((size_t)T * n * TILE * 4) + 2 * align256((size_t)T * m * TILE * 4) +
+               align256((size_t)T * m * TILE * (loc16 ? 2 : 1)) + align256((size_t)T * E * 16) +
+               align256((size_t)2 * T * 16) + align256((size_t)T * 16) + 4 * align256((size_t)T * TILE * 4);
+    }
+    if (need <= h->ws_bytes) return LDPC_OK;
+    if (h->ws) cudaFree(h->ws);
+    h->ws = nullptr;
+    h->ws_bytes = 0;
+    cudaError_t e = cudaMalloc(&h->ws, need);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return LDPC_ERR_OOM;
+    }
+    h->ws_bytes = need;
+    return LDPC_OK;
+}
+
+int check_async(ldpc_plan *h) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        h->poisoned = true;
+        return LDPC_ERR_CUDA;
+    }
+    return LDPC_OK;
+}
+
+int decode_stream(ldpc_plan *h, const float *llr, int64_t frames, int L, uint8_t *bits, int32_t *iters, float *post,
+                  uint8_t *conv, int64_t *stats, cudaStream_t st) {
+    const bool early = !(h->flags & LDPC_FLAG_NO_EARLY_STOP);
+    const bool literal = (h->flags & LDPC_FLAG_SIGN_PAPER_LITERAL) != 0;
+    const bool loc16 = h->g.max_row_deg > 255;
+    const Graph g = h->g.view();
+    int64_t cap_tiles = h->chunk_cap > 0 ? (h->chunk_cap + TILE - 1) / TILE : auto_chunk_tiles(h, loc16);
+    cap_tiles = std::min<int64_t>(cap_tiles, 65535);
+    const int64_t need_tiles = (frames + TILE - 1) / TILE;
+    const int T_max = (int)std::min<int64_t>(cap_tiles, need_tiles);
+    int rc = ensure_ws(h, T_max, loc16);
+    if (rc) return rc;
+    const int final_slot = (L + 1) & 1;
+    for (int64_t c0 = 0; c0 < frames; c0 += (int64_t)T_max * TILE) {
+        const int64_t fc = std::min<int64_t>((int64_t)T_max * TILE, frames - c0);
+        const int T = (int)((fc + TILE - 1) / TILE);
+        const StreamState w = carve(h->ws, T, h->g, loc16);
+        launch(h, LDPC_K_STAGE_IN, st, [&] { return launch_stage_in(g, w, llr + c0 * g.n, fc, st); });
+        for (int k = 1; k <= L; k++) {
+            launch(h, LDPC_K_CHECK_NODE, st,
+                   [&] { return launch_check_node(g, w, k, k == 1, early, literal, loc16, h->cfg, st); });
+            launch(h, LDPC_K_BIT_NODE, st, [&] { return launch_bit_node(g, w, k, early, literal, loc16, h->cfg, st); });
+        }
+        launch(h, LDPC_K_SYNDROME, st, [&] { return launch_syndrome(g, w, final_slot, h->cfg, st); });
+        launch(h, LDPC_K_FINALIZE, st, [&] {
+            int nl = launch_finalize(g, w, fc, post ? post + c0 * g.n : nullptr, bits ? bits + c0 * g.n : nullptr, st);
+            nl += launch_frame_stats(g, w, fc, L, early, final_slot, iters ? iters + c0 : nullptr,
+                                     conv ? conv + c0 : nullptr, reinterpret_cast<unsigned long long *>(stats), st);
+            return nl;
+        });
+        rc = check_async(h);
+        if (rc) return rc;
+    }
+    return LDPC_OK;
+}
+
+bool use_resident(ldpc_plan *h) {
+    if (h->flags & LDPC_FLAG_FORCE_STREAM) return false;
+    if (h->flags & LDPC_FLAG_FORCE_RESIDENT) return true;
+    return h->rp.ok;
+}
+
+int decode_resident(ldpc_plan *h, const float *llr, int64_t frames, int L, uint8_t *bits, int32_t *iters,
+                    float *post, uint8_t *conv, int64_t *stats, cudaStream_t st) {
+    if (!h->rp.ok) return LDPC_ERR_UNSUPPORTED;
+    const bool early = !(h->flags & LDPC_FLAG_NO_EARLY_STOP);
+    const bool literal = (h->flags & LDPC_FLAG_SIGN_PAPER_LITERAL) != 0;
+    const bool loc16 = h->g.max_row_deg > 255;
+    if (!h->work_counter) {
+        if (cudaMalloc(&h->work_counter, sizeof(int) * 2) != cudaSuccess) {
+            cudaGetLastError();
+            return LDPC_ERR_OOM;
+        }
+    }
+    const Graph g = h->g.view();
+    launch(h, LDPC_K_RESIDENT, st, [&] {
+        return launch_resident(g, h->rp, llr, frames, L, early, literal, loc16, post, bits, iters, conv,
+                               reinterpret_cast<unsigned long long *>(stats), h->work_counter, st);
+    });
+    return check_async(h);
+}
+
+int finish_prepare(ldpc_plan *p, int rc, uint32_t flags, ldpc_handle_t *out) {
+    if (rc != LDPC_OK) {
+        p->g.free_all();
+        delete p;
+        return rc;
+    }
+    p->flags = flags;
+    p->launches = p->g.launches;
+    cudaGetDevice(&p->device);
+    p->rp = plan_resident(p->g, p->g.max_row_deg > 255, p->device);
+    if (const char *s = getenv("LDPC_ROWS_PER_CTA")) p->cfg.rows_per_cta = std::max(8, atoi(s));
+    if (const char *s = getenv("LDPC_COLS_PER_CTA")) p->cfg.cols_per_cta = std::max(8, atoi(s));
+    *out = p;
+    return LDPC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ldpc_abi_version(void) { return LDPC_ABI_VERSION; }
+
+const char *ldpc_status_string(int code) {
+    switch (code) {
+        case LDPC_OK: return "ok";
+        case LDPC_ERR_INVALID_ARG: return "invalid argument";
+        case LDPC_ERR_NOT_BINARY: return "H has an entry outside {0,1}";
+        case LDPC_ERR_ROW_DEGREE: return "H has a row of degree < 2";
+        case LDPC_ERR_DUPLICATE_EDGE: return "H lists a (row, column) pair twice";
+        case LDPC_ERR_INDEX_RANGE: return "H lists an index outside [0,m) x [0,n)";
+        case LDPC_ERR_OOM: return "out of memory";
+        case LDPC_ERR_CUDA: return "CUDA error (handle poisoned)";
+        case LDPC_ERR_UNSUPPORTED: return "unsupported size";
+        default: return "unknown status";
+    }
+}
+
+int ldpc_prepare_dense(const uint8_t *H, int32_t m, int32_t n, uint32_t flags, ldpc_stream_t stream,
+                       ldpc_handle_t *out) {
+    if (!H || !out || m < 1 || n < 2) return LDPC_ERR_INVALID_ARG;
+    ldpc_plan *p = new (std::nothrow) ldpc_plan;
+    if (!p) return LDPC_ERR_OOM;
+    int rc = ingest_dense(H, m, n, static_cast<cudaStream_t>(stream), &p->g);
+    return finish_prepare(p, rc, flags, out);
+}
+
+int ldpc_prepare_coo(const int32_t *rows, const int32_t *cols, int64_t nnz, int32_t m, int32_t n, uint32_t flags,
+                     ldpc_stream_t stream, ldpc_handle_t *out) {
+    if (!rows || !cols || !out || m < 1 || n < 2 || nnz < 0) return LDPC_ERR_INVALID_ARG;
+    ldpc_plan *p = new (std::nothrow) ldpc_plan;
+    if (!p) return LDPC_ERR_OOM;
+    int rc = ingest_coo(rows, cols, nnz, m, n, static_cast<cudaStream_t>(stream), &p->g);
+    return finish_prepare(p, rc, flags, out);
+}
+
+int ldpc_decode(ldpc_handle_t h, const float *llr, int64_t frames, int32_t max_iter, uint8_t *bits_out,
+                int32_t *iters_out, float *posterior_out, uint8_t *converged_out, int64_t *stats_inout,
+                ldpc_stream_t stream) {
+    if (!h || frames < 0 || max_iter < 0) return LDPC_ERR_INVALID_ARG;
+    if (frames > 0 && !llr) return LDPC_ERR_INVALID_ARG;
+    if (h->poisoned) return LDPC_ERR_CUDA;
+    if (frames == 0) return LDPC_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (use_resident(h))
+        return decode_resident(h, llr, frames, max_iter, bits_out, iters_out, posterior_out, converged_out,
+                               stats_inout, st);
+    return decode_stream(h, llr, frames, max_iter, bits_out, iters_out, posterior_out, converged_out, stats_inout,
+                         st);
+}
+
+int ldpc_decode_host(ldpc_handle_t h, const float *llr, int64_t frames, int32_t max_iter, uint8_t *bits_out,
+                     int32_t *iters_out, float *posterior_out, uint8_t *converged_out, int64_t *stats_inout,
+                     ldpc_stream_t stream) {
+    if (!h || frames < 0 || max_iter < 0) return LDPC_ERR_INVALID_ARG;
+    if (frames > 0 && !llr) return LDPC_ERR_INVALID_ARG;
+    if (h->poisoned) return LDPC_ERR_CUDA;
+    if (frames == 0) return LDPC_OK;
+    const int64_t n = h->g.n;
+    // chunk of frames per pipeline stage
+    int64_t chunk = std::max<int64_t>(TILE, std::min<int64_t>(frames, (int64_t)(256u << 20) / (n * 4)));
+    chunk = (chunk + TILE - 1) / TILE * TILE;
+    const size_t per_frame = n * 4 + (bits_out ? n : 0) + (posterior_out ? n * 4 : 0) + 4 + 1;
+    const size_t set_bytes = align256(chunk * n * 4) + align256(chunk * n) + align256(chunk * n * 4) +
+                             align256(chunk * 4) + align256(chunk) + 256;
+    (void)per_frame;
+    cudaError_t e = cudaSuccess;
+    if (!h->hs[0]) {
+        for (int q = 0; q < 3; q++) e = cudaStreamCreateWithFlags(&h->hs[q], cudaStreamNonBlocking);
+        if (e != cudaSuccess) return status_of(e);
+    }
+    if (h->hbuf_bytes < set_bytes) {
+        for (int q = 0; q < 2; q++) {
+            cudaFree(h->hbuf[q]);
+            h->hbuf[q] = nullptr;
+        }
+        h->hbuf_bytes = 0;
+        for (int q = 0; q < 2; q++)
+            if (cudaMalloc(&h->hbuf[q], set_bytes) != cudaSuccess) {
+                cudaGetLastError();
+                return LDPC_ERR_OOM;
+            }
+        h->hbuf_bytes = set_bytes;
+    }
+    cudaStream_t user = static_cast<cudaStream_t>(stream);
+    cudaStream_t s_in = h->hs[0], s_run = h->hs[1], s_out = h->hs[2];
+    cudaEvent_t ev_start = get_event(h), ev_in[2] = {get_event(h), get_event(h)},
+                ev_run[2] = {get_event(h), get_event(h)}, ev_out[2] = {get_event(h), get_event(h)};
+    cudaEventRecord(ev_start, user);
+    cudaStreamWaitEvent(s_in, ev_start, 0);
+    cudaStreamWaitEvent(s_run, ev_start, 0);
+    cudaStreamWaitEvent(s_out, ev_start, 0);
+    unsigned long long *d_stats = nullptr;
+    if (stats_inout) {
+        if (cudaMalloc(&d_stats, 64) != cudaSuccess) return LDPC_ERR_OOM;
+        cudaMemsetAsync(d_stats, 0, 64, s_run);
+    }
+    int rc = LDPC_OK;
+    int idx = 0;
+    bool used[2] = {false, false};
+    for (int64_t c0 = 0; c0 < frames && rc == LDPC_OK; c0 += chunk, idx ^= 1) {
+        const int64_t fc = std::min(chunk, frames - c0);
+        char *base = static_cast<char *>(h->hbuf[idx]);
+        float *d_llr = reinterpret_cast<float *>(base);
+        uint8_t *d_bits = reinterpret_cast<uint8_t *>(base + align256(chunk * n * 4));
+        float *d_post = reinterpret_cast<float *>(base + align256(chunk * n * 4) + align256(chunk * n));
+        int32_t *d_iters = reinterpret_cast<int32_t *>(base + align256(chunk * n * 4) + align256(chunk * n) +
+                                                      align256(chunk * n * 4));
+        uint8_t *d_conv = reinterpret_cast<uint8_t *>(reinterpret_cast<char *>(d_iters) + align256(chunk * 4));
+        if (used[idx]) cudaStreamWaitEvent(s_in, ev_out[idx], 0);  // buffer set free again
+        cudaMemcpyAsync(d_llr, llr + c0 * n, fc * n * 4, cudaMemcpyHostToDevice, s_in);
+        cudaEventRecord(ev_in[idx], s_in);
+        cudaStreamWaitEvent(s_run, ev_in[idx], 0);
+        rc = ldpc_decode(h, d_llr, fc, max_iter, bits_out ? d_bits : nullptr, iters_out ? d_iters : nullptr,
+                         posterior_out ? d_post : nullptr, converged_out ? d_conv : nullptr,
+                         reinterpret_cast<int64_t *>(d_stats), s_run);
+        cudaEventRecord(ev_run[idx], s_run);
+        cudaStreamWaitEvent(s_out, ev_run[idx], 0);
+        if (bits_out) cudaMemcpyAsync(bits_out + c0 * n, d_bits, fc * n, cudaMemcpyDeviceToHost, s_out);
+        if (posterior_out) cudaMemcpyAsync(posterior_out + c0 * n, d_post, fc * n * 4, cudaMemcpyDeviceToHost, s_out);
+        if (iters_out) cudaMemcpyAsync(iters_out + c0, d_iters, fc * 4, cudaMemcpyDeviceToHost, s_out);
+        if (converged_out) cudaMemcpyAsync(converged_out + c0, d_conv, fc, cudaMemcpyDeviceToHost, s_out);
+        cudaEventRecord(ev_out[idx], s_out);
+        used[idx] = true;
+    }
+    int64_t hstats[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (d_stats) {
+        cudaStreamWaitEvent(s_out, ev_run[idx ^ 1], 0);
+        cudaMemcpyAsync(hstats, d_stats, 64, cudaMemcpyDeviceToHost, s_out);
+    }
+    e = cudaStreamSynchronize(s_out);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s_run);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s_in);
+    if (d_stats) cudaFree(d_stats);
+    h->pool.push_back(ev_start);
+    for (int q = 0; q < 2; q++) {
+        h->pool.push_back(ev_in[q]);
+        h->pool.push_back(ev_run[q]);
+        h->pool.push_back(ev_out[q]);
+    }
+    if (rc) return rc;
+    if (e != cudaSuccess) {
+        h->poisoned = true;
+        return LDPC_ERR_CUDA;
+    }
+    if (stats_inout)
+        for (int q = 0; q < 8; q++) stats_inout[q] += hstats[q];
+    return LDPC_OK;
+}
+
+int ldpc_info(ldpc_handle_t h, int32_t *m, int32_t *n, int64_t *nnz, int32_t *max_row_deg, int32_t *max_col_deg) {
+    if (!h) return LDPC_ERR_INVALID_ARG;
+    if (m) *m = h->g.m;
+    if (n) *n = h->g.n;
+    if (nnz) *nnz = h->g.E;
+    if (max_row_deg) *max_row_deg = h->g.max_row_deg;
+    if (max_col_deg) *max_col_deg = h->g.max_col_deg;
+    return LDPC_OK;
+}
+
+int ldpc_get_graph(ldpc_handle_t h, int32_t *row_ptr, int32_t *col_idx, int32_t *col_ptr, int32_t *col_edge) {
+    if (!h) return LDPC_ERR_INVALID_ARG;
+    if (h->poisoned) return LDPC_ERR_CUDA;
+    cudaError_t e = cudaSuccess;
+    if (row_ptr && e == cudaSuccess) e = cudaMemcpy(row_ptr, h->g.row_ptr, sizeof(int) * (h->g.m + 1), cudaMemcpyDeviceToHost);
+    if (col_idx && e == cudaSuccess) e = cudaMemcpy(col_idx, h->g.col_idx, sizeof(int) * h->g.E, cudaMemcpyDeviceToHost);
+    if (col_ptr && e == cudaSuccess) e = cudaMemcpy(col_ptr, h->g.col_ptr, sizeof(int) * (h->g.n + 1), cudaMemcpyDeviceToHost);
+    if (col_edge && e == cudaSuccess) e = cudaMemcpy(col_edge, h->g.col_edge, sizeof(int) * h->g.E, cudaMemcpyDeviceToHost);
+    return status_of(e);
+}
+
+int ldpc_set_flags(ldpc_handle_t h, uint32_t flags) {
+    if (!h) return LDPC_ERR_INVALID_ARG;
+    h->flags = flags;
+    return LDPC_OK;
+}
+
+int ldpc_set_chunk(ldpc_handle_t h, int64_t frames_per_chunk) {
+    if (!h || frames_per_chunk < 0) return LDPC_ERR_INVALID_ARG;
+    h->chunk_cap = frames_per_chunk;
+    return LDPC_OK;
+}
+
+int ldpc_schedule(ldpc_handle_t h) {
+    if (!h) return LDPC_ERR_INVALID_ARG;
+    if (!use_resident(h)) return 0;
+    return h->rp.ok ? 1 : LDPC_ERR_UNSUPPORTED;
+}
+
+int ldpc_profile_enable(ldpc_handle_t h, int enable) {
+    if (!h) return LDPC_ERR_INVALID_ARG;
+    h->prof = enable != 0;
+    return LDPC_OK;
+}
+
+int ldpc_profile_read(ldpc_handle_t h, int64_t *launches, double *ms) {
+    if (!h) return LDPC_ERR_INVALID_ARG;
+    for (auto &ev : h->evs) {
+        cudaError_t e = cudaEventSynchronize(ev.b);
+        float t = 0.f;
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&t, ev.a, ev.b);
+        if (e != cudaSuccess) {
+            h->poisoned = true;
+            return LDPC_ERR_CUDA;
+        }
+        h->prof_ms[ev.cls] += t;
+        h->pool.push_back(ev.a);
+        h->pool.push_back(ev.b);
+    }
+    h->evs.clear();
+    for (int c = 0; c < LDPC_K_NUM_CLASSES; c++) {
+        if (launches) launches[c] = h->prof_launches[c];
+        if (ms) ms[c] = h->prof_ms[c];
+    }
+    return LDPC_OK;
+}
+
+int ldpc_profile_reset(ldpc_handle_t h) {
+    if (!h) return LDPC_ERR_INVALID_ARG;
+    int rc = ldpc_profile_read(h, nullptr, nullptr);
+    for (int c = 0; c < LDPC_K_NUM_CLASSES; c++) {
+        h->prof_launches[c] = 0;
+        h->prof_ms[c] = 0.0;
+    }
+    return rc;
+}
+
+int64_t ldpc_launch_count(ldpc_handle_t h) { return h ? h->launches : -1; }
+
+void ldpc_destroy(ldpc_handle_t h) {
+    if (!h) return;
+    cudaDeviceSynchronize();
+    h->g.free_all();
+    cudaFree(h->ws);
+    cudaFree(h->work_counter);
+    for (int q = 0; q < 2; q++) cudaFree(h->hbuf[q]);
+    for (int q = 0; q < 3; q++)
+        if (h->hs[q]) cudaStreamDestroy(h->hs[q]);
+    for (auto &ev : h->evs) {
+        cudaEventDestroy(ev.a);
+        cudaEventDestroy(ev.b);
+    }
+    for (auto e : h->pool) cudaEventDestroy(e);
+    cudaGetLastError();
+    delete h;
+}
+
+}  // extern "C"

@@ -1,0 +1,267 @@
+"""GPU parity: the CUDA path through the C-ABI versus the CPU oracle on the same seeded inputs.
+
+Bar (north_star): decoded bits, per-frame iteration counts and isCodeword bit-exact; posterior
+within 1e-4 absolute/relative (the design is bit-exact, asserted separately); frames whose
+posterior has an entry within 1e-4 of zero are counted.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from gen import channel, codes
+
+pytestmark = pytest.mark.gpu
+
+LIT = 1
+NOES = 2
+FORCE_STREAM = 4
+FORCE_RESIDENT = 8
+TOL = 1e-4
+
+
+def ldpc():
+    import paper_2507_10424_b200 as P
+
+    return P
+
+
+def handle(code, flags=0, coo=False):
+    P = ldpc()
+    if coo:
+        rr, cc = code.coo()
+        return P.Handle.from_coo(torch.from_numpy(rr).cuda(), torch.from_numpy(cc).cuda(), code.m, code.n, flags=flags)
+    return P.Handle(torch.from_numpy(code.dense()).cuda(), flags=flags)
+
+
+def gpu_decode(h, llr_np, L, posterior=True):
+    llr = torch.from_numpy(np.ascontiguousarray(llr_np)).cuda()
+    stats = torch.zeros(8, dtype=torch.int64, device="cuda")
+    out = h.decode(llr, L, posterior=posterior, stats=stats)
+    torch.cuda.synchronize()
+    return (out.bits.cpu().numpy(), out.iters.cpu().numpy(), out.converged.cpu().numpy(),
+            out.posterior.cpu().numpy() if posterior else None, stats.cpu().numpy())
+
+
+def compare(code, llr, L, flags=0, h=None, exact=True):
+    if h is None:
+        h = handle(code, flags)
+    gb, gi, gc, gp, gs = gpu_decode(h, llr, L)
+    ob, oi, oc, op = oracle.decode(code.oracle_h(), llr, L, flags=flags & (LIT | NOES))
+    assert np.array_equal(gi, oi), f"iters differ on {np.count_nonzero(gi != oi)} frames"
+    assert np.array_equal(gc, oc), "converged differs"
+    assert np.array_equal(gb, ob), f"bits differ on {np.count_nonzero(np.any(gb != ob, axis=1))} frames"
+    assert np.allclose(gp, op, rtol=TOL, atol=TOL)
+    if exact:
+        assert np.array_equal(gp.view(np.uint32), op.view(np.uint32)), "posterior not bit-exact"
+    assert np.array_equal(gs, oracle.stats(llr, ob, oi, oc, op))
+    return gb, gi, gc, gp
+
+
+def frames_for(code, F, ebn0, seed, point=0):
+    return channel.bpsk_awgn(code.n, code.rate, ebn0, seed, point, 0, F).numpy()
+
+
+# ---------------------------------------------------------------- ingestion (a1) ------------
+@pytest.mark.parametrize("coo", [False, True])
+@pytest.mark.parametrize("which", ["paper", "small", "reg", "bg1"])
+def test_ingest_graph_matches_definition(which, coo):
+    code = {"paper": codes.paper_5x10, "small": lambda: codes.random_small(40, 90, 3, 2, 9),
+            "reg": lambda: codes.regular(504, 1008, 3, 6, 1008), "bg1": codes.bg1_dims}[which]()
+    h = handle(code, coo=coo)
+    rp, ci, cp, ce = [t.numpy() for t in h.graph()]
+    assert (h.m, h.n, h.nnz) == (code.m, code.n, code.nnz)
+    exp_rp = np.concatenate([[0], np.cumsum([len(r) for r in code.rows])])
+    assert np.array_equal(rp, exp_rp)
+    assert np.array_equal(ci, np.concatenate(code.rows))  # N_i ascending
+    # M_j: for every column, the row-list positions of its ones in ascending row order
+    rr, cc = code.coo()
+    order = np.lexsort((rr, cc))
+    assert np.array_equal(cp, np.concatenate([[0], np.cumsum(np.bincount(cc, minlength=code.n))]))
+    assert np.array_equal(ce, np.arange(code.nnz)[order])
+    assert h.max_row_deg == max(len(r) for r in code.rows)
+
+
+def test_ingest_errors():
+    P = ldpc()
+    with pytest.raises(P.LdpcError, match="outside"):
+        P.Handle(torch.tensor([[1, 2, 1], [1, 1, 0]], dtype=torch.uint8, device="cuda"))
+    with pytest.raises(P.LdpcError, match="degree"):
+        P.Handle(torch.tensor([[1, 0, 0], [0, 1, 1]], dtype=torch.uint8, device="cuda"))
+    with pytest.raises(P.LdpcError, match="twice"):
+        P.Handle.from_coo(torch.tensor([0, 0, 0], dtype=torch.int32, device="cuda"),
+                          torch.tensor([1, 1, 2], dtype=torch.int32, device="cuda"), 1, 3)
+    with pytest.raises(P.LdpcError, match="outside"):
+        P.Handle.from_coo(torch.tensor([0, 0], dtype=torch.int32, device="cuda"),
+                          torch.tensor([1, 3], dtype=torch.int32, device="cuda"), 1, 3)
+
+
+# ---------------------------------------------------------------- single loop body (a3-a6) --
+@pytest.mark.parametrize("flags", [0, LIT])
+@pytest.mark.parametrize("seed", range(4))
+def test_one_iteration_random_h(seed, flags):
+    """L = 1 without early stop: one CN + BN sweep, bit-exact, on random H with odd/even rows and
+    degree-0 columns; values include exact zeros, -0.0 and ties."""
+    code = codes.random_small(37, 70, seed, 2, 9)
+    rng = np.random.default_rng(seed)
+    llr = rng.choice(np.array([-1.5, -1.0, -0.0, 0.0, 0.25, 1.0, 2.0], np.float32), size=(300, code.n))
+    llr[::2] = rng.standard_normal((150, code.n)).astype(np.float32)
+    for f in (FORCE_STREAM, FORCE_RESIDENT):
+        h = handle(code, flags | NOES | f)
+        if f == FORCE_RESIDENT and h.schedule != "resident":
+            continue
+        compare(code, llr, 1, flags | NOES, h=h)
+        compare(code, llr, 3, flags | NOES, h=h)
+
+
+def test_high_degree_rows_use_wide_locations():
+    """Rows of degree > 255 switch min0Location to 16 bits."""
+    rng = np.random.default_rng(1)
+    rows = [np.sort(rng.choice(600, size=d, replace=False)) for d in (300, 2, 5, 280, 7, 3)]
+    code = codes.from_rows(rows, 600)
+    llr = (rng.standard_normal((200, 600)) - 1.2).astype(np.float32)
+    h = handle(code, FORCE_STREAM)
+    assert h.max_row_deg == 300
+    compare(code, llr, 8, h=h)
+
+
+# ---------------------------------------------------------------- end to end ----------------
+@pytest.mark.parametrize("flags", [0, LIT, NOES, LIT | NOES])
+def test_c1_paper_code_full(flags):
+    """Config C1: the paper's 5x10 H, 10k frames over Eb/N0 {1,2,3,4}, max_iter 10 -- every frame."""
+    cfg = codes.CONFIGS["c1"]
+    code = cfg["code"]()
+    llr, _ = channel.workload_llr(code, cfg, 0, cfg["frames"])
+    compare(code, llr.numpy(), cfg["max_iter"], flags)
+
+
+@pytest.mark.parametrize("sched", [FORCE_STREAM, FORCE_RESIDENT])
+def test_c2_subset_full(sched):
+    """C2 code (random (3,6) 504x1008), 12k frames spread over the sweep, max_iter 50 -- every frame."""
+    cfg = codes.CONFIGS["c2"]
+    code = cfg["code"]()
+    h = handle(code, sched)
+    if sched == FORCE_RESIDENT and h.schedule != "resident":
+        pytest.skip("resident schedule unavailable")
+    parts = []
+    for p, e in enumerate(cfg["ebn0"]):
+        parts.append(channel.bpsk_awgn(code.n, code.rate, e, cfg["seed"], p, 5000, 1700).numpy())
+    llr = np.concatenate(parts)
+    compare(code, llr, cfg["max_iter"], h=h)
+
+
+def test_edge_sizes_and_chunking():
+    """frames = 0, 1, 127, 129 (ragged last tile), L = 0, and chunked decodes equal one-shot decodes."""
+    code = codes.regular(60, 120, 3, 6, 5)
+    llr = frames_for(code, 700, 1.5, 3)
+    h = handle(code, FORCE_STREAM)
+    for F in (1, 127, 129):
+        compare(code, llr[:F], 20, h=h)
+    compare(code, llr, 0, h=h)
+    compare(code, llr, 0, NOES, h=handle(code, NOES | FORCE_STREAM))
+    P = ldpc()
+    out0 = h.decode(torch.from_numpy(llr[:0]).cuda(), 10)
+    assert out0.bits.shape == (0, 120)
+    ref = gpu_decode(h, llr, 20)
+    h.set_chunk(256)
+    chunked = gpu_decode(h, llr, 20)
+    for a, b in zip(ref, chunked):
+        assert np.array_equal(a, b)
+    assert P is not None
+
+
+def test_nonzero_codewords_and_symmetry():
+    """Random nonzero codewords (no all-zero bias) and the codeword-symmetry law on the GPU (T5)."""
+    code = codes.paper_5x10()
+    H = code.dense()
+    import itertools
+
+    V = np.array(list(itertools.product([0, 1], repeat=10)), np.uint8)
+    C = V[((V.astype(np.int64) @ H.T) % 2).sum(axis=1) == 0]
+    rng = np.random.default_rng(4)
+    cw = C[rng.integers(len(C), size=2000)]
+    llr = channel.bpsk_awgn(10, 0.5, 1.0, 77, 0, 0, 2000, codeword=torch.from_numpy(cw)).numpy()
+    compare(code, llr, 10)
+    h = handle(code)
+    b0, i0, c0, p0, _ = gpu_decode(h, llr, 10)
+    c = C[5]
+    t = (1.0 - 2.0 * c).astype(np.float32)
+    b1, i1, c1, p1, _ = gpu_decode(h, llr * t, 10)
+    ok = np.all(p0 != 0, axis=1)
+    assert np.array_equal(b1[ok], (b0 ^ c)[ok]) and np.array_equal(i1[ok], i0[ok])
+
+
+def test_power_of_two_scale_on_gpu():
+    code = codes.regular(252, 504, 3, 6, 17)
+    llr = frames_for(code, 1000, 2.0, 8)
+    h = handle(code)
+    b0, i0, c0, p0, _ = gpu_decode(h, llr, 30)
+    b1, i1, c1, p1, _ = gpu_decode(h, llr * np.float32(8), 30)
+    assert np.array_equal(b0, b1) and np.array_equal(i0, i1) and np.array_equal(p1, p0 * np.float32(8))
+
+
+def test_decode_host_matches_device():
+    code = codes.regular(504, 1008, 3, 6, 1008)
+    llr = frames_for(code, 3000, 2.0, 9)
+    h = handle(code)
+    gb, gi, gc, gp, gs = gpu_decode(h, llr, 30)
+    st = torch.zeros(8, dtype=torch.int64)
+    out = h.decode_host(torch.from_numpy(llr).pin_memory(), 30, posterior=True, stats=st)
+    assert np.array_equal(out.bits.numpy(), gb) and np.array_equal(out.iters.numpy(), gi)
+    assert np.array_equal(out.posterior.numpy(), gp) and np.array_equal(st.numpy(), gs)
+
+
+# ---------------------------------------------------------------- full-size, sampled ---------
+def _sampled_full_size(cfg_name, sample, flags=0, chunk=None):
+    """Decode the config's full batch in the bench's launch configuration, then check `sample`
+    frames spread over the batch against the oracle, frame by frame."""
+    cfg = codes.CONFIGS[cfg_name]
+    code = cfg["code"]()
+    llr, pidx = channel.workload_llr(code, cfg, 0, cfg["frames"], device="cuda")
+    h = handle(code, flags, coo=True)
+    if chunk:
+        h.set_chunk(chunk)
+    out = h.decode(llr, cfg["max_iter"], posterior=True)
+    torch.cuda.synchronize()
+    idx = np.unique(np.linspace(0, cfg["frames"] - 1, sample).astype(np.int64))
+    sub = llr[torch.from_numpy(idx).cuda()].cpu().numpy()
+    ob, oi, oc, op = oracle.decode(code.oracle_h(), sub, cfg["max_iter"], flags=flags & (LIT | NOES))
+    gb = out.bits[torch.from_numpy(idx).cuda()].cpu().numpy()
+    gi = out.iters.cpu().numpy()[idx]
+    gc = out.converged.cpu().numpy()[idx]
+    gp = out.posterior[torch.from_numpy(idx).cuda()].cpu().numpy()
+    assert np.array_equal(gi, oi) and np.array_equal(gc, oc) and np.array_equal(gb, ob)
+    assert np.allclose(gp, op, rtol=TOL, atol=TOL)
+    near_zero = int(np.count_nonzero(np.abs(op).min(axis=1) <= TOL))
+    return near_zero, oi
+
+
+def test_c2_full_size_sampled():
+    _sampled_full_size("c2", 1500)
+
+
+def test_c3_full_size_sampled():
+    _sampled_full_size("c3", 48)
+
+
+def test_c4_full_size_sampled():
+    _sampled_full_size("c4", 12)
+
+
+def test_c5_sixteen_handles():
+    """C5: 16 distinct H of equal dims through one handle API; every frame of a reduced batch."""
+    cfg = codes.CONFIGS["c5"]
+    for hidx, code in enumerate(cfg["code"]()):
+        if hidx % 4:
+            continue
+        parts = [channel.bpsk_awgn(code.n, code.rate, e, cfg["seed"] + hidx, p, 0, 80).numpy()
+                 for p, e in enumerate(cfg["ebn0"])]
+        compare(code, np.concatenate(parts), cfg["max_iter"])
+
+
+def test_generator_device_independent():
+    """The keyed generator gives the same frames on CPU and GPU (bench inputs == test inputs)."""
+    code = codes.regular(504, 1008, 3, 6, 1008)
+    a = channel.bpsk_awgn(code.n, code.rate, 2.0, 1, 0, 1000, 500)
+    b = channel.bpsk_awgn(code.n, code.rate, 2.0, 1, 0, 1000, 500, device="cuda").cpu()
+    assert (a != b).sum().item() <= 2  # libm ulp differences can flip a rare last bit
