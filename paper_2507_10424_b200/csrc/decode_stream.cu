@@ -215,6 +215,9 @@ __global__ void __launch_bounds__(CTA) k_bn(Graph g, StreamState w, int k, int c
         const uint4 dw = ldu4(w.done + (size_t)t * 4);
         const uint4 newly = make_uint4(~ua.x & ~dw.x, ~ua.y & ~dw.y, ~ua.z & ~dw.z, ~ua.w & ~dw.w);
         act = make_uint4(ua.x & ~dw.x, ua.y & ~dw.y, ua.z & ~dw.z, ua.w & ~dw.w);
+        // every thread of CTA 0 must read `done` before any thread rewrites it (other CTAs of the
+        // tile may see either value: act is the same for both, since newly and ua are disjoint)
+        __syncthreads();
         if (blockIdx.x == 0) {
             const int tid = threadIdx.x;
             if (tid < 4) {

@@ -83,6 +83,7 @@ struct ResidentPlan {
     int ctas = 0;        // persistent grid size
 };
 ResidentPlan plan_resident(const HostGraph &g, bool loc16, int device);
+size_t resident_scratch_bytes(const HostGraph &g, const ResidentPlan &rp);  // work counter + r scratch
 int launch_resident(const Graph &g, const ResidentPlan &rp, const float *llr, int64_t frames, int L, bool early,
                     bool literal, bool loc16, float *posterior, uint8_t *bits, int32_t *iters_out,
                     uint8_t *conv_out, unsigned long long *stats, int *work_counter, cudaStream_t st);

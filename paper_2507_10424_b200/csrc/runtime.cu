@@ -206,7 +206,7 @@ int decode_resident(ldpc_plan *h, const float *llr, int64_t frames, int L, uint8
     const bool literal = (h->flags & LDPC_FLAG_SIGN_PAPER_LITERAL) != 0;
     const bool loc16 = h->g.max_row_deg > 255;
     if (!h->work_counter) {
-        if (cudaMalloc(&h->work_counter, sizeof(int) * 2) != cudaSuccess) {
+        if (cudaMalloc(&h->work_counter, resident_scratch_bytes(h->g, h->rp)) != cudaSuccess) {
             cudaGetLastError();
             return LDPC_ERR_OOM;
         }
