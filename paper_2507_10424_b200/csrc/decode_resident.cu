@@ -2,21 +2,23 @@
 // time with the whole per-frame state in shared memory, and refills a frame slot the moment its
 // frame stops (per-frame early stop of Alg. 1, without batch-level waste).
 //
-// Per CTA, frame-interleaved over S slots (lane l of a warp owns slot l % S of row/column l / S):
-//   s   [n][S]  fp32           soft vector (Eq. sCalculation)
-//   st  [m][S]  {min0, min1}   Observation 1's minima; min0's sign bit holds the row's
-//                              sign parity (Obs. 2) times (-1)^{d_i} (reading A1)
-//   lc  [m][S]  u16            min0Location, stored as the edge id inside the row list
-//   sg  [E]     S bits         sign of lambda_e = s_j - eta_e for each slot
+// Per CTA, frame-interleaved over S slots (a lane owns 4 consecutive slots of one row or column):
+//   s    [n][S]  fp32          soft vector (Eq. sCalculation)
+//   min0 [m][S]  fp32          Observation 1's minimum; its sign bit holds the row's sign
+//                              parity (Obs. 2) times (-1)^{d_i} (reading A1)
+//   min1 [m][S]  fp32          Observation 1's second minimum
+//   lc   [m][S]  u16           min0Location, stored as the edge id inside the row lists (0xffff = none)
+//   sg   [E]     S bits        sign of lambda_e = s_j - eta_e for each slot
 // plus the Tanner graph itself as 16-bit lists (N_i, M_j).  r lives in a global scratch
 // [CTA][n][S] (L2-resident) read once per column per body.  Loop per round:
 //   A  finish stopped slots (k, isCodeword, counters) and refill empty slots from a global counter
-//   B  stage new frames into their slots (s = r, eta = 0 via k = 0)
+//   B  stage new frames into their slots (s = r, eta = 0)
 //   C  check-node pass over all rows + syndrome of b = slice(s) of every slot
 //   D  per slot: stop (codeword, or k = L) -> write b and s; else bit-node pass s = sum eta + r
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "ldpc_internal.cuh"
 
@@ -24,7 +26,6 @@ namespace ldpc {
 
 namespace {
 
-constexpr int RT = 1024;  // threads per resident CTA (32 warps)
 constexpr unsigned FULLM = 0xffffffffu;
 
 template <int S>
@@ -47,7 +48,7 @@ struct SWord<32> {
 };
 
 struct Layout {
-    size_t s, st, lc, sg, rp, cp, col, rec, meta, total;
+    size_t s, m0, m1, lc, sg, rp, cp, col, rec, meta, total;
 };
 
 constexpr size_t a16(size_t x) { return (x + 15) & ~(size_t)15; }
@@ -59,7 +60,8 @@ Layout layout_for(int S, int m, int n, int E) {
     size_t o = 0;
     const size_t swb = S <= 8 ? 1 : S / 8;
     L.s = o;    o = a16(o + (size_t)n * S * 4);
-    L.st = o;   o = a16(o + (size_t)m * S * 8);
+    L.m0 = o;   o = a16(o + (size_t)m * S * 4);
+    L.m1 = o;   o = a16(o + (size_t)m * S * 4);
     L.lc = o;   o = a16(o + (size_t)m * S * 2);
     L.sg = o;   o = a16(o + (size_t)E * swb);
     L.rp = o;   o = a16(o + (size_t)(m + 1) * 2);
@@ -86,14 +88,26 @@ struct ResArgs {
     Layout lay;
 };
 
-template <int S>
+__device__ __forceinline__ float f4c(const float4 &a, int v) { return v == 0 ? a.x : v == 1 ? a.y : v == 2 ? a.z : a.w; }
+__device__ __forceinline__ int u4c(const ushort4 &a, int v) {
+    return v == 0 ? (int)a.x : v == 1 ? (int)a.y : v == 2 ? (int)a.z : (int)a.w;
+}
+
+// Lane layout: a lane owns 4 consecutive slots (float4) of one row or column; LR = S/4 lanes cover a
+// row, G = 32/LR rows per warp.  Bit of slot q = 4*l + v inside an S-bit sign word: v*LR + l.
+template <int S, int RT>
 __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
+    constexpr int NWARP = RT / 32;
     using SWT = typename SWord<S>::T;
-    constexpr int G = 32 / S;  // rows (or columns) per warp
+    constexpr int LR = S / 4;
+    constexpr int G = 32 / LR;
+    constexpr unsigned LMASK = (LR == 32) ? 0xffffffffu : ((1u << LR) - 1u);
+    const float INF = __int_as_float(0x7f800000);
     extern __shared__ __align__(16) unsigned char sm[];
     const int m = a.g.m, n = a.g.n, E = a.g.E;
     float *s = reinterpret_cast<float *>(sm + a.lay.s);
-    float2 *st = reinterpret_cast<float2 *>(sm + a.lay.st);
+    float *mn0 = reinterpret_cast<float *>(sm + a.lay.m0);
+    float *mn1 = reinterpret_cast<float *>(sm + a.lay.m1);
     uint16_t *lc = reinterpret_cast<uint16_t *>(sm + a.lay.lc);
     SWT *sg = reinterpret_cast<SWT *>(sm + a.lay.sg);
     uint16_t *rp = reinterpret_cast<uint16_t *>(sm + a.lay.rp);
@@ -109,7 +123,8 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
     unsigned *ctl = reinterpret_cast<unsigned *>(meta + 256);  // [0] unsat, [1] new, [2] active, [3] exhausted
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int sub = lane / S, slot = lane % S;
+    const int sub = lane / LR, l = lane % LR;  // row group inside the warp, lane inside the row
+    const int q0 = 4 * l;                      // first slot of this lane
     float *rs = a.rs + (size_t)blockIdx.x * n * S;
 
     // ---- the Tanner graph into shared memory (16-bit lists)
@@ -194,10 +209,21 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
         const unsigned active = ctl[2], fresh_new = ctl[1];
         if (!active) break;
 
-        // ---------------- B: stage new frames (s = r; k = 0 means eta^prev = 0)
+        // ---------------- B: stage new frames: s = r, eta^prev = 0 (min0 = min1 = +0, no location,
+        //                     sign bits cleared)
         if (fresh_new) {
+            SWT clear = 0;
+#pragma unroll
+            for (int q = 0; q < S; q++)
+                if ((fresh_new >> q) & 1u) clear |= (SWT)(1u << ((q & 3) * LR + (q >> 2)));
+            for (int e = tid; e < E; e += RT) sg[e] &= (SWT)~clear;
             for (unsigned fm = fresh_new; fm; fm &= fm - 1) {
                 const int q = __ffs(fm) - 1;
+                for (int i = tid; i < m; i += RT) {
+                    mn0[i * S + q] = 0.f;
+                    mn1[i * S + q] = 0.f;
+                    lc[i * S + q] = 0xffffu;
+                }
                 const float *src = a.llr + (int64_t)slot_f[q] * n;
                 int raw = 0;
                 for (int j = tid; j < n; j += RT) {
@@ -212,63 +238,76 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
             __syncthreads();
         }
 
-        // ---------------- C: check-node pass + syndrome
+        // ---------------- C: check-node pass + syndrome of b = slice(s)
         {
-            const bool lane_act = (active >> slot) & 1u;
-            const bool fresh = slot_k[slot] == 0;
-            unsigned usyn = 0;
-            for (int rb = warp * G; rb < m; rb += 32 * G) {
+            unsigned syn_acc = 0;  // bit v: slot q0+v has an unsatisfied check
+            for (int rb = warp * G; rb < m; rb += NWARP * G) {
                 const int i = rb + sub;
                 const bool valid = i < m;
                 const int ra = valid ? rp[i] : 0;
                 const int d = valid ? (int)rp[i + 1] - ra : 0;
                 const int dmax = __reduce_max_sync(FULLM, d);
-                float m0 = 0.f, m1 = 0.f;
-                int ol = -1;
-                if (valid && !fresh) {
-                    const float2 o = st[i * S + slot];
-                    m0 = o.x;
-                    m1 = o.y;
-                    ol = lc[i * S + slot];
+                float4 om0 = make_float4(0.f, 0.f, 0.f, 0.f), om1 = om0;
+                ushort4 olc = make_ushort4(0xffffu, 0xffffu, 0xffffu, 0xffffu);
+                if (valid) {
+                    om0 = *reinterpret_cast<const float4 *>(mn0 + i * S + q0);
+                    om1 = *reinterpret_cast<const float4 *>(mn1 + i * S + q0);
+                    olc = *reinterpret_cast<const ushort4 *>(lc + i * S + q0);
                 }
-                float nm0 = __int_as_float(0x7f800000), nm1 = nm0;
-                int nloc = 0;
-                unsigned npar = 0, syn = 0;
+                float nm0[4] = {INF, INF, INF, INF}, nm1[4] = {INF, INF, INF, INF};
+                int nloc[4] = {0xffff, 0xffff, 0xffff, 0xffff};
+                unsigned parw[4] = {0, 0, 0, 0};
+                unsigned syn = 0;
                 for (int p = 0; p < dmax; p++) {
                     const bool has = p < d;
                     const int e = ra + p;
                     const int j = has ? col[e] : 0;
-                    const float sv = s[j * S + slot];
-                    float x = sv;
-                    if (!fresh) {
-                        const unsigned wb = has ? (unsigned)sg[e] : 0u;
-                        const float mag = (e == ol) ? m1 : fabsf(m0);  // Obs. 1
-                        const unsigned neg_eta = ((wb >> slot) & 1u) ^ (__float_as_uint(m0) >> 31);  // Obs. 2
-                        x = sv - (neg_eta ? -mag : mag);  // lambda_k - eta^prev_{i,k}
+                    const float4 sv = *reinterpret_cast<const float4 *>(s + j * S + q0);
+                    const unsigned w = has ? (unsigned)sg[e] : 0u;
+                    unsigned bal[4];
+#pragma unroll
+                    for (int v = 0; v < 4; v++) {
+                        const float sj = f4c(sv, v);
+                        const float m0v = f4c(om0, v);
+                        const float mag = (e == u4c(olc, v)) ? f4c(om1, v) : fabsf(m0v);  // Obs. 1
+                        // sign of eta^prev: own lambda sign xor the row parity (Obs. 2; A1 folded in)
+                        const unsigned sbit = ((w << (31 - (v * LR + l))) ^ __float_as_uint(m0v)) & 0x80000000u;
+                        const float x = sj - __uint_as_float(__float_as_uint(mag) | sbit);  // lambda - eta^prev
+                        const float ax = has ? fabsf(x) : INF;
+                        const bool lt = ax < nm0[v];  // first strict minimum (A13)
+                        nm1[v] = fminf(nm1[v], fmaxf(nm0[v], ax));
+                        nm0[v] = fminf(nm0[v], ax);
+                        nloc[v] = lt ? e : nloc[v];
+                        bal[v] = __ballot_sync(FULLM, has && x < 0.f);  // sign(0) = +1
+                        syn ^= (unsigned)(has && sj > 0.f) << v;         // b_j = slice(s_j)
                     }
-                    const float ax = fabsf(x);
-                    const bool lt = has && ax < nm0;  // first strict minimum (A13)
-                    nm1 = lt ? nm0 : (has ? fminf(nm1, ax) : nm1);
-                    nm0 = lt ? ax : nm0;
-                    nloc = lt ? e : nloc;
-                    const bool neg = has && x < 0.f;  // sign(0) = +1
-                    npar ^= (unsigned)neg;
-                    syn ^= (unsigned)(has && sv > 0.f);  // b_j = slice(s_j)
-                    const unsigned bal = __ballot_sync(FULLM, neg);
-                    if (has && slot == 0) sg[e] = (SWT)(S == 32 ? bal : (bal >> (sub * S)) & ((1u << S) - 1u));
+#pragma unroll
+                    for (int v = 0; v < 4; v++) parw[v] ^= bal[v];
+                    if (has && l == 0) {
+                        unsigned word = 0;
+#pragma unroll
+                        for (int v = 0; v < 4; v++) word |= ((bal[v] >> (sub * LR)) & LMASK) << (v * LR);
+                        sg[e] = (SWT)word;
+                    }
                 }
                 if (valid) {
                     const unsigned corr = (unsigned)(d & 1) & (unsigned)(!a.literal);  // reading A1
-                    st[i * S + slot] = make_float2(__uint_as_float(__float_as_uint(nm0) | ((npar ^ corr) << 31)), nm1);
-                    lc[i * S + slot] = (uint16_t)nloc;
+                    float4 o0, o1;
+                    o0.x = __uint_as_float(__float_as_uint(nm0[0]) | ((((parw[0] >> lane) & 1u) ^ corr) << 31));
+                    o0.y = __uint_as_float(__float_as_uint(nm0[1]) | ((((parw[1] >> lane) & 1u) ^ corr) << 31));
+                    o0.z = __uint_as_float(__float_as_uint(nm0[2]) | ((((parw[2] >> lane) & 1u) ^ corr) << 31));
+                    o0.w = __uint_as_float(__float_as_uint(nm0[3]) | ((((parw[3] >> lane) & 1u) ^ corr) << 31));
+                    o1 = make_float4(nm1[0], nm1[1], nm1[2], nm1[3]);
+                    *reinterpret_cast<float4 *>(mn0 + i * S + q0) = o0;
+                    *reinterpret_cast<float4 *>(mn1 + i * S + q0) = o1;
+                    *reinterpret_cast<ushort4 *>(lc + i * S + q0) =
+                        make_ushort4((uint16_t)nloc[0], (uint16_t)nloc[1], (uint16_t)nloc[2], (uint16_t)nloc[3]);
+                    syn_acc |= syn;
                 }
-                usyn |= __ballot_sync(FULLM, valid && lane_act && syn);
             }
-            // fold the G sub-groups onto slot bits
-            unsigned fold = 0;
-#pragma unroll
-            for (int q = 0; q < G; q++) fold |= (S == 32) ? usyn : ((usyn >> (q * S)) & ((1u << S) - 1u));
-            if (lane == 0 && fold) atomicOr(&ctl[0], fold);
+            const unsigned mine = (syn_acc << q0) & active;
+            const unsigned wmask = __reduce_or_sync(FULLM, mine);
+            if (lane == 0 && wmask) atomicOr(&ctl[0], wmask);
         }
         __syncthreads();
 
@@ -305,25 +344,36 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
                     if (nz) slot_nz[q] = 1;
                 }
             }
+            const unsigned cm = (cont_mask >> q0) & 0xfu;  // continuing slots of this lane
             if (cont_mask) {
-                const bool lane_cont = (cont_mask >> slot) & 1u;
-                for (int cb = warp * G; cb < n; cb += 32 * G) {
+                for (int cb = warp * G; cb < n; cb += NWARP * G) {
                     const int j = cb + sub;
-                    if (j >= n) continue;
-                    const float rj = rs[(size_t)j * S + slot];
+                    if (j >= n || !cm) continue;
+                    const float4 rj = *reinterpret_cast<const float4 *>(rs + (size_t)j * S + q0);
                     const int c0 = cp[j], dv = (int)cp[j + 1] - c0;
-                    float acc = 0.f;
-                    for (int q = 0; q < dv; q++) {
-                        const uint32_t rc = rec[c0 + q];
+                    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+                    for (int qq = 0; qq < dv; qq++) {
+                        const uint32_t rc = rec[c0 + qq];
                         const int e = (int)(rc >> 16), i = (int)(rc & 0xffffu);
-                        const float2 o = st[i * S + slot];
-                        const int ol = lc[i * S + slot];
-                        const unsigned wb = (unsigned)sg[e];
-                        const float mag = (e == ol) ? o.y : fabsf(o.x);
-                        const unsigned neg = ((wb >> slot) & 1u) ^ (__float_as_uint(o.x) >> 31);
-                        acc = acc + (neg ? -mag : mag);  // ascending rows from +0.0 (A14)
+                        const float4 m0 = *reinterpret_cast<const float4 *>(mn0 + i * S + q0);
+                        const float4 m1 = *reinterpret_cast<const float4 *>(mn1 + i * S + q0);
+                        const ushort4 lv = *reinterpret_cast<const ushort4 *>(lc + i * S + q0);
+                        const unsigned w = (unsigned)sg[e];
+#pragma unroll
+                        for (int v = 0; v < 4; v++) {
+                            const float m0v = f4c(m0, v);
+                            const float mag = (e == u4c(lv, v)) ? f4c(m1, v) : fabsf(m0v);  // Obs. 1
+                            const unsigned sbit = ((w << (31 - (v * LR + l))) ^ __float_as_uint(m0v)) & 0x80000000u;
+                            acc[v] = acc[v] + __uint_as_float(__float_as_uint(mag) | sbit);  // ascending rows (A14)
+                        }
                     }
-                    if (lane_cont) s[j * S + slot] = acc + rj;
+                    float *sp = s + j * S + q0;
+                    float4 o = *reinterpret_cast<const float4 *>(sp);
+                    if (cm & 1u) o.x = acc[0] + rj.x;
+                    if (cm & 2u) o.y = acc[1] + rj.y;
+                    if (cm & 4u) o.z = acc[2] + rj.z;
+                    if (cm & 8u) o.w = acc[3] + rj.w;
+                    *reinterpret_cast<float4 *>(sp) = o;
                 }
             }
         }
@@ -347,10 +397,16 @@ int max_smem_optin(int device) {
     return v;
 }
 
-template <int S>
+template <int S, int RT>
 void launch_s(const ResArgs &args, int ctas, size_t smem, cudaStream_t st) {
-    cudaFuncSetAttribute(k_resident<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_resident<S><<<ctas, RT, smem, st>>>(args);
+    cudaFuncSetAttribute(k_resident<S, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_resident<S, RT><<<ctas, RT, smem, st>>>(args);
+}
+
+template <int S>
+void launch_t(const ResArgs &args, int threads, int ctas, size_t smem, cudaStream_t st) {
+    if (threads == 1024) launch_s<S, 1024>(args, ctas, smem, st);
+    else launch_s<S, 512>(args, ctas, smem, st);
 }
 
 }  // namespace
@@ -368,7 +424,8 @@ ResidentPlan plan_resident(const HostGraph &g, bool loc16, int device) {
         if (L.total <= (size_t)cap) {
             rp.ok = true;
             rp.slots = S;
-            rp.threads = RT;
+            rp.threads = 512;
+            if (const char *e = getenv("LDPC_RES_THREADS")) rp.threads = atoi(e) == 1024 ? 1024 : 512;
             rp.smem = L.total;
             rp.ctas = sms;
             return rp;
@@ -399,10 +456,10 @@ int launch_resident(const Graph &g, const ResidentPlan &rp, const float *llr, in
     a.lay = layout_for(rp.slots, g.m, g.n, g.E);
     cudaMemsetAsync(work_counter, 0, sizeof(int), st);
     switch (rp.slots) {
-        case 32: launch_s<32>(a, rp.ctas, rp.smem, st); break;
-        case 16: launch_s<16>(a, rp.ctas, rp.smem, st); break;
-        case 8: launch_s<8>(a, rp.ctas, rp.smem, st); break;
-        default: launch_s<4>(a, rp.ctas, rp.smem, st); break;
+        case 32: launch_t<32>(a, rp.threads, rp.ctas, rp.smem, st); break;
+        case 16: launch_t<16>(a, rp.threads, rp.ctas, rp.smem, st); break;
+        case 8: launch_t<8>(a, rp.threads, rp.ctas, rp.smem, st); break;
+        default: launch_t<4>(a, rp.threads, rp.ctas, rp.smem, st); break;
     }
     return 1;
 }
