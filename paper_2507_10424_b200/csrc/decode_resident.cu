@@ -4,17 +4,19 @@
 //
 // Per CTA, frame-interleaved over S slots (a lane owns 4 consecutive slots of one row or column):
 //   s    [n][S]  fp32          soft vector (Eq. sCalculation)
-//   min0 [m][S]  fp32          Observation 1's minimum; its sign bit holds the row's sign
-//                              parity (Obs. 2) times (-1)^{d_i} (reading A1)
+//   min0 [m][S]  fp32          Observation 1's minimum
 //   min1 [m][S]  fp32          Observation 1's second minimum
 //   lc   [m][S]  u16           min0Location, stored as the edge id inside the row lists (0xffff = none)
+//   par  [m]     S bits        the row's sign parity (Obs. 2) times (-1)^{d_i} (reading A1)
 //   sg   [E]     S bits        sign of lambda_e = s_j - eta_e for each slot
 // plus the Tanner graph itself as 16-bit lists (N_i, M_j).  r lives in a global scratch
 // [CTA][n][S] (L2-resident) read once per column per body.  Loop per round:
 //   A  finish stopped slots (k, isCodeword, counters) and refill empty slots from a global counter
-//   B  stage new frames into their slots (s = r, eta = 0)
+//   B  stage new frames into their slots (s = r; eta^prev = 0 is applied by the next check-node pass)
 //   C  check-node pass over all rows + syndrome of b = slice(s) of every slot
 //   D  per slot: stop (codeword, or k = L) -> write b and s; else bit-node pass s = sum eta + r
+// Every sweep uses the same lane mapping (4 slots of one row/column per lane, 16-byte accesses), so
+// no sweep has shared-memory bank conflicts beyond the row/column gather itself.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -48,7 +50,7 @@ struct SWord<32> {
 };
 
 struct Layout {
-    size_t s, m0, m1, lc, sg, rp, cp, col, rec, meta, total;
+    size_t s, m0, m1, lc, sg, par, rp, cp, col, rec, meta, total;
 };
 
 constexpr size_t a16(size_t x) { return (x + 15) & ~(size_t)15; }
@@ -64,6 +66,7 @@ Layout layout_for(int S, int m, int n, int E) {
     L.m1 = o;   o = a16(o + (size_t)m * S * 4);
     L.lc = o;   o = a16(o + (size_t)m * S * 2);
     L.sg = o;   o = a16(o + (size_t)E * swb);
+    L.par = o;  o = a16(o + (size_t)m * swb);
     L.rp = o;   o = a16(o + (size_t)(m + 1) * 2);
     L.cp = o;   o = a16(o + (size_t)(n + 1) * 2);
     L.col = o;  o = a16(o + (size_t)E * 2);
@@ -89,8 +92,99 @@ struct ResArgs {
 };
 
 __device__ __forceinline__ float f4c(const float4 &a, int v) { return v == 0 ? a.x : v == 1 ? a.y : v == 2 ? a.z : a.w; }
-__device__ __forceinline__ int u4c(const ushort4 &a, int v) {
-    return v == 0 ? (int)a.x : v == 1 ? (int)a.y : v == 2 ? (int)a.z : (int)a.w;
+__device__ __forceinline__ void f4s(float4 &a, int v, float x) {
+    if (v == 0) a.x = x;
+    else if (v == 1) a.y = x;
+    else if (v == 2) a.z = x;
+    else a.w = x;
+}
+// min0Location test on two packed 16-bit edge ids: true iff the half selected by `hi` differs from e
+__device__ __forceinline__ bool loc_ne(unsigned pair, unsigned e2, bool hi) {
+    return ((pair ^ e2) & (hi ? 0xffff0000u : 0x0000ffffu)) != 0u;
+}
+
+// Check-node update of G rows (one per row group of the warp) for the 4 slots of this lane.
+// HAS: rows of the warp may have different degrees (irregular H), lanes past their degree idle.
+// fm: this lane's fresh slots (eta^prev = 0); nfw: S-bit word with the fresh slots' bits clear.
+template <int S, bool HAS>
+__device__ __forceinline__ void cn_rows(const float *s, float *mn0, float *mn1, uint16_t *lc,
+                                        typename SWord<S>::T *sg, typename SWord<S>::T *par,
+                                        const uint16_t *col, int i, bool valid, int ra, int d, int dmax,
+                                        int l, int sub, unsigned fm, unsigned nfw, unsigned corr_all,
+                                        unsigned &syn_acc) {
+    using SWT = typename SWord<S>::T;
+    constexpr int LR = S / 4;
+    constexpr unsigned LMASK = (LR == 32) ? 0xffffffffu : ((1u << LR) - 1u);
+    const float INF = __int_as_float(0x7f800000);
+    const int q0 = 4 * l;
+    float4 om0 = make_float4(0.f, 0.f, 0.f, 0.f), om1 = om0;
+    uint2 olc = make_uint2(0xffffffffu, 0xffffffffu);
+    unsigned P = 0;
+    const int ca = i * S + q0;
+    if (valid) {
+        om0 = *reinterpret_cast<const float4 *>(mn0 + ca);
+        om1 = *reinterpret_cast<const float4 *>(mn1 + ca);
+        olc = *reinterpret_cast<const uint2 *>(lc + ca);
+        P = (unsigned)par[i];
+        if (fm) {  // fresh slots start from eta = 0: min0 = min1 = +0, no location
+            if (fm & 1u) { om0.x = 0.f; om1.x = 0.f; olc.x |= 0x0000ffffu; }
+            if (fm & 2u) { om0.y = 0.f; om1.y = 0.f; olc.x |= 0xffff0000u; }
+            if (fm & 4u) { om0.z = 0.f; om1.z = 0.f; olc.y |= 0x0000ffffu; }
+            if (fm & 8u) { om0.w = 0.f; om1.w = 0.f; olc.y |= 0xffff0000u; }
+        }
+    }
+    unsigned mv[4];
+#pragma unroll
+    for (int v = 0; v < 4; v++) mv[v] = 1u << (v * LR + l);
+    float nm0[4] = {INF, INF, INF, INF}, nm1[4] = {INF, INF, INF, INF};
+    int nloc[4] = {0xffff, 0xffff, 0xffff, 0xffff};
+    unsigned parw[4] = {0, 0, 0, 0};
+    unsigned syn = 0;
+#pragma unroll 2
+    for (int p = 0; p < dmax; p++) {
+        const bool has = HAS ? (p < d) : true;
+        const int e = ra + p;
+        const unsigned e2 = (unsigned)e * 0x10001u;
+        const int j = has ? col[e] : 0;
+        const float4 sv = *reinterpret_cast<const float4 *>(s + j * S + q0);
+        // own sign of lambda^prev xor the row parity (Obs. 2, A1 folded in); fresh slots: +
+        const unsigned W = ((has ? (unsigned)sg[e] : 0u) ^ P) & nfw;
+        unsigned bal[4];
+#pragma unroll
+        for (int v = 0; v < 4; v++) {
+            const float sj = f4c(sv, v);
+            const float mag = loc_ne(v < 2 ? olc.x : olc.y, e2, v & 1) ? f4c(om0, v) : f4c(om1, v);  // Obs. 1
+            const float x = sj - ((W & mv[v]) ? -mag : mag);  // lambda - eta^prev
+            const float ax = HAS ? (has ? fabsf(x) : INF) : fabsf(x);
+            const bool lt = ax < nm0[v];  // first strict minimum (A13)
+            nm1[v] = fminf(nm1[v], fmaxf(nm0[v], ax));
+            nm0[v] = fminf(nm0[v], ax);
+            nloc[v] = lt ? e : nloc[v];
+            bal[v] = __ballot_sync(FULLM, (HAS ? has : true) && x < 0.f);  // sign(0) = +1
+            syn ^= (unsigned)((HAS ? has : true) && sj > 0.f) << v;        // b_j = slice(s_j)
+        }
+#pragma unroll
+        for (int v = 0; v < 4; v++) parw[v] ^= bal[v];
+        if (has && l == 0) {
+            unsigned word = 0;
+#pragma unroll
+            for (int v = 0; v < 4; v++) word |= ((bal[v] >> (sub * LR)) & LMASK) << (v * LR);
+            sg[e] = (SWT)word;
+        }
+    }
+    if (valid) {
+        *reinterpret_cast<float4 *>(mn0 + ca) = make_float4(nm0[0], nm0[1], nm0[2], nm0[3]);
+        *reinterpret_cast<float4 *>(mn1 + ca) = make_float4(nm1[0], nm1[1], nm1[2], nm1[3]);
+        *reinterpret_cast<uint2 *>(lc + ca) = make_uint2((unsigned)nloc[0] | ((unsigned)nloc[1] << 16),
+                                                         (unsigned)nloc[2] | ((unsigned)nloc[3] << 16));
+        if (l == 0) {
+            unsigned word = 0;
+#pragma unroll
+            for (int v = 0; v < 4; v++) word |= ((parw[v] >> (sub * LR)) & LMASK) << (v * LR);
+            par[i] = (SWT)(word ^ ((d & 1) ? corr_all : 0u));  // (-1)^{d_i}, reading A1
+        }
+        syn_acc |= syn;
+    }
 }
 
 // Lane layout: a lane owns 4 consecutive slots (float4) of one row or column; LR = S/4 lanes cover a
@@ -101,8 +195,6 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
     using SWT = typename SWord<S>::T;
     constexpr int LR = S / 4;
     constexpr int G = 32 / LR;
-    constexpr unsigned LMASK = (LR == 32) ? 0xffffffffu : ((1u << LR) - 1u);
-    const float INF = __int_as_float(0x7f800000);
     extern __shared__ __align__(16) unsigned char sm[];
     const int m = a.g.m, n = a.g.n, E = a.g.E;
     float *s = reinterpret_cast<float *>(sm + a.lay.s);
@@ -110,6 +202,7 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
     float *mn1 = reinterpret_cast<float *>(sm + a.lay.m1);
     uint16_t *lc = reinterpret_cast<uint16_t *>(sm + a.lay.lc);
     SWT *sg = reinterpret_cast<SWT *>(sm + a.lay.sg);
+    SWT *par = reinterpret_cast<SWT *>(sm + a.lay.par);
     uint16_t *rp = reinterpret_cast<uint16_t *>(sm + a.lay.rp);
     uint16_t *cp = reinterpret_cast<uint16_t *>(sm + a.lay.cp);
     uint16_t *col = reinterpret_cast<uint16_t *>(sm + a.lay.col);
@@ -126,6 +219,7 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
     const int sub = lane / LR, l = lane % LR;  // row group inside the warp, lane inside the row
     const int q0 = 4 * l;                      // first slot of this lane
     float *rs = a.rs + (size_t)blockIdx.x * n * S;
+    const unsigned corr_all = a.literal ? 0u : (S == 32 ? 0xffffffffu : ((1u << S) - 1u));
 
     // ---- the Tanner graph into shared memory (16-bit lists)
     for (int q = tid; q <= m; q += RT) rp[q] = (uint16_t)__ldg(a.g.row_ptr + q);
@@ -156,12 +250,13 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
         if (warp == 0) {
             const unsigned uns_all = ctl[0];
             const unsigned act_all = ctl[2];
-            if (lane < S && ((act_all >> lane) & 1u)) {
+            const bool mine = lane < S;
+            int f = mine ? slot_f[lane] : 0;
+            if (mine && ((act_all >> lane) & 1u)) {
                 const int k = slot_k[lane];
                 const bool uns = (uns_all >> lane) & 1u;
                 const bool fin = a.early ? (!uns || k == a.L) : (k == a.L);
                 if (fin) {
-                    const int64_t f = slot_f[lane];
                     const int conv = !uns;
                     if (a.iters) a.iters[f] = k;
                     if (a.conv) a.conv[f] = (uint8_t)conv;
@@ -174,33 +269,35 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
                     acc_stats[5] += conv;
                     acc_stats[6] += slot_nz[lane] != 0;
                     acc_stats[7] += (unsigned long long)slot_raw[lane];
-                    slot_f[lane] = -1;
+                    f = -1;
                 } else {
                     slot_k[lane] = k + 1;
                 }
             }
-            __syncwarp();
+            // refill: the free slots take consecutive frames from the global counter
+            const unsigned freem = __ballot_sync(FULLM, mine && f < 0);
+            long long base = 0;
+            if (lane == 0 && freem && !ctl[3]) base = atomicAdd(a.counter, __popc(freem));
+            base = __shfl_sync(FULLM, base, 0);
+            const bool exhausted = ctl[3] != 0;
+            unsigned fresh = 0;
+            if (freem && !exhausted) {
+                const long long mine_f = base + __popc(freem & ((1u << lane) - 1u));
+                const bool take = mine && f < 0 && mine_f < a.frames;
+                if (take) {
+                    f = (int)mine_f;
+                    slot_k[lane] = 0;
+                    slot_be[lane] = 0;
+                    slot_raw[lane] = 0;
+                    slot_nz[lane] = 0;
+                }
+                fresh = __ballot_sync(FULLM, take);
+                if (lane == 0 && base + __popc(freem) >= a.frames) ctl[3] = 1;
+            }
+            if (mine) slot_f[lane] = f;
+            const unsigned active = __ballot_sync(FULLM, mine && f >= 0);
             if (lane == 0) {
                 ctl[0] = 0;
-                unsigned fresh = 0, active = 0;
-                int nfree = 0;
-                for (int q = 0; q < S; q++) nfree += slot_f[q] < 0;
-                if (nfree && !ctl[3]) {
-                    long long base = atomicAdd(a.counter, nfree);
-                    for (int q = 0; q < S; q++) {
-                        if (slot_f[q] >= 0) continue;
-                        if (base < a.frames) {
-                            slot_f[q] = (int)base++;
-                            slot_k[q] = 0;
-                            slot_be[q] = 0;
-                            slot_raw[q] = 0;
-                            slot_nz[q] = 0;
-                            fresh |= 1u << q;
-                        }
-                    }
-                    if (base >= a.frames) ctl[3] = 1;
-                }
-                for (int q = 0; q < S; q++) active |= (unsigned)(slot_f[q] >= 0) << q;
                 ctl[1] = fresh;
                 ctl[2] = active;
             }
@@ -208,38 +305,46 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
         __syncthreads();
         const unsigned active = ctl[2], fresh_new = ctl[1];
         if (!active) break;
+        const unsigned fm = (fresh_new >> q0) & 0xfu;  // this lane's fresh slots
 
-        // ---------------- B: stage new frames: s = r, eta^prev = 0 (min0 = min1 = +0, no location,
-        //                     sign bits cleared)
+        // ---------------- B: stage new frames, s = r: column sweep in the float4 layout
         if (fresh_new) {
-            SWT clear = 0;
+            int fr[4];
 #pragma unroll
-            for (int q = 0; q < S; q++)
-                if ((fresh_new >> q) & 1u) clear |= (SWT)(1u << ((q & 3) * LR + (q >> 2)));
-            for (int e = tid; e < E; e += RT) sg[e] &= (SWT)~clear;
-            for (unsigned fm = fresh_new; fm; fm &= fm - 1) {
-                const int q = __ffs(fm) - 1;
-                for (int i = tid; i < m; i += RT) {
-                    mn0[i * S + q] = 0.f;
-                    mn1[i * S + q] = 0.f;
-                    lc[i * S + q] = 0xffffu;
+            for (int v = 0; v < 4; v++) fr[v] = slot_f[q0 + v];
+            int raw[4] = {0, 0, 0, 0};
+            for (int cb = warp * G; cb < n && fm; cb += NWARP * G) {
+                const int j = cb + sub;
+                if (j >= n) continue;
+                float *sp = s + j * S + q0;
+                float4 o = *reinterpret_cast<const float4 *>(sp);
+#pragma unroll
+                for (int v = 0; v < 4; v++) {
+                    if ((fm >> v) & 1u) {
+                        const float x = __ldg(a.llr + (int64_t)fr[v] * n + j);
+                        f4s(o, v, x);
+                        rs[(size_t)j * S + q0 + v] = x;
+                        raw[v] += x > 0.f;
+                    }
                 }
-                const float *src = a.llr + (int64_t)slot_f[q] * n;
-                int raw = 0;
-                for (int j = tid; j < n; j += RT) {
-                    const float v = __ldg(src + j);
-                    s[j * S + q] = v;
-                    rs[(size_t)j * S + q] = v;
-                    raw += v > 0.f;
-                }
-                for (int o = 16; o; o >>= 1) raw += __shfl_xor_sync(FULLM, raw, o);
-                if (lane == 0 && raw) atomicAdd(&slot_raw[q], raw);
+                *reinterpret_cast<float4 *>(sp) = o;
+            }
+            // per-slot counts: reduce over the row groups of the warp, then one atomic per slot
+#pragma unroll
+            for (int v = 0; v < 4; v++) {
+                int x = raw[v];
+                for (int o = LR; o < 32; o <<= 1) x += __shfl_xor_sync(FULLM, x, o);
+                if (sub == 0 && x) atomicAdd(&slot_raw[q0 + v], x);
             }
             __syncthreads();
         }
 
         // ---------------- C: check-node pass + syndrome of b = slice(s)
         {
+            SWT nfw = 0;
+#pragma unroll
+            for (int q = 0; q < S; q++)
+                if (!((fresh_new >> q) & 1u)) nfw |= (SWT)(1u << ((q & 3) * LR + (q >> 2)));
             unsigned syn_acc = 0;  // bit v: slot q0+v has an unsatisfied check
             for (int rb = warp * G; rb < m; rb += NWARP * G) {
                 const int i = rb + sub;
@@ -247,63 +352,12 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
                 const int ra = valid ? rp[i] : 0;
                 const int d = valid ? (int)rp[i + 1] - ra : 0;
                 const int dmax = __reduce_max_sync(FULLM, d);
-                float4 om0 = make_float4(0.f, 0.f, 0.f, 0.f), om1 = om0;
-                ushort4 olc = make_ushort4(0xffffu, 0xffffu, 0xffffu, 0xffffu);
-                if (valid) {
-                    om0 = *reinterpret_cast<const float4 *>(mn0 + i * S + q0);
-                    om1 = *reinterpret_cast<const float4 *>(mn1 + i * S + q0);
-                    olc = *reinterpret_cast<const ushort4 *>(lc + i * S + q0);
-                }
-                float nm0[4] = {INF, INF, INF, INF}, nm1[4] = {INF, INF, INF, INF};
-                int nloc[4] = {0xffff, 0xffff, 0xffff, 0xffff};
-                unsigned parw[4] = {0, 0, 0, 0};
-                unsigned syn = 0;
-                for (int p = 0; p < dmax; p++) {
-                    const bool has = p < d;
-                    const int e = ra + p;
-                    const int j = has ? col[e] : 0;
-                    const float4 sv = *reinterpret_cast<const float4 *>(s + j * S + q0);
-                    const unsigned w = has ? (unsigned)sg[e] : 0u;
-                    unsigned bal[4];
-#pragma unroll
-                    for (int v = 0; v < 4; v++) {
-                        const float sj = f4c(sv, v);
-                        const float m0v = f4c(om0, v);
-                        const float mag = (e == u4c(olc, v)) ? f4c(om1, v) : fabsf(m0v);  // Obs. 1
-                        // sign of eta^prev: own lambda sign xor the row parity (Obs. 2; A1 folded in)
-                        const unsigned sbit = ((w << (31 - (v * LR + l))) ^ __float_as_uint(m0v)) & 0x80000000u;
-                        const float x = sj - __uint_as_float(__float_as_uint(mag) | sbit);  // lambda - eta^prev
-                        const float ax = has ? fabsf(x) : INF;
-                        const bool lt = ax < nm0[v];  // first strict minimum (A13)
-                        nm1[v] = fminf(nm1[v], fmaxf(nm0[v], ax));
-                        nm0[v] = fminf(nm0[v], ax);
-                        nloc[v] = lt ? e : nloc[v];
-                        bal[v] = __ballot_sync(FULLM, has && x < 0.f);  // sign(0) = +1
-                        syn ^= (unsigned)(has && sj > 0.f) << v;         // b_j = slice(s_j)
-                    }
-#pragma unroll
-                    for (int v = 0; v < 4; v++) parw[v] ^= bal[v];
-                    if (has && l == 0) {
-                        unsigned word = 0;
-#pragma unroll
-                        for (int v = 0; v < 4; v++) word |= ((bal[v] >> (sub * LR)) & LMASK) << (v * LR);
-                        sg[e] = (SWT)word;
-                    }
-                }
-                if (valid) {
-                    const unsigned corr = (unsigned)(d & 1) & (unsigned)(!a.literal);  // reading A1
-                    float4 o0, o1;
-                    o0.x = __uint_as_float(__float_as_uint(nm0[0]) | ((((parw[0] >> lane) & 1u) ^ corr) << 31));
-                    o0.y = __uint_as_float(__float_as_uint(nm0[1]) | ((((parw[1] >> lane) & 1u) ^ corr) << 31));
-                    o0.z = __uint_as_float(__float_as_uint(nm0[2]) | ((((parw[2] >> lane) & 1u) ^ corr) << 31));
-                    o0.w = __uint_as_float(__float_as_uint(nm0[3]) | ((((parw[3] >> lane) & 1u) ^ corr) << 31));
-                    o1 = make_float4(nm1[0], nm1[1], nm1[2], nm1[3]);
-                    *reinterpret_cast<float4 *>(mn0 + i * S + q0) = o0;
-                    *reinterpret_cast<float4 *>(mn1 + i * S + q0) = o1;
-                    *reinterpret_cast<ushort4 *>(lc + i * S + q0) =
-                        make_ushort4((uint16_t)nloc[0], (uint16_t)nloc[1], (uint16_t)nloc[2], (uint16_t)nloc[3]);
-                    syn_acc |= syn;
-                }
+                if (__all_sync(FULLM, d == dmax))
+                    cn_rows<S, false>(s, mn0, mn1, lc, sg, par, col, i, valid, ra, d, dmax, l, sub, fm, nfw, corr_all,
+                                      syn_acc);
+                else
+                    cn_rows<S, true>(s, mn0, mn1, lc, sg, par, col, i, valid, ra, d, dmax, l, sub, fm, nfw, corr_all,
+                                     syn_acc);
             }
             const unsigned mine = (syn_acc << q0) & active;
             const unsigned wmask = __reduce_or_sync(FULLM, mine);
@@ -311,69 +365,87 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
         }
         __syncthreads();
 
-        // ---------------- D: per-slot decision, outputs of stopping slots, bit-node pass of the rest
+        // ---------------- D: per-slot decision; outputs of stopping slots and bit-node update of the
+        //                     continuing ones in one column sweep
         {
             const unsigned uns_all = ctl[0];
-            unsigned fin_mask = 0, cont_mask = 0;
-#pragma unroll 1
-            for (int q = 0; q < S; q++) {
-                if (!((active >> q) & 1u)) continue;
-                const int k = slot_k[q];
-                const bool uns = (uns_all >> q) & 1u;
-                const bool fin = a.early ? (!uns || k == a.L) : (k == a.L);
-                if (fin) fin_mask |= 1u << q;
-                else cont_mask |= 1u << q;
+            bool fin = false, cont = false;
+            if (lane < S && ((active >> lane) & 1u)) {
+                const int k = slot_k[lane];
+                const bool uns = (uns_all >> lane) & 1u;
+                fin = a.early ? (!uns || k == a.L) : (k == a.L);
+                cont = !fin;
             }
-            for (unsigned fm = fin_mask; fm; fm &= fm - 1) {
-                const int q = __ffs(fm) - 1;
-                const int64_t f = slot_f[q];
-                int be = 0;
-                bool nz = false;
-                for (int j = tid; j < n; j += RT) {
-                    const float v = s[j * S + q];
-                    const bool b = v > 0.f;  // Eq. slice
-                    if (a.post) a.post[f * n + j] = v;
-                    if (a.bits) a.bits[f * n + j] = (uint8_t)b;
-                    be += b;
-                    nz |= fabsf(v) <= 1e-4f;
-                }
-                for (int o = 16; o; o >>= 1) be += __shfl_xor_sync(FULLM, be, o);
-                nz = __any_sync(FULLM, nz);
-                if (lane == 0) {
-                    if (be) atomicAdd(&slot_be[q], be);
-                    if (nz) slot_nz[q] = 1;
-                }
-            }
+            const unsigned fin_mask = __ballot_sync(FULLM, fin), cont_mask = __ballot_sync(FULLM, cont);
             const unsigned cm = (cont_mask >> q0) & 0xfu;  // continuing slots of this lane
-            if (cont_mask) {
+            const unsigned fk = (fin_mask >> q0) & 0xfu;   // stopping slots of this lane
+            if (fin_mask | cont_mask) {
+                int64_t fo[4];
+#pragma unroll
+                for (int v = 0; v < 4; v++) fo[v] = (int64_t)slot_f[q0 + v] * n;
+                int be[4] = {0, 0, 0, 0};
+                unsigned nz = 0;
+                unsigned mv[4];
+#pragma unroll
+                for (int v = 0; v < 4; v++) mv[v] = 1u << (v * LR + l);
                 for (int cb = warp * G; cb < n; cb += NWARP * G) {
                     const int j = cb + sub;
-                    if (j >= n || !cm) continue;
-                    const float4 rj = *reinterpret_cast<const float4 *>(rs + (size_t)j * S + q0);
-                    const int c0 = cp[j], dv = (int)cp[j + 1] - c0;
-                    float acc[4] = {0.f, 0.f, 0.f, 0.f};
-                    for (int qq = 0; qq < dv; qq++) {
-                        const uint32_t rc = rec[c0 + qq];
-                        const int e = (int)(rc >> 16), i = (int)(rc & 0xffffu);
-                        const float4 m0 = *reinterpret_cast<const float4 *>(mn0 + i * S + q0);
-                        const float4 m1 = *reinterpret_cast<const float4 *>(mn1 + i * S + q0);
-                        const ushort4 lv = *reinterpret_cast<const ushort4 *>(lc + i * S + q0);
-                        const unsigned w = (unsigned)sg[e];
-#pragma unroll
-                        for (int v = 0; v < 4; v++) {
-                            const float m0v = f4c(m0, v);
-                            const float mag = (e == u4c(lv, v)) ? f4c(m1, v) : fabsf(m0v);  // Obs. 1
-                            const unsigned sbit = ((w << (31 - (v * LR + l))) ^ __float_as_uint(m0v)) & 0x80000000u;
-                            acc[v] = acc[v] + __uint_as_float(__float_as_uint(mag) | sbit);  // ascending rows (A14)
-                        }
-                    }
+                    if (j >= n || !(cm | fk)) continue;
                     float *sp = s + j * S + q0;
                     float4 o = *reinterpret_cast<const float4 *>(sp);
-                    if (cm & 1u) o.x = acc[0] + rj.x;
-                    if (cm & 2u) o.y = acc[1] + rj.y;
-                    if (cm & 4u) o.z = acc[2] + rj.z;
-                    if (cm & 8u) o.w = acc[3] + rj.w;
-                    *reinterpret_cast<float4 *>(sp) = o;
+                    if (fk) {
+#pragma unroll
+                        for (int v = 0; v < 4; v++) {
+                            if ((fk >> v) & 1u) {
+                                const float x = f4c(o, v);
+                                const bool b = x > 0.f;  // Eq. slice
+                                if (a.post) a.post[fo[v] + j] = x;
+                                if (a.bits) a.bits[fo[v] + j] = (uint8_t)b;
+                                be[v] += b;
+                                nz |= (unsigned)(fabsf(x) <= 1e-4f) << v;
+                            }
+                        }
+                    }
+                    if (cm) {
+                        const float4 rj = *reinterpret_cast<const float4 *>(rs + (size_t)j * S + q0);
+                        const int c0 = cp[j], dv = (int)cp[j + 1] - c0;
+                        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 2
+                        for (int qq = 0; qq < dv; qq++) {
+                            const uint32_t rc = rec[c0 + qq];
+                            const int e = (int)(rc >> 16), i = (int)(rc & 0xffffu);
+                            const unsigned e2 = (unsigned)e * 0x10001u;
+                            const int ca = i * S + q0;
+                            const float4 m0 = *reinterpret_cast<const float4 *>(mn0 + ca);
+                            const float4 m1 = *reinterpret_cast<const float4 *>(mn1 + ca);
+                            const uint2 lv = *reinterpret_cast<const uint2 *>(lc + ca);
+                            const unsigned W = (unsigned)sg[e] ^ (unsigned)par[i];
+#pragma unroll
+                            for (int v = 0; v < 4; v++) {
+                                const float mag = loc_ne(v < 2 ? lv.x : lv.y, e2, v & 1) ? f4c(m0, v) : f4c(m1, v);
+                                acc[v] = acc[v] + ((W & mv[v]) ? -mag : mag);  // ascending rows from +0.0 (A14)
+                            }
+                        }
+                        if (cm & 1u) o.x = acc[0] + rj.x;
+                        if (cm & 2u) o.y = acc[1] + rj.y;
+                        if (cm & 4u) o.z = acc[2] + rj.z;
+                        if (cm & 8u) o.w = acc[3] + rj.w;
+                        *reinterpret_cast<float4 *>(sp) = o;
+                    }
+                }
+                if (fin_mask) {
+#pragma unroll
+                    for (int v = 0; v < 4; v++) {
+                        int x = be[v];
+                        for (int o = LR; o < 32; o <<= 1) x += __shfl_xor_sync(FULLM, x, o);
+                        if (sub == 0 && x) atomicAdd(&slot_be[q0 + v], x);
+                    }
+                    unsigned z = nz;
+                    for (int o = LR; o < 32; o <<= 1) z |= __shfl_xor_sync(FULLM, z, o);
+                    if (sub == 0 && z)
+#pragma unroll
+                        for (int v = 0; v < 4; v++)
+                            if ((z >> v) & 1u) slot_nz[q0 + v] = 1;
                 }
             }
         }
