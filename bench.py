@@ -155,23 +155,34 @@ def build_workload(cfg_name, rank, dev):
     return cfg, code, llr, pts
 
 
+def units(iters: np.ndarray, L: int, early: bool):
+    """(check-node frame-bodies, bit-node frame-bodies): a frame stopping after k bodies is touched by
+    min(k+1, L) check-node sweeps (the sweep of body k+1 finds its codeword) and k bit-node sweeps."""
+    k = iters.astype(np.int64)
+    if not early:
+        return np.full_like(k, L), np.full_like(k, L)
+    return (np.minimum(k + 1, L) if L > 0 else np.zeros_like(k)), k
+
+
 def algorithmic_bytes(code, iters: np.ndarray, L: int, early: bool):
-    """Bytes the method must move with its state in HBM:
-    check node: gather s (4n) + read/write the compressed row state (9m + E/8 each way; body 1 has
-    no old state); bit node: read row state (9m + E/8) + r (4n) + write s (4n)."""
+    """Bytes the method must move per frame with its state in HBM (SURVEY 8(d) B_comp split by sweep;
+    DESIGN.md "Roofline"): check node = gather s (4n) + read and write the compressed row state
+    (9m + E/8 each way; the first body reads none); bit node = read row state (9m + E/8) + r (4n) + write
+    s (4n); I/O = llr in (4n) + posterior (4n) + bits (n) + k and isCodeword (5).  Returns (cn, bn, io)."""
     n, m, E = code.n, code.m, code.nnz
     state = 9 * m + E / 8
-    k = iters.astype(np.int64)
-    if early:
-        cn_units = np.minimum(k + 1, L) if L > 0 else np.zeros_like(k)  # CN bodies that touch frame f
-        bn_units = k  # BN bodies that update frame f
-    else:
-        cn_units = np.full_like(k, L)
-        bn_units = np.full_like(k, L)
-    F = len(k)
-    cn = float(cn_units.sum()) * (4 * n + 2 * state) - (F * state if L > 0 else 0.0)  # body 1 reads no state
-    bn = float(bn_units.sum()) * (8 * n + state)
-    return cn, bn
+    cu, bu = units(iters, L, early)
+    F = len(iters)
+    cn = float(cu.sum()) * (4 * n + 2 * state) - (F * state if L > 0 else 0.0)
+    bn = float(bu.sum()) * (8 * n + state)
+    io = F * (9 * n + 5.0)
+    return cn, bn, io
+
+
+# Minimal per-element work of the method (DESIGN.md "Roofline"): per frame and edge, the check node
+# does subtract, compare + two min updates + argmin select, sign parity, eta^prev rebuild (magnitude
+# select, sign) and the syndrome bit = 9 lane operations; the bit node rebuilds eta (2) and adds (1).
+OPS_CN, OPS_BN = 9, 3
 
 
 # ------------------------------------------------------------------ our arm ------------------
@@ -226,9 +237,13 @@ def run_ours(args):
     # ---- roofline of the dominant kernel (per-launch algorithmic bytes / per-launch device time)
     iters_np = out.iters.cpu().numpy()
     early = not (args.flags & P.FLAG_NO_EARLY_STOP)
-    cn_b, bn_b = algorithmic_bytes(code, iters_np, L, early)
+    cn_b, bn_b, io_b = algorithmic_bytes(code, iters_np, L, early)
+    cu, bu = units(iters_np, L, early)
     peak, peak_src = hbm_peak()
-    kern = {"check_node": cn_b, "bit_node": bn_b}
+    if h.schedule == "resident":
+        kern = {"resident": cn_b + bn_b + io_b}
+    else:
+        kern = {"check_node": cn_b, "bit_node": bn_b}
     dom = max(kern, key=lambda c: prof[c][1])
     n_launch, kms = prof[dom]
     roof = None
@@ -239,9 +254,24 @@ def run_ours(args):
         roof = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic_from_profiles(args.config, dom),
                 "algorithmic_bytes_per_launch": round(per_launch_bytes), "avg_launch_us": round(per_launch_s * 1e6, 2),
-                "share_of_step": round(kms / (ms_local * 1.0), 4), "peak_source": peak_src,
+                "share_of_step": round(kms / ms_local, 4), "peak_source": peak_src,
                 "kernel_ms": {k: round(v[1], 3) for k, v in prof.items() if v[0]},
                 "kernel_launches": {k: v[0] for k, v in prof.items() if v[0]}}
+        if dom == "resident":
+            roof["note"] = ("state is SMEM-resident: the algorithmic bytes (B_comp per frame-body, SURVEY 8(d)) "
+                            "stay on chip, DRAM carries only I/O (see traffic)")
+            sm_mhz = 1965.0
+            try:
+                with open(PEAKS_PATH) as f:
+                    sm_mhz = float(json.load(f).get("sm_max_mhz", sm_mhz))
+            except Exception:
+                pass
+            issue_peak = 148 * 4 * 32 * sm_mhz * 1e6 / 1e12  # lane-instructions per s, T
+            ops = (float(cu.sum()) * OPS_CN + float(bu.sum()) * OPS_BN) * code.nnz * args.steps
+            ach = ops / (kms / 1e3) / 1e12
+            roof["issue_roofline"] = {"bound": "alu", "achieved": round(ach, 3), "peak": round(issue_peak, 2),
+                                      "unit": "T lane-ops/s", "frac": round(ach / issue_peak, 4),
+                                      "ops_per_frame_edge": {"check_node": OPS_CN, "bit_node": OPS_BN}}
     total_bits = float(world) * F * n * args.steps
     value = total_bits / (ms / 1e3) / 1e9
 
