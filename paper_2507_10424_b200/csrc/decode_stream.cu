@@ -100,9 +100,20 @@ __global__ void __launch_bounds__(CTA) k_stage_in(const float *__restrict__ llr,
 // ------------------------------------------------------------------------------------------------
 // a3/a4/a6: check-node sweep of loop body k (k = 1..L), fused syndrome of b^(k-1).
 // FIRST: eta^prev = 0, so no old state is read.
+// Sign words: per (tile, edge) four u32; lane l's four bits (frames 4l..4l+3) are the nibble at bits
+// 4*(l%8) of word l/8, so a lane reads one u32 per edge.  The row parity stored in min0's sign bit
+// already includes the (-1)^{d_i} factor of reading A1.
+// The edges of a row are processed in chunks of CN_U: all index, s and sign loads of a chunk are
+// issued before any arithmetic, so each warp keeps 2*CN_U loads in flight.
 // ------------------------------------------------------------------------------------------------
-template <typename LocT, bool FIRST, bool EARLY>
-__global__ void __launch_bounds__(CTA) k_cn(Graph g, StreamState w, int k, int rows_per_cta, int literal) {
+template <int U>
+struct MinBlocks {
+    static constexpr int value = U <= 1 ? 4 : U == 2 ? 3 : 2;  // register budget 64 / 85 / 128 per thread
+};
+
+template <typename LocT, bool FIRST, bool EARLY, int CN_U>
+__global__ void __launch_bounds__(CTA, MinBlocks<CN_U>::value)
+    k_cn(Graph g, StreamState w, int k, int rows_per_cta, int literal) {
     using L4 = typename Vec4<LocT>::type;
     const int t = blockIdx.y;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -113,20 +124,28 @@ __global__ void __launch_bounds__(CTA) k_cn(Graph g, StreamState w, int k, int r
         if (threadIdx.x < 4) s_u[threadIdx.x] = 0;
         __syncthreads();
     }
+    const int *__restrict__ row_ptr = g.row_ptr;
+    const int *__restrict__ col_idx = g.col_idx;
+    const float *__restrict__ S = w.s;
+    uint32_t *__restrict__ SG = w.sgn;
+    float *__restrict__ M0 = w.min0;
+    float *__restrict__ M1 = w.min1;
+    LocT *__restrict__ LC = reinterpret_cast<LocT *>(w.loc);
     const int m = g.m, n = g.n, E = g.E;
     const size_t tm = (size_t)t * m, tn = (size_t)t * n, tE = (size_t)t * E;
+    const int sh = 4 * (lane & 7), wsel = lane >> 3;
     const int i0 = blockIdx.x * rows_per_cta, i1 = min(m, i0 + rows_per_cta);
     uint32_t u0 = 0, u1 = 0, u2 = 0, u3 = 0;
     for (int i = i0 + warp; i < i1; i += CTA / 32) {
-        const int a = __ldg(g.row_ptr + i), d = __ldg(g.row_ptr + i + 1) - a;
+        const int a = __ldg(row_ptr + i), d = __ldg(row_ptr + i + 1) - a;
         const unsigned corr = (unsigned)(d & 1) & (unsigned)(!literal);  // (-1)^{d_i}, reading A1
         const size_t st = (tm + i) * TILE + 4 * lane;
         float4 om0 = make_float4(0.f, 0.f, 0.f, 0.f), om1 = om0;
         L4 olc{};
         if (!FIRST) {
-            om0 = ld4(w.min0 + st);
-            om1 = ld4(w.min1 + st);
-            olc = *reinterpret_cast<const L4 *>(reinterpret_cast<const LocT *>(w.loc) + st);
+            om0 = ld4(M0 + st);
+            om1 = ld4(M1 + st);
+            olc = *reinterpret_cast<const L4 *>(LC + st);
         }
         float nm0[4], nm1[4];
         int nloc[4];
@@ -137,49 +156,64 @@ __global__ void __launch_bounds__(CTA) k_cn(Graph g, StreamState w, int k, int r
             nm1[v] = __int_as_float(0x7f800000);
             nloc[v] = 0;
         }
-        for (int p = 0; p < d; p++) {
-            const int e = a + p;
-            const int j = __ldg(g.col_idx + e);
-            const float4 sv = ld4(w.s + (tn + j) * TILE + 4 * lane);
-            uint4 sw = make_uint4(0, 0, 0, 0);
-            if (!FIRST) sw = ldu4(w.sgn + (tE + e) * 4);
-            unsigned nw[4];
+        for (int p0 = 0; p0 < d; p0 += CN_U) {
+            int jj[CN_U];
+            float4 sv[CN_U];
+            unsigned sw[CN_U];
 #pragma unroll
-            for (int v = 0; v < 4; v++) {
-                const float sj = comp(sv, v);
-                float x = sj;
-                if (!FIRST) {
-                    const float m0v = comp(om0, v);
-                    const float mag = (p == compl4(olc, v)) ? comp(om1, v) : fabsf(m0v);
-                    const unsigned neg_eta = ((comp(sw, v) >> lane) & 1u) ^ (__float_as_uint(m0v) >> 31) ^ corr;
-                    x = sj - (neg_eta ? -mag : mag);  // lambda_k - eta^prev_{i,k}
+            for (int u = 0; u < CN_U; u++) jj[u] = (p0 + u < d) ? __ldg(col_idx + a + p0 + u) : 0;
+#pragma unroll
+            for (int u = 0; u < CN_U; u++) {
+                if (p0 + u < d) {
+                    sv[u] = ld4(S + (tn + jj[u]) * TILE + 4 * lane);
+                    sw[u] = FIRST ? 0u : (SG[(tE + a + p0 + u) * 4 + wsel] >> sh);
                 }
-                const float ax = fabsf(x);
-                const bool lt = ax < nm0[v];  // first strict minimum (A13)
-                nm1[v] = lt ? nm0[v] : fminf(nm1[v], ax);
-                nm0[v] = lt ? ax : nm0[v];
-                nloc[v] = lt ? p : nloc[v];
-                const bool neg = x < 0.f;  // sign(0) = +1
-                npar ^= (unsigned)neg << v;
-                if (EARLY) syn ^= (unsigned)(sj > 0.f) << v;  // b_j = slice(s_j)
-                nw[v] = __ballot_sync(FULL, neg);
             }
-            if (lane == 0) *reinterpret_cast<uint4 *>(w.sgn + (tE + e) * 4) = make_uint4(nw[0], nw[1], nw[2], nw[3]);
+#pragma unroll
+            for (int u = 0; u < CN_U; u++) {
+                if (p0 + u >= d) break;
+                const int p = p0 + u;
+                unsigned nib = 0;
+#pragma unroll
+                for (int v = 0; v < 4; v++) {
+                    const float sj = comp(sv[u], v);
+                    float x = sj;
+                    if (!FIRST) {
+                        const float m0v = comp(om0, v);
+                        const float mag = (p == compl4(olc, v)) ? comp(om1, v) : fabsf(m0v);  // Obs. 1
+                        const unsigned neg_eta = ((sw[u] >> v) & 1u) ^ (__float_as_uint(m0v) >> 31);  // Obs. 2
+                        x = sj - (neg_eta ? -mag : mag);  // lambda_k - eta^prev_{i,k}
+                    }
+                    const float ax = fabsf(x);
+                    const bool lt = ax < nm0[v];  // first strict minimum (A13)
+                    nm1[v] = fminf(nm1[v], fmaxf(nm0[v], ax));
+                    nm0[v] = fminf(nm0[v], ax);
+                    nloc[v] = lt ? p : nloc[v];
+                    nib |= (unsigned)(x < 0.f) << v;  // sign(0) = +1
+                    if (EARLY) syn ^= (unsigned)(sj > 0.f) << v;  // b_j = slice(s_j)
+                }
+                npar ^= nib;
+                unsigned word = nib << sh;
+                word |= __shfl_xor_sync(FULL, word, 1);
+                word |= __shfl_xor_sync(FULL, word, 2);
+                word |= __shfl_xor_sync(FULL, word, 4);
+                if ((lane & 7) == 0) SG[(tE + a + p) * 4 + wsel] = word;
+            }
         }
-        float4 o0, o1;
-        o0.x = __uint_as_float(__float_as_uint(nm0[0]) | ((npar & 1u) << 31));
-        o0.y = __uint_as_float(__float_as_uint(nm0[1]) | (((npar >> 1) & 1u) << 31));
-        o0.z = __uint_as_float(__float_as_uint(nm0[2]) | (((npar >> 2) & 1u) << 31));
-        o0.w = __uint_as_float(__float_as_uint(nm0[3]) | (((npar >> 3) & 1u) << 31));
-        o1 = make_float4(nm1[0], nm1[1], nm1[2], nm1[3]);
-        st4(w.min0 + st, o0);
-        st4(w.min1 + st, o1);
+        const unsigned pc = npar ^ (corr ? 0xfu : 0u);
+        float4 o0;
+        o0.x = __uint_as_float(__float_as_uint(nm0[0]) | ((pc & 1u) << 31));
+        o0.y = __uint_as_float(__float_as_uint(nm0[1]) | (((pc >> 1) & 1u) << 31));
+        o0.z = __uint_as_float(__float_as_uint(nm0[2]) | (((pc >> 2) & 1u) << 31));
+        o0.w = __uint_as_float(__float_as_uint(nm0[3]) | (((pc >> 3) & 1u) << 31));
+        st4(M0 + st, o0);
+        st4(M1 + st, make_float4(nm1[0], nm1[1], nm1[2], nm1[3]));
         L4 nl;
         nl.x = (LocT)nloc[0];
         nl.y = (LocT)nloc[1];
         nl.z = (LocT)nloc[2];
         nl.w = (LocT)nloc[3];
-        *reinterpret_cast<L4 *>(reinterpret_cast<LocT *>(w.loc) + st) = nl;
+        *reinterpret_cast<L4 *>(LC + st) = nl;
         if (EARLY) {
             u0 |= __ballot_sync(FULL, syn & 1u);
             u1 |= __ballot_sync(FULL, syn & 2u);
@@ -202,10 +236,13 @@ __global__ void __launch_bounds__(CTA) k_cn(Graph g, StreamState w, int k, int r
 
 // ------------------------------------------------------------------------------------------------
 // a5/a6: bit-node sweep of loop body k; stops frames whose b^(k-1) satisfied every check.
+// Column edges in chunks of BN_U with all loads of a chunk in flight before the (ordered) sum.
 // ------------------------------------------------------------------------------------------------
-template <typename LocT, bool EARLY>
-__global__ void __launch_bounds__(CTA) k_bn(Graph g, StreamState w, int k, int cols_per_cta, int literal) {
+template <typename LocT, bool EARLY, int BN_U>
+__global__ void __launch_bounds__(CTA, BN_U <= 1 ? 6 : MinBlocks<BN_U>::value)
+    k_bn(Graph g, StreamState w, int k, int cols_per_cta, int literal) {
     using L4 = typename Vec4<LocT>::type;
+    (void)literal;
     const int t = blockIdx.y;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int T = w.T;
@@ -231,40 +268,81 @@ __global__ void __launch_bounds__(CTA) k_bn(Graph g, StreamState w, int k, int c
     }
     const unsigned mine = ((act.x >> lane) & 1u) | (((act.y >> lane) & 1u) << 1) | (((act.z >> lane) & 1u) << 2) |
                           (((act.w >> lane) & 1u) << 3);
+    const int *__restrict__ col_ptr = g.col_ptr;
+    const int4 *__restrict__ bn_edge = g.bn_edge;
+    const float *__restrict__ M0 = w.min0;
+    const float *__restrict__ M1 = w.min1;
+    const LocT *__restrict__ LC = reinterpret_cast<const LocT *>(w.loc);
+    const uint32_t *__restrict__ SG = w.sgn;
+    const float *__restrict__ R = w.r;
+    float *__restrict__ Sv = w.s;
     const int m = g.m, n = g.n, E = g.E;
     const size_t tm = (size_t)t * m, tn = (size_t)t * n, tE = (size_t)t * E;
+    const int sh = 4 * (lane & 7), wsel = lane >> 3;
     const int j0 = blockIdx.x * cols_per_cta, j1 = min(n, j0 + cols_per_cta);
     for (int j = j0 + warp; j < j1; j += CTA / 32) {
-        const int c0 = __ldg(g.col_ptr + j), dv = __ldg(g.col_ptr + j + 1) - c0;
+        const int c0 = __ldg(col_ptr + j), dv = __ldg(col_ptr + j + 1) - c0;
+        const size_t sj = (tn + j) * TILE + 4 * lane;
+        const float4 rv = ld4(R + sj);
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
-        for (int q = 0; q < dv; q++) {
-            const int4 ed = __ldg(g.bn_edge + c0 + q);  // {e, i, p, d_i & 1}, ascending i
-            const size_t st = (tm + ed.y) * TILE + 4 * lane;
-            const float4 m0 = ld4(w.min0 + st);
-            const float4 m1 = ld4(w.min1 + st);
-            const L4 lc = *reinterpret_cast<const L4 *>(reinterpret_cast<const LocT *>(w.loc) + st);
-            const uint4 sw = ldu4(w.sgn + (tE + ed.x) * 4);
-            const unsigned corr = (unsigned)ed.w & (unsigned)(!literal);
+        if (BN_U <= 1) {
+            for (int q = 0; q < dv; q++) {
+                const int4 ed = __ldg(bn_edge + c0 + q);  // {e, i, p, -}, ascending i
+                const size_t st = (tm + ed.y) * TILE + 4 * lane;
+                const float4 m0 = ld4(M0 + st);
+                const float4 m1 = ld4(M1 + st);
+                const L4 lc = *reinterpret_cast<const L4 *>(LC + st);
+                const unsigned sw = SG[(tE + ed.x) * 4 + wsel] >> sh;
 #pragma unroll
-            for (int v = 0; v < 4; v++) {
-                const float m0v = comp(m0, v);
-                const float mag = (ed.z == compl4(lc, v)) ? comp(m1, v) : fabsf(m0v);  // Obs. 1
-                const unsigned neg = ((comp(sw, v) >> lane) & 1u) ^ (__float_as_uint(m0v) >> 31) ^ corr;  // Obs. 2
-                acc[v] = acc[v] + (neg ? -mag : mag);
+                for (int v = 0; v < 4; v++) {
+                    const float m0v = comp(m0, v);
+                    const float mag = (ed.z == compl4(lc, v)) ? comp(m1, v) : fabsf(m0v);  // Obs. 1
+                    const unsigned neg = ((sw >> v) & 1u) ^ (__float_as_uint(m0v) >> 31);   // Obs. 2
+                    acc[v] = acc[v] + (neg ? -mag : mag);  // ascending rows from +0.0 (A14)
+                }
+            }
+        } else {
+            for (int q0 = 0; q0 < dv; q0 += BN_U) {
+                int4 ed[BN_U];
+                float4 m0[BN_U], m1[BN_U];
+                L4 lc[BN_U];
+                unsigned sw[BN_U];
+#pragma unroll
+                for (int u = 0; u < BN_U; u++)
+                    if (q0 + u < dv) ed[u] = __ldg(bn_edge + c0 + q0 + u);
+#pragma unroll
+                for (int u = 0; u < BN_U; u++) {
+                    if (q0 + u < dv) {
+                        const size_t st = (tm + ed[u].y) * TILE + 4 * lane;
+                        m0[u] = ld4(M0 + st);
+                        m1[u] = ld4(M1 + st);
+                        lc[u] = *reinterpret_cast<const L4 *>(LC + st);
+                        sw[u] = SG[(tE + ed[u].x) * 4 + wsel] >> sh;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < BN_U; u++) {
+                    if (q0 + u >= dv) break;
+#pragma unroll
+                    for (int v = 0; v < 4; v++) {
+                        const float m0v = comp(m0[u], v);
+                        const float mag = (ed[u].z == compl4(lc[u], v)) ? comp(m1[u], v) : fabsf(m0v);
+                        const unsigned neg = ((sw[u] >> v) & 1u) ^ (__float_as_uint(m0v) >> 31);
+                        acc[v] = acc[v] + (neg ? -mag : mag);
+                    }
+                }
             }
         }
-        const size_t sj = (tn + j) * TILE + 4 * lane;
-        const float4 rv = ld4(w.r + sj);
         float4 out = make_float4(acc[0] + rv.x, acc[1] + rv.y, acc[2] + rv.z, acc[3] + rv.w);
         if (mine == 0xFu) {
-            st4(w.s + sj, out);
+            st4(Sv + sj, out);
         } else if (mine) {
-            const float4 old = ld4(w.s + sj);
+            const float4 old = ld4(Sv + sj);
             out.x = (mine & 1u) ? out.x : old.x;
             out.y = (mine & 2u) ? out.y : old.y;
             out.z = (mine & 4u) ? out.z : old.z;
             out.w = (mine & 8u) ? out.w : old.w;
-            st4(w.s + sj, out);
+            st4(Sv + sj, out);
         }
     }
 }
@@ -400,32 +478,47 @@ int launch_stage_in(const Graph &g, const StreamState &w, const float *llr, int6
     return 1;
 }
 
+template <typename LT, bool F, bool EA>
+void cn_launch(dim3 grid, cudaStream_t st, const Graph &g, const StreamState &w, int k, int rpc, int lit, int u) {
+    if (u >= 4) k_cn<LT, F, EA, 4><<<grid, CTA, 0, st>>>(g, w, k, rpc, lit);
+    else if (u == 2) k_cn<LT, F, EA, 2><<<grid, CTA, 0, st>>>(g, w, k, rpc, lit);
+    else k_cn<LT, F, EA, 1><<<grid, CTA, 0, st>>>(g, w, k, rpc, lit);
+}
+
+template <typename LT, bool EA>
+void bn_launch(dim3 grid, cudaStream_t st, const Graph &g, const StreamState &w, int k, int cpc, int lit, int u) {
+    if (u >= 2) k_bn<LT, EA, 2><<<grid, CTA, 0, st>>>(g, w, k, cpc, lit);
+    else k_bn<LT, EA, 1><<<grid, CTA, 0, st>>>(g, w, k, cpc, lit);
+}
+
 int launch_check_node(const Graph &g, const StreamState &w, int k, bool first, bool early, bool literal, bool loc16,
                       const StreamLaunch &cfg, cudaStream_t st) {
     const dim3 grid = grid2((g.m + cfg.rows_per_cta - 1) / cfg.rows_per_cta, w.T);
-    const int lit = literal ? 1 : 0;
-#define CN_CASE(LT, F, EA) k_cn<LT, F, EA><<<grid, CTA, 0, st>>>(g, w, k, cfg.rows_per_cta, lit)
+    const int lit = literal ? 1 : 0, rpc = cfg.rows_per_cta, u = cfg.cn_unroll;
     if (loc16) {
-        if (first) { if (early) CN_CASE(uint16_t, true, true); else CN_CASE(uint16_t, true, false); }
-        else { if (early) CN_CASE(uint16_t, false, true); else CN_CASE(uint16_t, false, false); }
+        if (first) { if (early) cn_launch<uint16_t, true, true>(grid, st, g, w, k, rpc, lit, u);
+                     else cn_launch<uint16_t, true, false>(grid, st, g, w, k, rpc, lit, u); }
+        else { if (early) cn_launch<uint16_t, false, true>(grid, st, g, w, k, rpc, lit, u);
+               else cn_launch<uint16_t, false, false>(grid, st, g, w, k, rpc, lit, u); }
     } else {
-        if (first) { if (early) CN_CASE(uint8_t, true, true); else CN_CASE(uint8_t, true, false); }
-        else { if (early) CN_CASE(uint8_t, false, true); else CN_CASE(uint8_t, false, false); }
+        if (first) { if (early) cn_launch<uint8_t, true, true>(grid, st, g, w, k, rpc, lit, u);
+                     else cn_launch<uint8_t, true, false>(grid, st, g, w, k, rpc, lit, u); }
+        else { if (early) cn_launch<uint8_t, false, true>(grid, st, g, w, k, rpc, lit, u);
+               else cn_launch<uint8_t, false, false>(grid, st, g, w, k, rpc, lit, u); }
     }
-#undef CN_CASE
     return 1;
 }
 
 int launch_bit_node(const Graph &g, const StreamState &w, int k, bool early, bool literal, bool loc16,
                     const StreamLaunch &cfg, cudaStream_t st) {
     const dim3 grid = grid2((g.n + cfg.cols_per_cta - 1) / cfg.cols_per_cta, w.T);
-    const int lit = literal ? 1 : 0;
+    const int lit = literal ? 1 : 0, cpc = cfg.cols_per_cta, u = cfg.bn_unroll;
     if (loc16) {
-        if (early) k_bn<uint16_t, true><<<grid, CTA, 0, st>>>(g, w, k, cfg.cols_per_cta, lit);
-        else k_bn<uint16_t, false><<<grid, CTA, 0, st>>>(g, w, k, cfg.cols_per_cta, lit);
+        if (early) bn_launch<uint16_t, true>(grid, st, g, w, k, cpc, lit, u);
+        else bn_launch<uint16_t, false>(grid, st, g, w, k, cpc, lit, u);
     } else {
-        if (early) k_bn<uint8_t, true><<<grid, CTA, 0, st>>>(g, w, k, cfg.cols_per_cta, lit);
-        else k_bn<uint8_t, false><<<grid, CTA, 0, st>>>(g, w, k, cfg.cols_per_cta, lit);
+        if (early) bn_launch<uint8_t, true>(grid, st, g, w, k, cpc, lit, u);
+        else bn_launch<uint8_t, false>(grid, st, g, w, k, cpc, lit, u);
     }
     return 1;
 }

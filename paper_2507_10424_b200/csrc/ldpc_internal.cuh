@@ -61,6 +61,8 @@ struct HostGraph {  // device allocations owned by the plan
 struct StreamLaunch {
     int rows_per_cta = 32;
     int cols_per_cta = 32;
+    int cn_unroll = 1;  // check-node edges per load batch (1, 2, 4)
+    int bn_unroll = 1;  // bit-node edges per load batch (1, 2)
 };
 // Launch helpers; each returns the number of kernels launched.
 int launch_stage_in(const Graph &g, const StreamState &w, const float *llr, int64_t frames, cudaStream_t st);

@@ -231,6 +231,8 @@ int finish_prepare(ldpc_plan *p, int rc, uint32_t flags, ldpc_handle_t *out) {
     p->rp = plan_resident(p->g, p->g.max_row_deg > 255, p->device);
     if (const char *s = getenv("LDPC_ROWS_PER_CTA")) p->cfg.rows_per_cta = std::max(8, atoi(s));
     if (const char *s = getenv("LDPC_COLS_PER_CTA")) p->cfg.cols_per_cta = std::max(8, atoi(s));
+    if (const char *s = getenv("LDPC_CN_UNROLL")) p->cfg.cn_unroll = std::max(1, atoi(s));
+    if (const char *s = getenv("LDPC_BN_UNROLL")) p->cfg.bn_unroll = std::max(1, atoi(s));
     *out = p;
     return LDPC_OK;
 }
