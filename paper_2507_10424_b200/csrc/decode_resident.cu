@@ -2,21 +2,24 @@
 // time with the whole per-frame state in shared memory, and refills a frame slot the moment its
 // frame stops (per-frame early stop of Alg. 1, without batch-level waste).
 //
-// Per CTA, frame-interleaved over S slots (a lane owns 4 consecutive slots of one row or column):
+// Per CTA, frame-interleaved over S slots (a lane owns 4 consecutive slots of one row, edge or column):
+//   xe   [E][S]  fp32          lambda_e - eta_e, the check-node inputs, written by
+//                              the bit-node pass so the check node never rebuilds eta^prev
 //   s    [n][S]  fp32          soft vector (Eq. sCalculation)
 //   min0 [m][S]  fp32          Observation 1's minimum
 //   min1 [m][S]  fp32          Observation 1's second minimum
-//   lc   [m][S]  u16           min0Location, stored as the edge id inside the row lists (0xffff = none)
+//   lc   [m][S]  u32           min0Location, stored as the edge id inside the row lists (0xffff = none)
 //   par  [m]     S bits        the row's sign parity (Obs. 2) times (-1)^{d_i} (reading A1)
-//   sg   [E]     S bits        sign of lambda_e = s_j - eta_e for each slot
+//   sg   [E]     S bits        sign of lambda_e - eta_e for each slot
+//   hb   [n]     S bits        hard decision b_j = (s_j > 0) for the syndrome
 // plus the Tanner graph itself as 16-bit lists (N_i, M_j).  r lives in a global scratch
 // [CTA][n][S] (L2-resident) read once per column per body.  Loop per round:
 //   A  finish stopped slots (k, isCodeword, counters) and refill empty slots from a global counter
-//   B  stage new frames into their slots (s = r; eta^prev = 0 is applied by the next check-node pass)
-//   C  check-node pass over all rows + syndrome of b = slice(s) of every slot
-//   D  per slot: stop (codeword, or k = L) -> write b and s; else bit-node pass s = sum eta + r
-// Every sweep uses the same lane mapping (4 slots of one row/column per lane, 16-byte accesses), so
-// no sweep has shared-memory bank conflicts beyond the row/column gather itself.
+//   B  stage new frames into their slots (s = r, x_e = r_j, hard decisions of r)
+//   C  check-node pass over all rows (min0/min1/loc/parity/signs from x_e) + syndrome from hb words
+//   D  per slot: stop (codeword, or k = L) -> write b and s; else bit-node pass s = sum eta + r and
+//      the next x_e = s_j - eta_e (same fp32 subtraction as the oracle's lambda_k - eta^prev_{i,k})
+// Every sweep uses the same lane mapping (4 slots of one row/edge/column per lane, 16-byte accesses).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -50,23 +53,26 @@ struct SWord<32> {
 };
 
 struct Layout {
-    size_t s, m0, m1, lc, sg, par, rp, cp, col, rec, meta, total;
+    size_t xe, s, m0, m1, lc, sg, par, hb, rp, cp, col, rec, meta, total;
 };
 
 constexpr size_t a16(size_t x) { return (x + 15) & ~(size_t)15; }
 
 constexpr int META_INTS = 8 * 32 + 16;
+constexpr int DVMAX = 8;  // column degrees up to this keep their eta values in registers
 
 Layout layout_for(int S, int m, int n, int E) {
     Layout L{};
     size_t o = 0;
     const size_t swb = S <= 8 ? 1 : S / 8;
+    L.xe = o;   o = a16(o + (size_t)E * S * 4);
     L.s = o;    o = a16(o + (size_t)n * S * 4);
     L.m0 = o;   o = a16(o + (size_t)m * S * 4);
     L.m1 = o;   o = a16(o + (size_t)m * S * 4);
-    L.lc = o;   o = a16(o + (size_t)m * S * 2);
+    L.lc = o;   o = a16(o + (size_t)m * S * 4);
     L.sg = o;   o = a16(o + (size_t)E * swb);
     L.par = o;  o = a16(o + (size_t)m * swb);
+    L.hb = o;   o = a16(o + (size_t)n * swb);
     L.rp = o;   o = a16(o + (size_t)(m + 1) * 2);
     L.cp = o;   o = a16(o + (size_t)(n + 1) * 2);
     L.col = o;  o = a16(o + (size_t)E * 2);
@@ -103,92 +109,148 @@ __device__ __forceinline__ bool loc_ne(unsigned pair, unsigned e2, bool hi) {
     return ((pair ^ e2) & (hi ? 0xffff0000u : 0x0000ffffu)) != 0u;
 }
 
-// Check-node update of G rows (one per row group of the warp) for the 4 slots of this lane.
-// HAS: rows of the warp may have different degrees (irregular H), lanes past their degree idle.
-// fm: this lane's fresh slots (eta^prev = 0); nfw: S-bit word with the fresh slots' bits clear.
-template <int S, bool HAS>
-__device__ __forceinline__ void cn_rows(const float *s, float *mn0, float *mn1, uint16_t *lc,
-                                        typename SWord<S>::T *sg, typename SWord<S>::T *par,
-                                        const uint16_t *col, int i, bool valid, int ra, int d, int dmax,
-                                        int l, int sub, unsigned fm, unsigned nfw, unsigned corr_all,
-                                        unsigned &syn_acc) {
-    using SWT = typename SWord<S>::T;
+
+// 32-bit shared-window addresses: the hot loops address shared memory through plain registers
+// (no generic-to-shared conversion per access).
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ float4 lds_f4(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint4 lds_u4(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
+    uint16_t v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts_f4(uint32_t a, float4 v) {
+    asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
+__device__ __forceinline__ void sts_u4(uint32_t a, uint4 v) {
+    asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+template <int S>
+__device__ __forceinline__ uint32_t lds_sw(uint32_t a) {
+    return S == 32 ? lds_u32(a) : S == 16 ? lds_u16(a) : lds_u8(a);
+}
+template <int S>
+__device__ __forceinline__ void sts_sw(uint32_t a, uint32_t v) {
+    if (S == 32) asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+    else if (S == 16) asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((uint16_t)v) : "memory");
+    else asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+template <int S>
+constexpr int SWB() { return S <= 8 ? 1 : S / 8; }
+
+// S-bit word of a row group from the four per-component ballots: slot q = 4l+v sits at bit v*LR + l.
+template <int S>
+__device__ __forceinline__ unsigned gather_word(const unsigned bal[4], int sub) {
     constexpr int LR = S / 4;
     constexpr unsigned LMASK = (LR == 32) ? 0xffffffffu : ((1u << LR) - 1u);
+    unsigned word = 0;
+#pragma unroll
+    for (int v = 0; v < 4; v++) word |= ((bal[v] >> (sub * LR)) & LMASK) << (v * LR);
+    return word;
+}
+// this lane's 4 slot bits (bit v = slot 4l+v) of an S-bit word
+template <int S>
+__device__ __forceinline__ unsigned lane_bits(unsigned word, int l) {
+    constexpr int LR = S / 4;
+    return ((word >> l) & 1u) | (((word >> (LR + l)) & 1u) << 1) | (((word >> (2 * LR + l)) & 1u) << 2) |
+           (((word >> (3 * LR + l)) & 1u) << 3);
+}
+
+
+// Check-node update of one row per row group for the 4 slots of this lane, from x_e = lambda_e -
+// eta^prev_e: min0 / min0Location / min1 (Obs. 1), sign parity and sign bits (Obs. 2), plus the
+// row syndrome of b from the hard-decision words.  HAS: rows of the warp differ in degree.
+template <int S, bool HAS>
+__device__ __forceinline__ void cn_row(uint32_t SB, const Layout &lay, int i, bool valid, int ra, int d, int dmax,
+                                       int l, int sub, unsigned corr_all, unsigned &syn_acc) {
+    constexpr int SWBY = SWB<S>();
     const float INF = __int_as_float(0x7f800000);
     const int q0 = 4 * l;
-    float4 om0 = make_float4(0.f, 0.f, 0.f, 0.f), om1 = om0;
-    uint2 olc = make_uint2(0xffffffffu, 0xffffffffu);
-    unsigned P = 0;
-    const int ca = i * S + q0;
-    if (valid) {
-        om0 = *reinterpret_cast<const float4 *>(mn0 + ca);
-        om1 = *reinterpret_cast<const float4 *>(mn1 + ca);
-        olc = *reinterpret_cast<const uint2 *>(lc + ca);
-        P = (unsigned)par[i];
-        if (fm) {  // fresh slots start from eta = 0: min0 = min1 = +0, no location
-            if (fm & 1u) { om0.x = 0.f; om1.x = 0.f; olc.x |= 0x0000ffffu; }
-            if (fm & 2u) { om0.y = 0.f; om1.y = 0.f; olc.x |= 0xffff0000u; }
-            if (fm & 4u) { om0.z = 0.f; om1.z = 0.f; olc.y |= 0x0000ffffu; }
-            if (fm & 8u) { om0.w = 0.f; om1.w = 0.f; olc.y |= 0xffff0000u; }
-        }
-    }
-    unsigned mv[4];
-#pragma unroll
-    for (int v = 0; v < 4; v++) mv[v] = 1u << (v * LR + l);
+    const uint32_t XE = SB + (uint32_t)lay.xe, SG = SB + (uint32_t)lay.sg, HB = SB + (uint32_t)lay.hb,
+                   COL = SB + (uint32_t)lay.col;
     float nm0[4] = {INF, INF, INF, INF}, nm1[4] = {INF, INF, INF, INF};
     int nloc[4] = {0xffff, 0xffff, 0xffff, 0xffff};
     unsigned parw[4] = {0, 0, 0, 0};
-    unsigned syn = 0;
+    unsigned synw = 0;
 #pragma unroll 2
     for (int p = 0; p < dmax; p++) {
         const bool has = HAS ? (p < d) : true;
         const int e = ra + p;
-        const unsigned e2 = (unsigned)e * 0x10001u;
-        const int j = has ? col[e] : 0;
-        const float4 sv = *reinterpret_cast<const float4 *>(s + j * S + q0);
-        // own sign of lambda^prev xor the row parity (Obs. 2, A1 folded in); fresh slots: +
-        const unsigned W = ((has ? (unsigned)sg[e] : 0u) ^ P) & nfw;
+        float4 xv = make_float4(INF, INF, INF, INF);
+        if (has) {
+            xv = lds_f4(XE + (uint32_t)((e * S + q0) * 4));
+            synw ^= lds_sw<S>(HB + lds_u16(COL + 2u * (uint32_t)e) * SWBY);  // b_j = slice(s_j)
+        }
         unsigned bal[4];
 #pragma unroll
         for (int v = 0; v < 4; v++) {
-            const float sj = f4c(sv, v);
-            const float mag = loc_ne(v < 2 ? olc.x : olc.y, e2, v & 1) ? f4c(om0, v) : f4c(om1, v);  // Obs. 1
-            const float x = sj - ((W & mv[v]) ? -mag : mag);  // lambda - eta^prev
-            const float ax = HAS ? (has ? fabsf(x) : INF) : fabsf(x);
+            const float x = f4c(xv, v);
+            const float ax = fabsf(x);
             const bool lt = ax < nm0[v];  // first strict minimum (A13)
             nm1[v] = fminf(nm1[v], fmaxf(nm0[v], ax));
             nm0[v] = fminf(nm0[v], ax);
             nloc[v] = lt ? e : nloc[v];
-            bal[v] = __ballot_sync(FULLM, (HAS ? has : true) && x < 0.f);  // sign(0) = +1
-            syn ^= (unsigned)((HAS ? has : true) && sj > 0.f) << v;        // b_j = slice(s_j)
+            bal[v] = __ballot_sync(FULLM, x < 0.f);  // sign(0) = +1; INF is +
         }
 #pragma unroll
         for (int v = 0; v < 4; v++) parw[v] ^= bal[v];
-        if (has && l == 0) {
-            unsigned word = 0;
-#pragma unroll
-            for (int v = 0; v < 4; v++) word |= ((bal[v] >> (sub * LR)) & LMASK) << (v * LR);
-            sg[e] = (SWT)word;
-        }
+        if (has && l == 0) sts_sw<S>(SG + (uint32_t)(e * SWBY), gather_word<S>(bal, sub));
     }
     if (valid) {
-        *reinterpret_cast<float4 *>(mn0 + ca) = make_float4(nm0[0], nm0[1], nm0[2], nm0[3]);
-        *reinterpret_cast<float4 *>(mn1 + ca) = make_float4(nm1[0], nm1[1], nm1[2], nm1[3]);
-        *reinterpret_cast<uint2 *>(lc + ca) = make_uint2((unsigned)nloc[0] | ((unsigned)nloc[1] << 16),
-                                                         (unsigned)nloc[2] | ((unsigned)nloc[3] << 16));
-        if (l == 0) {
-            unsigned word = 0;
-#pragma unroll
-            for (int v = 0; v < 4; v++) word |= ((parw[v] >> (sub * LR)) & LMASK) << (v * LR);
-            par[i] = (SWT)(word ^ ((d & 1) ? corr_all : 0u));  // (-1)^{d_i}, reading A1
-        }
-        syn_acc |= syn;
+        const uint32_t ca = (uint32_t)((i * S + q0) * 4);
+        sts_f4(SB + (uint32_t)lay.m0 + ca, make_float4(nm0[0], nm0[1], nm0[2], nm0[3]));
+        sts_f4(SB + (uint32_t)lay.m1 + ca, make_float4(nm1[0], nm1[1], nm1[2], nm1[3]));
+        sts_u4(SB + (uint32_t)lay.lc + ca, make_uint4(nloc[0], nloc[1], nloc[2], nloc[3]));
+        if (l == 0)
+            sts_sw<S>(SB + (uint32_t)lay.par + (uint32_t)(i * SWBY),
+                      gather_word<S>(parw, sub) ^ ((d & 1) ? corr_all : 0u));  // (-1)^{d_i}, reading A1
+        syn_acc |= lane_bits<S>(synw, l);
     }
 }
 
-// Lane layout: a lane owns 4 consecutive slots (float4) of one row or column; LR = S/4 lanes cover a
-// row, G = 32/LR rows per warp.  Bit of slot q = 4*l + v inside an S-bit sign word: v*LR + l.
+// eta_{i,j} of one column edge (record rc = e << 16 | i) for the 4 slots of this lane (Obs. 1/2)
+template <int S>
+__device__ __forceinline__ void eta_of(uint32_t SB, const Layout &lay, uint32_t rc, int q0, const unsigned mv[4],
+                                       float et[4]) {
+    constexpr int SWBY = SWB<S>();
+    const int e = (int)(rc >> 16), i = (int)(rc & 0xffffu);
+    const uint32_t ca = (uint32_t)((i * S + q0) * 4);
+    const float4 m0 = lds_f4(SB + (uint32_t)lay.m0 + ca);
+    const float4 m1 = lds_f4(SB + (uint32_t)lay.m1 + ca);
+    const uint4 lv = lds_u4(SB + (uint32_t)lay.lc + ca);
+    const unsigned W = lds_sw<S>(SB + (uint32_t)lay.sg + (uint32_t)(e * SWBY)) ^
+                       lds_sw<S>(SB + (uint32_t)lay.par + (uint32_t)(i * SWBY));
+    const float mg0 = ((int)lv.x == e) ? m1.x : m0.x;
+    const float mg1 = ((int)lv.y == e) ? m1.y : m0.y;
+    const float mg2 = ((int)lv.z == e) ? m1.z : m0.z;
+    const float mg3 = ((int)lv.w == e) ? m1.w : m0.w;
+    et[0] = (W & mv[0]) ? -mg0 : mg0;
+    et[1] = (W & mv[1]) ? -mg1 : mg1;
+    et[2] = (W & mv[2]) ? -mg2 : mg2;
+    et[3] = (W & mv[3]) ? -mg3 : mg3;
+}
+
+// Lane layout: a lane owns 4 consecutive slots (float4) of one row, edge or column; LR = S/4 lanes
+// cover a row, G = 32/LR rows per warp.  Bit of slot q = 4*l + v inside an S-bit word: v*LR + l.
 template <int S, int RT>
 __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
     constexpr int NWARP = RT / 32;
@@ -197,12 +259,13 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
     constexpr int G = 32 / LR;
     extern __shared__ __align__(16) unsigned char sm[];
     const int m = a.g.m, n = a.g.n, E = a.g.E;
+    float *xe = reinterpret_cast<float *>(sm + a.lay.xe);
     float *s = reinterpret_cast<float *>(sm + a.lay.s);
     float *mn0 = reinterpret_cast<float *>(sm + a.lay.m0);
     float *mn1 = reinterpret_cast<float *>(sm + a.lay.m1);
-    uint16_t *lc = reinterpret_cast<uint16_t *>(sm + a.lay.lc);
     SWT *sg = reinterpret_cast<SWT *>(sm + a.lay.sg);
     SWT *par = reinterpret_cast<SWT *>(sm + a.lay.par);
+    SWT *hb = reinterpret_cast<SWT *>(sm + a.lay.hb);
     uint16_t *rp = reinterpret_cast<uint16_t *>(sm + a.lay.rp);
     uint16_t *cp = reinterpret_cast<uint16_t *>(sm + a.lay.cp);
     uint16_t *col = reinterpret_cast<uint16_t *>(sm + a.lay.col);
@@ -215,6 +278,7 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
     int *slot_nz = meta + 128;     // some |s_j| <= 1e-4
     unsigned *ctl = reinterpret_cast<unsigned *>(meta + 256);  // [0] unsat, [1] new, [2] active, [3] exhausted
 
+    const uint32_t SB = smem_u32(sm);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int sub = lane / LR, l = lane % LR;  // row group inside the warp, lane inside the row
     const int q0 = 4 * l;                      // first slot of this lane
@@ -243,6 +307,9 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
         ctl[3] = 0;
     }
     unsigned long long acc_stats[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // warp 0, lane = slot
+    unsigned mv[4];
+#pragma unroll
+    for (int v = 0; v < 4; v++) mv[v] = 1u << (v * LR + l);
     __syncthreads();
 
     for (;;) {
@@ -305,31 +372,52 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
         __syncthreads();
         const unsigned active = ctl[2], fresh_new = ctl[1];
         if (!active) break;
-        const unsigned fm = (fresh_new >> q0) & 0xfu;  // this lane's fresh slots
 
-        // ---------------- B: stage new frames, s = r: column sweep in the float4 layout
+        // ---------------- B: stage new frames: s = r, lambda_e - eta_e = r (eta = 0),
+        //                     hard decisions of r for the pre-loop test
         if (fresh_new) {
+            const unsigned fm = (fresh_new >> q0) & 0xfu;  // this lane's fresh slots
+            SWT fw = 0;                                     // S-bit word of the fresh slots
+#pragma unroll
+            for (int q = 0; q < S; q++)
+                if ((fresh_new >> q) & 1u) fw |= (SWT)(1u << ((q & 3) * LR + (q >> 2)));
             int fr[4];
 #pragma unroll
             for (int v = 0; v < 4; v++) fr[v] = slot_f[q0 + v];
             int raw[4] = {0, 0, 0, 0};
-            for (int cb = warp * G; cb < n && fm; cb += NWARP * G) {
+            for (int cb = warp * G; cb < n; cb += NWARP * G) {
                 const int j = cb + sub;
-                if (j >= n) continue;
-                float *sp = s + j * S + q0;
-                float4 o = *reinterpret_cast<const float4 *>(sp);
+                const bool jv = j < n;
+                float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (jv && fm) {
+                    float *sp = s + j * S + q0;
+                    o = *reinterpret_cast<const float4 *>(sp);
 #pragma unroll
-                for (int v = 0; v < 4; v++) {
-                    if ((fm >> v) & 1u) {
-                        const float x = __ldg(a.llr + (int64_t)fr[v] * n + j);
-                        f4s(o, v, x);
-                        rs[(size_t)j * S + q0 + v] = x;
-                        raw[v] += x > 0.f;
+                    for (int v = 0; v < 4; v++) {
+                        if ((fm >> v) & 1u) {
+                            const float x = __ldg(a.llr + (int64_t)fr[v] * n + j);
+                            f4s(o, v, x);
+                            rs[(size_t)j * S + q0 + v] = x;
+                            raw[v] += x > 0.f;
+                        }
+                    }
+                    *reinterpret_cast<float4 *>(sp) = o;
+                    const int c0 = cp[j], dv = (int)cp[j + 1] - c0;
+                    for (int qq = 0; qq < dv; qq++) {
+                        const int e = (int)(rec[c0 + qq] >> 16);
+                        float *xp = xe + e * S + q0;
+                        float4 xo = *reinterpret_cast<const float4 *>(xp);
+#pragma unroll
+                        for (int v = 0; v < 4; v++)
+                            if ((fm >> v) & 1u) f4s(xo, v, f4c(o, v));
+                        *reinterpret_cast<float4 *>(xp) = xo;
                     }
                 }
-                *reinterpret_cast<float4 *>(sp) = o;
+                unsigned bal[4];
+#pragma unroll
+                for (int v = 0; v < 4; v++) bal[v] = __ballot_sync(FULLM, jv && f4c(o, v) > 0.f);
+                if (jv && l == 0) hb[j] = (SWT)(((unsigned)hb[j] & ~(unsigned)fw) | (gather_word<S>(bal, sub) & fw));
             }
-            // per-slot counts: reduce over the row groups of the warp, then one atomic per slot
 #pragma unroll
             for (int v = 0; v < 4; v++) {
                 int x = raw[v];
@@ -339,12 +427,8 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
             __syncthreads();
         }
 
-        // ---------------- C: check-node pass + syndrome of b = slice(s)
+        // ---------------- C: check-node pass over x_e = s_j - eta^prev_e + syndrome of b
         {
-            SWT nfw = 0;
-#pragma unroll
-            for (int q = 0; q < S; q++)
-                if (!((fresh_new >> q) & 1u)) nfw |= (SWT)(1u << ((q & 3) * LR + (q >> 2)));
             unsigned syn_acc = 0;  // bit v: slot q0+v has an unsatisfied check
             for (int rb = warp * G; rb < m; rb += NWARP * G) {
                 const int i = rb + sub;
@@ -353,11 +437,9 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
                 const int d = valid ? (int)rp[i + 1] - ra : 0;
                 const int dmax = __reduce_max_sync(FULLM, d);
                 if (__all_sync(FULLM, d == dmax))
-                    cn_rows<S, false>(s, mn0, mn1, lc, sg, par, col, i, valid, ra, d, dmax, l, sub, fm, nfw, corr_all,
-                                      syn_acc);
+                    cn_row<S, false>(SB, a.lay, i, valid, ra, d, dmax, l, sub, corr_all, syn_acc);
                 else
-                    cn_rows<S, true>(s, mn0, mn1, lc, sg, par, col, i, valid, ra, d, dmax, l, sub, fm, nfw, corr_all,
-                                     syn_acc);
+                    cn_row<S, true>(SB, a.lay, i, valid, ra, d, dmax, l, sub, corr_all, syn_acc);
             }
             const unsigned mine = (syn_acc << q0) & active;
             const unsigned wmask = __reduce_or_sync(FULLM, mine);
@@ -365,8 +447,8 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
         }
         __syncthreads();
 
-        // ---------------- D: per-slot decision; outputs of stopping slots and bit-node update of the
-        //                     continuing ones in one column sweep
+        // ---------------- D: per-slot decision; outputs of stopping slots and the bit-node update
+        //                     (Eq. lambda_j) of the continuing ones in one column sweep
         {
             const unsigned uns_all = ctl[0];
             bool fin = false, cont = false;
@@ -385,15 +467,12 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
                 for (int v = 0; v < 4; v++) fo[v] = (int64_t)slot_f[q0 + v] * n;
                 int be[4] = {0, 0, 0, 0};
                 unsigned nz = 0;
-                unsigned mv[4];
-#pragma unroll
-                for (int v = 0; v < 4; v++) mv[v] = 1u << (v * LR + l);
                 for (int cb = warp * G; cb < n; cb += NWARP * G) {
                     const int j = cb + sub;
-                    if (j >= n || !(cm | fk)) continue;
-                    float *sp = s + j * S + q0;
-                    float4 o = *reinterpret_cast<const float4 *>(sp);
-                    if (fk) {
+                    const bool jv = j < n;
+                    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (jv && fk) {
+                        o = *reinterpret_cast<const float4 *>(s + j * S + q0);
 #pragma unroll
                         for (int v = 0; v < 4; v++) {
                             if ((fk >> v) & 1u) {
@@ -406,32 +485,53 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
                             }
                         }
                     }
-                    if (cm) {
+                    const bool work = jv && cm;
+                    if (work) {
                         const float4 rj = *reinterpret_cast<const float4 *>(rs + (size_t)j * S + q0);
                         const int c0 = cp[j], dv = (int)cp[j + 1] - c0;
                         float acc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 2
-                        for (int qq = 0; qq < dv; qq++) {
-                            const uint32_t rc = rec[c0 + qq];
-                            const int e = (int)(rc >> 16), i = (int)(rc & 0xffffu);
-                            const unsigned e2 = (unsigned)e * 0x10001u;
-                            const int ca = i * S + q0;
-                            const float4 m0 = *reinterpret_cast<const float4 *>(mn0 + ca);
-                            const float4 m1 = *reinterpret_cast<const float4 *>(mn1 + ca);
-                            const uint2 lv = *reinterpret_cast<const uint2 *>(lc + ca);
-                            const unsigned W = (unsigned)sg[e] ^ (unsigned)par[i];
+                        float eta[DVMAX][4];
+                        int ee[DVMAX];
 #pragma unroll
-                            for (int v = 0; v < 4; v++) {
-                                const float mag = loc_ne(v < 2 ? lv.x : lv.y, e2, v & 1) ? f4c(m0, v) : f4c(m1, v);
-                                acc[v] = acc[v] + ((W & mv[v]) ? -mag : mag);  // ascending rows from +0.0 (A14)
+                        for (int qq = 0; qq < DVMAX; qq++) {
+                            if (qq < dv) {
+                                const uint32_t rc = rec[c0 + qq];
+                                ee[qq] = (int)(rc >> 16);
+                                eta_of<S>(SB, a.lay, rc, q0, mv, eta[qq]);
+#pragma unroll
+                                for (int v = 0; v < 4; v++) acc[v] = acc[v] + eta[qq][v];  // ascending rows (A14)
                             }
                         }
-                        if (cm & 1u) o.x = acc[0] + rj.x;
-                        if (cm & 2u) o.y = acc[1] + rj.y;
-                        if (cm & 4u) o.z = acc[2] + rj.z;
-                        if (cm & 8u) o.w = acc[3] + rj.w;
-                        *reinterpret_cast<float4 *>(sp) = o;
+                        for (int qq = DVMAX; qq < dv; qq++) {
+                            float et[4];
+                            eta_of<S>(SB, a.lay, rec[c0 + qq], q0, mv, et);
+#pragma unroll
+                            for (int v = 0; v < 4; v++) acc[v] = acc[v] + et[v];
+                        }
+                        float4 sn = make_float4(acc[0] + rj.x, acc[1] + rj.y, acc[2] + rj.z, acc[3] + rj.w);
+                        sts_f4(SB + (uint32_t)a.lay.s + (uint32_t)((j * S + q0) * 4), sn);
+                        // extrinsic values for the next check-node pass: x_e = s_j - eta_e
+#pragma unroll
+                        for (int qq = 0; qq < DVMAX; qq++) {
+                            if (qq < dv)
+                                sts_f4(SB + (uint32_t)a.lay.xe + (uint32_t)((ee[qq] * S + q0) * 4),
+                                       make_float4(sn.x - eta[qq][0], sn.y - eta[qq][1], sn.z - eta[qq][2],
+                                                   sn.w - eta[qq][3]));
+                        }
+                        for (int qq = DVMAX; qq < dv; qq++) {
+                            const uint32_t rc = rec[c0 + qq];
+                            float et[4];
+                            eta_of<S>(SB, a.lay, rc, q0, mv, et);
+                            sts_f4(SB + (uint32_t)a.lay.xe + (uint32_t)(((int)(rc >> 16) * S + q0) * 4),
+                                   make_float4(sn.x - et[0], sn.y - et[1], sn.z - et[2], sn.w - et[3]));
+                        }
+                        o = sn;
                     }
+                    // hard decisions of the new s for the next syndrome (continuing slots only matter)
+                    unsigned bal[4];
+#pragma unroll
+                    for (int v = 0; v < 4; v++) bal[v] = __ballot_sync(FULLM, work && f4c(o, v) > 0.f);
+                    if (jv && l == 0 && cont_mask) hb[j] = (SWT)gather_word<S>(bal, sub);
                 }
                 if (fin_mask) {
 #pragma unroll
@@ -478,6 +578,7 @@ void launch_s(const ResArgs &args, int ctas, size_t smem, cudaStream_t st) {
 template <int S>
 void launch_t(const ResArgs &args, int threads, int ctas, size_t smem, cudaStream_t st) {
     if (threads == 1024) launch_s<S, 1024>(args, ctas, smem, st);
+    else if (threads == 768) launch_s<S, 768>(args, ctas, smem, st);
     else launch_s<S, 512>(args, ctas, smem, st);
 }
 
@@ -497,7 +598,10 @@ ResidentPlan plan_resident(const HostGraph &g, bool loc16, int device) {
             rp.ok = true;
             rp.slots = S;
             rp.threads = 512;
-            if (const char *e = getenv("LDPC_RES_THREADS")) rp.threads = atoi(e) == 1024 ? 1024 : 512;
+            if (const char *e = getenv("LDPC_RES_THREADS")) {
+                const int t = atoi(e);
+                rp.threads = (t == 1024 || t == 768) ? t : 512;
+            }
             rp.smem = L.total;
             rp.ctas = sms;
             return rp;
