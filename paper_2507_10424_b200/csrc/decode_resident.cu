@@ -3,22 +3,19 @@
 // frame stops (per-frame early stop of Alg. 1, without batch-level waste).
 //
 // Per CTA, frame-interleaved over S slots (a lane owns 4 consecutive slots of one row, edge or column):
-//   xe   [E][S]  fp32          lambda_e - eta_e, the check-node inputs, written by
-//                              the bit-node pass so the check node never rebuilds eta^prev
-//   s    [n][S]  fp32          soft vector (Eq. sCalculation)
-//   min0 [m][S]  fp32          Observation 1's minimum
-//   min1 [m][S]  fp32          Observation 1's second minimum
-//   lc   [m][S]  u32           min0Location, stored as the edge id inside the row lists (0xffff = none)
-//   par  [m]     S bits        the row's sign parity (Obs. 2) times (-1)^{d_i} (reading A1)
-//   sg   [E]     S bits        sign of lambda_e - eta_e for each slot
-//   hb   [n]     S bits        hard decision b_j = (s_j > 0) for the syndrome
-// plus the Tanner graph itself as 16-bit lists (N_i, M_j).  r lives in a global scratch
-// [CTA][n][S] (L2-resident) read once per column per body.  Loop per round:
+//   xe [E][S] fp32   the per-edge message of the paper's map-reduce form (Alg. 2) restricted
+//                    to the edges of H: it holds lambda(i,j) = s(j) - eta(i,j) before the
+//                    check-node pass and eta(i,j) (Eq. etaCalculation) after it
+//   s  [n][S] fp32   soft vector (Eq. sCalculation)
+//   hb [n]    S bits hard decision b_j = (s_j > 0) (Eq. slice) for the syndrome
+// plus the Tanner graph as 16-bit lists (N_i, M_j); r lives in an L2-resident global scratch
+// [CTA][n][S] read once per column per body.  Loop per round:
 //   A  finish stopped slots (k, isCodeword, counters) and refill empty slots from a global counter
-//   B  stage new frames into their slots (s = r, x_e = r_j, hard decisions of r)
-//   C  check-node pass over all rows (min0/min1/loc/parity/signs from x_e) + syndrome from hb words
-//   D  per slot: stop (codeword, or k = L) -> write b and s; else bit-node pass s = sum eta + r and
-//      the next x_e = s_j - eta_e (same fp32 subtraction as the oracle's lambda_k - eta^prev_{i,k})
+//   B  stage new frames into their slots (s = r, lambda = r on every edge, hard decisions of r)
+//   C  check-node pass over all rows: reduce lambda to min0/min0Location/min1/parity (Obs. 1/2), then
+//      write eta in place; the same pass XORs the hard decisions of the row into the syndrome
+//   D  per slot: stop (codeword, or k = L) -> write b and s; else column sums s = sum eta + r and the
+//      next lambda = s - eta (fp32, ascending rows from +0.0 then + r, reading A14)
 // Every sweep uses the same lane mapping (4 slots of one row/edge/column per lane, 16-byte accesses).
 #include <cuda_runtime.h>
 
@@ -53,30 +50,25 @@ struct SWord<32> {
 };
 
 struct Layout {
-    size_t xe, s, m0, m1, lc, sg, par, hb, rp, cp, col, rec, meta, total;
+    size_t xe, s, hb, rp, rb, cp, col, ce, meta, total;
 };
 
 constexpr size_t a16(size_t x) { return (x + 15) & ~(size_t)15; }
 
 constexpr int META_INTS = 8 * 32 + 16;
-constexpr int DVMAX = 8;  // column degrees up to this keep their eta values in registers
 
 Layout layout_for(int S, int m, int n, int E) {
     Layout L{};
     size_t o = 0;
     const size_t swb = S <= 8 ? 1 : S / 8;
-    L.xe = o;   o = a16(o + (size_t)E * S * 4);
+    L.xe = o;   o = a16(o + (size_t)(E + m) * S * 4);  // edge blocks, rows padded to an odd length
     L.s = o;    o = a16(o + (size_t)n * S * 4);
-    L.m0 = o;   o = a16(o + (size_t)m * S * 4);
-    L.m1 = o;   o = a16(o + (size_t)m * S * 4);
-    L.lc = o;   o = a16(o + (size_t)m * S * 4);
-    L.sg = o;   o = a16(o + (size_t)E * swb);
-    L.par = o;  o = a16(o + (size_t)m * swb);
     L.hb = o;   o = a16(o + (size_t)n * swb);
     L.rp = o;   o = a16(o + (size_t)(m + 1) * 2);
+    L.rb = o;   o = a16(o + (size_t)(m + 1) * 2);
     L.cp = o;   o = a16(o + (size_t)(n + 1) * 2);
     L.col = o;  o = a16(o + (size_t)E * 2);
-    L.rec = o;  o = a16(o + (size_t)E * 4);
+    L.ce = o;   o = a16(o + (size_t)E * 2);
     L.meta = o; o = a16(o + (size_t)META_INTS * 4 + 8 * 8);
     L.total = o;
     return L;
@@ -104,58 +96,6 @@ __device__ __forceinline__ void f4s(float4 &a, int v, float x) {
     else if (v == 2) a.z = x;
     else a.w = x;
 }
-// min0Location test on two packed 16-bit edge ids: true iff the half selected by `hi` differs from e
-__device__ __forceinline__ bool loc_ne(unsigned pair, unsigned e2, bool hi) {
-    return ((pair ^ e2) & (hi ? 0xffff0000u : 0x0000ffffu)) != 0u;
-}
-
-
-// 32-bit shared-window addresses: the hot loops address shared memory through plain registers
-// (no generic-to-shared conversion per access).
-__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ float4 lds_f4(uint32_t a) {
-    float4 v;
-    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ uint4 lds_u4(uint32_t a) {
-    uint4 v;
-    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
-    uint32_t v;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
-    uint16_t v;
-    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
-    uint32_t v;
-    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ void sts_f4(uint32_t a, float4 v) {
-    asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
-}
-__device__ __forceinline__ void sts_u4(uint32_t a, uint4 v) {
-    asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
-}
-template <int S>
-__device__ __forceinline__ uint32_t lds_sw(uint32_t a) {
-    return S == 32 ? lds_u32(a) : S == 16 ? lds_u16(a) : lds_u8(a);
-}
-template <int S>
-__device__ __forceinline__ void sts_sw(uint32_t a, uint32_t v) {
-    if (S == 32) asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
-    else if (S == 16) asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((uint16_t)v) : "memory");
-    else asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
-}
-template <int S>
-constexpr int SWB() { return S <= 8 ? 1 : S / 8; }
 
 // S-bit word of a row group from the four per-component ballots: slot q = 4l+v sits at bit v*LR + l.
 template <int S>
@@ -175,32 +115,23 @@ __device__ __forceinline__ unsigned lane_bits(unsigned word, int l) {
            (((word >> (3 * LR + l)) & 1u) << 3);
 }
 
-
-// Check-node update of one row per row group for the 4 slots of this lane, from x_e = lambda_e -
-// eta^prev_e: min0 / min0Location / min1 (Obs. 1), sign parity and sign bits (Obs. 2), plus the
-// row syndrome of b from the hard-decision words.  HAS: rows of the warp differ in degree.
+// Check-node update of one row per row group for the 4 slots of this lane (Eq. etaCalculation,
+// P:327-336).  Pass 1 reduces lambda(i,j) of the row to min0, min0Location, min1 (Obs. 1) and the sign
+// parity (Obs. 2) -- the paper's four vectors -- and XORs the row's hard decisions into the
+// syndrome.  Pass 2 overwrites lambda(i,j) with eta(i,j) in place.  HAS: rows of the warp differ in degree.
 template <int S, bool HAS>
-__device__ __forceinline__ void cn_row(uint32_t SB, const Layout &lay, int i, bool valid, int ra, int d, int dmax,
-                                       int l, int sub, unsigned corr_all, unsigned &syn_acc) {
-    constexpr int SWBY = SWB<S>();
+__device__ __forceinline__ void cn_row(float *xe, const uint16_t *col, const typename SWord<S>::T *hb, int i,
+                                       bool valid, int ra, int xb, int d, int dmax, int l, int lane,
+                                       bool corr_lit, unsigned &syn_acc) {
+    constexpr int DR = 8;  // row degrees up to DR keep lambda in registers between the two passes
     const float INF = __int_as_float(0x7f800000);
     const int q0 = 4 * l;
-    const uint32_t XE = SB + (uint32_t)lay.xe, SG = SB + (uint32_t)lay.sg, HB = SB + (uint32_t)lay.hb,
-                   COL = SB + (uint32_t)lay.col;
     float nm0[4] = {INF, INF, INF, INF}, nm1[4] = {INF, INF, INF, INF};
-    int nloc[4] = {0xffff, 0xffff, 0xffff, 0xffff};
+    int nloc[4] = {-1, -1, -1, -1};
     unsigned parw[4] = {0, 0, 0, 0};
     unsigned synw = 0;
-#pragma unroll 2
-    for (int p = 0; p < dmax; p++) {
-        const bool has = HAS ? (p < d) : true;
-        const int e = ra + p;
-        float4 xv = make_float4(INF, INF, INF, INF);
-        if (has) {
-            xv = lds_f4(XE + (uint32_t)((e * S + q0) * 4));
-            synw ^= lds_sw<S>(HB + lds_u16(COL + 2u * (uint32_t)e) * SWBY);  // b_j = slice(s_j)
-        }
-        unsigned bal[4];
+    float4 xr[DR];
+    auto scan = [&](int p, float4 xv) {
 #pragma unroll
         for (int v = 0; v < 4; v++) {
             const float x = f4c(xv, v);
@@ -208,45 +139,61 @@ __device__ __forceinline__ void cn_row(uint32_t SB, const Layout &lay, int i, bo
             const bool lt = ax < nm0[v];  // first strict minimum (A13)
             nm1[v] = fminf(nm1[v], fmaxf(nm0[v], ax));
             nm0[v] = fminf(nm0[v], ax);
-            nloc[v] = lt ? e : nloc[v];
-            bal[v] = __ballot_sync(FULLM, x < 0.f);  // sign(0) = +1; INF is +
+            nloc[v] = lt ? p : nloc[v];
+            parw[v] ^= __ballot_sync(FULLM, x < 0.f);  // sign(0) = +1; INF is +
         }
+    };
+    const bool small = dmax <= DR;
+    if (small) {
 #pragma unroll
-        for (int v = 0; v < 4; v++) parw[v] ^= bal[v];
-        if (has && l == 0) sts_sw<S>(SG + (uint32_t)(e * SWBY), gather_word<S>(bal, sub));
+        for (int p = 0; p < DR; p++) {
+            if (p < dmax) {
+                const bool has = HAS ? (p < d) : true;
+                xr[p] = make_float4(INF, INF, INF, INF);
+                if (has) {
+                    xr[p] = *reinterpret_cast<const float4 *>(xe + (xb + p) * S + q0);
+                    synw ^= (unsigned)hb[col[ra + p]];  // b_j = slice(s_j)
+                }
+                scan(p, xr[p]);
+            }
+        }
+    } else {
+        for (int p = 0; p < dmax; p++) {
+            const bool has = HAS ? (p < d) : true;
+            float4 xv = make_float4(INF, INF, INF, INF);
+            if (has) {
+                xv = *reinterpret_cast<const float4 *>(xe + (xb + p) * S + q0);
+                synw ^= (unsigned)hb[col[ra + p]];
+            }
+            scan(p, xv);
+        }
     }
     if (valid) {
-        const uint32_t ca = (uint32_t)((i * S + q0) * 4);
-        sts_f4(SB + (uint32_t)lay.m0 + ca, make_float4(nm0[0], nm0[1], nm0[2], nm0[3]));
-        sts_f4(SB + (uint32_t)lay.m1 + ca, make_float4(nm1[0], nm1[1], nm1[2], nm1[3]));
-        sts_u4(SB + (uint32_t)lay.lc + ca, make_uint4(nloc[0], nloc[1], nloc[2], nloc[3]));
-        if (l == 0)
-            sts_sw<S>(SB + (uint32_t)lay.par + (uint32_t)(i * SWBY),
-                      gather_word<S>(parw, sub) ^ ((d & 1) ? corr_all : 0u));  // (-1)^{d_i}, reading A1
+        // row parity of this lane's slots, times (-1)^{d_i} (reading A1)
+        const unsigned flip = (corr_lit && (d & 1)) ? 1u : 0u;
+        unsigned pv[4];
+#pragma unroll
+        for (int v = 0; v < 4; v++) pv[v] = ((parw[v] >> lane) & 1u) ^ flip;
+        auto emit = [&](int p, float4 xv) {
+            float4 o;
+#pragma unroll
+            for (int v = 0; v < 4; v++) {
+                const float x = f4c(xv, v);
+                const float mag = (p == nloc[v]) ? nm1[v] : nm0[v];       // Obs. 1 (delta placement, A2)
+                const bool neg = ((unsigned)(x < 0.f) ^ pv[v]) != 0u;    // Obs. 2: parity x own sign
+                f4s(o, v, neg ? -mag : mag);
+            }
+            *reinterpret_cast<float4 *>(xe + (xb + p) * S + q0) = o;
+        };
+        if (small) {
+#pragma unroll
+            for (int p = 0; p < DR; p++)
+                if (p < d) emit(p, xr[p]);
+        } else {
+            for (int p = 0; p < d; p++) emit(p, *reinterpret_cast<const float4 *>(xe + (xb + p) * S + q0));
+        }
         syn_acc |= lane_bits<S>(synw, l);
     }
-}
-
-// eta_{i,j} of one column edge (record rc = e << 16 | i) for the 4 slots of this lane (Obs. 1/2)
-template <int S>
-__device__ __forceinline__ void eta_of(uint32_t SB, const Layout &lay, uint32_t rc, int q0, const unsigned mv[4],
-                                       float et[4]) {
-    constexpr int SWBY = SWB<S>();
-    const int e = (int)(rc >> 16), i = (int)(rc & 0xffffu);
-    const uint32_t ca = (uint32_t)((i * S + q0) * 4);
-    const float4 m0 = lds_f4(SB + (uint32_t)lay.m0 + ca);
-    const float4 m1 = lds_f4(SB + (uint32_t)lay.m1 + ca);
-    const uint4 lv = lds_u4(SB + (uint32_t)lay.lc + ca);
-    const unsigned W = lds_sw<S>(SB + (uint32_t)lay.sg + (uint32_t)(e * SWBY)) ^
-                       lds_sw<S>(SB + (uint32_t)lay.par + (uint32_t)(i * SWBY));
-    const float mg0 = ((int)lv.x == e) ? m1.x : m0.x;
-    const float mg1 = ((int)lv.y == e) ? m1.y : m0.y;
-    const float mg2 = ((int)lv.z == e) ? m1.z : m0.z;
-    const float mg3 = ((int)lv.w == e) ? m1.w : m0.w;
-    et[0] = (W & mv[0]) ? -mg0 : mg0;
-    et[1] = (W & mv[1]) ? -mg1 : mg1;
-    et[2] = (W & mv[2]) ? -mg2 : mg2;
-    et[3] = (W & mv[3]) ? -mg3 : mg3;
 }
 
 // Lane layout: a lane owns 4 consecutive slots (float4) of one row, edge or column; LR = S/4 lanes
@@ -261,15 +208,12 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
     const int m = a.g.m, n = a.g.n, E = a.g.E;
     float *xe = reinterpret_cast<float *>(sm + a.lay.xe);
     float *s = reinterpret_cast<float *>(sm + a.lay.s);
-    float *mn0 = reinterpret_cast<float *>(sm + a.lay.m0);
-    float *mn1 = reinterpret_cast<float *>(sm + a.lay.m1);
-    SWT *sg = reinterpret_cast<SWT *>(sm + a.lay.sg);
-    SWT *par = reinterpret_cast<SWT *>(sm + a.lay.par);
     SWT *hb = reinterpret_cast<SWT *>(sm + a.lay.hb);
     uint16_t *rp = reinterpret_cast<uint16_t *>(sm + a.lay.rp);
+    uint16_t *rbk = reinterpret_cast<uint16_t *>(sm + a.lay.rb);
     uint16_t *cp = reinterpret_cast<uint16_t *>(sm + a.lay.cp);
     uint16_t *col = reinterpret_cast<uint16_t *>(sm + a.lay.col);
-    uint32_t *rec = reinterpret_cast<uint32_t *>(sm + a.lay.rec);
+    uint16_t *ce = reinterpret_cast<uint16_t *>(sm + a.lay.ce);
     int *meta = reinterpret_cast<int *>(sm + a.lay.meta);
     int *slot_f = meta;            // frame index of the slot, -1 = empty
     int *slot_k = meta + 32;       // completed loop bodies
@@ -278,20 +222,31 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
     int *slot_nz = meta + 128;     // some |s_j| <= 1e-4
     unsigned *ctl = reinterpret_cast<unsigned *>(meta + 256);  // [0] unsat, [1] new, [2] active, [3] exhausted
 
-    const uint32_t SB = smem_u32(sm);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int sub = lane / LR, l = lane % LR;  // row group inside the warp, lane inside the row
     const int q0 = 4 * l;                      // first slot of this lane
     float *rs = a.rs + (size_t)blockIdx.x * n * S;
-    const unsigned corr_all = a.literal ? 0u : (S == 32 ? 0xffffffffu : ((1u << S) - 1u));
+    const bool corr = !a.literal;
 
     // ---- the Tanner graph into shared memory (16-bit lists)
     for (int q = tid; q <= m; q += RT) rp[q] = (uint16_t)__ldg(a.g.row_ptr + q);
     for (int q = tid; q <= n; q += RT) cp[q] = (uint16_t)__ldg(a.g.col_ptr + q);
-    for (int e = tid; e < E; e += RT) {
-        col[e] = (uint16_t)__ldg(a.g.col_idx + e);
-        const int4 be = __ldg(a.g.bn_edge + e);  // {edge id, row, pos, parity}
-        rec[e] = ((uint32_t)be.x << 16) | (uint32_t)be.y;
+    for (int e = tid; e < E; e += RT) col[e] = (uint16_t)__ldg(a.g.col_idx + e);
+    // message blocks: row i occupies d_i blocks from rb[i], rows padded to an odd length so that the
+    // rows of a quarter-warp start in different 32-byte bank groups (conflict-free check-node sweeps)
+    if (tid == 0) {
+        int acc = 0;
+        for (int i = 0; i < m; i++) {
+            rbk[i] = (uint16_t)acc;
+            const int d = __ldg(a.g.row_ptr + i + 1) - __ldg(a.g.row_ptr + i);
+            acc += d + ((d & 1) ? 0 : 1);
+        }
+        rbk[m] = (uint16_t)acc;
+    }
+    __syncthreads();
+    for (int q = tid; q < E; q += RT) {
+        const int4 be = __ldg(a.g.bn_edge + q);  // {edge id, row, position in N_i, -}: M_j, ascending rows
+        ce[q] = (uint16_t)(rbk[be.y] + be.z);
     }
     if (tid < 32) {
         slot_f[tid] = -1;
@@ -307,9 +262,6 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
         ctl[3] = 0;
     }
     unsigned long long acc_stats[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // warp 0, lane = slot
-    unsigned mv[4];
-#pragma unroll
-    for (int v = 0; v < 4; v++) mv[v] = 1u << (v * LR + l);
     __syncthreads();
 
     for (;;) {
@@ -373,14 +325,14 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
         const unsigned active = ctl[2], fresh_new = ctl[1];
         if (!active) break;
 
-        // ---------------- B: stage new frames: s = r, lambda_e - eta_e = r (eta = 0),
-        //                     hard decisions of r for the pre-loop test
+        // ---------------- B: stage new frames: s = r and lambda(i,j) = r(j) on every edge (eta = 0,
+        //                     P:124-127), hard decisions of r for the pre-loop test
         if (fresh_new) {
             const unsigned fm = (fresh_new >> q0) & 0xfu;  // this lane's fresh slots
-            SWT fw = 0;                                     // S-bit word of the fresh slots
+            unsigned fw = 0;                                // S-bit word of the fresh slots
 #pragma unroll
             for (int q = 0; q < S; q++)
-                if ((fresh_new >> q) & 1u) fw |= (SWT)(1u << ((q & 3) * LR + (q >> 2)));
+                if ((fresh_new >> q) & 1u) fw |= 1u << ((q & 3) * LR + (q >> 2));
             int fr[4];
 #pragma unroll
             for (int v = 0; v < 4; v++) fr[v] = slot_f[q0 + v];
@@ -404,8 +356,7 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
                     *reinterpret_cast<float4 *>(sp) = o;
                     const int c0 = cp[j], dv = (int)cp[j + 1] - c0;
                     for (int qq = 0; qq < dv; qq++) {
-                        const int e = (int)(rec[c0 + qq] >> 16);
-                        float *xp = xe + e * S + q0;
+                        float *xp = xe + (int)ce[c0 + qq] * S + q0;
                         float4 xo = *reinterpret_cast<const float4 *>(xp);
 #pragma unroll
                         for (int v = 0; v < 4; v++)
@@ -416,7 +367,7 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
                 unsigned bal[4];
 #pragma unroll
                 for (int v = 0; v < 4; v++) bal[v] = __ballot_sync(FULLM, jv && f4c(o, v) > 0.f);
-                if (jv && l == 0) hb[j] = (SWT)(((unsigned)hb[j] & ~(unsigned)fw) | (gather_word<S>(bal, sub) & fw));
+                if (jv && l == 0) hb[j] = (SWT)(((unsigned)hb[j] & ~fw) | (gather_word<S>(bal, sub) & fw));
             }
 #pragma unroll
             for (int v = 0; v < 4; v++) {
@@ -427,7 +378,7 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
             __syncthreads();
         }
 
-        // ---------------- C: check-node pass over x_e = s_j - eta^prev_e + syndrome of b
+        // ---------------- C: check-node pass: lambda -> eta on every edge + syndrome of b
         {
             unsigned syn_acc = 0;  // bit v: slot q0+v has an unsatisfied check
             for (int rb = warp * G; rb < m; rb += NWARP * G) {
@@ -437,9 +388,9 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
                 const int d = valid ? (int)rp[i + 1] - ra : 0;
                 const int dmax = __reduce_max_sync(FULLM, d);
                 if (__all_sync(FULLM, d == dmax))
-                    cn_row<S, false>(SB, a.lay, i, valid, ra, d, dmax, l, sub, corr_all, syn_acc);
+                    cn_row<S, false>(xe, col, hb, i, valid, ra, valid ? rbk[i] : 0, d, dmax, l, lane, corr, syn_acc);
                 else
-                    cn_row<S, true>(SB, a.lay, i, valid, ra, d, dmax, l, sub, corr_all, syn_acc);
+                    cn_row<S, true>(xe, col, hb, i, valid, ra, valid ? rbk[i] : 0, d, dmax, l, lane, corr, syn_acc);
             }
             const unsigned mine = (syn_acc << q0) & active;
             const unsigned wmask = __reduce_or_sync(FULLM, mine);
@@ -447,8 +398,9 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
         }
         __syncthreads();
 
-        // ---------------- D: per-slot decision; outputs of stopping slots and the bit-node update
-        //                     (Eq. lambda_j) of the continuing ones in one column sweep
+        // ---------------- D: per-slot decision; outputs of stopping slots and, for the continuing
+        //                     ones, the column sums s_j = sum eta + r (Eq. sCalculation) and
+        //                     the next lambda(i,j) = s(j) - eta(i,j) in one column sweep
         {
             const unsigned uns_all = ctl[0];
             bool fin = false, cont = false;
@@ -489,41 +441,23 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
                     if (work) {
                         const float4 rj = *reinterpret_cast<const float4 *>(rs + (size_t)j * S + q0);
                         const int c0 = cp[j], dv = (int)cp[j + 1] - c0;
-                        float acc[4] = {0.f, 0.f, 0.f, 0.f};
-                        float eta[DVMAX][4];
-                        int ee[DVMAX];
-#pragma unroll
-                        for (int qq = 0; qq < DVMAX; qq++) {
-                            if (qq < dv) {
-                                const uint32_t rc = rec[c0 + qq];
-                                ee[qq] = (int)(rc >> 16);
-                                eta_of<S>(SB, a.lay, rc, q0, mv, eta[qq]);
-#pragma unroll
-                                for (int v = 0; v < 4; v++) acc[v] = acc[v] + eta[qq][v];  // ascending rows (A14)
-                            }
+                        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+                        for (int qq = 0; qq < dv; qq++) {
+                            const float4 et = *reinterpret_cast<const float4 *>(xe + (int)ce[c0 + qq] * S + q0);
+                            acc.x = acc.x + et.x;  // ascending rows from +0.0 (A14)
+                            acc.y = acc.y + et.y;
+                            acc.z = acc.z + et.z;
+                            acc.w = acc.w + et.w;
                         }
-                        for (int qq = DVMAX; qq < dv; qq++) {
-                            float et[4];
-                            eta_of<S>(SB, a.lay, rec[c0 + qq], q0, mv, et);
-#pragma unroll
-                            for (int v = 0; v < 4; v++) acc[v] = acc[v] + et[v];
-                        }
-                        float4 sn = make_float4(acc[0] + rj.x, acc[1] + rj.y, acc[2] + rj.z, acc[3] + rj.w);
-                        sts_f4(SB + (uint32_t)a.lay.s + (uint32_t)((j * S + q0) * 4), sn);
-                        // extrinsic values for the next check-node pass: x_e = s_j - eta_e
-#pragma unroll
-                        for (int qq = 0; qq < DVMAX; qq++) {
-                            if (qq < dv)
-                                sts_f4(SB + (uint32_t)a.lay.xe + (uint32_t)((ee[qq] * S + q0) * 4),
-                                       make_float4(sn.x - eta[qq][0], sn.y - eta[qq][1], sn.z - eta[qq][2],
-                                                   sn.w - eta[qq][3]));
-                        }
-                        for (int qq = DVMAX; qq < dv; qq++) {
-                            const uint32_t rc = rec[c0 + qq];
-                            float et[4];
-                            eta_of<S>(SB, a.lay, rc, q0, mv, et);
-                            sts_f4(SB + (uint32_t)a.lay.xe + (uint32_t)(((int)(rc >> 16) * S + q0) * 4),
-                                   make_float4(sn.x - et[0], sn.y - et[1], sn.z - et[2], sn.w - et[3]));
+                        const float4 sn = make_float4(acc.x + rj.x, acc.y + rj.y, acc.z + rj.z, acc.w + rj.w);
+                        *reinterpret_cast<float4 *>(s + j * S + q0) = sn;
+#pragma unroll 4
+                        for (int qq = 0; qq < dv; qq++) {
+                            float *xp = xe + (int)ce[c0 + qq] * S + q0;
+                            const float4 et = *reinterpret_cast<const float4 *>(xp);
+                            *reinterpret_cast<float4 *>(xp) =
+                                make_float4(sn.x - et.x, sn.y - et.y, sn.z - et.z, sn.w - et.w);
                         }
                         o = sn;
                     }
@@ -587,7 +521,7 @@ void launch_t(const ResArgs &args, int threads, int ctas, size_t smem, cudaStrea
 ResidentPlan plan_resident(const HostGraph &g, bool loc16, int device) {
     (void)loc16;
     ResidentPlan rp;
-    if (g.n >= 65535 || g.m >= 65535 || g.E >= 65535 || g.E == 0) return rp;
+    if (g.n >= 65535 || g.m >= 65535 || (int64_t)g.E + g.m >= 65535 || g.E == 0) return rp;
     const int cap = max_smem_optin(device);
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
