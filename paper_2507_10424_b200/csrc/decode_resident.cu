@@ -6,10 +6,10 @@
 //   xe [E][S] fp32   the per-edge message of the paper's map-reduce form (Alg. 2) restricted
 //                    to the edges of H: it holds lambda(i,j) = s(j) - eta(i,j) before the
 //                    check-node pass and eta(i,j) (Eq. etaCalculation) after it
-//   s  [n][S] fp32   soft vector (Eq. sCalculation)
 //   hb [n]    S bits hard decision b_j = (s_j > 0) (Eq. slice) for the syndrome
-// plus the Tanner graph as 16-bit lists (N_i, M_j); r lives in an L2-resident global scratch
-// [CTA][n][S] read once per column per body.  Loop per round:
+// plus the Tanner graph as 16-bit lists (N_i, M_j).  r and the soft vector s (Eq. sCalculation,
+// P:337-344) live in L2-resident global scratch [CTA][n][S]: the check node never reads s (it reads
+// lambda), so s is only written by the column sums and read back for the output.  Loop per round:
 //   A  finish stopped slots (k, isCodeword, counters) and refill empty slots from a global counter
 //   B  stage new frames into their slots (s = r, lambda = r on every edge, hard decisions of r)
 //   C  check-node pass over all rows: reduce lambda to min0/min0Location/min1/parity (Obs. 1/2), then
@@ -50,7 +50,7 @@ struct SWord<32> {
 };
 
 struct Layout {
-    size_t xe, s, hb, rp, rb, cp, col, ce, meta, total;
+    size_t xe, hb, rp, cp, col, ce, meta, total;
 };
 
 constexpr size_t a16(size_t x) { return (x + 15) & ~(size_t)15; }
@@ -61,11 +61,9 @@ Layout layout_for(int S, int m, int n, int E) {
     Layout L{};
     size_t o = 0;
     const size_t swb = S <= 8 ? 1 : S / 8;
-    L.xe = o;   o = a16(o + (size_t)(E + m) * S * 4);  // edge blocks, rows padded to an odd length
-    L.s = o;    o = a16(o + (size_t)n * S * 4);
+    L.xe = o;   o = a16(o + (size_t)E * S * 4);
     L.hb = o;   o = a16(o + (size_t)n * swb);
     L.rp = o;   o = a16(o + (size_t)(m + 1) * 2);
-    L.rb = o;   o = a16(o + (size_t)(m + 1) * 2);
     L.cp = o;   o = a16(o + (size_t)(n + 1) * 2);
     L.col = o;  o = a16(o + (size_t)E * 2);
     L.ce = o;   o = a16(o + (size_t)E * 2);
@@ -85,7 +83,8 @@ struct ResArgs {
     uint8_t *conv;
     unsigned long long *stats;
     int *counter;
-    float *rs;
+    float *rs;  // [CTA][n][S] channel values r of the slots (global, L2-resident)
+    float *ss;  // [CTA][n][S] soft vectors s of the slots (global, L2-resident)
     Layout lay;
 };
 
@@ -207,10 +206,8 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
     extern __shared__ __align__(16) unsigned char sm[];
     const int m = a.g.m, n = a.g.n, E = a.g.E;
     float *xe = reinterpret_cast<float *>(sm + a.lay.xe);
-    float *s = reinterpret_cast<float *>(sm + a.lay.s);
     SWT *hb = reinterpret_cast<SWT *>(sm + a.lay.hb);
     uint16_t *rp = reinterpret_cast<uint16_t *>(sm + a.lay.rp);
-    uint16_t *rbk = reinterpret_cast<uint16_t *>(sm + a.lay.rb);
     uint16_t *cp = reinterpret_cast<uint16_t *>(sm + a.lay.cp);
     uint16_t *col = reinterpret_cast<uint16_t *>(sm + a.lay.col);
     uint16_t *ce = reinterpret_cast<uint16_t *>(sm + a.lay.ce);
@@ -226,28 +223,14 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
     const int sub = lane / LR, l = lane % LR;  // row group inside the warp, lane inside the row
     const int q0 = 4 * l;                      // first slot of this lane
     float *rs = a.rs + (size_t)blockIdx.x * n * S;
+    float *ssg = a.ss + (size_t)blockIdx.x * n * S;
     const bool corr = !a.literal;
 
     // ---- the Tanner graph into shared memory (16-bit lists)
     for (int q = tid; q <= m; q += RT) rp[q] = (uint16_t)__ldg(a.g.row_ptr + q);
     for (int q = tid; q <= n; q += RT) cp[q] = (uint16_t)__ldg(a.g.col_ptr + q);
     for (int e = tid; e < E; e += RT) col[e] = (uint16_t)__ldg(a.g.col_idx + e);
-    // message blocks: row i occupies d_i blocks from rb[i], rows padded to an odd length so that the
-    // rows of a quarter-warp start in different 32-byte bank groups (conflict-free check-node sweeps)
-    if (tid == 0) {
-        int acc = 0;
-        for (int i = 0; i < m; i++) {
-            rbk[i] = (uint16_t)acc;
-            const int d = __ldg(a.g.row_ptr + i + 1) - __ldg(a.g.row_ptr + i);
-            acc += d + ((d & 1) ? 0 : 1);
-        }
-        rbk[m] = (uint16_t)acc;
-    }
-    __syncthreads();
-    for (int q = tid; q < E; q += RT) {
-        const int4 be = __ldg(a.g.bn_edge + q);  // {edge id, row, position in N_i, -}: M_j, ascending rows
-        ce[q] = (uint16_t)(rbk[be.y] + be.z);
-    }
+    for (int q = tid; q < E; q += RT) ce[q] = (uint16_t)__ldg(&a.g.bn_edge[q].x);  // M_j as edge ids
     if (tid < 32) {
         slot_f[tid] = -1;
         slot_k[tid] = 0;
@@ -342,18 +325,16 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
                 const bool jv = j < n;
                 float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
                 if (jv && fm) {
-                    float *sp = s + j * S + q0;
-                    o = *reinterpret_cast<const float4 *>(sp);
 #pragma unroll
                     for (int v = 0; v < 4; v++) {
                         if ((fm >> v) & 1u) {
                             const float x = __ldg(a.llr + (int64_t)fr[v] * n + j);
                             f4s(o, v, x);
                             rs[(size_t)j * S + q0 + v] = x;
+                            ssg[(size_t)j * S + q0 + v] = x;
                             raw[v] += x > 0.f;
                         }
                     }
-                    *reinterpret_cast<float4 *>(sp) = o;
                     const int c0 = cp[j], dv = (int)cp[j + 1] - c0;
                     for (int qq = 0; qq < dv; qq++) {
                         float *xp = xe + (int)ce[c0 + qq] * S + q0;
@@ -388,9 +369,9 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
                 const int d = valid ? (int)rp[i + 1] - ra : 0;
                 const int dmax = __reduce_max_sync(FULLM, d);
                 if (__all_sync(FULLM, d == dmax))
-                    cn_row<S, false>(xe, col, hb, i, valid, ra, valid ? rbk[i] : 0, d, dmax, l, lane, corr, syn_acc);
+                    cn_row<S, false>(xe, col, hb, i, valid, ra, ra, d, dmax, l, lane, corr, syn_acc);
                 else
-                    cn_row<S, true>(xe, col, hb, i, valid, ra, valid ? rbk[i] : 0, d, dmax, l, lane, corr, syn_acc);
+                    cn_row<S, true>(xe, col, hb, i, valid, ra, ra, d, dmax, l, lane, corr, syn_acc);
             }
             const unsigned mine = (syn_acc << q0) & active;
             const unsigned wmask = __reduce_or_sync(FULLM, mine);
@@ -424,7 +405,7 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
                     const bool jv = j < n;
                     float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
                     if (jv && fk) {
-                        o = *reinterpret_cast<const float4 *>(s + j * S + q0);
+                        o = *reinterpret_cast<const float4 *>(ssg + (size_t)j * S + q0);
 #pragma unroll
                         for (int v = 0; v < 4; v++) {
                             if ((fk >> v) & 1u) {
@@ -451,7 +432,7 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
                             acc.w = acc.w + et.w;
                         }
                         const float4 sn = make_float4(acc.x + rj.x, acc.y + rj.y, acc.z + rj.z, acc.w + rj.w);
-                        *reinterpret_cast<float4 *>(s + j * S + q0) = sn;
+                        *reinterpret_cast<float4 *>(ssg + (size_t)j * S + q0) = sn;
 #pragma unroll 4
                         for (int qq = 0; qq < dv; qq++) {
                             float *xp = xe + (int)ce[c0 + qq] * S + q0;
@@ -563,6 +544,7 @@ int launch_resident(const Graph &g, const ResidentPlan &rp, const float *llr, in
     a.stats = stats;
     a.counter = work_counter;
     a.rs = reinterpret_cast<float *>(reinterpret_cast<char *>(work_counter) + 256);
+    a.ss = a.rs + (size_t)rp.ctas * g.n * rp.slots;
     a.lay = layout_for(rp.slots, g.m, g.n, g.E);
     cudaMemsetAsync(work_counter, 0, sizeof(int), st);
     switch (rp.slots) {
@@ -575,7 +557,7 @@ int launch_resident(const Graph &g, const ResidentPlan &rp, const float *llr, in
 }
 
 size_t resident_scratch_bytes(const HostGraph &g, const ResidentPlan &rp) {
-    return 256 + (size_t)rp.ctas * g.n * rp.slots * 4;
+    return 256 + 2 * (size_t)rp.ctas * g.n * rp.slots * 4;
 }
 
 }  // namespace ldpc
