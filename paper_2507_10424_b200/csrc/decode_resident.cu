@@ -2,21 +2,21 @@
 // time with the whole per-frame state in shared memory, and refills a frame slot the moment its
 // frame stops (per-frame early stop of Alg. 1, without batch-level waste).
 //
-// Per CTA, frame-interleaved over S slots (a lane owns 4 consecutive slots of one row, edge or column):
-//   xe [E][S] fp32   the per-edge message of the paper's map-reduce form (Alg. 2) restricted
-//                    to the edges of H: it holds lambda(i,j) = s(j) - eta(i,j) before the
-//                    check-node pass and eta(i,j) (Eq. etaCalculation) after it
-//   hb [n]    S bits hard decision b_j = (s_j > 0) (Eq. slice) for the syndrome
-// plus the Tanner graph as 16-bit lists (N_i, M_j).  r and the soft vector s (Eq. sCalculation,
-// P:337-344) live in L2-resident global scratch [CTA][n][S]: the check node never reads s (it reads
-// lambda), so s is only written by the column sums and read back for the output.  Loop per round:
+// Per CTA, frame-interleaved over S slots (a lane owns 4 consecutive slots of one row or column):
+//   s    [n][S]  fp32          soft vector (Eq. sCalculation)
+//   min0 [m][S]  fp32          Observation 1's minimum
+//   min1 [m][S]  fp32          Observation 1's second minimum
+//   lc   [m][S]  u16           min0Location, stored as the edge id inside the row lists (0xffff = none)
+//   par  [m]     S bits        the row's sign parity (Obs. 2) times (-1)^{d_i} (reading A1)
+//   sg   [E]     S bits        sign of lambda_e = s_j - eta_e for each slot
+// plus the Tanner graph itself as 16-bit lists (N_i, M_j).  r lives in a global scratch
+// [CTA][n][S] (L2-resident) read once per column per body.  Loop per round:
 //   A  finish stopped slots (k, isCodeword, counters) and refill empty slots from a global counter
-//   B  stage new frames into their slots (s = r, lambda = r on every edge, hard decisions of r)
-//   C  check-node pass over all rows: reduce lambda to min0/min0Location/min1/parity (Obs. 1/2), then
-//      write eta in place; the same pass XORs the hard decisions of the row into the syndrome
-//   D  per slot: stop (codeword, or k = L) -> write b and s; else column sums s = sum eta + r and the
-//      next lambda = s - eta (fp32, ascending rows from +0.0 then + r, reading A14)
-// Every sweep uses the same lane mapping (4 slots of one row/edge/column per lane, 16-byte accesses).
+//   B  stage new frames into their slots (s = r; eta^prev = 0 is applied by the next check-node pass)
+//   C  check-node pass over all rows + syndrome of b = slice(s) of every slot
+//   D  per slot: stop (codeword, or k = L) -> write b and s; else bit-node pass s = sum eta + r
+// Every sweep uses the same lane mapping (4 slots of one row/column per lane, 16-byte accesses), so
+// no sweep has shared-memory bank conflicts beyond the row/column gather itself.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -50,7 +50,7 @@ struct SWord<32> {
 };
 
 struct Layout {
-    size_t xe, hb, rp, cp, col, ce, meta, total;
+    size_t s, m0, m1, lc, sg, par, rp, cp, col, rec, meta, total;
 };
 
 constexpr size_t a16(size_t x) { return (x + 15) & ~(size_t)15; }
@@ -61,12 +61,16 @@ Layout layout_for(int S, int m, int n, int E) {
     Layout L{};
     size_t o = 0;
     const size_t swb = S <= 8 ? 1 : S / 8;
-    L.xe = o;   o = a16(o + (size_t)E * S * 4);
-    L.hb = o;   o = a16(o + (size_t)n * swb);
+    L.s = o;    o = a16(o + (size_t)n * S * 4);
+    L.m0 = o;   o = a16(o + (size_t)m * S * 4);
+    L.m1 = o;   o = a16(o + (size_t)m * S * 4);
+    L.lc = o;   o = a16(o + (size_t)m * S * 2);
+    L.sg = o;   o = a16(o + (size_t)E * swb);
+    L.par = o;  o = a16(o + (size_t)m * swb);
     L.rp = o;   o = a16(o + (size_t)(m + 1) * 2);
     L.cp = o;   o = a16(o + (size_t)(n + 1) * 2);
     L.col = o;  o = a16(o + (size_t)E * 2);
-    L.ce = o;   o = a16(o + (size_t)E * 2);
+    L.rec = o;  o = a16(o + (size_t)E * 4);
     L.meta = o; o = a16(o + (size_t)META_INTS * 4 + 8 * 8);
     L.total = o;
     return L;
@@ -83,8 +87,7 @@ struct ResArgs {
     uint8_t *conv;
     unsigned long long *stats;
     int *counter;
-    float *rs;  // [CTA][n][S] channel values r of the slots (global, L2-resident)
-    float *ss;  // [CTA][n][S] soft vectors s of the slots (global, L2-resident)
+    float *rs;
     Layout lay;
 };
 
@@ -95,108 +98,97 @@ __device__ __forceinline__ void f4s(float4 &a, int v, float x) {
     else if (v == 2) a.z = x;
     else a.w = x;
 }
+// min0Location test on two packed 16-bit edge ids: true iff the half selected by `hi` differs from e
+__device__ __forceinline__ bool loc_ne(unsigned pair, unsigned e2, bool hi) {
+    return ((pair ^ e2) & (hi ? 0xffff0000u : 0x0000ffffu)) != 0u;
+}
 
-// S-bit word of a row group from the four per-component ballots: slot q = 4l+v sits at bit v*LR + l.
-template <int S>
-__device__ __forceinline__ unsigned gather_word(const unsigned bal[4], int sub) {
+// Check-node update of G rows (one per row group of the warp) for the 4 slots of this lane.
+// HAS: rows of the warp may have different degrees (irregular H), lanes past their degree idle.
+// fm: this lane's fresh slots (eta^prev = 0); nfw: S-bit word with the fresh slots' bits clear.
+template <int S, bool HAS>
+__device__ __forceinline__ void cn_rows(const float *s, float *mn0, float *mn1, uint16_t *lc,
+                                        typename SWord<S>::T *sg, typename SWord<S>::T *par,
+                                        const uint16_t *col, int i, bool valid, int ra, int d, int dmax,
+                                        int l, int sub, unsigned fm, unsigned nfw, unsigned corr_all,
+                                        unsigned &syn_acc) {
+    using SWT = typename SWord<S>::T;
     constexpr int LR = S / 4;
     constexpr unsigned LMASK = (LR == 32) ? 0xffffffffu : ((1u << LR) - 1u);
-    unsigned word = 0;
-#pragma unroll
-    for (int v = 0; v < 4; v++) word |= ((bal[v] >> (sub * LR)) & LMASK) << (v * LR);
-    return word;
-}
-// this lane's 4 slot bits (bit v = slot 4l+v) of an S-bit word
-template <int S>
-__device__ __forceinline__ unsigned lane_bits(unsigned word, int l) {
-    constexpr int LR = S / 4;
-    return ((word >> l) & 1u) | (((word >> (LR + l)) & 1u) << 1) | (((word >> (2 * LR + l)) & 1u) << 2) |
-           (((word >> (3 * LR + l)) & 1u) << 3);
-}
-
-// Check-node update of one row per row group for the 4 slots of this lane (Eq. etaCalculation,
-// P:327-336).  Pass 1 reduces lambda(i,j) of the row to min0, min0Location, min1 (Obs. 1) and the sign
-// parity (Obs. 2) -- the paper's four vectors -- and XORs the row's hard decisions into the
-// syndrome.  Pass 2 overwrites lambda(i,j) with eta(i,j) in place.  HAS: rows of the warp differ in degree.
-template <int S, bool HAS>
-__device__ __forceinline__ void cn_row(float *xe, const uint16_t *col, const typename SWord<S>::T *hb, int i,
-                                       bool valid, int ra, int xb, int d, int dmax, int l, int lane,
-                                       bool corr_lit, unsigned &syn_acc) {
-    constexpr int DR = 8;  // row degrees up to DR keep lambda in registers between the two passes
     const float INF = __int_as_float(0x7f800000);
     const int q0 = 4 * l;
+    float4 om0 = make_float4(0.f, 0.f, 0.f, 0.f), om1 = om0;
+    uint2 olc = make_uint2(0xffffffffu, 0xffffffffu);
+    unsigned P = 0;
+    const int ca = i * S + q0;
+    if (valid) {
+        om0 = *reinterpret_cast<const float4 *>(mn0 + ca);
+        om1 = *reinterpret_cast<const float4 *>(mn1 + ca);
+        olc = *reinterpret_cast<const uint2 *>(lc + ca);
+        P = (unsigned)par[i];
+        if (fm) {  // fresh slots start from eta = 0: min0 = min1 = +0, no location
+            if (fm & 1u) { om0.x = 0.f; om1.x = 0.f; olc.x |= 0x0000ffffu; }
+            if (fm & 2u) { om0.y = 0.f; om1.y = 0.f; olc.x |= 0xffff0000u; }
+            if (fm & 4u) { om0.z = 0.f; om1.z = 0.f; olc.y |= 0x0000ffffu; }
+            if (fm & 8u) { om0.w = 0.f; om1.w = 0.f; olc.y |= 0xffff0000u; }
+        }
+    }
+    unsigned mv[4];
+#pragma unroll
+    for (int v = 0; v < 4; v++) mv[v] = 1u << (v * LR + l);
     float nm0[4] = {INF, INF, INF, INF}, nm1[4] = {INF, INF, INF, INF};
-    int nloc[4] = {-1, -1, -1, -1};
+    int nloc[4] = {0xffff, 0xffff, 0xffff, 0xffff};
     unsigned parw[4] = {0, 0, 0, 0};
-    unsigned synw = 0;
-    float4 xr[DR];
-    auto scan = [&](int p, float4 xv) {
+    unsigned syn = 0;
+#pragma unroll 2
+    for (int p = 0; p < dmax; p++) {
+        const bool has = HAS ? (p < d) : true;
+        const int e = ra + p;
+        const unsigned e2 = (unsigned)e * 0x10001u;
+        const int j = has ? col[e] : 0;
+        const float4 sv = *reinterpret_cast<const float4 *>(s + j * S + q0);
+        // own sign of lambda^prev xor the row parity (Obs. 2, A1 folded in); fresh slots: +
+        const unsigned W = ((has ? (unsigned)sg[e] : 0u) ^ P) & nfw;
+        unsigned bal[4];
 #pragma unroll
         for (int v = 0; v < 4; v++) {
-            const float x = f4c(xv, v);
-            const float ax = fabsf(x);
+            const float sj = f4c(sv, v);
+            const float mag = loc_ne(v < 2 ? olc.x : olc.y, e2, v & 1) ? f4c(om0, v) : f4c(om1, v);  // Obs. 1
+            const float x = sj - ((W & mv[v]) ? -mag : mag);  // lambda - eta^prev
+            const float ax = HAS ? (has ? fabsf(x) : INF) : fabsf(x);
             const bool lt = ax < nm0[v];  // first strict minimum (A13)
             nm1[v] = fminf(nm1[v], fmaxf(nm0[v], ax));
             nm0[v] = fminf(nm0[v], ax);
-            nloc[v] = lt ? p : nloc[v];
-            parw[v] ^= __ballot_sync(FULLM, x < 0.f);  // sign(0) = +1; INF is +
+            nloc[v] = lt ? e : nloc[v];
+            bal[v] = __ballot_sync(FULLM, (HAS ? has : true) && x < 0.f);  // sign(0) = +1
+            syn ^= (unsigned)((HAS ? has : true) && sj > 0.f) << v;        // b_j = slice(s_j)
         }
-    };
-    const bool small = dmax <= DR;
-    if (small) {
 #pragma unroll
-        for (int p = 0; p < DR; p++) {
-            if (p < dmax) {
-                const bool has = HAS ? (p < d) : true;
-                xr[p] = make_float4(INF, INF, INF, INF);
-                if (has) {
-                    xr[p] = *reinterpret_cast<const float4 *>(xe + (xb + p) * S + q0);
-                    synw ^= (unsigned)hb[col[ra + p]];  // b_j = slice(s_j)
-                }
-                scan(p, xr[p]);
-            }
-        }
-    } else {
-        for (int p = 0; p < dmax; p++) {
-            const bool has = HAS ? (p < d) : true;
-            float4 xv = make_float4(INF, INF, INF, INF);
-            if (has) {
-                xv = *reinterpret_cast<const float4 *>(xe + (xb + p) * S + q0);
-                synw ^= (unsigned)hb[col[ra + p]];
-            }
-            scan(p, xv);
+        for (int v = 0; v < 4; v++) parw[v] ^= bal[v];
+        if (has && l == 0) {
+            unsigned word = 0;
+#pragma unroll
+            for (int v = 0; v < 4; v++) word |= ((bal[v] >> (sub * LR)) & LMASK) << (v * LR);
+            sg[e] = (SWT)word;
         }
     }
     if (valid) {
-        // row parity of this lane's slots, times (-1)^{d_i} (reading A1)
-        const unsigned flip = (corr_lit && (d & 1)) ? 1u : 0u;
-        unsigned pv[4];
+        *reinterpret_cast<float4 *>(mn0 + ca) = make_float4(nm0[0], nm0[1], nm0[2], nm0[3]);
+        *reinterpret_cast<float4 *>(mn1 + ca) = make_float4(nm1[0], nm1[1], nm1[2], nm1[3]);
+        *reinterpret_cast<uint2 *>(lc + ca) = make_uint2((unsigned)nloc[0] | ((unsigned)nloc[1] << 16),
+                                                         (unsigned)nloc[2] | ((unsigned)nloc[3] << 16));
+        if (l == 0) {
+            unsigned word = 0;
 #pragma unroll
-        for (int v = 0; v < 4; v++) pv[v] = ((parw[v] >> lane) & 1u) ^ flip;
-        auto emit = [&](int p, float4 xv) {
-            float4 o;
-#pragma unroll
-            for (int v = 0; v < 4; v++) {
-                const float x = f4c(xv, v);
-                const float mag = (p == nloc[v]) ? nm1[v] : nm0[v];       // Obs. 1 (delta placement, A2)
-                const bool neg = ((unsigned)(x < 0.f) ^ pv[v]) != 0u;    // Obs. 2: parity x own sign
-                f4s(o, v, neg ? -mag : mag);
-            }
-            *reinterpret_cast<float4 *>(xe + (xb + p) * S + q0) = o;
-        };
-        if (small) {
-#pragma unroll
-            for (int p = 0; p < DR; p++)
-                if (p < d) emit(p, xr[p]);
-        } else {
-            for (int p = 0; p < d; p++) emit(p, *reinterpret_cast<const float4 *>(xe + (xb + p) * S + q0));
+            for (int v = 0; v < 4; v++) word |= ((parw[v] >> (sub * LR)) & LMASK) << (v * LR);
+            par[i] = (SWT)(word ^ ((d & 1) ? corr_all : 0u));  // (-1)^{d_i}, reading A1
         }
-        syn_acc |= lane_bits<S>(synw, l);
+        syn_acc |= syn;
     }
 }
 
-// Lane layout: a lane owns 4 consecutive slots (float4) of one row, edge or column; LR = S/4 lanes
-// cover a row, G = 32/LR rows per warp.  Bit of slot q = 4*l + v inside an S-bit word: v*LR + l.
+// Lane layout: a lane owns 4 consecutive slots (float4) of one row or column; LR = S/4 lanes cover a
+// row, G = 32/LR rows per warp.  Bit of slot q = 4*l + v inside an S-bit sign word: v*LR + l.
 template <int S, int RT>
 __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
     constexpr int NWARP = RT / 32;
@@ -205,12 +197,16 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
     constexpr int G = 32 / LR;
     extern __shared__ __align__(16) unsigned char sm[];
     const int m = a.g.m, n = a.g.n, E = a.g.E;
-    float *xe = reinterpret_cast<float *>(sm + a.lay.xe);
-    SWT *hb = reinterpret_cast<SWT *>(sm + a.lay.hb);
+    float *s = reinterpret_cast<float *>(sm + a.lay.s);
+    float *mn0 = reinterpret_cast<float *>(sm + a.lay.m0);
+    float *mn1 = reinterpret_cast<float *>(sm + a.lay.m1);
+    uint16_t *lc = reinterpret_cast<uint16_t *>(sm + a.lay.lc);
+    SWT *sg = reinterpret_cast<SWT *>(sm + a.lay.sg);
+    SWT *par = reinterpret_cast<SWT *>(sm + a.lay.par);
     uint16_t *rp = reinterpret_cast<uint16_t *>(sm + a.lay.rp);
     uint16_t *cp = reinterpret_cast<uint16_t *>(sm + a.lay.cp);
     uint16_t *col = reinterpret_cast<uint16_t *>(sm + a.lay.col);
-    uint16_t *ce = reinterpret_cast<uint16_t *>(sm + a.lay.ce);
+    uint32_t *rec = reinterpret_cast<uint32_t *>(sm + a.lay.rec);
     int *meta = reinterpret_cast<int *>(sm + a.lay.meta);
     int *slot_f = meta;            // frame index of the slot, -1 = empty
     int *slot_k = meta + 32;       // completed loop bodies
@@ -223,14 +219,16 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
     const int sub = lane / LR, l = lane % LR;  // row group inside the warp, lane inside the row
     const int q0 = 4 * l;                      // first slot of this lane
     float *rs = a.rs + (size_t)blockIdx.x * n * S;
-    float *ssg = a.ss + (size_t)blockIdx.x * n * S;
-    const bool corr = !a.literal;
+    const unsigned corr_all = a.literal ? 0u : (S == 32 ? 0xffffffffu : ((1u << S) - 1u));
 
     // ---- the Tanner graph into shared memory (16-bit lists)
     for (int q = tid; q <= m; q += RT) rp[q] = (uint16_t)__ldg(a.g.row_ptr + q);
     for (int q = tid; q <= n; q += RT) cp[q] = (uint16_t)__ldg(a.g.col_ptr + q);
-    for (int e = tid; e < E; e += RT) col[e] = (uint16_t)__ldg(a.g.col_idx + e);
-    for (int q = tid; q < E; q += RT) ce[q] = (uint16_t)__ldg(&a.g.bn_edge[q].x);  // M_j as edge ids
+    for (int e = tid; e < E; e += RT) {
+        col[e] = (uint16_t)__ldg(a.g.col_idx + e);
+        const int4 be = __ldg(a.g.bn_edge + e);  // {edge id, row, pos, parity}
+        rec[e] = ((uint32_t)be.x << 16) | (uint32_t)be.y;
+    }
     if (tid < 32) {
         slot_f[tid] = -1;
         slot_k[tid] = 0;
@@ -307,49 +305,31 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
         __syncthreads();
         const unsigned active = ctl[2], fresh_new = ctl[1];
         if (!active) break;
+        const unsigned fm = (fresh_new >> q0) & 0xfu;  // this lane's fresh slots
 
-        // ---------------- B: stage new frames: s = r and lambda(i,j) = r(j) on every edge (eta = 0,
-        //                     P:124-127), hard decisions of r for the pre-loop test
+        // ---------------- B: stage new frames, s = r: column sweep in the float4 layout
         if (fresh_new) {
-            const unsigned fm = (fresh_new >> q0) & 0xfu;  // this lane's fresh slots
-            unsigned fw = 0;                                // S-bit word of the fresh slots
-#pragma unroll
-            for (int q = 0; q < S; q++)
-                if ((fresh_new >> q) & 1u) fw |= 1u << ((q & 3) * LR + (q >> 2));
             int fr[4];
 #pragma unroll
             for (int v = 0; v < 4; v++) fr[v] = slot_f[q0 + v];
             int raw[4] = {0, 0, 0, 0};
-            for (int cb = warp * G; cb < n; cb += NWARP * G) {
+            for (int cb = warp * G; cb < n && fm; cb += NWARP * G) {
                 const int j = cb + sub;
-                const bool jv = j < n;
-                float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (jv && fm) {
+                if (j >= n) continue;
+                float *sp = s + j * S + q0;
+                float4 o = *reinterpret_cast<const float4 *>(sp);
 #pragma unroll
-                    for (int v = 0; v < 4; v++) {
-                        if ((fm >> v) & 1u) {
-                            const float x = __ldg(a.llr + (int64_t)fr[v] * n + j);
-                            f4s(o, v, x);
-                            rs[(size_t)j * S + q0 + v] = x;
-                            ssg[(size_t)j * S + q0 + v] = x;
-                            raw[v] += x > 0.f;
-                        }
-                    }
-                    const int c0 = cp[j], dv = (int)cp[j + 1] - c0;
-                    for (int qq = 0; qq < dv; qq++) {
-                        float *xp = xe + (int)ce[c0 + qq] * S + q0;
-                        float4 xo = *reinterpret_cast<const float4 *>(xp);
-#pragma unroll
-                        for (int v = 0; v < 4; v++)
-                            if ((fm >> v) & 1u) f4s(xo, v, f4c(o, v));
-                        *reinterpret_cast<float4 *>(xp) = xo;
+                for (int v = 0; v < 4; v++) {
+                    if ((fm >> v) & 1u) {
+                        const float x = __ldg(a.llr + (int64_t)fr[v] * n + j);
+                        f4s(o, v, x);
+                        rs[(size_t)j * S + q0 + v] = x;
+                        raw[v] += x > 0.f;
                     }
                 }
-                unsigned bal[4];
-#pragma unroll
-                for (int v = 0; v < 4; v++) bal[v] = __ballot_sync(FULLM, jv && f4c(o, v) > 0.f);
-                if (jv && l == 0) hb[j] = (SWT)(((unsigned)hb[j] & ~fw) | (gather_word<S>(bal, sub) & fw));
+                *reinterpret_cast<float4 *>(sp) = o;
             }
+            // per-slot counts: reduce over the row groups of the warp, then one atomic per slot
 #pragma unroll
             for (int v = 0; v < 4; v++) {
                 int x = raw[v];
@@ -359,8 +339,12 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
             __syncthreads();
         }
 
-        // ---------------- C: check-node pass: lambda -> eta on every edge + syndrome of b
+        // ---------------- C: check-node pass + syndrome of b = slice(s)
         {
+            SWT nfw = 0;
+#pragma unroll
+            for (int q = 0; q < S; q++)
+                if (!((fresh_new >> q) & 1u)) nfw |= (SWT)(1u << ((q & 3) * LR + (q >> 2)));
             unsigned syn_acc = 0;  // bit v: slot q0+v has an unsatisfied check
             for (int rb = warp * G; rb < m; rb += NWARP * G) {
                 const int i = rb + sub;
@@ -369,9 +353,11 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
                 const int d = valid ? (int)rp[i + 1] - ra : 0;
                 const int dmax = __reduce_max_sync(FULLM, d);
                 if (__all_sync(FULLM, d == dmax))
-                    cn_row<S, false>(xe, col, hb, i, valid, ra, ra, d, dmax, l, lane, corr, syn_acc);
+                    cn_rows<S, false>(s, mn0, mn1, lc, sg, par, col, i, valid, ra, d, dmax, l, sub, fm, nfw, corr_all,
+                                      syn_acc);
                 else
-                    cn_row<S, true>(xe, col, hb, i, valid, ra, ra, d, dmax, l, lane, corr, syn_acc);
+                    cn_rows<S, true>(s, mn0, mn1, lc, sg, par, col, i, valid, ra, d, dmax, l, sub, fm, nfw, corr_all,
+                                     syn_acc);
             }
             const unsigned mine = (syn_acc << q0) & active;
             const unsigned wmask = __reduce_or_sync(FULLM, mine);
@@ -379,9 +365,8 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
         }
         __syncthreads();
 
-        // ---------------- D: per-slot decision; outputs of stopping slots and, for the continuing
-        //                     ones, the column sums s_j = sum eta + r (Eq. sCalculation) and
-        //                     the next lambda(i,j) = s(j) - eta(i,j) in one column sweep
+        // ---------------- D: per-slot decision; outputs of stopping slots and bit-node update of the
+        //                     continuing ones in one column sweep
         {
             const unsigned uns_all = ctl[0];
             bool fin = false, cont = false;
@@ -400,12 +385,15 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
                 for (int v = 0; v < 4; v++) fo[v] = (int64_t)slot_f[q0 + v] * n;
                 int be[4] = {0, 0, 0, 0};
                 unsigned nz = 0;
+                unsigned mv[4];
+#pragma unroll
+                for (int v = 0; v < 4; v++) mv[v] = 1u << (v * LR + l);
                 for (int cb = warp * G; cb < n; cb += NWARP * G) {
                     const int j = cb + sub;
-                    const bool jv = j < n;
-                    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (jv && fk) {
-                        o = *reinterpret_cast<const float4 *>(ssg + (size_t)j * S + q0);
+                    if (j >= n || !(cm | fk)) continue;
+                    float *sp = s + j * S + q0;
+                    float4 o = *reinterpret_cast<const float4 *>(sp);
+                    if (fk) {
 #pragma unroll
                         for (int v = 0; v < 4; v++) {
                             if ((fk >> v) & 1u) {
@@ -418,35 +406,32 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
                             }
                         }
                     }
-                    const bool work = jv && cm;
-                    if (work) {
+                    if (cm) {
                         const float4 rj = *reinterpret_cast<const float4 *>(rs + (size_t)j * S + q0);
                         const int c0 = cp[j], dv = (int)cp[j + 1] - c0;
-                        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 4
+                        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 2
                         for (int qq = 0; qq < dv; qq++) {
-                            const float4 et = *reinterpret_cast<const float4 *>(xe + (int)ce[c0 + qq] * S + q0);
-                            acc.x = acc.x + et.x;  // ascending rows from +0.0 (A14)
-                            acc.y = acc.y + et.y;
-                            acc.z = acc.z + et.z;
-                            acc.w = acc.w + et.w;
-                        }
-                        const float4 sn = make_float4(acc.x + rj.x, acc.y + rj.y, acc.z + rj.z, acc.w + rj.w);
-                        *reinterpret_cast<float4 *>(ssg + (size_t)j * S + q0) = sn;
-#pragma unroll 4
-                        for (int qq = 0; qq < dv; qq++) {
-                            float *xp = xe + (int)ce[c0 + qq] * S + q0;
-                            const float4 et = *reinterpret_cast<const float4 *>(xp);
-                            *reinterpret_cast<float4 *>(xp) =
-                                make_float4(sn.x - et.x, sn.y - et.y, sn.z - et.z, sn.w - et.w);
-                        }
-                        o = sn;
-                    }
-                    // hard decisions of the new s for the next syndrome (continuing slots only matter)
-                    unsigned bal[4];
+                            const uint32_t rc = rec[c0 + qq];
+                            const int e = (int)(rc >> 16), i = (int)(rc & 0xffffu);
+                            const unsigned e2 = (unsigned)e * 0x10001u;
+                            const int ca = i * S + q0;
+                            const float4 m0 = *reinterpret_cast<const float4 *>(mn0 + ca);
+                            const float4 m1 = *reinterpret_cast<const float4 *>(mn1 + ca);
+                            const uint2 lv = *reinterpret_cast<const uint2 *>(lc + ca);
+                            const unsigned W = (unsigned)sg[e] ^ (unsigned)par[i];
 #pragma unroll
-                    for (int v = 0; v < 4; v++) bal[v] = __ballot_sync(FULLM, work && f4c(o, v) > 0.f);
-                    if (jv && l == 0 && cont_mask) hb[j] = (SWT)gather_word<S>(bal, sub);
+                            for (int v = 0; v < 4; v++) {
+                                const float mag = loc_ne(v < 2 ? lv.x : lv.y, e2, v & 1) ? f4c(m0, v) : f4c(m1, v);
+                                acc[v] = acc[v] + ((W & mv[v]) ? -mag : mag);  // ascending rows from +0.0 (A14)
+                            }
+                        }
+                        if (cm & 1u) o.x = acc[0] + rj.x;
+                        if (cm & 2u) o.y = acc[1] + rj.y;
+                        if (cm & 4u) o.z = acc[2] + rj.z;
+                        if (cm & 8u) o.w = acc[3] + rj.w;
+                        *reinterpret_cast<float4 *>(sp) = o;
+                    }
                 }
                 if (fin_mask) {
 #pragma unroll
@@ -493,7 +478,6 @@ void launch_s(const ResArgs &args, int ctas, size_t smem, cudaStream_t st) {
 template <int S>
 void launch_t(const ResArgs &args, int threads, int ctas, size_t smem, cudaStream_t st) {
     if (threads == 1024) launch_s<S, 1024>(args, ctas, smem, st);
-    else if (threads == 768) launch_s<S, 768>(args, ctas, smem, st);
     else launch_s<S, 512>(args, ctas, smem, st);
 }
 
@@ -502,7 +486,7 @@ void launch_t(const ResArgs &args, int threads, int ctas, size_t smem, cudaStrea
 ResidentPlan plan_resident(const HostGraph &g, bool loc16, int device) {
     (void)loc16;
     ResidentPlan rp;
-    if (g.n >= 65535 || g.m >= 65535 || (int64_t)g.E + g.m >= 65535 || g.E == 0) return rp;
+    if (g.n >= 65535 || g.m >= 65535 || g.E >= 65535 || g.E == 0) return rp;
     const int cap = max_smem_optin(device);
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
@@ -513,10 +497,7 @@ ResidentPlan plan_resident(const HostGraph &g, bool loc16, int device) {
             rp.ok = true;
             rp.slots = S;
             rp.threads = 512;
-            if (const char *e = getenv("LDPC_RES_THREADS")) {
-                const int t = atoi(e);
-                rp.threads = (t == 1024 || t == 768) ? t : 512;
-            }
+            if (const char *e = getenv("LDPC_RES_THREADS")) rp.threads = atoi(e) == 1024 ? 1024 : 512;
             rp.smem = L.total;
             rp.ctas = sms;
             return rp;
@@ -544,7 +525,6 @@ int launch_resident(const Graph &g, const ResidentPlan &rp, const float *llr, in
     a.stats = stats;
     a.counter = work_counter;
     a.rs = reinterpret_cast<float *>(reinterpret_cast<char *>(work_counter) + 256);
-    a.ss = a.rs + (size_t)rp.ctas * g.n * rp.slots;
     a.lay = layout_for(rp.slots, g.m, g.n, g.E);
     cudaMemsetAsync(work_counter, 0, sizeof(int), st);
     switch (rp.slots) {
@@ -557,7 +537,7 @@ int launch_resident(const Graph &g, const ResidentPlan &rp, const float *llr, in
 }
 
 size_t resident_scratch_bytes(const HostGraph &g, const ResidentPlan &rp) {
-    return 256 + 2 * (size_t)rp.ctas * g.n * rp.slots * 4;
+    return 256 + (size_t)rp.ctas * g.n * rp.slots * 4;
 }
 
 }  // namespace ldpc
