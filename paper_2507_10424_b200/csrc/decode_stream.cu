@@ -56,7 +56,8 @@ __device__ __forceinline__ uint4 ldu4(const uint32_t *p) { return *reinterpret_c
 __global__ void __launch_bounds__(CTA) k_stage_in(const float *__restrict__ llr, int64_t frames, int n, int T,
                                                   float *__restrict__ r, float *__restrict__ s,
                                                   uint32_t *__restrict__ unsat, uint32_t *__restrict__ done,
-                                                  int *__restrict__ fbe, int *__restrict__ fraw, int *__restrict__ fnz) {
+                                                  int *__restrict__ fbe, int *__restrict__ fraw, int *__restrict__ fnz,
+                                                  int *__restrict__ tcount, int *__restrict__ tlist) {
     __shared__ float tile[32][TILE + 1];
     const int t = blockIdx.y, j0 = blockIdx.x * 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -89,6 +90,13 @@ __global__ void __launch_bounds__(CTA) k_stage_in(const float *__restrict__ llr,
             unsat[(size_t)t * 4 + tid] = 0;
             unsat[((size_t)T + t) * 4 + tid] = 0;
         }
+        if (tid == 0) {
+            tlist[(size_t)T + t] = t;  // body 1 runs every tile
+            if (t == 0) {
+                tcount[0] = 0;
+                tcount[1] = T;
+            }
+        }
         if (tid < TILE) {
             fbe[(size_t)t * TILE + tid] = 0;
             fraw[(size_t)t * TILE + tid] = 0;
@@ -115,12 +123,16 @@ template <typename LocT, bool FIRST, bool EARLY, int CN_U>
 __global__ void __launch_bounds__(CTA, MinBlocks<CN_U>::value)
     k_cn(Graph g, StreamState w, int k, int rows_per_cta, int literal) {
     using L4 = typename Vec4<LocT>::type;
-    const int t = blockIdx.y;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     __shared__ uint32_t s_u[4];
+    // the tiles of body k are the ones with a running frame (list rebuilt by k_bn of body k-1)
+    const int cnt = w.tcount[k & 1];
+    if (blockIdx.x == 0 && threadIdx.x == 0) w.tcount[(k + 1) & 1] = 0;  // rebuilt by k_bn of body k
+    if ((int)blockIdx.y >= cnt) return;  // active tiles are compacted to the front of the list
+    {
+    const int t = w.tlist[(size_t)(k & 1) * w.T + blockIdx.y];
+    const int rblk = blockIdx.x;
     if (EARLY) {
-        const uint4 dw = ldu4(w.done + (size_t)t * 4);
-        if ((dw.x & dw.y & dw.z & dw.w) == FULL) return;  // every frame of the tile has stopped
         if (threadIdx.x < 4) s_u[threadIdx.x] = 0;
         __syncthreads();
     }
@@ -134,7 +146,7 @@ __global__ void __launch_bounds__(CTA, MinBlocks<CN_U>::value)
     const int m = g.m, n = g.n, E = g.E;
     const size_t tm = (size_t)t * m, tn = (size_t)t * n, tE = (size_t)t * E;
     const int sh = 4 * (lane & 7), wsel = lane >> 3;
-    const int i0 = blockIdx.x * rows_per_cta, i1 = min(m, i0 + rows_per_cta);
+    const int i0 = rblk * rows_per_cta, i1 = min(m, i0 + rows_per_cta);
     uint32_t u0 = 0, u1 = 0, u2 = 0, u3 = 0;
     for (int i = i0 + warp; i < i1; i += CTA / 32) {
         const int a = __ldg(row_ptr + i), d = __ldg(row_ptr + i + 1) - a;
@@ -232,6 +244,7 @@ __global__ void __launch_bounds__(CTA, MinBlocks<CN_U>::value)
         if (threadIdx.x < 4 && s_u[threadIdx.x])
             atomicOr(w.unsat + ((size_t)(k & 1) * w.T + t) * 4 + threadIdx.x, s_u[threadIdx.x]);
     }
+    }
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -243,19 +256,23 @@ __global__ void __launch_bounds__(CTA, BN_U <= 1 ? 6 : MinBlocks<BN_U>::value)
     k_bn(Graph g, StreamState w, int k, int cols_per_cta, int literal) {
     using L4 = typename Vec4<LocT>::type;
     (void)literal;
-    const int t = blockIdx.y;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int T = w.T;
+    const int cnt = w.tcount[k & 1];
+    if ((int)blockIdx.y >= cnt) return;
+    {
+    const int t = w.tlist[(size_t)(k & 1) * T + blockIdx.y];
+    const int cblk = blockIdx.x;
     uint4 act = make_uint4(FULL, FULL, FULL, FULL);
     if (EARLY) {
         const uint4 ua = ldu4(w.unsat + ((size_t)(k & 1) * T + t) * 4);
         const uint4 dw = ldu4(w.done + (size_t)t * 4);
         const uint4 newly = make_uint4(~ua.x & ~dw.x, ~ua.y & ~dw.y, ~ua.z & ~dw.z, ~ua.w & ~dw.w);
         act = make_uint4(ua.x & ~dw.x, ua.y & ~dw.y, ua.z & ~dw.z, ua.w & ~dw.w);
-        // every thread of CTA 0 must read `done` before any thread rewrites it (other CTAs of the
-        // tile may see either value: act is the same for both, since newly and ua are disjoint)
+        // every thread must read `done` before the tile's bookkeeping item rewrites it (other items of
+        // the tile may see either value: act is the same for both, since newly and ua are disjoint)
         __syncthreads();
-        if (blockIdx.x == 0) {
+        if (cblk == 0) {
             const int tid = threadIdx.x;
             if (tid < 4) {
                 w.done[(size_t)t * 4 + tid] = comp(dw, tid) | comp(newly, tid);
@@ -263,8 +280,15 @@ __global__ void __launch_bounds__(CTA, BN_U <= 1 ? 6 : MinBlocks<BN_U>::value)
             }
             if (tid < TILE && ((comp(newly, tid & 3) >> (tid >> 2)) & 1u))
                 w.iters[(size_t)t * TILE + tid] = k - 1;  // stopped after k-1 bodies
+            if (tid == 0 && (act.x | act.y | act.z | act.w)) {  // tile still runs in body k+1
+                const int pos = atomicAdd(w.tcount + ((k + 1) & 1), 1);
+                w.tlist[(size_t)((k + 1) & 1) * T + pos] = t;
+            }
         }
         if ((act.x | act.y | act.z | act.w) == 0) return;
+    } else if (cblk == 0 && threadIdx.x == 0) {
+        const int pos = atomicAdd(w.tcount + ((k + 1) & 1), 1);
+        w.tlist[(size_t)((k + 1) & 1) * T + pos] = t;
     }
     const unsigned mine = ((act.x >> lane) & 1u) | (((act.y >> lane) & 1u) << 1) | (((act.z >> lane) & 1u) << 2) |
                           (((act.w >> lane) & 1u) << 3);
@@ -279,7 +303,7 @@ __global__ void __launch_bounds__(CTA, BN_U <= 1 ? 6 : MinBlocks<BN_U>::value)
     const int m = g.m, n = g.n, E = g.E;
     const size_t tm = (size_t)t * m, tn = (size_t)t * n, tE = (size_t)t * E;
     const int sh = 4 * (lane & 7), wsel = lane >> 3;
-    const int j0 = blockIdx.x * cols_per_cta, j1 = min(n, j0 + cols_per_cta);
+    const int j0 = cblk * cols_per_cta, j1 = min(n, j0 + cols_per_cta);
     for (int j = j0 + warp; j < j1; j += CTA / 32) {
         const int c0 = __ldg(col_ptr + j), dv = __ldg(col_ptr + j + 1) - c0;
         const size_t sj = (tn + j) * TILE + 4 * lane;
@@ -345,21 +369,24 @@ __global__ void __launch_bounds__(CTA, BN_U <= 1 ? 6 : MinBlocks<BN_U>::value)
             st4(Sv + sj, out);
         }
     }
+    }
 }
 
 // ------------------------------------------------------------------------------------------------
 // a6: syndrome of b^(L) (the test after the last body), into unsat[slot].
 // ------------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(CTA) k_syndrome(Graph g, StreamState w, int slot, int rows_per_cta) {
-    const int t = blockIdx.y;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     __shared__ uint32_t s_u[4];
-    const uint4 dw = ldu4(w.done + (size_t)t * 4);
-    if ((dw.x & dw.y & dw.z & dw.w) == FULL) return;
+    const int cnt = w.tcount[slot];  // tiles still running after the last body
+    if ((int)blockIdx.y >= cnt) return;
+    {
+    const int t = w.tlist[(size_t)slot * w.T + blockIdx.y];
+    const int rblk = blockIdx.x;
     if (threadIdx.x < 4) s_u[threadIdx.x] = 0;
     __syncthreads();
     const size_t tn = (size_t)t * g.n;
-    const int i0 = blockIdx.x * rows_per_cta, i1 = min(g.m, i0 + rows_per_cta);
+    const int i0 = rblk * rows_per_cta, i1 = min(g.m, i0 + rows_per_cta);
     uint32_t u[4] = {0, 0, 0, 0};
     for (int i = i0 + warp; i < i1; i += CTA / 32) {
         const int a = __ldg(g.row_ptr + i), d = __ldg(g.row_ptr + i + 1) - a;
@@ -380,6 +407,7 @@ __global__ void __launch_bounds__(CTA) k_syndrome(Graph g, StreamState w, int sl
     __syncthreads();
     if (threadIdx.x < 4 && s_u[threadIdx.x])
         atomicOr(w.unsat + ((size_t)slot * w.T + t) * 4 + threadIdx.x, s_u[threadIdx.x]);
+    }
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -474,7 +502,7 @@ inline dim3 grid2(int64_t x, int y) { return dim3((unsigned)std::max<int64_t>(1,
 
 int launch_stage_in(const Graph &g, const StreamState &w, const float *llr, int64_t frames, cudaStream_t st) {
     k_stage_in<<<grid2((g.n + 31) / 32, w.T), CTA, 0, st>>>(llr, frames, g.n, w.T, w.r, w.s, w.unsat, w.done, w.fbe,
-                                                           w.fraw, w.fnz);
+                                                           w.fraw, w.fnz, w.tcount, w.tlist);
     return 1;
 }
 

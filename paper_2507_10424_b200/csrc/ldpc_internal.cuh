@@ -41,6 +41,8 @@ struct StreamState {
     void *loc;
     uint32_t *sgn, *unsat, *done;
     int *iters, *fbe, *fraw, *fnz;
+    int *tcount;  // [2]     number of tiles with a running frame, per body parity
+    int *tlist;   // [2][T]  those tiles
 };
 
 // ---- ingest (ingest.cu) ----
@@ -63,6 +65,8 @@ struct StreamLaunch {
     int cols_per_cta = 32;
     int cn_unroll = 1;  // check-node edges per load batch (1, 2, 4)
     int bn_unroll = 1;  // bit-node edges per load batch (1, 2)
+    int cn_ctas = 4736;  // grid caps of the (tile x block) work loops: a few waves of resident CTAs
+    int bn_ctas = 7104;
 };
 // Launch helpers; each returns the number of kernels launched.
 int launch_stage_in(const Graph &g, const StreamState &w, const float *llr, int64_t frames, cudaStream_t st);

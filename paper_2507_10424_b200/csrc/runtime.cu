@@ -89,6 +89,7 @@ size_t tile_bytes(const HostGraph &g, bool loc16) {
     b += align256(E * 16);                           // sgn
     b += 3 * 256;                                    // unsat x2, done
     b += 4 * align256(TILE * 4);                     // iters, fbe, fraw, fnz
+    b += 3 * 4 + 256;                                // tcount, tlist
     return b;
 }
 
@@ -115,6 +116,8 @@ StreamState carve(void *base, int T, const HostGraph &g, bool loc16) {
     w.fbe = reinterpret_cast<int *>(take((size_t)T * TILE * 4));
     w.fraw = reinterpret_cast<int *>(take((size_t)T * TILE * 4));
     w.fnz = reinterpret_cast<int *>(take((size_t)T * TILE * 4));
+    w.tcount = reinterpret_cast<int *>(take(2 * 4));
+    w.tlist = reinterpret_cast<int *>(take((size_t)2 * T * 4));
     return w;
 }
 
@@ -133,7 +136,8 @@ int ensure_ws(ldpc_plan *h, int T, bool loc16) {
         const size_t m = h->g.m, n = h->g.n, E = h->g.E;
         need = 2 * align256((size_t)T * n * TILE * 4) + 2 * align256((size_t)T * m * TILE * 4) +
                align256((size_t)T * m * TILE * (loc16 ? 2 : 1)) + align256((size_t)T * E * 16) +
-               align256((size_t)2 * T * 16) + align256((size_t)T * 16) + 4 * align256((size_t)T * TILE * 4);
+               align256((size_t)2 * T * 16) + align256((size_t)T * 16) + 4 * align256((size_t)T * TILE * 4) +
+               align256(8) + align256((size_t)2 * T * 4);
     }
     if (need <= h->ws_bytes) return LDPC_OK;
     if (h->ws) cudaFree(h->ws);
@@ -231,6 +235,12 @@ int finish_prepare(ldpc_plan *p, int rc, uint32_t flags, ldpc_handle_t *out) {
     p->rp = plan_resident(p->g, p->g.max_row_deg > 255, p->device);
     if (const char *s = getenv("LDPC_ROWS_PER_CTA")) p->cfg.rows_per_cta = std::max(8, atoi(s));
     if (const char *s = getenv("LDPC_COLS_PER_CTA")) p->cfg.cols_per_cta = std::max(8, atoi(s));
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
+    p->cfg.cn_ctas = sms * 4 * 2;  // 4 resident CTAs per SM (64-register kernel), two waves
+    p->cfg.bn_ctas = sms * 6 * 2;
+    if (const char *s = getenv("LDPC_CN_CTAS")) p->cfg.cn_ctas = std::max(1, atoi(s));
+    if (const char *s = getenv("LDPC_BN_CTAS")) p->cfg.bn_ctas = std::max(1, atoi(s));
     if (const char *s = getenv("LDPC_CN_UNROLL")) p->cfg.cn_unroll = std::max(1, atoi(s));
     if (const char *s = getenv("LDPC_BN_UNROLL")) p->cfg.bn_unroll = std::max(1, atoi(s));
     *out = p;

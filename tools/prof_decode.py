@@ -15,6 +15,7 @@ ap.add_argument("--point", type=int, default=0)
 ap.add_argument("--frames", type=int, default=0, help="0 = the config's block size")
 ap.add_argument("--flags", type=int, default=0)
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--max-iter", type=int, default=0)
 args = ap.parse_args()
 cfg = codes.CONFIGS[args.config]
 code = cfg["code"]()
@@ -29,7 +30,7 @@ print("schedule", h.schedule, "frames", F)
 st = torch.zeros(8, dtype=torch.int64, device="cuda")
 h.profile(True)
 for _ in range(args.reps):
-    out = h.decode(llr, cfg["max_iter"], posterior=True, stats=st)
+    out = h.decode(llr, args.max_iter or cfg["max_iter"], posterior=True, stats=st)
 torch.cuda.synchronize()
 print(h.profile_read())
 print(P.stats_dict(st))
