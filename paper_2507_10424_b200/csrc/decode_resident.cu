@@ -165,6 +165,7 @@ __device__ __forceinline__ void cn_rows(const float *s, float *mn0, float *mn1, 
         }
 #pragma unroll
         for (int v = 0; v < 4; v++) parw[v] ^= bal[v];
+        __syncwarp();  // the row group's reads of sg[e] precede its rewrite (memory order, not just convergence)
         if (has && l == 0) {
             unsigned word = 0;
 #pragma unroll
@@ -275,11 +276,11 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
                 }
             }
             // refill: the free slots take consecutive frames from the global counter
+            const bool exhausted = ctl[3] != 0;
             const unsigned freem = __ballot_sync(FULLM, mine && f < 0);
             long long base = 0;
-            if (lane == 0 && freem && !ctl[3]) base = atomicAdd(a.counter, __popc(freem));
+            if (lane == 0 && freem && !exhausted) base = atomicAdd(a.counter, __popc(freem));
             base = __shfl_sync(FULLM, base, 0);
-            const bool exhausted = ctl[3] != 0;
             unsigned fresh = 0;
             if (freem && !exhausted) {
                 const long long mine_f = base + __popc(freem & ((1u << lane) - 1u));
@@ -292,10 +293,12 @@ __global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
                     slot_nz[lane] = 0;
                 }
                 fresh = __ballot_sync(FULLM, take);
+                __syncwarp();  // every lane has read ctl[3] before lane 0 sets it
                 if (lane == 0 && base + __popc(freem) >= a.frames) ctl[3] = 1;
             }
             if (mine) slot_f[lane] = f;
             const unsigned active = __ballot_sync(FULLM, mine && f >= 0);
+            __syncwarp();  // every lane has read ctl[] before lane 0 rewrites it
             if (lane == 0) {
                 ctl[0] = 0;
                 ctl[1] = fresh;
