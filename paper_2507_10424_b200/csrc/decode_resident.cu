@@ -191,7 +191,7 @@ __device__ __forceinline__ void cn_rows(const float *s, float *mn0, float *mn1, 
 // Lane layout: a lane owns 4 consecutive slots (float4) of one row or column; LR = S/4 lanes cover a
 // row, G = 32/LR rows per warp.  Bit of slot q = 4*l + v inside an S-bit sign word: v*LR + l.
 template <int S, int RT>
-__global__ void __launch_bounds__(RT, 1) k_resident(ResArgs a) {
+__global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? 2 : 1) k_resident(ResArgs a) {
     constexpr int NWARP = RT / 32;
     using SWT = typename SWord<S>::T;
     constexpr int LR = S / 4;
@@ -481,6 +481,8 @@ void launch_s(const ResArgs &args, int ctas, size_t smem, cudaStream_t st) {
 template <int S>
 void launch_t(const ResArgs &args, int threads, int ctas, size_t smem, cudaStream_t st) {
     if (threads == 1024) launch_s<S, 1024>(args, ctas, smem, st);
+    else if (threads == 256) launch_s<S, 256>(args, ctas, smem, st);
+    else if (threads == 128) launch_s<S, 128>(args, ctas, smem, st);
     else launch_s<S, 512>(args, ctas, smem, st);
 }
 
@@ -491,19 +493,30 @@ ResidentPlan plan_resident(const HostGraph &g, bool loc16, int device) {
     ResidentPlan rp;
     if (g.n >= 65535 || g.m >= 65535 || g.E >= 65535 || g.E == 0) return rp;
     const int cap = max_smem_optin(device);
-    int sms = 0;
+    int sms = 0, sm_smem = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    cudaDeviceGetAttribute(&sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
     if (cap <= 0 || sms <= 0) return rp;
-    for (int S : {32, 16, 8, 4}) {
-        const Layout L = layout_for(S, g.m, g.n, g.E);
-        if (L.total <= (size_t)cap) {
+    int force_s = 0, force_t = 0;
+    if (const char *e = getenv("LDPC_RES_SLOTS")) force_s = atoi(e);
+    if (const char *e = getenv("LDPC_RES_THREADS")) force_t = atoi(e);
+    // Prefer the largest S with two CTAs per SM (their phases interleave: measured 3-12 % faster on
+    // the C2 code than one CTA of 2S slots), else the largest S with one CTA per SM.
+    for (int pass = 0; pass < 2 && !rp.ok; pass++) {
+        for (int S : {32, 16, 8, 4}) {
+            if (force_s && S != force_s) continue;
+            const Layout L = layout_for(S, g.m, g.n, g.E);
+            if (L.total > (size_t)cap) continue;
+            const int per_sm = std::max(1, std::min(2, sm_smem / (int)(L.total + 1024)));
+            if (pass == 0 && per_sm < 2 && !force_s) continue;
             rp.ok = true;
             rp.slots = S;
-            rp.threads = 512;
-            if (const char *e = getenv("LDPC_RES_THREADS")) rp.threads = atoi(e) == 1024 ? 1024 : 512;
             rp.smem = L.total;
-            rp.ctas = sms;
-            return rp;
+            rp.threads = per_sm >= 2 ? 256 : 512;
+            if (force_t == 128 || force_t == 256 || force_t == 512 || force_t == 1024) rp.threads = force_t;
+            const int fit = rp.threads == 128 ? per_sm : rp.threads == 256 ? std::min(per_sm, 2) : 1;
+            rp.ctas = sms * fit;
+            break;
         }
     }
     return rp;

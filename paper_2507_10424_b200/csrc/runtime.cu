@@ -310,7 +310,7 @@ int ldpc_decode_host(ldpc_handle_t h, const float *llr, int64_t frames, int32_t 
     if (frames == 0) return LDPC_OK;
     const int64_t n = h->g.n;
     // chunk of frames per pipeline stage
-    int64_t chunk = std::max<int64_t>(TILE, std::min<int64_t>(frames, (int64_t)(256u << 20) / (n * 4)));
+    int64_t chunk = std::max<int64_t>(TILE, std::min<int64_t>(frames, (int64_t)(96u << 20) / (n * 4)));
     chunk = (chunk + TILE - 1) / TILE * TILE;
     const size_t per_frame = n * 4 + (bits_out ? n : 0) + (posterior_out ? n * 4 : 0) + 4 + 1;
     const size_t set_bytes = align256(chunk * n * 4) + align256(chunk * n) + align256(chunk * n * 4) +
