@@ -76,8 +76,11 @@ enum ldpc_flags {
     LDPC_FLAG_NO_EARLY_STOP = 2u,      /* no pre-check, no early exit: every frame runs exactly max_iter
                                           bodies; converged = (H.b == 0) after the last body */
     LDPC_FLAG_FORCE_STREAM = 4u,       /* always use the HBM-streaming schedule (per-iteration CN/BN sweeps) */
-    LDPC_FLAG_FORCE_RESIDENT = 8u      /* always use the SMEM-resident schedule (fails with UNSUPPORTED if the
+    LDPC_FLAG_FORCE_RESIDENT = 8u,     /* always use the SMEM-resident schedule (fails with UNSUPPORTED if the
                                           per-frame state of H does not fit shared memory) */
+    LDPC_FLAG_NO_GRAPH = 16u           /* streaming schedule: issue every loop body as plain stream-ordered
+                                          launches instead of one CUDA graph per chunk (whose conditional
+                                          WHILE node stops launching bodies once every frame has stopped) */
 };
 
 /*

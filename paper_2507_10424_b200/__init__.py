@@ -22,6 +22,7 @@ FLAG_SIGN_PAPER_LITERAL = 1
 FLAG_NO_EARLY_STOP = 2
 FLAG_FORCE_STREAM = 4
 FLAG_FORCE_RESIDENT = 8
+FLAG_NO_GRAPH = 16
 
 KERNEL_CLASSES = ("ingest", "stage_in", "check_node", "bit_node", "syndrome", "finalize", "resident")
 

@@ -121,8 +121,9 @@ struct MinBlocks {
 
 template <typename LocT, bool FIRST, bool EARLY, int CN_U>
 __global__ void __launch_bounds__(CTA, MinBlocks<CN_U>::value)
-    k_cn(Graph g, StreamState w, int k, int rows_per_cta, int literal) {
+    k_cn(Graph g, StreamState w, int k, int rows_per_cta, int literal, const int *kdev) {
     using L4 = typename Vec4<LocT>::type;
+    if (kdev) k = *kdev;  // body index supplied by the graph-driven loop
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     __shared__ uint32_t s_u[4];
     // the tiles of body k are the ones with a running frame (list rebuilt by k_bn of body k-1)
@@ -253,8 +254,9 @@ __global__ void __launch_bounds__(CTA, MinBlocks<CN_U>::value)
 // ------------------------------------------------------------------------------------------------
 template <typename LocT, bool EARLY, int BN_U>
 __global__ void __launch_bounds__(CTA, BN_U <= 1 ? 6 : MinBlocks<BN_U>::value)
-    k_bn(Graph g, StreamState w, int k, int cols_per_cta, int literal) {
+    k_bn(Graph g, StreamState w, int k, int cols_per_cta, int literal, const int *kdev) {
     using L4 = typename Vec4<LocT>::type;
+    if (kdev) k = *kdev;
     (void)literal;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int T = w.T;
@@ -496,6 +498,24 @@ __global__ void __launch_bounds__(CTA) k_frame_stats(StreamState w, int64_t fram
     }
 }
 
+// Graph-driven loop control (CUDA conditional WHILE node): body k runs while k <= L and some tile
+// still has a running frame.  On an early end, the list the final syndrome pass reads is emptied.
+__global__ void k_loop_pre(StreamState w, int L, cudaGraphConditionalHandle h) {
+    const int k = 2;
+    const bool run = k <= L && w.tcount[k & 1] > 0;
+    *w.kdev = k;
+    if (!run) w.tcount[(L + 1) & 1] = 0;
+    cudaGraphSetConditional(h, run ? 1u : 0u);
+}
+
+__global__ void k_loop_step(StreamState w, int L, cudaGraphConditionalHandle h) {
+    const int k = *w.kdev + 1;
+    const bool run = k <= L && w.tcount[k & 1] > 0;
+    *w.kdev = k;
+    if (!run && k <= L) w.tcount[(L + 1) & 1] = 0;
+    cudaGraphSetConditional(h, run ? 1u : 0u);
+}
+
 inline dim3 grid2(int64_t x, int y) { return dim3((unsigned)std::max<int64_t>(1, x), (unsigned)y); }
 
 }  // namespace
@@ -507,46 +527,48 @@ int launch_stage_in(const Graph &g, const StreamState &w, const float *llr, int6
 }
 
 template <typename LT, bool F, bool EA>
-void cn_launch(dim3 grid, cudaStream_t st, const Graph &g, const StreamState &w, int k, int rpc, int lit, int u) {
-    if (u >= 4) k_cn<LT, F, EA, 4><<<grid, CTA, 0, st>>>(g, w, k, rpc, lit);
-    else if (u == 2) k_cn<LT, F, EA, 2><<<grid, CTA, 0, st>>>(g, w, k, rpc, lit);
-    else k_cn<LT, F, EA, 1><<<grid, CTA, 0, st>>>(g, w, k, rpc, lit);
+void cn_launch(dim3 grid, cudaStream_t st, const Graph &g, const StreamState &w, int k, int rpc, int lit, int u,
+               const int *kdev) {
+    if (u >= 4) k_cn<LT, F, EA, 4><<<grid, CTA, 0, st>>>(g, w, k, rpc, lit, kdev);
+    else if (u == 2) k_cn<LT, F, EA, 2><<<grid, CTA, 0, st>>>(g, w, k, rpc, lit, kdev);
+    else k_cn<LT, F, EA, 1><<<grid, CTA, 0, st>>>(g, w, k, rpc, lit, kdev);
 }
 
 template <typename LT, bool EA>
-void bn_launch(dim3 grid, cudaStream_t st, const Graph &g, const StreamState &w, int k, int cpc, int lit, int u) {
-    if (u >= 2) k_bn<LT, EA, 2><<<grid, CTA, 0, st>>>(g, w, k, cpc, lit);
-    else k_bn<LT, EA, 1><<<grid, CTA, 0, st>>>(g, w, k, cpc, lit);
+void bn_launch(dim3 grid, cudaStream_t st, const Graph &g, const StreamState &w, int k, int cpc, int lit, int u,
+               const int *kdev) {
+    if (u >= 2) k_bn<LT, EA, 2><<<grid, CTA, 0, st>>>(g, w, k, cpc, lit, kdev);
+    else k_bn<LT, EA, 1><<<grid, CTA, 0, st>>>(g, w, k, cpc, lit, kdev);
 }
 
 int launch_check_node(const Graph &g, const StreamState &w, int k, bool first, bool early, bool literal, bool loc16,
-                      const StreamLaunch &cfg, cudaStream_t st) {
+                      const StreamLaunch &cfg, cudaStream_t st, const int *kdev) {
     const dim3 grid = grid2((g.m + cfg.rows_per_cta - 1) / cfg.rows_per_cta, w.T);
     const int lit = literal ? 1 : 0, rpc = cfg.rows_per_cta, u = cfg.cn_unroll;
     if (loc16) {
-        if (first) { if (early) cn_launch<uint16_t, true, true>(grid, st, g, w, k, rpc, lit, u);
-                     else cn_launch<uint16_t, true, false>(grid, st, g, w, k, rpc, lit, u); }
-        else { if (early) cn_launch<uint16_t, false, true>(grid, st, g, w, k, rpc, lit, u);
-               else cn_launch<uint16_t, false, false>(grid, st, g, w, k, rpc, lit, u); }
+        if (first) { if (early) cn_launch<uint16_t, true, true>(grid, st, g, w, k, rpc, lit, u, kdev);
+                     else cn_launch<uint16_t, true, false>(grid, st, g, w, k, rpc, lit, u, kdev); }
+        else { if (early) cn_launch<uint16_t, false, true>(grid, st, g, w, k, rpc, lit, u, kdev);
+               else cn_launch<uint16_t, false, false>(grid, st, g, w, k, rpc, lit, u, kdev); }
     } else {
-        if (first) { if (early) cn_launch<uint8_t, true, true>(grid, st, g, w, k, rpc, lit, u);
-                     else cn_launch<uint8_t, true, false>(grid, st, g, w, k, rpc, lit, u); }
-        else { if (early) cn_launch<uint8_t, false, true>(grid, st, g, w, k, rpc, lit, u);
-               else cn_launch<uint8_t, false, false>(grid, st, g, w, k, rpc, lit, u); }
+        if (first) { if (early) cn_launch<uint8_t, true, true>(grid, st, g, w, k, rpc, lit, u, kdev);
+                     else cn_launch<uint8_t, true, false>(grid, st, g, w, k, rpc, lit, u, kdev); }
+        else { if (early) cn_launch<uint8_t, false, true>(grid, st, g, w, k, rpc, lit, u, kdev);
+               else cn_launch<uint8_t, false, false>(grid, st, g, w, k, rpc, lit, u, kdev); }
     }
     return 1;
 }
 
 int launch_bit_node(const Graph &g, const StreamState &w, int k, bool early, bool literal, bool loc16,
-                    const StreamLaunch &cfg, cudaStream_t st) {
+                    const StreamLaunch &cfg, cudaStream_t st, const int *kdev) {
     const dim3 grid = grid2((g.n + cfg.cols_per_cta - 1) / cfg.cols_per_cta, w.T);
     const int lit = literal ? 1 : 0, cpc = cfg.cols_per_cta, u = cfg.bn_unroll;
     if (loc16) {
-        if (early) bn_launch<uint16_t, true>(grid, st, g, w, k, cpc, lit, u);
-        else bn_launch<uint16_t, false>(grid, st, g, w, k, cpc, lit, u);
+        if (early) bn_launch<uint16_t, true>(grid, st, g, w, k, cpc, lit, u, kdev);
+        else bn_launch<uint16_t, false>(grid, st, g, w, k, cpc, lit, u, kdev);
     } else {
-        if (early) bn_launch<uint8_t, true>(grid, st, g, w, k, cpc, lit, u);
-        else bn_launch<uint8_t, false>(grid, st, g, w, k, cpc, lit, u);
+        if (early) bn_launch<uint8_t, true>(grid, st, g, w, k, cpc, lit, u, kdev);
+        else bn_launch<uint8_t, false>(grid, st, g, w, k, cpc, lit, u, kdev);
     }
     return 1;
 }
@@ -554,6 +576,16 @@ int launch_bit_node(const Graph &g, const StreamState &w, int k, bool early, boo
 int launch_syndrome(const Graph &g, const StreamState &w, int slot, const StreamLaunch &cfg, cudaStream_t st) {
     k_syndrome<<<grid2((g.m + cfg.rows_per_cta - 1) / cfg.rows_per_cta, w.T), CTA, 0, st>>>(g, w, slot,
                                                                                              cfg.rows_per_cta);
+    return 1;
+}
+
+int launch_loop_pre(const StreamState &w, int L, cudaGraphConditionalHandle h, cudaStream_t st) {
+    k_loop_pre<<<1, 1, 0, st>>>(w, L, h);
+    return 1;
+}
+
+int launch_loop_step(const StreamState &w, int L, cudaGraphConditionalHandle h, cudaStream_t st) {
+    k_loop_step<<<1, 1, 0, st>>>(w, L, h);
     return 1;
 }
 

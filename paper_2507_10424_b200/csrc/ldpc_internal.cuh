@@ -43,6 +43,7 @@ struct StreamState {
     int *iters, *fbe, *fraw, *fnz;
     int *tcount;  // [2]     number of tiles with a running frame, per body parity
     int *tlist;   // [2][T]  those tiles
+    int *kdev;    // body index of the graph-driven loop
 };
 
 // ---- ingest (ingest.cu) ----
@@ -71,9 +72,11 @@ struct StreamLaunch {
 // Launch helpers; each returns the number of kernels launched.
 int launch_stage_in(const Graph &g, const StreamState &w, const float *llr, int64_t frames, cudaStream_t st);
 int launch_check_node(const Graph &g, const StreamState &w, int k, bool first, bool early, bool literal, bool loc16,
-                      const StreamLaunch &cfg, cudaStream_t st);
+                      const StreamLaunch &cfg, cudaStream_t st, const int *kdev = nullptr);
 int launch_bit_node(const Graph &g, const StreamState &w, int k, bool early, bool literal, bool loc16,
-                    const StreamLaunch &cfg, cudaStream_t st);
+                    const StreamLaunch &cfg, cudaStream_t st, const int *kdev = nullptr);
+int launch_loop_pre(const StreamState &w, int L, cudaGraphConditionalHandle h, cudaStream_t st);
+int launch_loop_step(const StreamState &w, int L, cudaGraphConditionalHandle h, cudaStream_t st);
 int launch_syndrome(const Graph &g, const StreamState &w, int slot, const StreamLaunch &cfg, cudaStream_t st);
 int launch_finalize(const Graph &g, const StreamState &w, int64_t frames, float *posterior, uint8_t *bits,
                     cudaStream_t st);

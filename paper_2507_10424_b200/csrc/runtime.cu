@@ -37,6 +37,21 @@ struct ldpc_plan {
     std::vector<cudaEvent_t> pool;
     int64_t prof_launches[LDPC_K_NUM_CLASSES] = {};
     double prof_ms[LDPC_K_NUM_CLASSES] = {};
+    // graph-driven decode loops (one instantiated graph per distinct chunk launch)
+    struct GraphEntry {
+        const void *key[8];
+        int64_t fc;
+        int L;
+        uint32_t flags;
+        void *ws;
+        cudaGraph_t graph;
+        cudaGraphExec_t exec;
+        uint64_t used;
+    };
+    std::vector<GraphEntry> graphs;
+    uint64_t graph_clock = 0;
+    bool use_graphs = true;
+    cudaStream_t cap[2] = {nullptr, nullptr};
     // host pipeline
     cudaStream_t hs[3] = {nullptr, nullptr, nullptr};
     void *hbuf[2] = {nullptr, nullptr};
@@ -118,6 +133,7 @@ StreamState carve(void *base, int T, const HostGraph &g, bool loc16) {
     w.fnz = reinterpret_cast<int *>(take((size_t)T * TILE * 4));
     w.tcount = reinterpret_cast<int *>(take(2 * 4));
     w.tlist = reinterpret_cast<int *>(take((size_t)2 * T * 4));
+    w.kdev = reinterpret_cast<int *>(take(4));
     return w;
 }
 
@@ -137,9 +153,14 @@ int ensure_ws(ldpc_plan *h, int T, bool loc16) {
         need = 2 * align256((size_t)T * n * TILE * 4) + 2 * align256((size_t)T * m * TILE * 4) +
                align256((size_t)T * m * TILE * (loc16 ? 2 : 1)) + align256((size_t)T * E * 16) +
                align256((size_t)2 * T * 16) + align256((size_t)T * 16) + 4 * align256((size_t)T * TILE * 4) +
-               align256(8) + align256((size_t)2 * T * 4);
+               align256(8) + align256((size_t)2 * T * 4) + align256(4);
     }
     if (need <= h->ws_bytes) return LDPC_OK;
+    for (auto &ge : h->graphs) {  // graphs embed workspace pointers
+        cudaGraphExecDestroy(ge.exec);
+        cudaGraphDestroy(ge.graph);
+    }
+    h->graphs.clear();
     if (h->ws) cudaFree(h->ws);
     h->ws = nullptr;
     h->ws_bytes = 0;
@@ -161,6 +182,101 @@ int check_async(ldpc_plan *h) {
     return LDPC_OK;
 }
 
+// One chunk as a CUDA graph: stage-in, body 1, then a conditional WHILE node whose body (check node,
+// bit node, loop step) repeats while a frame is still running and k <= L, then the final syndrome
+// pass and stage-out.  No host round trip and no launch for bodies after the last frame stopped.
+template <typename Tail>
+int run_graph(ldpc_plan *h, const Graph &g, const StreamState &w, const float *llr, int64_t fc, int L, bool early,
+              bool literal, bool loc16, float *post, uint8_t *bits, int32_t *iters, uint8_t *conv, int64_t *stats,
+              cudaStream_t st, Tail &&tail) {
+    const void *key[8] = {llr, post, bits, iters, conv, stats, w.r, nullptr};
+    for (auto &ge : h->graphs) {
+        if (std::equal(key, key + 8, ge.key) && ge.fc == fc && ge.L == L && ge.flags == h->flags && ge.ws == h->ws) {
+            ge.used = ++h->graph_clock;
+            if (cudaGraphLaunch(ge.exec, st) != cudaSuccess) {
+                h->poisoned = true;
+                return LDPC_ERR_CUDA;
+            }
+            h->launches += 4 + 3 + 3 * L;  // upper bound: stage-in, body 1, pre, bodies, tail
+            return LDPC_OK;
+        }
+    }
+    if (!h->cap[0]) {
+        for (int q = 0; q < 2; q++)
+            if (cudaStreamCreateWithFlags(&h->cap[q], cudaStreamNonBlocking) != cudaSuccess) return LDPC_ERR_CUDA;
+    }
+    cudaStream_t c0 = h->cap[0], c1 = h->cap[1];
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamBeginCapture(c0, cudaStreamCaptureModeRelaxed);
+    if (e != cudaSuccess) return status_of(e);
+    launch_stage_in(g, w, llr, fc, c0);
+    launch_check_node(g, w, 1, true, early, literal, loc16, h->cfg, c0);
+    launch_bit_node(g, w, 1, early, literal, loc16, h->cfg, c0);
+    cudaStreamCaptureStatus cs;
+    cudaGraph_t capg = nullptr;
+    const cudaGraphNode_t *deps = nullptr;
+    size_t ndeps = 0;
+    e = cudaStreamGetCaptureInfo(c0, &cs, nullptr, &capg, &deps, &ndeps);
+    cudaGraphConditionalHandle handle{};
+    if (e == cudaSuccess) e = cudaGraphConditionalHandleCreate(&handle, capg, 0, cudaGraphCondAssignDefault);
+    if (e == cudaSuccess) launch_loop_pre(w, L, handle, c0);
+    if (e == cudaSuccess) e = cudaStreamGetCaptureInfo(c0, &cs, nullptr, &capg, &deps, &ndeps);
+    cudaGraphNode_t cond = nullptr;
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = handle;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    if (e == cudaSuccess) e = cudaGraphAddNode(&cond, capg, deps, ndeps, &cp);
+    if (e == cudaSuccess) e = cudaStreamUpdateCaptureDependencies(c0, &cond, 1, cudaStreamSetCaptureDependencies);
+    if (e == cudaSuccess) {
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        e = cudaStreamBeginCaptureToGraph(c1, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed);
+        if (e == cudaSuccess) {
+            launch_check_node(g, w, 2, false, early, literal, loc16, h->cfg, c1, w.kdev);
+            launch_bit_node(g, w, 2, early, literal, loc16, h->cfg, c1, w.kdev);
+            launch_loop_step(w, L, handle, c1);
+            cudaGraph_t out = nullptr;
+            e = cudaStreamEndCapture(c1, &out);
+        }
+    }
+    if (e == cudaSuccess) tail(c0);
+    cudaError_t e2 = cudaStreamEndCapture(c0, &graph);
+    if (e == cudaSuccess) e = e2;
+    cudaGraphExec_t exec = nullptr;
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&exec, graph, 0);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        if (graph) cudaGraphDestroy(graph);
+        h->use_graphs = false;  // fall back to plain stream-ordered launches on this handle
+        return LDPC_ERR_UNSUPPORTED;
+    }
+    if (h->graphs.size() >= 32) {  // evict the least recently used graph
+        size_t v = 0;
+        for (size_t q = 1; q < h->graphs.size(); q++)
+            if (h->graphs[q].used < h->graphs[v].used) v = q;
+        cudaGraphExecDestroy(h->graphs[v].exec);
+        cudaGraphDestroy(h->graphs[v].graph);
+        h->graphs.erase(h->graphs.begin() + v);
+    }
+    ldpc_plan::GraphEntry ge;
+    std::copy(key, key + 8, ge.key);
+    ge.fc = fc;
+    ge.L = L;
+    ge.flags = h->flags;
+    ge.ws = h->ws;
+    ge.graph = graph;
+    ge.exec = exec;
+    ge.used = ++h->graph_clock;
+    h->graphs.push_back(ge);
+    if (cudaGraphLaunch(exec, st) != cudaSuccess) {
+        h->poisoned = true;
+        return LDPC_ERR_CUDA;
+    }
+    h->launches += 4 + 3 + 3 * L;
+    return LDPC_OK;
+}
+
 int decode_stream(ldpc_plan *h, const float *llr, int64_t frames, int L, uint8_t *bits, int32_t *iters, float *post,
                   uint8_t *conv, int64_t *stats, cudaStream_t st) {
     const bool early = !(h->flags & LDPC_FLAG_NO_EARLY_STOP);
@@ -174,11 +290,29 @@ int decode_stream(ldpc_plan *h, const float *llr, int64_t frames, int L, uint8_t
     int rc = ensure_ws(h, T_max, loc16);
     if (rc) return rc;
     const int final_slot = (L + 1) & 1;
+    const bool graphs = h->use_graphs && !h->prof && L >= 2 && !(h->flags & LDPC_FLAG_NO_GRAPH);
     for (int64_t c0 = 0; c0 < frames; c0 += (int64_t)T_max * TILE) {
         const int64_t fc = std::min<int64_t>((int64_t)T_max * TILE, frames - c0);
         const int T = (int)((fc + TILE - 1) / TILE);
         const StreamState w = carve(h->ws, T, h->g, loc16);
-        launch(h, LDPC_K_STAGE_IN, st, [&] { return launch_stage_in(g, w, llr + c0 * g.n, fc, st); });
+        const float *cl = llr + c0 * g.n;
+        float *cp = post ? post + c0 * g.n : nullptr;
+        uint8_t *cb = bits ? bits + c0 * g.n : nullptr;
+        int32_t *ci = iters ? iters + c0 : nullptr;
+        uint8_t *cc = conv ? conv + c0 : nullptr;
+        auto tail = [&](cudaStream_t s2) {
+            int nl = launch_syndrome(g, w, final_slot, h->cfg, s2);
+            nl += launch_finalize(g, w, fc, cp, cb, s2);
+            nl += launch_frame_stats(g, w, fc, L, early, final_slot, ci, cc,
+                                     reinterpret_cast<unsigned long long *>(stats), s2);
+            return nl;
+        };
+        if (graphs && h->use_graphs) {
+            rc = run_graph(h, g, w, cl, fc, L, early, literal, loc16, cp, cb, ci, cc, stats, st, tail);
+            if (rc == LDPC_OK) continue;
+            if (rc != LDPC_ERR_UNSUPPORTED) return rc;
+        }
+        launch(h, LDPC_K_STAGE_IN, st, [&] { return launch_stage_in(g, w, cl, fc, st); });
         for (int k = 1; k <= L; k++) {
             launch(h, LDPC_K_CHECK_NODE, st,
                    [&] { return launch_check_node(g, w, k, k == 1, early, literal, loc16, h->cfg, st); });
@@ -186,9 +320,9 @@ int decode_stream(ldpc_plan *h, const float *llr, int64_t frames, int L, uint8_t
         }
         launch(h, LDPC_K_SYNDROME, st, [&] { return launch_syndrome(g, w, final_slot, h->cfg, st); });
         launch(h, LDPC_K_FINALIZE, st, [&] {
-            int nl = launch_finalize(g, w, fc, post ? post + c0 * g.n : nullptr, bits ? bits + c0 * g.n : nullptr, st);
-            nl += launch_frame_stats(g, w, fc, L, early, final_slot, iters ? iters + c0 : nullptr,
-                                     conv ? conv + c0 : nullptr, reinterpret_cast<unsigned long long *>(stats), st);
+            int nl = launch_finalize(g, w, fc, cp, cb, st);
+            nl += launch_frame_stats(g, w, fc, L, early, final_slot, ci, cc,
+                                     reinterpret_cast<unsigned long long *>(stats), st);
             return nl;
         });
         rc = check_async(h);
@@ -242,6 +376,7 @@ int finish_prepare(ldpc_plan *p, int rc, uint32_t flags, ldpc_handle_t *out) {
     if (const char *s = getenv("LDPC_CN_CTAS")) p->cfg.cn_ctas = std::max(1, atoi(s));
     if (const char *s = getenv("LDPC_BN_CTAS")) p->cfg.bn_ctas = std::max(1, atoi(s));
     if (const char *s = getenv("LDPC_CN_UNROLL")) p->cfg.cn_unroll = std::max(1, atoi(s));
+    if (const char *s = getenv("LDPC_NO_GRAPHS")) p->use_graphs = atoi(s) == 0;
     if (const char *s = getenv("LDPC_BN_UNROLL")) p->cfg.bn_unroll = std::max(1, atoi(s));
     *out = p;
     return LDPC_OK;
@@ -493,6 +628,12 @@ void ldpc_destroy(ldpc_handle_t h) {
         cudaEventDestroy(ev.b);
     }
     for (auto e : h->pool) cudaEventDestroy(e);
+    for (auto &ge : h->graphs) {
+        cudaGraphExecDestroy(ge.exec);
+        cudaGraphDestroy(ge.graph);
+    }
+    for (int q = 0; q < 2; q++)
+        if (h->cap[q]) cudaStreamDestroy(h->cap[q]);
     cudaGetLastError();
     delete h;
 }
