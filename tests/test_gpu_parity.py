@@ -4,6 +4,8 @@ Bar (north_star): decoded bits, per-frame iteration counts and isCodeword bit-ex
 within 1e-4 absolute/relative (the design is bit-exact, asserted separately); frames whose
 posterior has an entry within 1e-4 of zero are counted.
 """
+import sys
+
 import numpy as np
 import pytest
 import torch
@@ -279,3 +281,21 @@ def test_generator_device_independent():
     a = channel.bpsk_awgn(code.n, code.rate, 2.0, 1, 0, 1000, 500)
     b = channel.bpsk_awgn(code.n, code.rate, 2.0, 1, 0, 1000, 500, device="cuda").cpu()
     assert (a != b).sum().item() <= 2  # libm ulp differences can flip a rare last bit
+
+
+def test_compute_sanitizer_clean():
+    """memcheck and racecheck report nothing on small decodes of both schedules (T6)."""
+    import os
+    import shutil
+    import subprocess
+
+    cs = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    if not os.path.exists(cs):
+        pytest.skip("compute-sanitizer not available")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for tool in ("memcheck", "racecheck"):
+        r = subprocess.run([cs, "--tool", tool, "--error-exitcode", "3", sys.executable,
+                            os.path.join(root, "tools", "sanitize_run.py")], capture_output=True, text=True,
+                           timeout=900)
+        assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+        assert "0 errors" in r.stdout or "0 hazards" in r.stdout, r.stdout[-2000:]
