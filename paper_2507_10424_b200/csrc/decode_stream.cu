@@ -249,6 +249,200 @@ __global__ void __launch_bounds__(CTA, MinBlocks<CN_U>::value)
 }
 
 // ------------------------------------------------------------------------------------------------
+// Check-node sweep with TMA-style bulk-copy staging (cp.async.bulk + mbarrier, per-warp double
+// buffer).  A warp owns ROWS_PER_WARP rows of the block; while it computes row q from shared
+// memory, the bulk copies of row q+2 (the d gathered 512-byte s segments, the d sign words and the
+// old row state) are in flight, so every warp keeps a whole row of loads outstanding without
+// holding them in registers.  Same arithmetic and results as k_cn.
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_addr(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+constexpr int ROWS_PER_WARP = 8;
+
+// shared-memory bytes of one staging buffer for rows of degree <= dm
+__host__ __device__ constexpr int cn_stage_bytes(int dm, int locb) { return dm * 512 + dm * 16 + 1024 + 128 * locb + 16; }
+
+template <typename LocT, bool FIRST, bool EARLY>
+__global__ void __launch_bounds__(CTA) k_cn_tma(Graph g, StreamState w, int k, int dm, int literal, const int *kdev) {
+    using L4 = typename Vec4<LocT>::type;
+    if (kdev) k = *kdev;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ uint32_t s_u[4];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int cnt = w.tcount[k & 1];
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) w.tcount[(k + 1) & 1] = 0;
+    if ((int)blockIdx.y >= cnt) return;  // active tiles are compacted to the front of the list
+    const int t = w.tlist[(size_t)(k & 1) * w.T + blockIdx.y];
+    if (EARLY && threadIdx.x < 4) s_u[threadIdx.x] = 0;
+    const int sbytes = cn_stage_bytes(dm, (int)sizeof(LocT));
+    unsigned char *wbase = smem + (size_t)warp * 2 * sbytes;
+    // stage layout: s[dm][128] f32 | sw[dm][4] u32 | min0[128] | min1[128] | loc[128] | mbarrier
+    auto sbuf = [&](int b) { return reinterpret_cast<float *>(wbase + b * sbytes); };
+    auto swbuf = [&](int b) { return reinterpret_cast<uint32_t *>(wbase + b * sbytes + dm * 512); };
+    auto m0buf = [&](int b) { return reinterpret_cast<float *>(wbase + b * sbytes + dm * 528); };
+    auto m1buf = [&](int b) { return reinterpret_cast<float *>(wbase + b * sbytes + dm * 528 + 512); };
+    auto lcbuf = [&](int b) { return reinterpret_cast<LocT *>(wbase + b * sbytes + dm * 528 + 1024); };
+    auto bar = [&](int b) {
+        return reinterpret_cast<uint64_t *>(wbase + b * sbytes + dm * 528 + 1024 + 128 * sizeof(LocT));
+    };
+    if (lane == 0) {
+        mbar_init(bar(0), 1);
+        mbar_init(bar(1), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    const int *__restrict__ row_ptr = g.row_ptr;
+    const int *__restrict__ col_idx = g.col_idx;
+    const float *S = w.s;
+    uint32_t *SG = w.sgn;
+    float *M0 = w.min0;
+    float *M1 = w.min1;
+    LocT *LC = reinterpret_cast<LocT *>(w.loc);
+    const int m = g.m, n = g.n, E = g.E;
+    const size_t tm = (size_t)t * m, tn = (size_t)t * n, tE = (size_t)t * E;
+    const int sh = 4 * (lane & 7), wsel = lane >> 3;
+    const int rpc = (CTA / 32) * ROWS_PER_WARP;
+    const int i0 = blockIdx.x * rpc;
+    const int nq = max(0, min(ROWS_PER_WARP, (m - i0 - warp + (CTA / 32) - 1) / (CTA / 32)));
+
+    auto stage = [&](int q, int b) {
+        const int i = i0 + warp + (CTA / 32) * q;
+        const int a = __ldg(row_ptr + i), d = __ldg(row_ptr + i + 1) - a;
+        const unsigned bytes = (unsigned)d * (FIRST ? 512u : 528u) + (FIRST ? 0u : (unsigned)(1024 + 128 * sizeof(LocT)));
+        if (lane == 0) mbar_expect_tx(bar(b), bytes);
+        __syncwarp();
+        for (int p = lane; p < d; p += 32) {
+            const int j = __ldg(col_idx + a + p);
+            bulk_g2s(sbuf(b) + p * TILE, S + (tn + j) * TILE, 512, bar(b));
+            if (!FIRST) bulk_g2s(swbuf(b) + p * 4, SG + (tE + a + p) * 4, 16, bar(b));
+        }
+        if (!FIRST && lane == 31) {
+            const size_t st = (tm + i) * TILE;
+            bulk_g2s(m0buf(b), M0 + st, 512, bar(b));
+            bulk_g2s(m1buf(b), M1 + st, 512, bar(b));
+            bulk_g2s(lcbuf(b), LC + st, 128 * sizeof(LocT), bar(b));
+        }
+    };
+
+    if (nq > 0) stage(0, 0);
+    if (nq > 1) stage(1, 1);
+    uint32_t u0 = 0, u1 = 0, u2 = 0, u3 = 0;
+    for (int q = 0; q < nq; q++) {
+        const int b = q & 1;
+        const int i = i0 + warp + (CTA / 32) * q;
+        const int a = __ldg(row_ptr + i), d = __ldg(row_ptr + i + 1) - a;
+        const unsigned corr = (unsigned)(d & 1) & (unsigned)(!literal);  // (-1)^{d_i}, reading A1
+        mbar_wait(bar(b), (unsigned)(q >> 1) & 1u);
+        float4 om0 = make_float4(0.f, 0.f, 0.f, 0.f), om1 = om0;
+        L4 olc{};
+        if (!FIRST) {
+            om0 = *reinterpret_cast<const float4 *>(m0buf(b) + 4 * lane);
+            om1 = *reinterpret_cast<const float4 *>(m1buf(b) + 4 * lane);
+            olc = *reinterpret_cast<const L4 *>(lcbuf(b) + 4 * lane);
+        }
+        float nm0[4], nm1[4];
+        int nloc[4];
+        unsigned npar = 0, syn = 0;
+#pragma unroll
+        for (int v = 0; v < 4; v++) {
+            nm0[v] = __int_as_float(0x7f800000);
+            nm1[v] = __int_as_float(0x7f800000);
+            nloc[v] = 0;
+        }
+        for (int p = 0; p < d; p++) {
+            const float4 sv = *reinterpret_cast<const float4 *>(sbuf(b) + p * TILE + 4 * lane);
+            const unsigned sw = FIRST ? 0u : (swbuf(b)[p * 4 + wsel] >> sh);
+            unsigned nib = 0;
+#pragma unroll
+            for (int v = 0; v < 4; v++) {
+                const float sj = comp(sv, v);
+                float x = sj;
+                if (!FIRST) {
+                    const float m0v = comp(om0, v);
+                    const float mag = (p == compl4(olc, v)) ? comp(om1, v) : fabsf(m0v);  // Obs. 1
+                    const unsigned neg_eta = ((sw >> v) & 1u) ^ (__float_as_uint(m0v) >> 31);  // Obs. 2
+                    x = sj - (neg_eta ? -mag : mag);  // lambda_k - eta^prev_{i,k}
+                }
+                const float ax = fabsf(x);
+                const bool lt = ax < nm0[v];  // first strict minimum (A13)
+                nm1[v] = fminf(nm1[v], fmaxf(nm0[v], ax));
+                nm0[v] = fminf(nm0[v], ax);
+                nloc[v] = lt ? p : nloc[v];
+                nib |= (unsigned)(x < 0.f) << v;  // sign(0) = +1
+                if (EARLY) syn ^= (unsigned)(sj > 0.f) << v;  // b_j = slice(s_j)
+            }
+            npar ^= nib;
+            unsigned word = nib << sh;
+            word |= __shfl_xor_sync(FULL, word, 1);
+            word |= __shfl_xor_sync(FULL, word, 2);
+            word |= __shfl_xor_sync(FULL, word, 4);
+            if ((lane & 7) == 0) SG[(tE + a + p) * 4 + wsel] = word;
+        }
+        const size_t st = (tm + i) * TILE + 4 * lane;
+        const unsigned pc = npar ^ (corr ? 0xfu : 0u);
+        float4 o0;
+        o0.x = __uint_as_float(__float_as_uint(nm0[0]) | ((pc & 1u) << 31));
+        o0.y = __uint_as_float(__float_as_uint(nm0[1]) | (((pc >> 1) & 1u) << 31));
+        o0.z = __uint_as_float(__float_as_uint(nm0[2]) | (((pc >> 2) & 1u) << 31));
+        o0.w = __uint_as_float(__float_as_uint(nm0[3]) | (((pc >> 3) & 1u) << 31));
+        st4(M0 + st, o0);
+        st4(M1 + st, make_float4(nm1[0], nm1[1], nm1[2], nm1[3]));
+        L4 nl;
+        nl.x = (LocT)nloc[0];
+        nl.y = (LocT)nloc[1];
+        nl.z = (LocT)nloc[2];
+        nl.w = (LocT)nloc[3];
+        *reinterpret_cast<L4 *>(LC + st) = nl;
+        if (EARLY) {
+            u0 |= __ballot_sync(FULL, syn & 1u);
+            u1 |= __ballot_sync(FULL, syn & 2u);
+            u2 |= __ballot_sync(FULL, syn & 4u);
+            u3 |= __ballot_sync(FULL, syn & 8u);
+        }
+        // the generic-proxy reads of buffer b are done before the async proxy refills it
+        __syncwarp();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (q + 2 < nq) stage(q + 2, b);
+    }
+    if (EARLY) {
+        if (lane == 0) {
+            if (u0) atomicOr(&s_u[0], u0);
+            if (u1) atomicOr(&s_u[1], u1);
+            if (u2) atomicOr(&s_u[2], u2);
+            if (u3) atomicOr(&s_u[3], u3);
+        }
+        __syncthreads();
+        if (threadIdx.x < 4 && s_u[threadIdx.x])
+            atomicOr(w.unsat + ((size_t)(k & 1) * w.T + t) * 4 + threadIdx.x, s_u[threadIdx.x]);
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
 // a5/a6: bit-node sweep of loop body k; stops frames whose b^(k-1) satisfied every check.
 // Column edges in chunks of BN_U with all loads of a chunk in flight before the (ordered) sum.
 // ------------------------------------------------------------------------------------------------
@@ -541,8 +735,32 @@ void bn_launch(dim3 grid, cudaStream_t st, const Graph &g, const StreamState &w,
     else k_bn<LT, EA, 1><<<grid, CTA, 0, st>>>(g, w, k, cpc, lit, kdev);
 }
 
+template <typename LT, bool F, bool EA>
+void cn_tma_launch(const Graph &g, const StreamState &w, int k, int dm, int lit, const int *kdev, cudaStream_t st) {
+    const int rpc = (CTA / 32) * ROWS_PER_WARP;
+    const dim3 grid = grid2((g.m + rpc - 1) / rpc, w.T);
+    const size_t smem = (size_t)(CTA / 32) * 2 * cn_stage_bytes(dm, (int)sizeof(LT));
+    cudaFuncSetAttribute(k_cn_tma<LT, F, EA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_cn_tma<LT, F, EA><<<grid, CTA, smem, st>>>(g, w, k, dm, lit, kdev);
+}
+
 int launch_check_node(const Graph &g, const StreamState &w, int k, bool first, bool early, bool literal, bool loc16,
                       const StreamLaunch &cfg, cudaStream_t st, const int *kdev) {
+    if (cfg.cn_tma_dm > 0) {  // bulk-copy staged variant
+        const int dm = cfg.cn_tma_dm, lit = literal ? 1 : 0;
+        if (loc16) {
+            if (first) { if (early) cn_tma_launch<uint16_t, true, true>(g, w, k, dm, lit, kdev, st);
+                         else cn_tma_launch<uint16_t, true, false>(g, w, k, dm, lit, kdev, st); }
+            else { if (early) cn_tma_launch<uint16_t, false, true>(g, w, k, dm, lit, kdev, st);
+                   else cn_tma_launch<uint16_t, false, false>(g, w, k, dm, lit, kdev, st); }
+        } else {
+            if (first) { if (early) cn_tma_launch<uint8_t, true, true>(g, w, k, dm, lit, kdev, st);
+                         else cn_tma_launch<uint8_t, true, false>(g, w, k, dm, lit, kdev, st); }
+            else { if (early) cn_tma_launch<uint8_t, false, true>(g, w, k, dm, lit, kdev, st);
+                   else cn_tma_launch<uint8_t, false, false>(g, w, k, dm, lit, kdev, st); }
+        }
+        return 1;
+    }
     const dim3 grid = grid2((g.m + cfg.rows_per_cta - 1) / cfg.rows_per_cta, w.T);
     const int lit = literal ? 1 : 0, rpc = cfg.rows_per_cta, u = cfg.cn_unroll;
     if (loc16) {

@@ -66,6 +66,7 @@ struct StreamLaunch {
     int cols_per_cta = 32;
     int cn_unroll = 1;  // check-node edges per load batch (1, 2, 4)
     int bn_unroll = 1;  // bit-node edges per load batch (1, 2)
+    int cn_tma_dm = 0;   // > 0: bulk-copy staged check node for rows of degree <= this
     int cn_ctas = 4736;  // grid caps of the (tile x block) work loops: a few waves of resident CTAs
     int bn_ctas = 7104;
 };

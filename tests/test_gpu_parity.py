@@ -186,6 +186,20 @@ def test_graph_loop_equals_plain_launches(cfg_name, frames):
             assert np.array_equal(a, b)
 
 
+def test_bulk_copy_check_node_variant(monkeypatch):
+    """The opt-in cp.async.bulk/mbarrier-staged check node (LDPC_CN_TMA=1) is bit-identical."""
+    monkeypatch.setenv("LDPC_CN_TMA", "1")
+    cfg = codes.CONFIGS["c2"]
+    code = cfg["code"]()
+    parts = [channel.bpsk_awgn(code.n, code.rate, e, cfg["seed"], p, 100, 300).numpy() for p, e in enumerate(cfg["ebn0"])]
+    llr = np.concatenate(parts)
+    for flags in (FORCE_STREAM, FORCE_STREAM | 16, FORCE_STREAM | NOES | LIT):
+        compare(code, llr, cfg["max_iter"], flags, h=handle(code, flags))
+    code3 = codes.random_small(37, 70, 2, 2, 9)
+    llr3 = (np.random.default_rng(3).standard_normal((300, code3.n)) - 0.5).astype(np.float32)
+    compare(code3, llr3, 12, h=handle(code3, FORCE_STREAM))
+
+
 def test_nonzero_codewords_and_symmetry():
     """Random nonzero codewords (no all-zero bias) and the codeword-symmetry law on the GPU (T5)."""
     code = codes.paper_5x10()
