@@ -145,6 +145,14 @@ LDPC_API int ldpc_get_graph(ldpc_handle_t h, int32_t *row_ptr, int32_t *col_idx,
 /* Replace the handle's flags (ldpc_flags) for later decodes. */
 LDPC_API int ldpc_set_flags(ldpc_handle_t h, uint32_t flags);
 
+/*
+ * Codeword-test interval T >= 1 for later decodes (default 1 = Alg. 1): the test after loop
+ * body k runs when k % T == 0 or k == max_iter; the pre-loop test (k = 0) always runs.  T = 6 is the
+ * paper's experimental setting ("Termination was checked for every 6 iterations").
+ * Errors: INVALID_ARG (T < 1).
+ */
+LDPC_API int ldpc_set_check_every(ldpc_handle_t h, int32_t T);
+
 /* Cap the frames processed per workspace chunk (0 = automatic).  Rounded up to a multiple of 128. */
 LDPC_API int ldpc_set_chunk(ldpc_handle_t h, int64_t frames_per_chunk);
 

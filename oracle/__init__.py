@@ -57,7 +57,7 @@ def lib():
             f = getattr(L, f"oracle_decode_{sfx}")
             f.restype = ctypes.c_int
             f.argtypes = [P, P, ctypes.c_int64, ctypes.c_int, ctypes.c_int, P, ctypes.c_int64, ctypes.c_int,
-                          ctypes.c_int, ctypes.c_int, P, P, P, P]
+                          ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P, P, P]
             g = getattr(L, f"oracle_check_node_{sfx}")
             g.restype = None
             g.argtypes = [P, ctypes.c_int, ctypes.c_int, P]
@@ -88,13 +88,14 @@ def _coo(H):
     return rows.astype(np.int32), cols.astype(np.int32), Hd.shape[0], Hd.shape[1]
 
 
-_ERR = {-1: "index out of range", -2: "duplicate one in H", -3: "row of degree < 2"}
+_ERR = {-1: "index out of range", -2: "duplicate one in H", -3: "row of degree < 2", -4: "check_every must be >= 1"}
 
 
-def decode(H, r, max_iter: int, flags: int = 0, threads: int = 0, precision: str = "f32"):
+def decode(H, r, max_iter: int, flags: int = 0, threads: int = 0, precision: str = "f32", check_every: int = 1):
     """Decode frames r[F, n] (float32).  Returns (bits u8[F,n], iters i32[F], converged u8[F], posterior[F,n]).
 
-    posterior is float32 for precision="f32" and float64 for the fp64 shadow.
+    posterior is float32 for precision="f32" and float64 for the fp64 shadow.  check_every = T: the codeword
+    test after body k runs when k % T == 0 or k == max_iter; the pre-loop test always runs.
     """
     rows, cols, m, n = _coo(H)
     r = np.ascontiguousarray(r, dtype=np.float32)
@@ -110,8 +111,8 @@ def decode(H, r, max_iter: int, flags: int = 0, threads: int = 0, precision: str
     conv = np.zeros(F, np.uint8)
     post = np.zeros((F, n), np.float32 if precision == "f32" else np.float64)
     fn = getattr(lib(), f"oracle_decode_{precision}")
-    rc = fn(_ptr(rows), _ptr(cols), len(rows), m, n, _ptr(r), F, int(max_iter), int(flags), int(threads),
-            _ptr(bits), _ptr(iters), _ptr(conv), _ptr(post))
+    rc = fn(_ptr(rows), _ptr(cols), len(rows), m, n, _ptr(r), F, int(max_iter), int(check_every), int(flags),
+            int(threads), _ptr(bits), _ptr(iters), _ptr(conv), _ptr(post))
     if rc:
         raise ValueError(_ERR.get(rc, f"oracle error {rc}"))
     return bits, iters, conv, post

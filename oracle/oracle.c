@@ -163,7 +163,7 @@ void NAME(oracle_check_node)(const REAL *x, int d, int flags, REAL *eta) {
     check_node(x, d, flags & ORACLE_SIGN_PAPER_LITERAL, eta);
 }
 
-static void decode_frame(const graph_t *g, const float *r_in, int L, int flags, REAL *s, REAL *r, REAL *eta,
+static void decode_frame(const graph_t *g, const float *r_in, int L, int T, int flags, REAL *s, REAL *r, REAL *eta,
                          REAL *xbuf, REAL *ebuf, uint8_t *b, uint8_t *bits_out, int32_t *iters_out,
                          uint8_t *conv_out, REAL *post_out) {
     const int m = g->m, n = g->n;
@@ -192,7 +192,9 @@ static void decode_frame(const graph_t *g, const float *r_in, int L, int flags, 
         }
         k = k + 1; /* P:171 */
         for (int j = 0; j < n; j++) b[j] = (s[j] > (REAL)0) ? 1 : 0;
-        if (early && syndrome_weight(g, b) == 0) is_codeword = 1; /* P:165-170 */
+        /* the codeword test runs every T bodies and after the last one ("Termination was checked for
+           every 6 iterations", P:498; SPEC checkEvery, S:226); T = 1 is Alg. 1 (P:165-170) */
+        if (early && (k % T == 0 || k == L) && syndrome_weight(g, b) == 0) is_codeword = 1;
     }
     if (!early) is_codeword = (syndrome_weight(g, b) == 0);
     for (int j = 0; j < n; j++) bits_out[j] = b[j];
@@ -204,13 +206,15 @@ static void decode_frame(const graph_t *g, const float *r_in, int L, int flags, 
 
 /*
  * Decode `frames` independent frames r[f*n .. f*n+n) with the same H given as
- * its list of ones (rows[t], cols[t]), t < nnz, 0-based.  Outputs as in
+ * its list of ones (rows[t], cols[t]), t < nnz, 0-based.  check_every = T >= 1: the
+ * codeword test after loop body k runs when k % T == 0 or k == L (the pre-loop test always).  Outputs as in
  * Alg. 1's KwOut: bits, k, isCodeword, plus the soft vector s.
  * Returns 0 or a negative graph_build error.  threads <= 0 -> library default.
  */
 int NAME(oracle_decode)(const int32_t *rows, const int32_t *cols, int64_t nnz, int m, int n, const float *r,
-                        int64_t frames, int L, int flags, int threads, uint8_t *bits_out, int32_t *iters_out,
-                        uint8_t *conv_out, REAL *post_out) {
+                        int64_t frames, int L, int check_every, int flags, int threads, uint8_t *bits_out,
+                        int32_t *iters_out, uint8_t *conv_out, REAL *post_out) {
+    if (check_every < 1) return -4;
     graph_t g;
     int rc = graph_build(&g, rows, cols, nnz, m, n);
     if (rc) return rc;
@@ -232,7 +236,7 @@ int NAME(oracle_decode)(const int32_t *rows, const int32_t *cols, int64_t nnz, i
 #pragma omp for schedule(dynamic, 1)
 #endif
         for (int64_t f = 0; f < frames; f++)
-            decode_frame(&g, r + f * n, L, flags, s, rr, eta, xb, eb, b, bits_out + f * n, iters_out + f,
+            decode_frame(&g, r + f * n, L, check_every, flags, s, rr, eta, xb, eb, b, bits_out + f * n, iters_out + f,
                          conv_out + f, post_out ? post_out + f * n : NULL);
         free(s); free(rr); free(eta); free(xb); free(eb); free(b);
     }

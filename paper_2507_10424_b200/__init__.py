@@ -172,6 +172,10 @@ class Handle:
     def set_flags(self, flags: int):
         _check(self._lib.ldpc_set_flags(self._h, flags), "ldpc_set_flags")
 
+    def set_check_every(self, T: int):
+        """Codeword test every T loop bodies (and after the last); T = 6 is the paper's setting."""
+        _check(self._lib.ldpc_set_check_every(self._h, int(T)), "ldpc_set_check_every")
+
     def set_chunk(self, frames: int):
         _check(self._lib.ldpc_set_chunk(self._h, frames), "ldpc_set_chunk")
 

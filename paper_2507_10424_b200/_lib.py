@@ -22,6 +22,7 @@ SIGNATURES = {
     "ldpc_get_graph": (ctypes.c_int, [P, P, P, P, P]),
     "ldpc_set_flags": (ctypes.c_int, [P, U32]),
     "ldpc_set_chunk": (ctypes.c_int, [P, I64]),
+    "ldpc_set_check_every": (ctypes.c_int, [P, I32]),
     "ldpc_schedule": (ctypes.c_int, [P]),
     "ldpc_profile_enable": (ctypes.c_int, [P, ctypes.c_int]),
     "ldpc_profile_read": (ctypes.c_int, [P, P, P]),

@@ -80,7 +80,7 @@ struct ResArgs {
     Graph g;
     const float *llr;
     int64_t frames;
-    int L, early, literal;
+    int L, T, early, literal;
     float *post;
     uint8_t *bits;
     int32_t *iters;
@@ -256,7 +256,8 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? 2 : 1) k_resid
             if (mine && ((act_all >> lane) & 1u)) {
                 const int k = slot_k[lane];
                 const bool uns = (uns_all >> lane) & 1u;
-                const bool fin = a.early ? (!uns || k == a.L) : (k == a.L);
+                // a clean syndrome stops the frame only at a check point k % T == 0
+                const bool fin = a.early ? ((!uns && k % a.T == 0) || k == a.L) : (k == a.L);
                 if (fin) {
                     const int conv = !uns;
                     if (a.iters) a.iters[f] = k;
@@ -376,7 +377,7 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? 2 : 1) k_resid
             if (lane < S && ((active >> lane) & 1u)) {
                 const int k = slot_k[lane];
                 const bool uns = (uns_all >> lane) & 1u;
-                fin = a.early ? (!uns || k == a.L) : (k == a.L);
+                fin = a.early ? ((!uns && k % a.T == 0) || k == a.L) : (k == a.L);
                 cont = !fin;
             }
             const unsigned fin_mask = __ballot_sync(FULLM, fin), cont_mask = __ballot_sync(FULLM, cont);
@@ -523,7 +524,7 @@ ResidentPlan plan_resident(const HostGraph &g, bool loc16, int device) {
 }
 
 // rs scratch is carved after the two counter ints of work_counter's allocation owner (runtime.cu)
-int launch_resident(const Graph &g, const ResidentPlan &rp, const float *llr, int64_t frames, int L, bool early,
+int launch_resident(const Graph &g, const ResidentPlan &rp, const float *llr, int64_t frames, int L, int T, bool early,
                     bool literal, bool loc16, float *posterior, uint8_t *bits, int32_t *iters_out, uint8_t *conv_out,
                     unsigned long long *stats, int *work_counter, cudaStream_t st) {
     (void)loc16;
@@ -532,6 +533,7 @@ int launch_resident(const Graph &g, const ResidentPlan &rp, const float *llr, in
     a.llr = llr;
     a.frames = frames;
     a.L = L;
+    a.T = T;
     a.early = early ? 1 : 0;
     a.literal = literal ? 1 : 0;
     a.post = posterior;

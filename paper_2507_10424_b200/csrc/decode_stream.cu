@@ -448,7 +448,7 @@ __global__ void __launch_bounds__(CTA) k_cn_tma(Graph g, StreamState w, int k, i
 // ------------------------------------------------------------------------------------------------
 template <typename LocT, bool EARLY, int BN_U>
 __global__ void __launch_bounds__(CTA, BN_U <= 1 ? 6 : MinBlocks<BN_U>::value)
-    k_bn(Graph g, StreamState w, int k, int cols_per_cta, int literal, const int *kdev) {
+    k_bn(Graph g, StreamState w, int k, int cols_per_cta, int literal, const int *kdev, int check_every) {
     using L4 = typename Vec4<LocT>::type;
     if (kdev) k = *kdev;
     (void)literal;
@@ -461,7 +461,9 @@ __global__ void __launch_bounds__(CTA, BN_U <= 1 ? 6 : MinBlocks<BN_U>::value)
     const int cblk = blockIdx.x;
     uint4 act = make_uint4(FULL, FULL, FULL, FULL);
     if (EARLY) {
-        const uint4 ua = ldu4(w.unsat + ((size_t)(k & 1) * T + t) * 4);
+        // the syndrome of k_cn(k) tests b^(k-1); it may stop frames only at a check point (k-1) % T == 0
+        const bool check = ((k - 1) % check_every) == 0;
+        const uint4 ua = check ? ldu4(w.unsat + ((size_t)(k & 1) * T + t) * 4) : make_uint4(FULL, FULL, FULL, FULL);
         const uint4 dw = ldu4(w.done + (size_t)t * 4);
         const uint4 newly = make_uint4(~ua.x & ~dw.x, ~ua.y & ~dw.y, ~ua.z & ~dw.z, ~ua.w & ~dw.w);
         act = make_uint4(ua.x & ~dw.x, ua.y & ~dw.y, ua.z & ~dw.z, ua.w & ~dw.w);
@@ -730,9 +732,9 @@ void cn_launch(dim3 grid, cudaStream_t st, const Graph &g, const StreamState &w,
 
 template <typename LT, bool EA>
 void bn_launch(dim3 grid, cudaStream_t st, const Graph &g, const StreamState &w, int k, int cpc, int lit, int u,
-               const int *kdev) {
-    if (u >= 2) k_bn<LT, EA, 2><<<grid, CTA, 0, st>>>(g, w, k, cpc, lit, kdev);
-    else k_bn<LT, EA, 1><<<grid, CTA, 0, st>>>(g, w, k, cpc, lit, kdev);
+               const int *kdev, int te) {
+    if (u >= 2) k_bn<LT, EA, 2><<<grid, CTA, 0, st>>>(g, w, k, cpc, lit, kdev, te);
+    else k_bn<LT, EA, 1><<<grid, CTA, 0, st>>>(g, w, k, cpc, lit, kdev, te);
 }
 
 template <typename LT, bool F, bool EA>
@@ -782,11 +784,11 @@ int launch_bit_node(const Graph &g, const StreamState &w, int k, bool early, boo
     const dim3 grid = grid2((g.n + cfg.cols_per_cta - 1) / cfg.cols_per_cta, w.T);
     const int lit = literal ? 1 : 0, cpc = cfg.cols_per_cta, u = cfg.bn_unroll;
     if (loc16) {
-        if (early) bn_launch<uint16_t, true>(grid, st, g, w, k, cpc, lit, u, kdev);
-        else bn_launch<uint16_t, false>(grid, st, g, w, k, cpc, lit, u, kdev);
+        if (early) bn_launch<uint16_t, true>(grid, st, g, w, k, cpc, lit, u, kdev, cfg.check_every);
+        else bn_launch<uint16_t, false>(grid, st, g, w, k, cpc, lit, u, kdev, cfg.check_every);
     } else {
-        if (early) bn_launch<uint8_t, true>(grid, st, g, w, k, cpc, lit, u, kdev);
-        else bn_launch<uint8_t, false>(grid, st, g, w, k, cpc, lit, u, kdev);
+        if (early) bn_launch<uint8_t, true>(grid, st, g, w, k, cpc, lit, u, kdev, cfg.check_every);
+        else bn_launch<uint8_t, false>(grid, st, g, w, k, cpc, lit, u, kdev, cfg.check_every);
     }
     return 1;
 }

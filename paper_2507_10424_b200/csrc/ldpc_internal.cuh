@@ -66,6 +66,7 @@ struct StreamLaunch {
     int cols_per_cta = 32;
     int cn_unroll = 1;  // check-node edges per load batch (1, 2, 4)
     int bn_unroll = 1;  // bit-node edges per load batch (1, 2)
+    int check_every = 1;  // codeword test after body k when k % T == 0 (and after body L)
     int cn_tma_dm = 0;   // > 0: bulk-copy staged check node for rows of degree <= this
     int cn_ctas = 4736;  // grid caps of the (tile x block) work loops: a few waves of resident CTAs
     int bn_ctas = 7104;
@@ -94,7 +95,7 @@ struct ResidentPlan {
 };
 ResidentPlan plan_resident(const HostGraph &g, bool loc16, int device);
 size_t resident_scratch_bytes(const HostGraph &g, const ResidentPlan &rp);  // work counter + r scratch
-int launch_resident(const Graph &g, const ResidentPlan &rp, const float *llr, int64_t frames, int L, bool early,
+int launch_resident(const Graph &g, const ResidentPlan &rp, const float *llr, int64_t frames, int L, int T, bool early,
                     bool literal, bool loc16, float *posterior, uint8_t *bits, int32_t *iters_out,
                     uint8_t *conv_out, unsigned long long *stats, int *work_counter, cudaStream_t st);
 

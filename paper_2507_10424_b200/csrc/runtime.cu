@@ -15,6 +15,7 @@ using namespace ldpc;
 struct ldpc_plan {
     HostGraph g;
     uint32_t flags = 0;
+    int check_every = 1;
     int device = 0;
     bool poisoned = false;
     // streaming workspace
@@ -42,6 +43,7 @@ struct ldpc_plan {
         const void *key[8];
         int64_t fc;
         int L;
+        int T;
         uint32_t flags;
         void *ws;
         cudaGraph_t graph;
@@ -191,7 +193,8 @@ int run_graph(ldpc_plan *h, const Graph &g, const StreamState &w, const float *l
               cudaStream_t st, Tail &&tail) {
     const void *key[8] = {llr, post, bits, iters, conv, stats, w.r, nullptr};
     for (auto &ge : h->graphs) {
-        if (std::equal(key, key + 8, ge.key) && ge.fc == fc && ge.L == L && ge.flags == h->flags && ge.ws == h->ws) {
+        if (std::equal(key, key + 8, ge.key) && ge.fc == fc && ge.L == L && ge.flags == h->flags && ge.ws == h->ws &&
+            ge.T == h->check_every) {
             ge.used = ++h->graph_clock;
             if (cudaGraphLaunch(ge.exec, st) != cudaSuccess) {
                 h->poisoned = true;
@@ -263,6 +266,7 @@ int run_graph(ldpc_plan *h, const Graph &g, const StreamState &w, const float *l
     std::copy(key, key + 8, ge.key);
     ge.fc = fc;
     ge.L = L;
+    ge.T = h->check_every;
     ge.flags = h->flags;
     ge.ws = h->ws;
     ge.graph = graph;
@@ -351,8 +355,8 @@ int decode_resident(ldpc_plan *h, const float *llr, int64_t frames, int L, uint8
     }
     const Graph g = h->g.view();
     launch(h, LDPC_K_RESIDENT, st, [&] {
-        return launch_resident(g, h->rp, llr, frames, L, early, literal, loc16, post, bits, iters, conv,
-                               reinterpret_cast<unsigned long long *>(stats), h->work_counter, st);
+        return launch_resident(g, h->rp, llr, frames, L, h->check_every, early, literal, loc16, post, bits, iters,
+                               conv, reinterpret_cast<unsigned long long *>(stats), h->work_counter, st);
     });
     return check_async(h);
 }
@@ -564,6 +568,13 @@ int ldpc_get_graph(ldpc_handle_t h, int32_t *row_ptr, int32_t *col_idx, int32_t 
 int ldpc_set_flags(ldpc_handle_t h, uint32_t flags) {
     if (!h) return LDPC_ERR_INVALID_ARG;
     h->flags = flags;
+    return LDPC_OK;
+}
+
+int ldpc_set_check_every(ldpc_handle_t h, int32_t T) {
+    if (!h || T < 1) return LDPC_ERR_INVALID_ARG;
+    h->check_every = T;
+    h->cfg.check_every = T;
     return LDPC_OK;
 }
 

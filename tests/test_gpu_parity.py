@@ -45,11 +45,13 @@ def gpu_decode(h, llr_np, L, posterior=True):
             out.posterior.cpu().numpy() if posterior else None, stats.cpu().numpy())
 
 
-def compare(code, llr, L, flags=0, h=None, exact=True):
+def compare(code, llr, L, flags=0, h=None, exact=True, check_every=1):
     if h is None:
         h = handle(code, flags)
+    if check_every != 1:
+        h.set_check_every(check_every)
     gb, gi, gc, gp, gs = gpu_decode(h, llr, L)
-    ob, oi, oc, op = oracle.decode(code.oracle_h(), llr, L, flags=flags & (LIT | NOES))
+    ob, oi, oc, op = oracle.decode(code.oracle_h(), llr, L, flags=flags & (LIT | NOES), check_every=check_every)
     assert np.array_equal(gi, oi), f"iters differ on {np.count_nonzero(gi != oi)} frames"
     assert np.array_equal(gc, oc), "converged differs"
     assert np.array_equal(gb, ob), f"bits differ on {np.count_nonzero(np.any(gb != ob, axis=1))} frames"
@@ -150,6 +152,22 @@ def test_c2_subset_full(sched):
         parts.append(channel.bpsk_awgn(code.n, code.rate, e, cfg["seed"], p, 5000, 1700).numpy())
     llr = np.concatenate(parts)
     compare(code, llr, cfg["max_iter"], h=h)
+
+
+@pytest.mark.parametrize("sched", [FORCE_STREAM, FORCE_STREAM | 16, FORCE_RESIDENT])
+@pytest.mark.parametrize("T", [2, 6])
+def test_check_every(sched, T):
+    """checkEvery = T: codeword tests only after bodies k % T == 0 and after body L."""
+    cfg = codes.CONFIGS["c2"]
+    code = cfg["code"]()
+    h = handle(code, sched)
+    if h.schedule == "unavailable":
+        pytest.skip("resident schedule unavailable")
+    parts = [channel.bpsk_awgn(code.n, code.rate, e, cfg["seed"], p, 900, 400).numpy() for p, e in enumerate(cfg["ebn0"])]
+    compare(code, np.concatenate(parts), 47, h=h, check_every=T)
+    c1 = codes.paper_5x10()
+    llr1 = channel.bpsk_awgn(10, 0.5, 1.0, 5, 0, 0, 3000).numpy()
+    compare(c1, llr1, 10, h=handle(c1, sched & ~16 if sched == FORCE_RESIDENT else sched), check_every=T)
 
 
 def test_edge_sizes_and_chunking():

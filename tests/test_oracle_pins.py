@@ -354,6 +354,33 @@ def test_p12_termination_and_independence(oracle_mod, flags):
         assert np.array_equal(p1[0], post[f])
 
 
+def test_check_every_semantics(oracle_mod):
+    """checkEvery = T ("Termination was checked for every 6 iterations"): the T-run
+    stops at the first k in {0, T, 2T, ...} or k = L at which the (check-independent) trajectory's
+    hard decision is a codeword, with the same bits and soft vector as that trajectory at k."""
+    code = codes.regular(60, 120, 3, 6, 21)
+    r = _random_frames(code, 60, 1.8, 31)
+    L, T = 20, 6
+    H = code.dense()
+    traj = {}
+    for k in range(L + 1):
+        b, _, _, p = oracle_mod.decode(code.oracle_h(), r, k, flags=NO_EARLY_STOP)
+        traj[k] = (b, p, ((b.astype(np.int64) @ H.T) % 2).sum(axis=1) == 0)
+    bits, iters, conv, post = oracle_mod.decode(code.oracle_h(), r, L, check_every=T)
+    checks = [k for k in range(L + 1) if k % T == 0 or k == L]
+    for f in range(len(r)):
+        stop = next((k for k in checks if traj[k][2][f]), None)
+        if stop is None:
+            assert iters[f] == L and conv[f] == 0
+            stop = L
+        else:
+            assert iters[f] == stop and conv[f] == 1
+        assert np.array_equal(bits[f], traj[stop][0][f]) and np.array_equal(post[f], traj[stop][1][f])
+    assert np.any(iters % T != 0)  # some frames run to L = 20 (not a multiple of 6) or stop at 0 / 6 / 12 / 18
+    _, i1, c1, _ = oracle_mod.decode(code.oracle_h(), r, L, check_every=1)
+    assert np.all(iters[c1 == 1] >= i1[c1 == 1])  # checking less often never stops earlier
+
+
 # ---------------------------------------------------------------- P13 ---------------------
 def test_p13_coding_gain(oracle_mod):
     """P13: past the waterfall the decoded BER is below the raw BER (C2-shaped code)."""
