@@ -45,8 +45,10 @@ def hbm_peak():
 
 
 def describe(cfg_name, cfg, code):
+    te = cfg.get("check_every", 1)
     return (f"{cfg_name}: {code.name} ({code.m}x{code.n}, nnz {code.nnz}), {cfg['frames']} frames per GPU over "
-            f"Eb/N0 {cfg['ebn0']} dB, max_iter {cfg['max_iter']}, BPSK/AWGN all-zero codeword")
+            f"Eb/N0 {cfg['ebn0']} dB, max_iter {cfg['max_iter']}"
+            + (f", codeword test every {te} bodies" if te != 1 else "") + ", BPSK/AWGN all-zero codeword")
 
 
 # ------------------------------------------------------------------ distributed plumbing -------
@@ -197,6 +199,9 @@ def run_ours(args):
     rr, cc = code.coo()
     h = P.Handle.from_coo(torch.from_numpy(rr).to(dev), torch.from_numpy(cc).to(dev), code.m, code.n,
                           flags=args.flags)
+    T = cfg.get("check_every", 1)
+    if T != 1:
+        h.set_check_every(T)
     out = P.DecodeResult(torch.empty((F, n), dtype=torch.uint8, device=dev),
                          torch.empty(F, dtype=torch.int32, device=dev),
                          torch.empty(F, dtype=torch.uint8, device=dev),
@@ -291,7 +296,7 @@ def run_ours(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": describe(args.config, cfg, code), "global_batch": world * F,
                        "frames_per_gpu": F, "m": code.m, "n": code.n, "nnz": code.nnz, "max_iter": L,
-                       "ebn0_db": cfg["ebn0"], "schedule": h.schedule, "flags": args.flags,
+                       "ebn0_db": cfg["ebn0"], "check_every": T, "schedule": h.schedule, "flags": args.flags,
                        "parallelism": f"dp{world} (frame shards, no data-path collective)",
                        "l2": f"inputs {F * n * 4 / 1e9:.2f} GB per GPU > 126 MB L2 (no flush needed)"},
             "roofline": roof,
@@ -376,13 +381,13 @@ def cpu_baseline(cfg, code, args, budget_s: float = 15.0):
     # calibrate on a small sample, then size the timed sample for ~budget_s of CPU work
     cal = sample(max(1, threads // len(pts) + 1))
     t0 = time.perf_counter()
-    oracle.decode(code.oracle_h(), cal, cfg["max_iter"], threads=threads)
+    oracle.decode(code.oracle_h(), cal, cfg["max_iter"], threads=threads, check_every=cfg.get("check_every", 1))
     t_cal = time.perf_counter() - t0
     per_frame = t_cal / len(cal)
     per_point = int(max(1, min(5000, budget_s / max(per_frame, 1e-6) / len(pts))))
     llr = sample(per_point)
     t0 = time.perf_counter()
-    oracle.decode(code.oracle_h(), llr, cfg["max_iter"], threads=threads)
+    oracle.decode(code.oracle_h(), llr, cfg["max_iter"], threads=threads, check_every=cfg.get("check_every", 1))
     secs = time.perf_counter() - t0
     gbps = len(llr) * code.n / secs / 1e9
     return {"value": round(gbps, 6), "unit": "Gbit/s", "cores": threads, "kind": "oracle",
@@ -405,7 +410,7 @@ def run_reference(args):
     threads = oracle.max_threads()
     F = cfg["frames"]
     pts = codes.point_ranges(F, len(cfg["ebn0"]))
-    per_point = max(1, int(os.environ.get("REF_FRAMES_PER_POINT", "24")))
+    per_point = max(1, int(os.environ.get("REF_FRAMES_PER_POINT", "1024")))
 
     def sample(step_idx):
         parts = []
@@ -416,12 +421,13 @@ def run_reference(args):
         return np.concatenate(parts)
 
     for w in range(args.warmup):
-        oracle.decode(code.oracle_h(), sample(1000 + w), cfg["max_iter"], threads=threads)
+        oracle.decode(code.oracle_h(), sample(1000 + w), cfg["max_iter"], threads=threads,
+                      check_every=cfg.get("check_every", 1))
     tot_t, tot_frames = 0.0, 0
     for s in range(args.steps):
         llr = sample(s)
         t0 = time.perf_counter()
-        oracle.decode(code.oracle_h(), llr, cfg["max_iter"], threads=threads)
+        oracle.decode(code.oracle_h(), llr, cfg["max_iter"], threads=threads, check_every=cfg.get("check_every", 1))
         tot_t += time.perf_counter() - t0
         tot_frames += len(llr)
     value = tot_frames * code.n / tot_t / 1e9

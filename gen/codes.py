@@ -192,3 +192,93 @@ def point_ranges(frames: int, npoints: int):
 def shard_range(total: int, rank: int, world: int):
     """Contiguous global-index range [lo, hi) of rank `rank` of `world` (equal split, PAR-1)."""
     return (rank * total) // world, ((rank + 1) * total) // world
+
+
+# --- quasi-cyclic codes and the alist format (input plumbing; SPEC S:55-81) --------------------
+def expand_qc(row_blocks: int, col_blocks: int, Z: int, shifts) -> Code:
+    """Expand a quasi-cyclic spec: block (a, b) with shift s puts a one at (a*Z + r, b*Z + (r+s) mod Z)
+    for every r in [0, Z) (SPEC S:73-81 convention); shifts[a][b] is a list of distinct offsets
+    (empty = zero block, several = superimposed circulants)."""
+    rows = [[] for _ in range(row_blocks * Z)]
+    for a in range(row_blocks):
+        for b in range(col_blocks):
+            sh = list(shifts[a][b])
+            if len(set(sh)) != len(sh):
+                raise ValueError(f"block ({a},{b}) repeats a shift")
+            for s in sh:
+                if not 0 <= s < Z:
+                    raise ValueError("shift out of range")
+                for r in range(Z):
+                    rows[a * Z + r].append(b * Z + (r + s) % Z)
+    return Code(row_blocks * Z, col_blocks * Z, [np.array(sorted(r), np.int32) for r in rows],
+                f"qc{row_blocks}x{col_blocks}_Z{Z}")
+
+
+def qc_random(row_blocks: int = 2, col_blocks: int = 16, Z: int = 511, weight: int = 2, seed: int = 8176) -> Code:
+    """Random QC code with the structure of the paper's benchmark code ("Quasi-Cyclic 8176,1022",
+    CCSDS 2007): a 2 x 16 array of 511 x 511 circulants of weight 2 -> 1022 x 8176, row degree 32,
+    column degree 4.  The CCSDS shift table is not in the paper, so the shifts are seeded random."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    shifts = [[sorted(rng.choice(Z, size=weight, replace=False).tolist()) for _ in range(col_blocks)]
+              for _ in range(row_blocks)]
+    c = expand_qc(row_blocks, col_blocks, Z, shifts)
+    c.name = f"qc_ccsds_shape_{row_blocks * Z}x{col_blocks * Z}_s{seed}"
+    c.shifts = shifts
+    return c
+
+
+def to_alist(code: Code) -> str:
+    """Canonical alist text (MacKay format, 1-based, zero-padded lists, LF endings)."""
+    cols = [[] for _ in range(code.n)]
+    for i, r in enumerate(code.rows):
+        for j in r:
+            cols[int(j)].append(i)
+    cd = [len(c) for c in cols]
+    rd = [len(r) for r in code.rows]
+    mc, mr = max(cd) if cd else 0, max(rd) if rd else 0
+    out = [f"{code.n} {code.m}", f"{mc} {mr}", " ".join(map(str, cd)), " ".join(map(str, rd))]
+    for c in cols:
+        out.append(" ".join(str(i + 1) for i in c) + "".join(" 0" for _ in range(mc - len(c))) if c else
+                   " ".join("0" for _ in range(mc)))
+    for r in code.rows:
+        out.append(" ".join(str(int(j) + 1) for j in r) + "".join(" 0" for _ in range(mr - len(r))))
+    return "\n".join(out) + "\n"
+
+
+def parse_alist(text: str, name: str = "") -> Code:
+    """Parse alist text; the column and row sections are cross-checked against each other."""
+    tok = text.split()
+    pos = 0
+
+    def nxt():
+        nonlocal pos
+        v = int(tok[pos])
+        pos += 1
+        return v
+
+    try:
+        n, m = nxt(), nxt()
+        mc, mr = nxt(), nxt()
+        cd = [nxt() for _ in range(n)]
+        rd = [nxt() for _ in range(m)]
+        cols = []
+        for j in range(n):
+            lst = [nxt() for _ in range(mc)]
+            cols.append(sorted(x - 1 for x in lst if x > 0))
+        rows = []
+        for i in range(m):
+            lst = [nxt() for _ in range(mr)]
+            rows.append(sorted(x - 1 for x in lst if x > 0))
+    except (IndexError, ValueError) as e:
+        raise ValueError(f"malformed alist: {e}")
+    if any(len(c) != d for c, d in zip(cols, cd)) or any(len(r) != d for r, d in zip(rows, rd)):
+        raise ValueError("alist degree list inconsistent with its adjacency section")
+    a = {(i, j) for i, r in enumerate(rows) for j in r}
+    b = {(i, j) for j, c in enumerate(cols) for i in c}
+    if a != b:
+        raise ValueError("alist column and row sections disagree")
+    return Code(m, n, [np.array(r, np.int32) for r in rows], name or f"alist_{m}x{n}")
+
+
+CONFIGS["c6"] = dict(code=lambda: qc_random(), frames=1 << 15, max_iter=60, check_every=6,
+                     ebn0=[3.0, 3.2, 3.4, 3.6], seed=8176)

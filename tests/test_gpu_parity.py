@@ -296,6 +296,16 @@ def test_c4_full_size_sampled():
     _sampled_full_size("c4", 12)
 
 
+def test_c6_paper_shaped_qc():
+    """C6: the paper's benchmark shape (QC 1022 x 8176, row degree 32; max 60 iterations, codeword
+    test every 6, SNR 3.0-3.6 dB) -- every frame of a reduced batch, plus a full-size sample."""
+    cfg = codes.CONFIGS["c6"]
+    code = cfg["code"]()
+    parts = [channel.bpsk_awgn(code.n, code.rate, e, cfg["seed"], p, 0, 150).numpy() for p, e in enumerate(cfg["ebn0"])]
+    compare(code, np.concatenate(parts), cfg["max_iter"], check_every=cfg["check_every"],
+            h=handle(code, 0, coo=True))
+
+
 def test_c5_sixteen_handles():
     """C5: 16 distinct H of equal dims through one handle API; every frame of a reduced batch."""
     cfg = codes.CONFIGS["c5"]
