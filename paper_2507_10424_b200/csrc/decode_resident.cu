@@ -6,9 +6,10 @@
 //   s    [n][S]  fp32          soft vector (Eq. sCalculation)
 //   min0 [m][S]  fp32          Observation 1's minimum
 //   min1 [m][S]  fp32          Observation 1's second minimum
-//   lc   [m][S]  u16           min0Location, stored as the edge id inside the row lists (0xffff = none)
-//   par  [m]     S bits        the row's sign parity (Obs. 2) times (-1)^{d_i} (reading A1)
-//   sg   [E]     S bits        sign of lambda_e = s_j - eta_e for each slot
+//   lc   [m][S]  u32           min0Location, stored as the edge id inside the row lists (-1 = none)
+//   sgb  [m/G][dmax] 4 x u32   sign of lambda_e = s_j - eta_e, kept as the warp ballots of the check
+//                              node (bit (i % G) * LR + l of component v = row i, slot 4l + v)
+//   parb [m/G]   4 x u32       the rows' sign parity (Obs. 2) x (-1)^{d_i} (reading A1), same bits
 // plus the Tanner graph itself as 16-bit lists (N_i, M_j).  r lives in a global scratch
 // [CTA][n][S] (L2-resident) read once per column per body.  Loop per round:
 //   A  finish stopped slots (k, isCodeword, counters) and refill empty slots from a global counter
@@ -30,47 +31,35 @@ namespace {
 
 constexpr unsigned FULLM = 0xffffffffu;
 
-template <int S>
-struct SWord;
-template <>
-struct SWord<4> {
-    using T = uint8_t;
-};
-template <>
-struct SWord<8> {
-    using T = uint8_t;
-};
-template <>
-struct SWord<16> {
-    using T = uint16_t;
-};
-template <>
-struct SWord<32> {
-    using T = uint32_t;
-};
 
 struct Layout {
-    size_t s, m0, m1, lc, sg, par, rp, cp, col, rec, meta, total;
+    size_t s, m0, m1, lc, sgb, parb, rp, cp, col, rec, rec2, meta, total;
 };
 
 constexpr size_t a16(size_t x) { return (x + 15) & ~(size_t)15; }
 
 constexpr int META_INTS = 8 * 32 + 16;
 
-Layout layout_for(int S, int m, int n, int E) {
+// Sign bits are kept as the warp ballots that produced them: for the block of G rows a warp sweeps
+// together (rg = i / G), position p of the rows and slot component v, one u32 whose bit
+// (i % G) * LR + l is the sign of lambda for row i, slot 4l + v.  The writer stores four words per
+// edge position with one 16-byte store; readers test a lane bit.
+Layout layout_for(int S, int m, int n, int E, int dm) {
     Layout L{};
+    const int G = 128 / S;
+    const size_t nrg = (size_t)(m + G - 1) / G;
     size_t o = 0;
-    const size_t swb = S <= 8 ? 1 : S / 8;
     L.s = o;    o = a16(o + (size_t)n * S * 4);
     L.m0 = o;   o = a16(o + (size_t)m * S * 4);
     L.m1 = o;   o = a16(o + (size_t)m * S * 4);
-    L.lc = o;   o = a16(o + (size_t)m * S * 2);
-    L.sg = o;   o = a16(o + (size_t)E * swb);
-    L.par = o;  o = a16(o + (size_t)m * swb);
+    L.lc = o;   o = a16(o + (size_t)m * S * 4);
+    L.sgb = o;  o = a16(o + nrg * dm * 16);
+    L.parb = o; o = a16(o + nrg * 16);
     L.rp = o;   o = a16(o + (size_t)(m + 1) * 2);
     L.cp = o;   o = a16(o + (size_t)(n + 1) * 2);
     L.col = o;  o = a16(o + (size_t)E * 2);
     L.rec = o;  o = a16(o + (size_t)E * 4);
+    L.rec2 = o; o = a16(o + (size_t)E * 2);
     L.meta = o; o = a16(o + (size_t)META_INTS * 4 + 8 * 8);
     L.total = o;
     return L;
@@ -80,7 +69,7 @@ struct ResArgs {
     Graph g;
     const float *llr;
     int64_t frames;
-    int L, T, early, literal;
+    int L, T, early, literal, dm;
     float *post;
     uint8_t *bits;
     int32_t *iters;
@@ -98,63 +87,55 @@ __device__ __forceinline__ void f4s(float4 &a, int v, float x) {
     else if (v == 2) a.z = x;
     else a.w = x;
 }
-// min0Location test on two packed 16-bit edge ids: true iff the half selected by `hi` differs from e
-__device__ __forceinline__ bool loc_ne(unsigned pair, unsigned e2, bool hi) {
-    return ((pair ^ e2) & (hi ? 0xffff0000u : 0x0000ffffu)) != 0u;
-}
 
 // Check-node update of G rows (one per row group of the warp) for the 4 slots of this lane.
 // HAS: rows of the warp may have different degrees (irregular H), lanes past their degree idle.
-// fm: this lane's fresh slots (eta^prev = 0); nfw: S-bit word with the fresh slots' bits clear.
+// fm: this lane's fresh slots (eta^prev = 0).  sgb/parb: the ballot words of this row block.
 template <int S, bool HAS>
-__device__ __forceinline__ void cn_rows(const float *s, float *mn0, float *mn1, uint16_t *lc,
-                                        typename SWord<S>::T *sg, typename SWord<S>::T *par,
-                                        const uint16_t *col, int i, bool valid, int ra, int d, int dmax,
-                                        int l, int sub, unsigned fm, unsigned nfw, unsigned corr_all,
-                                        unsigned &syn_acc) {
-    using SWT = typename SWord<S>::T;
-    constexpr int LR = S / 4;
-    constexpr unsigned LMASK = (LR == 32) ? 0xffffffffu : ((1u << LR) - 1u);
+__device__ __forceinline__ void cn_rows(const float *s, float *mn0, float *mn1, uint32_t *lc, uint4 *sgb, uint4 *parb,
+                                        const uint16_t *col, int i, bool valid, int ra, int d, int dmax, int l,
+                                        int lane, unsigned fm, bool corr, unsigned &syn_acc) {
     const float INF = __int_as_float(0x7f800000);
     const int q0 = 4 * l;
     float4 om0 = make_float4(0.f, 0.f, 0.f, 0.f), om1 = om0;
-    uint2 olc = make_uint2(0xffffffffu, 0xffffffffu);
-    unsigned P = 0;
+    uint4 olc = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
     const int ca = i * S + q0;
     if (valid) {
         om0 = *reinterpret_cast<const float4 *>(mn0 + ca);
         om1 = *reinterpret_cast<const float4 *>(mn1 + ca);
-        olc = *reinterpret_cast<const uint2 *>(lc + ca);
-        P = (unsigned)par[i];
+        olc = *reinterpret_cast<const uint4 *>(lc + ca);
         if (fm) {  // fresh slots start from eta = 0: min0 = min1 = +0, no location
-            if (fm & 1u) { om0.x = 0.f; om1.x = 0.f; olc.x |= 0x0000ffffu; }
-            if (fm & 2u) { om0.y = 0.f; om1.y = 0.f; olc.x |= 0xffff0000u; }
-            if (fm & 4u) { om0.z = 0.f; om1.z = 0.f; olc.y |= 0x0000ffffu; }
-            if (fm & 8u) { om0.w = 0.f; om1.w = 0.f; olc.y |= 0xffff0000u; }
+            if (fm & 1u) { om0.x = 0.f; om1.x = 0.f; olc.x = 0xffffffffu; }
+            if (fm & 2u) { om0.y = 0.f; om1.y = 0.f; olc.y = 0xffffffffu; }
+            if (fm & 4u) { om0.z = 0.f; om1.z = 0.f; olc.z = 0xffffffffu; }
+            if (fm & 8u) { om0.w = 0.f; om1.w = 0.f; olc.w = 0xffffffffu; }
         }
     }
-    unsigned mv[4];
+    const uint4 P = *parb;  // row sign parities x (-1)^{d_i} of the previous body, one bit per lane
+    const unsigned lm = 1u << lane;
+    unsigned mk[4];  // this lane's bit, cleared for fresh slots (their eta^prev is +0)
 #pragma unroll
-    for (int v = 0; v < 4; v++) mv[v] = 1u << (v * LR + l);
+    for (int v = 0; v < 4; v++) mk[v] = ((fm >> v) & 1u) ? 0u : lm;
     float nm0[4] = {INF, INF, INF, INF}, nm1[4] = {INF, INF, INF, INF};
-    int nloc[4] = {0xffff, 0xffff, 0xffff, 0xffff};
+    int nloc[4] = {-1, -1, -1, -1};
     unsigned parw[4] = {0, 0, 0, 0};
     unsigned syn = 0;
 #pragma unroll 2
     for (int p = 0; p < dmax; p++) {
         const bool has = HAS ? (p < d) : true;
         const int e = ra + p;
-        const unsigned e2 = (unsigned)e * 0x10001u;
         const int j = has ? col[e] : 0;
         const float4 sv = *reinterpret_cast<const float4 *>(s + j * S + q0);
-        // own sign of lambda^prev xor the row parity (Obs. 2, A1 folded in); fresh slots: +
-        const unsigned W = ((has ? (unsigned)sg[e] : 0u) ^ P) & nfw;
+        const uint4 W = sgb[p];  // own sign of lambda^prev per component (Obs. 2)
+        const float mg[4] = {((int)olc.x == e) ? om1.x : om0.x, ((int)olc.y == e) ? om1.y : om0.y,
+                             ((int)olc.z == e) ? om1.z : om0.z, ((int)olc.w == e) ? om1.w : om0.w};  // Obs. 1
+        const bool ng[4] = {((W.x ^ P.x) & mk[0]) != 0u, ((W.y ^ P.y) & mk[1]) != 0u, ((W.z ^ P.z) & mk[2]) != 0u,
+                            ((W.w ^ P.w) & mk[3]) != 0u};
         unsigned bal[4];
 #pragma unroll
         for (int v = 0; v < 4; v++) {
             const float sj = f4c(sv, v);
-            const float mag = loc_ne(v < 2 ? olc.x : olc.y, e2, v & 1) ? f4c(om0, v) : f4c(om1, v);  // Obs. 1
-            const float x = sj - ((W & mv[v]) ? -mag : mag);  // lambda - eta^prev
+            const float x = sj - (ng[v] ? -mg[v] : mg[v]);  // lambda - eta^prev
             const float ax = HAS ? (has ? fabsf(x) : INF) : fabsf(x);
             const bool lt = ax < nm0[v];  // first strict minimum (A13)
             nm1[v] = fminf(nm1[v], fmaxf(nm0[v], ax));
@@ -165,35 +146,26 @@ __device__ __forceinline__ void cn_rows(const float *s, float *mn0, float *mn1, 
         }
 #pragma unroll
         for (int v = 0; v < 4; v++) parw[v] ^= bal[v];
-        __syncwarp();  // the row group's reads of sg[e] precede its rewrite (memory order, not just convergence)
-        if (has && l == 0) {
-            unsigned word = 0;
-#pragma unroll
-            for (int v = 0; v < 4; v++) word |= ((bal[v] >> (sub * LR)) & LMASK) << (v * LR);
-            sg[e] = (SWT)word;
-        }
+        __syncwarp();  // every lane has read sgb[p] before lane 0 rewrites it
+        if (lane == 0) sgb[p] = make_uint4(bal[0], bal[1], bal[2], bal[3]);
     }
+    // row parity words of this block; rows of odd degree flip under the CORRECTED rule (reading A1)
+    const unsigned flip = __ballot_sync(FULLM, valid && corr && (d & 1));
     if (valid) {
         *reinterpret_cast<float4 *>(mn0 + ca) = make_float4(nm0[0], nm0[1], nm0[2], nm0[3]);
         *reinterpret_cast<float4 *>(mn1 + ca) = make_float4(nm1[0], nm1[1], nm1[2], nm1[3]);
-        *reinterpret_cast<uint2 *>(lc + ca) = make_uint2((unsigned)nloc[0] | ((unsigned)nloc[1] << 16),
-                                                         (unsigned)nloc[2] | ((unsigned)nloc[3] << 16));
-        if (l == 0) {
-            unsigned word = 0;
-#pragma unroll
-            for (int v = 0; v < 4; v++) word |= ((parw[v] >> (sub * LR)) & LMASK) << (v * LR);
-            par[i] = (SWT)(word ^ ((d & 1) ? corr_all : 0u));  // (-1)^{d_i}, reading A1
-        }
+        *reinterpret_cast<uint4 *>(lc + ca) = make_uint4(nloc[0], nloc[1], nloc[2], nloc[3]);
         syn_acc |= syn;
     }
+    __syncwarp();  // every lane has read *parb before lane 0 rewrites it
+    if (lane == 0) *parb = make_uint4(parw[0] ^ flip, parw[1] ^ flip, parw[2] ^ flip, parw[3] ^ flip);
 }
 
 // Lane layout: a lane owns 4 consecutive slots (float4) of one row or column; LR = S/4 lanes cover a
 // row, G = 32/LR rows per warp.  Bit of slot q = 4*l + v inside an S-bit sign word: v*LR + l.
 template <int S, int RT>
-__global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? 2 : 1) k_resident(ResArgs a) {
+__global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 2) : 1) k_resident(ResArgs a) {
     constexpr int NWARP = RT / 32;
-    using SWT = typename SWord<S>::T;
     constexpr int LR = S / 4;
     constexpr int G = 32 / LR;
     extern __shared__ __align__(16) unsigned char sm[];
@@ -201,13 +173,14 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? 2 : 1) k_resid
     float *s = reinterpret_cast<float *>(sm + a.lay.s);
     float *mn0 = reinterpret_cast<float *>(sm + a.lay.m0);
     float *mn1 = reinterpret_cast<float *>(sm + a.lay.m1);
-    uint16_t *lc = reinterpret_cast<uint16_t *>(sm + a.lay.lc);
-    SWT *sg = reinterpret_cast<SWT *>(sm + a.lay.sg);
-    SWT *par = reinterpret_cast<SWT *>(sm + a.lay.par);
+    uint32_t *lc = reinterpret_cast<uint32_t *>(sm + a.lay.lc);
+    uint4 *sgb = reinterpret_cast<uint4 *>(sm + a.lay.sgb);
+    uint4 *parb = reinterpret_cast<uint4 *>(sm + a.lay.parb);
     uint16_t *rp = reinterpret_cast<uint16_t *>(sm + a.lay.rp);
     uint16_t *cp = reinterpret_cast<uint16_t *>(sm + a.lay.cp);
     uint16_t *col = reinterpret_cast<uint16_t *>(sm + a.lay.col);
     uint32_t *rec = reinterpret_cast<uint32_t *>(sm + a.lay.rec);
+    uint16_t *rec2 = reinterpret_cast<uint16_t *>(sm + a.lay.rec2);
     int *meta = reinterpret_cast<int *>(sm + a.lay.meta);
     int *slot_f = meta;            // frame index of the slot, -1 = empty
     int *slot_k = meta + 32;       // completed loop bodies
@@ -220,7 +193,8 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? 2 : 1) k_resid
     const int sub = lane / LR, l = lane % LR;  // row group inside the warp, lane inside the row
     const int q0 = 4 * l;                      // first slot of this lane
     float *rs = a.rs + (size_t)blockIdx.x * n * S;
-    const unsigned corr_all = a.literal ? 0u : (S == 32 ? 0xffffffffu : ((1u << S) - 1u));
+    const bool corr = !a.literal;
+    const int dm = a.dm;
 
     // ---- the Tanner graph into shared memory (16-bit lists)
     for (int q = tid; q <= m; q += RT) rp[q] = (uint16_t)__ldg(a.g.row_ptr + q);
@@ -229,6 +203,7 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? 2 : 1) k_resid
         col[e] = (uint16_t)__ldg(a.g.col_idx + e);
         const int4 be = __ldg(a.g.bn_edge + e);  // {edge id, row, pos, parity}
         rec[e] = ((uint32_t)be.x << 16) | (uint32_t)be.y;
+        rec2[e] = (uint16_t)((be.y / G) * dm + be.z);  // ballot-word index of the edge
     }
     if (tid < 32) {
         slot_f[tid] = -1;
@@ -345,10 +320,6 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? 2 : 1) k_resid
 
         // ---------------- C: check-node pass + syndrome of b = slice(s)
         {
-            SWT nfw = 0;
-#pragma unroll
-            for (int q = 0; q < S; q++)
-                if (!((fresh_new >> q) & 1u)) nfw |= (SWT)(1u << ((q & 3) * LR + (q >> 2)));
             unsigned syn_acc = 0;  // bit v: slot q0+v has an unsatisfied check
             for (int rb = warp * G; rb < m; rb += NWARP * G) {
                 const int i = rb + sub;
@@ -356,11 +327,13 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? 2 : 1) k_resid
                 const int ra = valid ? rp[i] : 0;
                 const int d = valid ? (int)rp[i + 1] - ra : 0;
                 const int dmax = __reduce_max_sync(FULLM, d);
+                uint4 *wsg = sgb + (size_t)(rb / G) * dm;
+                uint4 *wpar = parb + rb / G;
                 if (__all_sync(FULLM, d == dmax))
-                    cn_rows<S, false>(s, mn0, mn1, lc, sg, par, col, i, valid, ra, d, dmax, l, sub, fm, nfw, corr_all,
+                    cn_rows<S, false>(s, mn0, mn1, lc, wsg, wpar, col, i, valid, ra, d, dmax, l, lane, fm, corr,
                                       syn_acc);
                 else
-                    cn_rows<S, true>(s, mn0, mn1, lc, sg, par, col, i, valid, ra, d, dmax, l, sub, fm, nfw, corr_all,
+                    cn_rows<S, true>(s, mn0, mn1, lc, wsg, wpar, col, i, valid, ra, d, dmax, l, lane, fm, corr,
                                      syn_acc);
             }
             const unsigned mine = (syn_acc << q0) & active;
@@ -389,9 +362,6 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? 2 : 1) k_resid
                 for (int v = 0; v < 4; v++) fo[v] = (int64_t)slot_f[q0 + v] * n;
                 int be[4] = {0, 0, 0, 0};
                 unsigned nz = 0;
-                unsigned mv[4];
-#pragma unroll
-                for (int v = 0; v < 4; v++) mv[v] = 1u << (v * LR + l);
                 for (int cb = warp * G; cb < n; cb += NWARP * G) {
                     const int j = cb + sub;
                     if (j >= n || !(cm | fk)) continue;
@@ -418,17 +388,20 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? 2 : 1) k_resid
                         for (int qq = 0; qq < dv; qq++) {
                             const uint32_t rc = rec[c0 + qq];
                             const int e = (int)(rc >> 16), i = (int)(rc & 0xffffu);
-                            const unsigned e2 = (unsigned)e * 0x10001u;
                             const int ca = i * S + q0;
                             const float4 m0 = *reinterpret_cast<const float4 *>(mn0 + ca);
                             const float4 m1 = *reinterpret_cast<const float4 *>(mn1 + ca);
-                            const uint2 lv = *reinterpret_cast<const uint2 *>(lc + ca);
-                            const unsigned W = (unsigned)sg[e] ^ (unsigned)par[i];
+                            const uint4 lv = *reinterpret_cast<const uint4 *>(lc + ca);
+                            const uint4 W = sgb[rec2[c0 + qq]];
+                            const uint4 Pw = parb[i / G];
+                            const unsigned bm = 1u << ((i % G) * LR + l);  // this lane's bit of row i
+                            const float mg[4] = {((int)lv.x == e) ? m1.x : m0.x, ((int)lv.y == e) ? m1.y : m0.y,
+                                                 ((int)lv.z == e) ? m1.z : m0.z, ((int)lv.w == e) ? m1.w : m0.w};
+                            const bool ng[4] = {((W.x ^ Pw.x) & bm) != 0u, ((W.y ^ Pw.y) & bm) != 0u,
+                                                ((W.z ^ Pw.z) & bm) != 0u, ((W.w ^ Pw.w) & bm) != 0u};
 #pragma unroll
-                            for (int v = 0; v < 4; v++) {
-                                const float mag = loc_ne(v < 2 ? lv.x : lv.y, e2, v & 1) ? f4c(m0, v) : f4c(m1, v);
-                                acc[v] = acc[v] + ((W & mv[v]) ? -mag : mag);  // ascending rows from +0.0 (A14)
-                            }
+                            for (int v = 0; v < 4; v++)
+                                acc[v] = acc[v] + (ng[v] ? -mg[v] : mg[v]);  // ascending rows from +0.0 (A14)
                         }
                         if (cm & 1u) o.x = acc[0] + rj.x;
                         if (cm & 2u) o.y = acc[1] + rj.y;
@@ -490,6 +463,7 @@ void launch_t(const ResArgs &args, int threads, int ctas, size_t smem, cudaStrea
 }  // namespace
 
 ResidentPlan plan_resident(const HostGraph &g, bool loc16, int device) {
+    const int dm = std::max(1, g.max_row_deg);
     (void)loc16;
     ResidentPlan rp;
     if (g.n >= 65535 || g.m >= 65535 || g.E >= 65535 || g.E == 0) return rp;
@@ -506,16 +480,17 @@ ResidentPlan plan_resident(const HostGraph &g, bool loc16, int device) {
     for (int pass = 0; pass < 2 && !rp.ok; pass++) {
         for (int S : {32, 16, 8, 4}) {
             if (force_s && S != force_s) continue;
-            const Layout L = layout_for(S, g.m, g.n, g.E);
+            const Layout L = layout_for(S, g.m, g.n, g.E, dm);
             if (L.total > (size_t)cap) continue;
-            const int per_sm = std::max(1, std::min(2, sm_smem / (int)(L.total + 1024)));
+            const int per_sm = std::max(1, std::min(S == 4 ? 3 : 2, sm_smem / (int)(L.total + 1024)));
             if (pass == 0 && per_sm < 2 && !force_s) continue;
             rp.ok = true;
             rp.slots = S;
+            rp.dm = dm;
             rp.smem = L.total;
             rp.threads = per_sm >= 2 ? 256 : 512;
             if (force_t == 128 || force_t == 256 || force_t == 512 || force_t == 1024) rp.threads = force_t;
-            const int fit = rp.threads == 128 ? per_sm : rp.threads == 256 ? std::min(per_sm, 2) : 1;
+            const int fit = rp.threads == 128 ? per_sm : rp.threads == 256 ? std::min(per_sm, S == 4 ? 3 : 2) : 1;
             rp.ctas = sms * fit;
             break;
         }
@@ -543,7 +518,8 @@ int launch_resident(const Graph &g, const ResidentPlan &rp, const float *llr, in
     a.stats = stats;
     a.counter = work_counter;
     a.rs = reinterpret_cast<float *>(reinterpret_cast<char *>(work_counter) + 256);
-    a.lay = layout_for(rp.slots, g.m, g.n, g.E);
+    a.dm = rp.dm;
+    a.lay = layout_for(rp.slots, g.m, g.n, g.E, rp.dm);
     cudaMemsetAsync(work_counter, 0, sizeof(int), st);
     switch (rp.slots) {
         case 32: launch_t<32>(a, rp.threads, rp.ctas, rp.smem, st); break;

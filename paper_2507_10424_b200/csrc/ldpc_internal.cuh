@@ -92,6 +92,7 @@ struct ResidentPlan {
     int threads = 0;     // threads per CTA
     size_t smem = 0;     // dynamic shared memory bytes
     int ctas = 0;        // persistent grid size
+    int dm = 0;          // max row degree (ballot-word rows)
 };
 ResidentPlan plan_resident(const HostGraph &g, bool loc16, int device);
 size_t resident_scratch_bytes(const HostGraph &g, const ResidentPlan &rp);  // work counter + r scratch
