@@ -6,7 +6,7 @@
 //   s    [n][S]  fp32          soft vector (Eq. sCalculation)
 //   min0 [m][S]  fp32          Observation 1's minimum
 //   min1 [m][S]  fp32          Observation 1's second minimum
-//   lc   [m][S]  u32           min0Location, stored as the edge id inside the row lists (-1 = none)
+//   lc   [m][S]  u8            min0Location as the position p inside row i's list (0xff = none)
 //   sgb  [m/G][dmax] 4 x u32   sign of lambda_e = s_j - eta_e, kept as the warp ballots of the check
 //                              node (bit (i % G) * LR + l of component v = row i, slot 4l + v)
 //   parb [m/G]   4 x u32       the rows' sign parity (Obs. 2) x (-1)^{d_i} (reading A1), same bits
@@ -34,6 +34,7 @@ constexpr unsigned FULLM = 0xffffffffu;
 
 struct Layout {
     size_t s, m0, m1, lc, sgb, parb, rp, cp, col, rec, rec2, meta, total;
+    size_t sgb_half, parb_half;  // words per buffer (sign words are double-buffered by loop pass)
 };
 
 constexpr size_t a16(size_t x) { return (x + 15) & ~(size_t)15; }
@@ -52,9 +53,11 @@ Layout layout_for(int S, int m, int n, int E, int dm) {
     L.s = o;    o = a16(o + (size_t)n * S * 4);
     L.m0 = o;   o = a16(o + (size_t)m * S * 4);
     L.m1 = o;   o = a16(o + (size_t)m * S * 4);
-    L.lc = o;   o = a16(o + (size_t)m * S * 4);
-    L.sgb = o;  o = a16(o + nrg * dm * 16);
-    L.parb = o; o = a16(o + nrg * 16);
+    L.lc = o;   o = a16(o + (size_t)m * S);
+    L.sgb_half = nrg * dm;
+    L.parb_half = nrg;
+    L.sgb = o;  o = a16(o + 2 * nrg * dm * 16);
+    L.parb = o; o = a16(o + 2 * nrg * 16);
     L.rp = o;   o = a16(o + (size_t)(m + 1) * 2);
     L.cp = o;   o = a16(o + (size_t)(n + 1) * 2);
     L.col = o;  o = a16(o + (size_t)E * 2);
@@ -90,34 +93,37 @@ __device__ __forceinline__ void f4s(float4 &a, int v, float x) {
 
 // Check-node update of G rows (one per row group of the warp) for the 4 slots of this lane.
 // HAS: rows of the warp may have different degrees (irregular H), lanes past their degree idle.
-// fm: this lane's fresh slots (eta^prev = 0).  sgb/parb: the ballot words of this row block.
+// fm: this lane's fresh slots (eta^prev = 0).  sgi/pai: the ballot words of this row block from
+// the previous body, sgo/pao: where this body's go (the other buffer, so no lane waits for the others).
 template <int S, bool HAS>
-__device__ __forceinline__ void cn_rows(const float *s, float *mn0, float *mn1, uint32_t *lc, uint4 *sgb, uint4 *parb,
+__device__ __forceinline__ void cn_rows(const float *__restrict__ s, float *mn0, float *mn1, uint8_t *lc,
+                                        const uint4 *__restrict__ sgi, const uint4 *__restrict__ pai,
+                                        uint4 *__restrict__ sgo, uint4 *__restrict__ pao,
                                         const uint16_t *col, int i, bool valid, int ra, int d, int dmax, int l,
-                                        int lane, unsigned fm, bool corr, unsigned &syn_acc) {
+                                        int lane, unsigned fm, uint32_t fmb, bool corr, unsigned &syn_acc) {
     const float INF = __int_as_float(0x7f800000);
     const int q0 = 4 * l;
     float4 om0 = make_float4(0.f, 0.f, 0.f, 0.f), om1 = om0;
-    uint4 olc = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+    uint32_t olc = 0xffffffffu;  // byte v: min0Location of slot q0 + v
     const int ca = i * S + q0;
     if (valid) {
         om0 = *reinterpret_cast<const float4 *>(mn0 + ca);
         om1 = *reinterpret_cast<const float4 *>(mn1 + ca);
-        olc = *reinterpret_cast<const uint4 *>(lc + ca);
+        olc = *reinterpret_cast<const uint32_t *>(lc + ca) | fmb;
         if (fm) {  // fresh slots start from eta = 0: min0 = min1 = +0, no location
-            if (fm & 1u) { om0.x = 0.f; om1.x = 0.f; olc.x = 0xffffffffu; }
-            if (fm & 2u) { om0.y = 0.f; om1.y = 0.f; olc.y = 0xffffffffu; }
-            if (fm & 4u) { om0.z = 0.f; om1.z = 0.f; olc.z = 0xffffffffu; }
-            if (fm & 8u) { om0.w = 0.f; om1.w = 0.f; olc.w = 0xffffffffu; }
+            if (fm & 1u) { om0.x = 0.f; om1.x = 0.f; }
+            if (fm & 2u) { om0.y = 0.f; om1.y = 0.f; }
+            if (fm & 4u) { om0.z = 0.f; om1.z = 0.f; }
+            if (fm & 8u) { om0.w = 0.f; om1.w = 0.f; }
         }
     }
-    const uint4 P = *parb;  // row sign parities x (-1)^{d_i} of the previous body, one bit per lane
+    const uint4 P = *pai;  // row sign parities x (-1)^{d_i} of the previous body, one bit per lane
     const unsigned lm = 1u << lane;
     unsigned mk[4];  // this lane's bit, cleared for fresh slots (their eta^prev is +0)
 #pragma unroll
     for (int v = 0; v < 4; v++) mk[v] = ((fm >> v) & 1u) ? 0u : lm;
     float nm0[4] = {INF, INF, INF, INF}, nm1[4] = {INF, INF, INF, INF};
-    int nloc[4] = {-1, -1, -1, -1};
+    int nloc[4] = {0xff, 0xff, 0xff, 0xff};
     unsigned parw[4] = {0, 0, 0, 0};
     unsigned syn = 0;
 #pragma unroll 2
@@ -125,10 +131,12 @@ __device__ __forceinline__ void cn_rows(const float *s, float *mn0, float *mn1, 
         const bool has = HAS ? (p < d) : true;
         const int e = ra + p;
         const int j = has ? col[e] : 0;
+        const uint32_t pp = (uint32_t)p * 0x01010101u;
         const float4 sv = *reinterpret_cast<const float4 *>(s + j * S + q0);
-        const uint4 W = sgb[p];  // own sign of lambda^prev per component (Obs. 2)
-        const float mg[4] = {((int)olc.x == e) ? om1.x : om0.x, ((int)olc.y == e) ? om1.y : om0.y,
-                             ((int)olc.z == e) ? om1.z : om0.z, ((int)olc.w == e) ? om1.w : om0.w};  // Obs. 1
+        const uint4 W = sgi[p];  // own sign of lambda^prev per component (Obs. 2)
+        const float mg[4] = {((olc ^ pp) & 0xffu) ? om0.x : om1.x, ((olc ^ pp) & 0xff00u) ? om0.y : om1.y,
+                             ((olc ^ pp) & 0xff0000u) ? om0.z : om1.z,
+                             ((olc ^ pp) & 0xff000000u) ? om0.w : om1.w};  // Obs. 1
         const bool ng[4] = {((W.x ^ P.x) & mk[0]) != 0u, ((W.y ^ P.y) & mk[1]) != 0u, ((W.z ^ P.z) & mk[2]) != 0u,
                             ((W.w ^ P.w) & mk[3]) != 0u};
         unsigned bal[4];
@@ -140,31 +148,30 @@ __device__ __forceinline__ void cn_rows(const float *s, float *mn0, float *mn1, 
             const bool lt = ax < nm0[v];  // first strict minimum (A13)
             nm1[v] = fminf(nm1[v], fmaxf(nm0[v], ax));
             nm0[v] = fminf(nm0[v], ax);
-            nloc[v] = lt ? e : nloc[v];
+            nloc[v] = lt ? p : nloc[v];
             bal[v] = __ballot_sync(FULLM, (HAS ? has : true) && x < 0.f);  // sign(0) = +1
             syn ^= (unsigned)((HAS ? has : true) && sj > 0.f) << v;        // b_j = slice(s_j)
         }
 #pragma unroll
         for (int v = 0; v < 4; v++) parw[v] ^= bal[v];
-        __syncwarp();  // every lane has read sgb[p] before lane 0 rewrites it
-        if (lane == 0) sgb[p] = make_uint4(bal[0], bal[1], bal[2], bal[3]);
+        if (lane == 0) sgo[p] = make_uint4(bal[0], bal[1], bal[2], bal[3]);
     }
     // row parity words of this block; rows of odd degree flip under the CORRECTED rule (reading A1)
     const unsigned flip = __ballot_sync(FULLM, valid && corr && (d & 1));
     if (valid) {
         *reinterpret_cast<float4 *>(mn0 + ca) = make_float4(nm0[0], nm0[1], nm0[2], nm0[3]);
         *reinterpret_cast<float4 *>(mn1 + ca) = make_float4(nm1[0], nm1[1], nm1[2], nm1[3]);
-        *reinterpret_cast<uint4 *>(lc + ca) = make_uint4(nloc[0], nloc[1], nloc[2], nloc[3]);
+        *reinterpret_cast<uint32_t *>(lc + ca) =
+            (uint32_t)nloc[0] | ((uint32_t)nloc[1] << 8) | ((uint32_t)nloc[2] << 16) | ((uint32_t)nloc[3] << 24);
         syn_acc |= syn;
     }
-    __syncwarp();  // every lane has read *parb before lane 0 rewrites it
-    if (lane == 0) *parb = make_uint4(parw[0] ^ flip, parw[1] ^ flip, parw[2] ^ flip, parw[3] ^ flip);
+    if (lane == 0) *pao = make_uint4(parw[0] ^ flip, parw[1] ^ flip, parw[2] ^ flip, parw[3] ^ flip);
 }
 
 // Lane layout: a lane owns 4 consecutive slots (float4) of one row or column; LR = S/4 lanes cover a
 // row, G = 32/LR rows per warp.  Bit of slot q = 4*l + v inside an S-bit sign word: v*LR + l.
 template <int S, int RT>
-__global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 2) : 1) k_resident(ResArgs a) {
+__global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 2) : RT == 384 ? 2 : 1) k_resident(ResArgs a) {
     constexpr int NWARP = RT / 32;
     constexpr int LR = S / 4;
     constexpr int G = 32 / LR;
@@ -173,7 +180,7 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
     float *s = reinterpret_cast<float *>(sm + a.lay.s);
     float *mn0 = reinterpret_cast<float *>(sm + a.lay.m0);
     float *mn1 = reinterpret_cast<float *>(sm + a.lay.m1);
-    uint32_t *lc = reinterpret_cast<uint32_t *>(sm + a.lay.lc);
+    uint8_t *lc = reinterpret_cast<uint8_t *>(sm + a.lay.lc);
     uint4 *sgb = reinterpret_cast<uint4 *>(sm + a.lay.sgb);
     uint4 *parb = reinterpret_cast<uint4 *>(sm + a.lay.parb);
     uint16_t *rp = reinterpret_cast<uint16_t *>(sm + a.lay.rp);
@@ -202,7 +209,7 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
     for (int e = tid; e < E; e += RT) {
         col[e] = (uint16_t)__ldg(a.g.col_idx + e);
         const int4 be = __ldg(a.g.bn_edge + e);  // {edge id, row, pos, parity}
-        rec[e] = ((uint32_t)be.x << 16) | (uint32_t)be.y;
+        rec[e] = ((uint32_t)be.z << 16) | (uint32_t)be.y;  // {pos p in row i, row i}
         rec2[e] = (uint16_t)((be.y / G) * dm + be.z);  // ballot-word index of the edge
     }
     if (tid < 32) {
@@ -221,7 +228,10 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
     unsigned long long acc_stats[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // warp 0, lane = slot
     __syncthreads();
 
-    for (;;) {
+    for (int pass = 0;; pass++) {
+        const int cur = pass & 1;  // sign words of the previous body are in buffer cur, this body's in cur ^ 1
+        const uint4 *sgi = sgb + (cur ? a.lay.sgb_half : 0), *pai = parb + (cur ? a.lay.parb_half : 0);
+        uint4 *sgo = sgb + (cur ? 0 : a.lay.sgb_half), *pao = parb + (cur ? 0 : a.lay.parb_half);
         // ---------------- A: finish stopped slots, advance continuing ones, refill (warp 0)
         if (warp == 0) {
             const unsigned uns_all = ctl[0];
@@ -285,6 +295,7 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
         const unsigned active = ctl[2], fresh_new = ctl[1];
         if (!active) break;
         const unsigned fm = (fresh_new >> q0) & 0xfu;  // this lane's fresh slots
+        const uint32_t fmb = (fm & 1u) * 0xffu | (fm & 2u) * 0x7f80u | (fm & 4u) * 0x3fc000u | (fm & 8u) * 0x1fe00000u;
 
         // ---------------- B: stage new frames, s = r: column sweep in the float4 layout
         if (fresh_new) {
@@ -327,14 +338,13 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
                 const int ra = valid ? rp[i] : 0;
                 const int d = valid ? (int)rp[i + 1] - ra : 0;
                 const int dmax = __reduce_max_sync(FULLM, d);
-                uint4 *wsg = sgb + (size_t)(rb / G) * dm;
-                uint4 *wpar = parb + rb / G;
+                const size_t rg = (size_t)(rb / G);
                 if (__all_sync(FULLM, d == dmax))
-                    cn_rows<S, false>(s, mn0, mn1, lc, wsg, wpar, col, i, valid, ra, d, dmax, l, lane, fm, corr,
-                                      syn_acc);
+                    cn_rows<S, false>(s, mn0, mn1, lc, sgi + rg * dm, pai + rg, sgo + rg * dm, pao + rg, col, i,
+                                      valid, ra, d, dmax, l, lane, fm, fmb, corr, syn_acc);
                 else
-                    cn_rows<S, true>(s, mn0, mn1, lc, wsg, wpar, col, i, valid, ra, d, dmax, l, lane, fm, corr,
-                                     syn_acc);
+                    cn_rows<S, true>(s, mn0, mn1, lc, sgi + rg * dm, pai + rg, sgo + rg * dm, pao + rg, col, i,
+                                     valid, ra, d, dmax, l, lane, fm, fmb, corr, syn_acc);
             }
             const unsigned mine = (syn_acc << q0) & active;
             const unsigned wmask = __reduce_or_sync(FULLM, mine);
@@ -387,16 +397,17 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
 #pragma unroll 2
                         for (int qq = 0; qq < dv; qq++) {
                             const uint32_t rc = rec[c0 + qq];
-                            const int e = (int)(rc >> 16), i = (int)(rc & 0xffffu);
+                            const int i = (int)(rc & 0xffffu);
+                            const uint32_t pp = (rc >> 16) * 0x01010101u;  // position of the edge in row i
                             const int ca = i * S + q0;
                             const float4 m0 = *reinterpret_cast<const float4 *>(mn0 + ca);
                             const float4 m1 = *reinterpret_cast<const float4 *>(mn1 + ca);
-                            const uint4 lv = *reinterpret_cast<const uint4 *>(lc + ca);
-                            const uint4 W = sgb[rec2[c0 + qq]];
-                            const uint4 Pw = parb[i / G];
+                            const uint32_t lv = *reinterpret_cast<const uint32_t *>(lc + ca) ^ pp;
+                            const uint4 W = sgo[rec2[c0 + qq]];
+                            const uint4 Pw = pao[i / G];
                             const unsigned bm = 1u << ((i % G) * LR + l);  // this lane's bit of row i
-                            const float mg[4] = {((int)lv.x == e) ? m1.x : m0.x, ((int)lv.y == e) ? m1.y : m0.y,
-                                                 ((int)lv.z == e) ? m1.z : m0.z, ((int)lv.w == e) ? m1.w : m0.w};
+                            const float mg[4] = {(lv & 0xffu) ? m0.x : m1.x, (lv & 0xff00u) ? m0.y : m1.y,
+                                                 (lv & 0xff0000u) ? m0.z : m1.z, (lv & 0xff000000u) ? m0.w : m1.w};
                             const bool ng[4] = {((W.x ^ Pw.x) & bm) != 0u, ((W.y ^ Pw.y) & bm) != 0u,
                                                 ((W.z ^ Pw.z) & bm) != 0u, ((W.w ^ Pw.w) & bm) != 0u};
 #pragma unroll
@@ -456,6 +467,7 @@ template <int S>
 void launch_t(const ResArgs &args, int threads, int ctas, size_t smem, cudaStream_t st) {
     if (threads == 1024) launch_s<S, 1024>(args, ctas, smem, st);
     else if (threads == 256) launch_s<S, 256>(args, ctas, smem, st);
+    else if (threads == 384) launch_s<S, 384>(args, ctas, smem, st);
     else if (threads == 128) launch_s<S, 128>(args, ctas, smem, st);
     else launch_s<S, 512>(args, ctas, smem, st);
 }
@@ -466,7 +478,7 @@ ResidentPlan plan_resident(const HostGraph &g, bool loc16, int device) {
     const int dm = std::max(1, g.max_row_deg);
     (void)loc16;
     ResidentPlan rp;
-    if (g.n >= 65535 || g.m >= 65535 || g.E >= 65535 || g.E == 0) return rp;
+    if (g.n >= 65535 || g.m >= 65535 || g.E >= 65535 || g.E == 0 || dm > 254) return rp;  // u16 lists, u8 positions
     const int cap = max_smem_optin(device);
     int sms = 0, sm_smem = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
@@ -489,8 +501,12 @@ ResidentPlan plan_resident(const HostGraph &g, bool loc16, int device) {
             rp.dm = dm;
             rp.smem = L.total;
             rp.threads = per_sm >= 2 ? 256 : 512;
-            if (force_t == 128 || force_t == 256 || force_t == 512 || force_t == 1024) rp.threads = force_t;
-            const int fit = rp.threads == 128 ? per_sm : rp.threads == 256 ? std::min(per_sm, S == 4 ? 3 : 2) : 1;
+            if (force_t == 128 || force_t == 256 || force_t == 384 || force_t == 512 || force_t == 1024)
+                rp.threads = force_t;
+            const int fit = rp.threads == 128   ? per_sm
+                            : rp.threads == 256 ? std::min(per_sm, S == 4 ? 3 : 2)
+                            : rp.threads == 384 ? std::min(per_sm, 2)
+                                                : 1;
             rp.ctas = sms * fit;
             break;
         }
