@@ -5,7 +5,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(HERE, "libldpc.so")
+SO_PATH = os.environ.get("LDPC_LIB") or os.path.join(HERE, "libldpc.so")  # LDPC_LIB: A/B builds
 
 P = ctypes.c_void_p
 I32 = ctypes.c_int32

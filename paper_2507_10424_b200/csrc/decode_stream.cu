@@ -45,13 +45,16 @@ __device__ __forceinline__ int compl4(const V &a, int v) {
     return v == 0 ? (int)a.x : v == 1 ? (int)a.y : v == 2 ? (int)a.z : (int)a.w;
 }
 
-__device__ __forceinline__ float4 ldg4(const float *p) { return __ldg(reinterpret_cast<const float4 *>(p)); }
 __device__ __forceinline__ float4 ld4(const float *p) { return *reinterpret_cast<const float4 *>(p); }
 __device__ __forceinline__ void st4(float *p, float4 v) { *reinterpret_cast<float4 *>(p) = v; }
 __device__ __forceinline__ uint4 ldu4(const uint32_t *p) { return *reinterpret_cast<const uint4 *>(p); }
 
 // ------------------------------------------------------------------------------------------------
 // a2: stage-in.  llr [F][n] -> r, s [T][n][128] (s = r), init per-tile flags.
+// s is stored canonically (-0 -> +0; same slice and same sign() under reading A12), so that the later
+// sweeps can read both the decision b = slice(s) and the sign of lambda = s - eta^prev straight from
+// IEEE bits: after this no s and no lambda is ever -0 (x - y = -0 only for x = -0 and y = +0, and a
+// bit-node sum started at +0.0 is never -0).
 // ------------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(CTA) k_stage_in(const float *__restrict__ llr, int64_t frames, int n, int T,
                                                   float *__restrict__ r, float *__restrict__ s,
@@ -76,7 +79,7 @@ __global__ void __launch_bounds__(CTA) k_stage_in(const float *__restrict__ llr,
         for (int q = 0; q < 4; q++) {
             float v = tile[jl][lane + 32 * q];
             r[base + lane + 32 * q] = v;
-            s[base + lane + 32 * q] = v;
+            s[base + lane + 32 * q] = __fadd_rn(v, 0.0f);  // canonical zero
         }
     }
     if (blockIdx.x == 0) {
@@ -106,23 +109,75 @@ __global__ void __launch_bounds__(CTA) k_stage_in(const float *__restrict__ llr,
 }
 
 // ------------------------------------------------------------------------------------------------
-// a3/a4/a6: check-node sweep of loop body k (k = 1..L), fused syndrome of b^(k-1).
-// FIRST: eta^prev = 0 (P:135), so no old state is read.
-// Sign words: per (tile, edge) four u32; lane l's four bits (frames 4l..4l+3) are the nibble at bits
-// 4*(l%8) of word l/8, so a lane reads one u32 per edge.  The row parity stored in min0's sign bit
-// already includes the (-1)^{d_i} factor of reading A1.
-// The edges of a row are processed in chunks of CN_U: all index, s and sign loads of a chunk are
-// issued before any arithmetic, so each warp keeps 2*CN_U loads in flight.
+// Encoding of the check-node state (it IS eta: Obs. 1 and 2, reading A2):
+//   min0, min1   fp32, both with SIGN BIT = the row's sign parity x (-1)^{d_i} (reading A1), so the
+//                magnitude picked by Obs. 1 already carries the row factor of Obs. 2;
+//   loc          u8 / u16 min0Location (position inside N_i);
+//   sgn          per (tile, edge) four u32 in "ballot layout": bit l of word v is the sign of
+//                lambda_e for frame 4l + v -- exactly the four warp ballots the check node produces.
+// eta_e = (loc == p ? min1 : min0) with its sign bit XORed with sgn bit: one FSEL and one LOP3 per
+// frame-edge; a lane moves its ballot bit to bit 31 with one integer multiply by 2^(31-lane) (FMA
+// pipe), which keeps the ALU pipe -- the sweeps' real limiter -- for the min/argmin work.
 // ------------------------------------------------------------------------------------------------
-template <int U>
-struct MinBlocks {
-    static constexpr int value = U <= 1 ? 4 : U == 2 ? 3 : 2;  // register budget 64 / 85 / 128 per thread
+template <typename LocT>
+struct LocOps;
+template <>
+struct LocOps<uint8_t> {
+    using W = uint32_t;  // the 4 locations of a lane, one byte each
+    static __device__ __forceinline__ W load(const uint8_t *p) { return *reinterpret_cast<const uint32_t *>(p); }
+    static __device__ __forceinline__ void store(uint8_t *p, const int l[4]) {
+        *reinterpret_cast<uint32_t *>(p) =
+            (uint32_t)l[0] | ((uint32_t)l[1] << 8) | ((uint32_t)l[2] << 16) | ((uint32_t)l[3] << 24);
+    }
+    static __device__ __forceinline__ W key(W w, int p) { return w ^ ((uint32_t)p * 0x01010101u); }
+    static __device__ __forceinline__ bool hit(W x, int v) { return (x & (0xffu << (8 * v))) == 0u; }
+};
+template <>
+struct LocOps<uint16_t> {
+    using W = uint2;
+    static __device__ __forceinline__ W load(const uint16_t *p) { return *reinterpret_cast<const uint2 *>(p); }
+    static __device__ __forceinline__ void store(uint16_t *p, const int l[4]) {
+        *reinterpret_cast<uint2 *>(p) = make_uint2((uint32_t)l[0] | ((uint32_t)l[1] << 16),
+                                                   (uint32_t)l[2] | ((uint32_t)l[3] << 16));
+    }
+    static __device__ __forceinline__ W key(W w, int p) {
+        const uint32_t q = (uint32_t)p * 0x00010001u;
+        return make_uint2(w.x ^ q, w.y ^ q);
+    }
+    static __device__ __forceinline__ bool hit(W x, int v) {
+        return ((v < 2 ? x.x : x.y) & (0xffffu << (16 * (v & 1)))) == 0u;
+    }
 };
 
-template <typename LocT, bool FIRST, bool EARLY, int CN_U>
-__global__ void __launch_bounds__(CTA, MinBlocks<CN_U>::value)
+// the sign of a magnitude picked by Obs. 1 flipped by one stored sign bit (already moved to bit 31)
+__device__ __forceinline__ float flip31(float mag, uint32_t bit31) {
+    return __uint_as_float(__float_as_uint(mag) ^ (bit31 & 0x80000000u));
+}
+
+constexpr int CN_CHUNK = 8;  // edges per sign word and per batch of gathers (4 frames x 8 edges = 32 bits)
+constexpr int BN_CHUNK = 4;  // column edges per batch of row-state gathers
+#ifndef CN_MINB
+#define CN_MINB 2
+#endif
+#ifndef BN_MINB
+#define BN_MINB 3
+#endif
+
+// ------------------------------------------------------------------------------------------------
+// a3/a4/a6: check-node sweep of loop body k (k = 1..L), fused syndrome of b^(k-1).
+// FIRST: eta^prev = 0 (P:135), so no old state is read.
+// A warp owns rows i0 + warp + 8q.  Per row, every load -- the d gathers of s (512-byte float4
+// segments, lane = 4 frames), the row state and the lane's old sign word -- is issued before any
+// arithmetic, and the column indices of the next row are prefetched meanwhile, so each row costs one
+// memory latency, overlapped across the warps of the SM.  Per frame-edge: lambda = s_j - eta^prev
+// (SEL, LOP3, FADD), first-strict-minimum tracking (FSETP, 3 FMNMX, SEL; reading A13), sign parity
+// (LOP3 on the IEEE bits), the new sign bit into the lane's own word, and, when EARLY, the decision
+// parity (slice(s) = 0 iff bit 31 of bits(s) - 1 is set, s never -0).
+// ------------------------------------------------------------------------------------------------
+template <typename LocT, bool FIRST, bool EARLY>
+__global__ void __launch_bounds__(CTA, CN_MINB)
     k_cn(Graph g, StreamState w, int k, int rows_per_cta, int literal, const int *kdev) {
-    using L4 = typename Vec4<LocT>::type;
+    using LO = LocOps<LocT>;
     if (kdev) k = *kdev;  // body index supplied by the graph-driven loop
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     __shared__ uint32_t s_u[4];
@@ -130,109 +185,117 @@ __global__ void __launch_bounds__(CTA, MinBlocks<CN_U>::value)
     const int cnt = w.tcount[k & 1];
     if (blockIdx.x == 0 && threadIdx.x == 0) w.tcount[(k + 1) & 1] = 0;  // rebuilt by k_bn of body k
     if ((int)blockIdx.y >= cnt) return;  // active tiles are compacted to the front of the list
-    {
     const int t = w.tlist[(size_t)(k & 1) * w.T + blockIdx.y];
-    const int rblk = blockIdx.x;
     if (EARLY) {
         if (threadIdx.x < 4) s_u[threadIdx.x] = 0;
         __syncthreads();
     }
-    const int *__restrict__ row_ptr = g.row_ptr;
-    const int *__restrict__ col_idx = g.col_idx;
-    const float *__restrict__ S = w.s;
-    uint32_t *__restrict__ SG = w.sgn;
-    float *__restrict__ M0 = w.min0;
-    float *__restrict__ M1 = w.min1;
-    LocT *__restrict__ LC = reinterpret_cast<LocT *>(w.loc);
-    const int m = g.m, n = g.n, E = g.E;
-    const size_t tm = (size_t)t * m, tn = (size_t)t * n, tE = (size_t)t * E;
-    const int sh = 4 * (lane & 7), wsel = lane >> 3;
-    const int i0 = rblk * rows_per_cta, i1 = min(m, i0 + rows_per_cta);
+    const int m = g.m, n = g.n, wr = g.wr;
+    const float *__restrict__ Sl = w.s + (size_t)t * n * TILE + 4 * lane;
+    uint32_t *__restrict__ SGl = w.sgn + (size_t)t * m * wr * 32 + lane;
+    float *__restrict__ M0l = w.min0 + (size_t)t * m * TILE + 4 * lane;
+    float *__restrict__ M1l = w.min1 + (size_t)t * m * TILE + 4 * lane;
+    LocT *__restrict__ LCl = reinterpret_cast<LocT *>(w.loc) + (size_t)t * m * TILE + 4 * lane;
+    const float INF = __int_as_float(0x7f800000);
+    const int i0 = blockIdx.x * rows_per_cta + warp, i1 = min(m, blockIdx.x * rows_per_cta + rows_per_cta);
+    const int nr = i0 < i1 ? (i1 - i0 + 7) / 8 : 0;  // rows of this warp (<= 32)
+    int ra = 0, rb = 0;  // lane q: row_ptr of the warp's row q
+    if (lane < nr) {
+        ra = __ldg(g.row_ptr + i0 + 8 * lane);
+        rb = __ldg(g.row_ptr + i0 + 8 * lane + 1);
+    }
+    int a = __shfl_sync(FULL, ra, 0), d = __shfl_sync(FULL, rb, 0) - a;
+    int cj = (nr > 0 && lane < d) ? __ldg(g.col_idx + a + lane) : 0;  // lane q: column of edge q
     uint32_t u0 = 0, u1 = 0, u2 = 0, u3 = 0;
-    for (int i = i0 + warp; i < i1; i += CTA / 32) {
-        const int a = __ldg(row_ptr + i), d = __ldg(row_ptr + i + 1) - a;
-        const unsigned corr = (unsigned)(d & 1) & (unsigned)(!literal);  // (-1)^{d_i}, reading A1
-        const size_t st = (tm + i) * TILE + 4 * lane;
-        float4 om0 = make_float4(0.f, 0.f, 0.f, 0.f), om1 = om0;
-        L4 olc{};
+    for (int q = 0; q < nr; q++) {
+        const int i = i0 + 8 * q;
+        const int an = __shfl_sync(FULL, ra, (q + 1) & 31), dn = __shfl_sync(FULL, rb, (q + 1) & 31) - an;
+        const uint32_t corr = (uint32_t)(d & 1) & (uint32_t)(!literal);  // (-1)^{d_i}, reading A1
+        float om0[4] = {0.f, 0.f, 0.f, 0.f}, om1[4] = {0.f, 0.f, 0.f, 0.f};
+        typename LO::W olc{};
         if (!FIRST) {
-            om0 = ld4(M0 + st);
-            om1 = ld4(M1 + st);
-            olc = *reinterpret_cast<const L4 *>(LC + st);
+            const float4 A = ld4(M0l + (size_t)i * TILE), B = ld4(M1l + (size_t)i * TILE);
+            om0[0] = A.x; om0[1] = A.y; om0[2] = A.z; om0[3] = A.w;
+            om1[0] = B.x; om1[1] = B.y; om1[2] = B.z; om1[3] = B.w;
+            olc = LO::load(LCl + (size_t)i * TILE);
         }
-        float nm0[4], nm1[4];
-        int nloc[4];
-        unsigned npar = 0, syn = 0;
+        float nm0[4] = {INF, INF, INF, INF}, nm1[4] = {INF, INF, INF, INF};
+        int nloc[4] = {0, 0, 0, 0};
+        uint32_t par[4] = {0u, 0u, 0u, 0u}, syn[4] = {0u, 0u, 0u, 0u};
+        for (int p0 = 0; p0 < d; p0 += CN_CHUNK) {
+            if (p0 > 0 && (p0 & 31) == 0) cj = (lane < d - p0) ? __ldg(g.col_idx + a + p0 + lane) : 0;
+            uint32_t *sgp = SGl + ((size_t)i * wr + (p0 >> 3)) * 32;
+            float4 sv[CN_CHUNK];
 #pragma unroll
-        for (int v = 0; v < 4; v++) {
-            nm0[v] = __int_as_float(0x7f800000);
-            nm1[v] = __int_as_float(0x7f800000);
-            nloc[v] = 0;
-        }
-        for (int p0 = 0; p0 < d; p0 += CN_U) {
-            int jj[CN_U];
-            float4 sv[CN_U];
-            unsigned sw[CN_U];
+            for (int u = 0; u < CN_CHUNK; u++) {
+                const int j = __shfl_sync(FULL, cj, (p0 + u) & 31);
+#if defined(CN_PROBE) && CN_PROBE == 2
+                if (p0 + u < d) sv[u] = ld4(Sl + (size_t)(j & 7) * TILE);  // probe: gathers served by L1
+#else
+                if (p0 + u < d) sv[u] = ld4(Sl + (size_t)j * TILE);
+#endif
+            }
+            const uint32_t wold = FIRST ? 0u : *sgp;
+            uint32_t wnew = 0;
 #pragma unroll
-            for (int u = 0; u < CN_U; u++) jj[u] = (p0 + u < d) ? __ldg(col_idx + a + p0 + u) : 0;
-#pragma unroll
-            for (int u = 0; u < CN_U; u++) {
+            for (int u = 0; u < CN_CHUNK; u++) {
+#if defined(CN_PROBE) && CN_PROBE == 1
+                if (p0 + u < d) {  // probe: memory traffic only
+                    nm0[0] = fminf(nm0[0], sv[u].x + sv[u].y + sv[u].z + sv[u].w + om0[u & 3] + om1[u & 3]);
+                    wnew ^= __float_as_uint(sv[u].x) ^ wold;
+                }
+                if (false) {
+#else
                 if (p0 + u < d) {
-                    sv[u] = ld4(S + (tn + jj[u]) * TILE + 4 * lane);
-                    sw[u] = FIRST ? 0u : (SG[(tE + a + p0 + u) * 4 + wsel] >> sh);
-                }
-            }
+#endif
+                    const int p = p0 + u;
+                    typename LO::W key{};
+                    if (!FIRST) key = LO::key(olc, p);
 #pragma unroll
-            for (int u = 0; u < CN_U; u++) {
-                if (p0 + u >= d) break;
-                const int p = p0 + u;
-                unsigned nib = 0;
-#pragma unroll
-                for (int v = 0; v < 4; v++) {
-                    const float sj = comp(sv[u], v);
-                    float x = sj;
-                    if (!FIRST) {
-                        const float m0v = comp(om0, v);
-                        const float mag = (p == compl4(olc, v)) ? comp(om1, v) : fabsf(m0v);  // Obs. 1
-                        const unsigned neg_eta = ((sw[u] >> v) & 1u) ^ (__float_as_uint(m0v) >> 31);  // Obs. 2
-                        x = sj - (neg_eta ? -mag : mag);  // lambda_k - eta^prev_{i,k}
+                    for (int v = 0; v < 4; v++) {
+                        const float sj = comp(sv[u], v);
+                        float x = sj;
+                        if (!FIRST) {
+                            const float mag = LO::hit(key, v) ? om1[v] : om0[v];  // Obs. 1 (+ row parity)
+                            x = sj - flip31(mag, wold << (31 - 4 * u - v));        // lambda_k - eta^prev_{i,k}
+                        }
+                        const float ax = fabsf(x);
+                        const bool lt = ax < nm0[v];  // first strict minimum (A13)
+                        nm1[v] = fminf(nm1[v], fmaxf(nm0[v], ax));
+                        nm0[v] = fminf(nm0[v], ax);
+                        nloc[v] = lt ? p : nloc[v];
+                        par[v] ^= __float_as_uint(x);                          // sign parity (Obs. 2)
+                        if (EARLY) syn[v] ^= __float_as_uint(sj) - 1u;         // bit 31: slice(s_j) == 0
+                        wnew |= (__float_as_uint(x) >> 31) << (4 * u + v);     // sign(0) = +1
                     }
-                    const float ax = fabsf(x);
-                    const bool lt = ax < nm0[v];  // first strict minimum (A13)
-                    nm1[v] = fminf(nm1[v], fmaxf(nm0[v], ax));
-                    nm0[v] = fminf(nm0[v], ax);
-                    nloc[v] = lt ? p : nloc[v];
-                    nib |= (unsigned)(x < 0.f) << v;  // sign(0) = +1
-                    if (EARLY) syn ^= (unsigned)(sj > 0.f) << v;  // b_j = slice(s_j)
                 }
-                npar ^= nib;
-                unsigned word = nib << sh;
-                word |= __shfl_xor_sync(FULL, word, 1);
-                word |= __shfl_xor_sync(FULL, word, 2);
-                word |= __shfl_xor_sync(FULL, word, 4);
-                if ((lane & 7) == 0) SG[(tE + a + p) * 4 + wsel] = word;
             }
+            *sgp = wnew;
         }
-        const unsigned pc = npar ^ (corr ? 0xfu : 0u);
-        float4 o0;
-        o0.x = __uint_as_float(__float_as_uint(nm0[0]) | ((pc & 1u) << 31));
-        o0.y = __uint_as_float(__float_as_uint(nm0[1]) | (((pc >> 1) & 1u) << 31));
-        o0.z = __uint_as_float(__float_as_uint(nm0[2]) | (((pc >> 2) & 1u) << 31));
-        o0.w = __uint_as_float(__float_as_uint(nm0[3]) | (((pc >> 3) & 1u) << 31));
-        st4(M0 + st, o0);
-        st4(M1 + st, make_float4(nm1[0], nm1[1], nm1[2], nm1[3]));
-        L4 nl;
-        nl.x = (LocT)nloc[0];
-        nl.y = (LocT)nloc[1];
-        nl.z = (LocT)nloc[2];
-        nl.w = (LocT)nloc[3];
-        *reinterpret_cast<L4 *>(LC + st) = nl;
+        // prefetch the next row's column indices (its state and gathers are issued at its start)
+        cj = (q + 1 < nr && lane < dn) ? __ldg(g.col_idx + an + lane) : 0;
+        float4 o0, o1;
+        {
+            const uint32_t c31 = corr << 31;
+            const uint32_t s0 = (par[0] & 0x80000000u) ^ c31, s1 = (par[1] & 0x80000000u) ^ c31;
+            const uint32_t s2 = (par[2] & 0x80000000u) ^ c31, s3 = (par[3] & 0x80000000u) ^ c31;
+            o0 = make_float4(__uint_as_float(__float_as_uint(nm0[0]) | s0), __uint_as_float(__float_as_uint(nm0[1]) | s1),
+                             __uint_as_float(__float_as_uint(nm0[2]) | s2), __uint_as_float(__float_as_uint(nm0[3]) | s3));
+            o1 = make_float4(__uint_as_float(__float_as_uint(nm1[0]) | s0), __uint_as_float(__float_as_uint(nm1[1]) | s1),
+                             __uint_as_float(__float_as_uint(nm1[2]) | s2), __uint_as_float(__float_as_uint(nm1[3]) | s3));
+        }
+        st4(M0l + (size_t)i * TILE, o0);
+        st4(M1l + (size_t)i * TILE, o1);
+        LO::store(LCl + (size_t)i * TILE, nloc);
         if (EARLY) {
-            u0 |= __ballot_sync(FULL, syn & 1u);
-            u1 |= __ballot_sync(FULL, syn & 2u);
-            u2 |= __ballot_sync(FULL, syn & 4u);
-            u3 |= __ballot_sync(FULL, syn & 8u);
+            const uint32_t dp = (uint32_t)(d & 1);  // XOR_j b_j = d_i mod 2 xor XOR_j (1 - b_j)
+            u0 |= __ballot_sync(FULL, ((syn[0] >> 31) ^ dp) != 0u);
+            u1 |= __ballot_sync(FULL, ((syn[1] >> 31) ^ dp) != 0u);
+            u2 |= __ballot_sync(FULL, ((syn[2] >> 31) ^ dp) != 0u);
+            u3 |= __ballot_sync(FULL, ((syn[3] >> 31) ^ dp) != 0u);
         }
+        a = an;
+        d = dn;
     }
     if (EARLY) {
         if (lane == 0) {
@@ -245,196 +308,147 @@ __global__ void __launch_bounds__(CTA, MinBlocks<CN_U>::value)
         if (threadIdx.x < 4 && s_u[threadIdx.x])
             atomicOr(w.unsat + ((size_t)(k & 1) * w.T + t) * 4 + threadIdx.x, s_u[threadIdx.x]);
     }
-    }
 }
 
 // ------------------------------------------------------------------------------------------------
-// Check-node sweep with TMA-style bulk-copy staging (cp.async.bulk + mbarrier, per-warp double
-// buffer).  A warp owns ROWS_PER_WARP rows of the block; while it computes row q from shared
-// memory, the bulk copies of row q+2 (the d gathered 512-byte s segments, the d sign words and the
-// old row state) are in flight, so every warp keeps a whole row of loads outstanding without
-// holding them in registers.  Same arithmetic and results as k_cn.
+// Software-pipelined check-node sweep for codes whose rows all have degree <= CH (<= 8: one sign
+// word per row and lane).  Two row buffers in registers: while a warp computes row q from buffer A,
+// every load of row q+1 -- its CH gathers of s, its state and its old sign word -- is already in
+// flight into buffer B, and the column indices of row q+2 are being fetched.  All loads are
+// unconditional (edges past d_i read column 0 of the tile, rows past the warp's last read its first
+// row), so the compiler issues them back to back instead of behind predicated moves.
 // ------------------------------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_addr(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_addr(bar)),
-        "r"(phase)
-        : "memory");
-}
+template <int CH, typename LocT>
+struct CnRow {
+    float4 sv[CH];
+    float4 m0, m1;
+    typename LocOps<LocT>::W lc;
+    uint32_t wold;
+};
 
-constexpr int ROWS_PER_WARP = 8;
-
-// shared-memory bytes of one staging buffer for rows of degree <= dm
-__host__ __device__ constexpr int cn_stage_bytes(int dm, int locb) { return dm * 512 + dm * 16 + 1024 + 128 * locb + 16; }
-
-template <typename LocT, bool FIRST, bool EARLY>
-__global__ void __launch_bounds__(CTA) k_cn_tma(Graph g, StreamState w, int k, int dm, int literal, const int *kdev) {
-    using L4 = typename Vec4<LocT>::type;
-    if (kdev) k = *kdev;
-    extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ uint32_t s_u[4];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int cnt = w.tcount[k & 1];
-    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) w.tcount[(k + 1) & 1] = 0;
-    if ((int)blockIdx.y >= cnt) return;  // active tiles are compacted to the front of the list
-    const int t = w.tlist[(size_t)(k & 1) * w.T + blockIdx.y];
-    if (EARLY && threadIdx.x < 4) s_u[threadIdx.x] = 0;
-    const int sbytes = cn_stage_bytes(dm, (int)sizeof(LocT));
-    unsigned char *wbase = smem + (size_t)warp * 2 * sbytes;
-    // stage layout: s[dm][128] f32 | sw[dm][4] u32 | min0[128] | min1[128] | loc[128] | mbarrier
-    auto sbuf = [&](int b) { return reinterpret_cast<float *>(wbase + b * sbytes); };
-    auto swbuf = [&](int b) { return reinterpret_cast<uint32_t *>(wbase + b * sbytes + dm * 512); };
-    auto m0buf = [&](int b) { return reinterpret_cast<float *>(wbase + b * sbytes + dm * 528); };
-    auto m1buf = [&](int b) { return reinterpret_cast<float *>(wbase + b * sbytes + dm * 528 + 512); };
-    auto lcbuf = [&](int b) { return reinterpret_cast<LocT *>(wbase + b * sbytes + dm * 528 + 1024); };
-    auto bar = [&](int b) {
-        return reinterpret_cast<uint64_t *>(wbase + b * sbytes + dm * 528 + 1024 + 128 * sizeof(LocT));
-    };
-    if (lane == 0) {
-        mbar_init(bar(0), 1);
-        mbar_init(bar(1), 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+template <int CH, typename LocT, bool FIRST>
+__device__ __forceinline__ void cn_fetch(CnRow<CH, LocT> &R, int cj, int i, const float *__restrict__ Sl,
+                                         const uint32_t *__restrict__ SGl, const float *__restrict__ M0l,
+                                         const float *__restrict__ M1l, const LocT *__restrict__ LCl) {
+    if (!FIRST) {
+        R.wold = SGl[(size_t)i * 32];
+        R.m0 = ld4(M0l + (size_t)i * TILE);
+        R.m1 = ld4(M1l + (size_t)i * TILE);
+        R.lc = LocOps<LocT>::load(LCl + (size_t)i * TILE);
     }
-    __syncthreads();
-
-    const int *__restrict__ row_ptr = g.row_ptr;
-    const int *__restrict__ col_idx = g.col_idx;
-    const float *S = w.s;
-    uint32_t *SG = w.sgn;
-    float *M0 = w.min0;
-    float *M1 = w.min1;
-    LocT *LC = reinterpret_cast<LocT *>(w.loc);
-    const int m = g.m, n = g.n, E = g.E;
-    const size_t tm = (size_t)t * m, tn = (size_t)t * n, tE = (size_t)t * E;
-    const int sh = 4 * (lane & 7), wsel = lane >> 3;
-    const int rpc = (CTA / 32) * ROWS_PER_WARP;
-    const int i0 = blockIdx.x * rpc;
-    const int nq = max(0, min(ROWS_PER_WARP, (m - i0 - warp + (CTA / 32) - 1) / (CTA / 32)));
-
-    auto stage = [&](int q, int b) {
-        const int i = i0 + warp + (CTA / 32) * q;
-        const int a = __ldg(row_ptr + i), d = __ldg(row_ptr + i + 1) - a;
-        const unsigned bytes = (unsigned)d * (FIRST ? 512u : 528u) + (FIRST ? 0u : (unsigned)(1024 + 128 * sizeof(LocT)));
-        if (lane == 0) mbar_expect_tx(bar(b), bytes);
-        __syncwarp();
-        for (int p = lane; p < d; p += 32) {
-            const int j = __ldg(col_idx + a + p);
-            bulk_g2s(sbuf(b) + p * TILE, S + (tn + j) * TILE, 512, bar(b));
-            if (!FIRST) bulk_g2s(swbuf(b) + p * 4, SG + (tE + a + p) * 4, 16, bar(b));
-        }
-        if (!FIRST && lane == 31) {
-            const size_t st = (tm + i) * TILE;
-            bulk_g2s(m0buf(b), M0 + st, 512, bar(b));
-            bulk_g2s(m1buf(b), M1 + st, 512, bar(b));
-            bulk_g2s(lcbuf(b), LC + st, 128 * sizeof(LocT), bar(b));
-        }
-    };
-
-    if (nq > 0) stage(0, 0);
-    if (nq > 1) stage(1, 1);
-    uint32_t u0 = 0, u1 = 0, u2 = 0, u3 = 0;
-    for (int q = 0; q < nq; q++) {
-        const int b = q & 1;
-        const int i = i0 + warp + (CTA / 32) * q;
-        const int a = __ldg(row_ptr + i), d = __ldg(row_ptr + i + 1) - a;
-        const unsigned corr = (unsigned)(d & 1) & (unsigned)(!literal);  // (-1)^{d_i}, reading A1
-        mbar_wait(bar(b), (unsigned)(q >> 1) & 1u);
-        float4 om0 = make_float4(0.f, 0.f, 0.f, 0.f), om1 = om0;
-        L4 olc{};
-        if (!FIRST) {
-            om0 = *reinterpret_cast<const float4 *>(m0buf(b) + 4 * lane);
-            om1 = *reinterpret_cast<const float4 *>(m1buf(b) + 4 * lane);
-            olc = *reinterpret_cast<const L4 *>(lcbuf(b) + 4 * lane);
-        }
-        float nm0[4], nm1[4];
-        int nloc[4];
-        unsigned npar = 0, syn = 0;
 #pragma unroll
-        for (int v = 0; v < 4; v++) {
-            nm0[v] = __int_as_float(0x7f800000);
-            nm1[v] = __int_as_float(0x7f800000);
-            nloc[v] = 0;
-        }
-        for (int p = 0; p < d; p++) {
-            const float4 sv = *reinterpret_cast<const float4 *>(sbuf(b) + p * TILE + 4 * lane);
-            const unsigned sw = FIRST ? 0u : (swbuf(b)[p * 4 + wsel] >> sh);
-            unsigned nib = 0;
+    for (int u = 0; u < CH; u++) {
+        const int j = __shfl_sync(FULL, cj, u);
+        R.sv[u] = ld4(Sl + (size_t)j * TILE);
+    }
+}
+
+template <int CH, typename LocT, bool FIRST, bool EARLY>
+__device__ __forceinline__ void cn_compute(const CnRow<CH, LocT> &R, int i, int d, int literal,
+                                           uint32_t *__restrict__ SGl, float *__restrict__ M0l,
+                                           float *__restrict__ M1l, LocT *__restrict__ LCl, uint32_t (&u)[4]) {
+    using LO = LocOps<LocT>;
+    const float INF = __int_as_float(0x7f800000);
+    const uint32_t corr = (uint32_t)(d & 1) & (uint32_t)(!literal);  // (-1)^{d_i}, reading A1
+    const float om0[4] = {R.m0.x, R.m0.y, R.m0.z, R.m0.w}, om1[4] = {R.m1.x, R.m1.y, R.m1.z, R.m1.w};
+    float nm0[4] = {INF, INF, INF, INF}, nm1[4] = {INF, INF, INF, INF};
+    int nloc[4] = {0, 0, 0, 0};
+    uint32_t par[4] = {0u, 0u, 0u, 0u}, syn[4] = {0u, 0u, 0u, 0u}, wnew = 0;
+#pragma unroll
+    for (int p = 0; p < CH; p++) {
+        if (p < d) {
+            typename LO::W key{};
+            if (!FIRST) key = LO::key(R.lc, p);
 #pragma unroll
             for (int v = 0; v < 4; v++) {
-                const float sj = comp(sv, v);
+                const float sj = comp(R.sv[p], v);
                 float x = sj;
                 if (!FIRST) {
-                    const float m0v = comp(om0, v);
-                    const float mag = (p == compl4(olc, v)) ? comp(om1, v) : fabsf(m0v);  // Obs. 1
-                    const unsigned neg_eta = ((sw >> v) & 1u) ^ (__float_as_uint(m0v) >> 31);  // Obs. 2
-                    x = sj - (neg_eta ? -mag : mag);  // lambda_k - eta^prev_{i,k}
+                    const float mag = LO::hit(key, v) ? om1[v] : om0[v];  // Obs. 1 (+ row parity)
+                    x = sj - flip31(mag, R.wold << (31 - 4 * p - v));     // lambda_k - eta^prev_{i,k}
                 }
                 const float ax = fabsf(x);
                 const bool lt = ax < nm0[v];  // first strict minimum (A13)
                 nm1[v] = fminf(nm1[v], fmaxf(nm0[v], ax));
                 nm0[v] = fminf(nm0[v], ax);
                 nloc[v] = lt ? p : nloc[v];
-                nib |= (unsigned)(x < 0.f) << v;  // sign(0) = +1
-                if (EARLY) syn ^= (unsigned)(sj > 0.f) << v;  // b_j = slice(s_j)
+                par[v] ^= __float_as_uint(x);                       // sign parity (Obs. 2)
+                if (EARLY) syn[v] ^= __float_as_uint(sj) - 1u;      // bit 31: slice(s_j) == 0
+                wnew |= (__float_as_uint(x) >> 31) << (4 * p + v);  // sign(0) = +1
             }
-            npar ^= nib;
-            unsigned word = nib << sh;
-            word |= __shfl_xor_sync(FULL, word, 1);
-            word |= __shfl_xor_sync(FULL, word, 2);
-            word |= __shfl_xor_sync(FULL, word, 4);
-            if ((lane & 7) == 0) SG[(tE + a + p) * 4 + wsel] = word;
         }
-        const size_t st = (tm + i) * TILE + 4 * lane;
-        const unsigned pc = npar ^ (corr ? 0xfu : 0u);
-        float4 o0;
-        o0.x = __uint_as_float(__float_as_uint(nm0[0]) | ((pc & 1u) << 31));
-        o0.y = __uint_as_float(__float_as_uint(nm0[1]) | (((pc >> 1) & 1u) << 31));
-        o0.z = __uint_as_float(__float_as_uint(nm0[2]) | (((pc >> 2) & 1u) << 31));
-        o0.w = __uint_as_float(__float_as_uint(nm0[3]) | (((pc >> 3) & 1u) << 31));
-        st4(M0 + st, o0);
-        st4(M1 + st, make_float4(nm1[0], nm1[1], nm1[2], nm1[3]));
-        L4 nl;
-        nl.x = (LocT)nloc[0];
-        nl.y = (LocT)nloc[1];
-        nl.z = (LocT)nloc[2];
-        nl.w = (LocT)nloc[3];
-        *reinterpret_cast<L4 *>(LC + st) = nl;
-        if (EARLY) {
-            u0 |= __ballot_sync(FULL, syn & 1u);
-            u1 |= __ballot_sync(FULL, syn & 2u);
-            u2 |= __ballot_sync(FULL, syn & 4u);
-            u3 |= __ballot_sync(FULL, syn & 8u);
-        }
-        // the generic-proxy reads of buffer b are done before the async proxy refills it
-        __syncwarp();
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        if (q + 2 < nq) stage(q + 2, b);
+    }
+    SGl[(size_t)i * 32] = wnew;
+    const uint32_t c31 = corr << 31;
+    const uint32_t s0 = (par[0] & 0x80000000u) ^ c31, s1 = (par[1] & 0x80000000u) ^ c31;
+    const uint32_t s2 = (par[2] & 0x80000000u) ^ c31, s3 = (par[3] & 0x80000000u) ^ c31;
+    st4(M0l + (size_t)i * TILE,
+        make_float4(__uint_as_float(__float_as_uint(nm0[0]) | s0), __uint_as_float(__float_as_uint(nm0[1]) | s1),
+                    __uint_as_float(__float_as_uint(nm0[2]) | s2), __uint_as_float(__float_as_uint(nm0[3]) | s3)));
+    st4(M1l + (size_t)i * TILE,
+        make_float4(__uint_as_float(__float_as_uint(nm1[0]) | s0), __uint_as_float(__float_as_uint(nm1[1]) | s1),
+                    __uint_as_float(__float_as_uint(nm1[2]) | s2), __uint_as_float(__float_as_uint(nm1[3]) | s3)));
+    LO::store(LCl + (size_t)i * TILE, nloc);
+    if (EARLY) {
+        const uint32_t dp = (uint32_t)(d & 1);  // XOR_j b_j = d_i mod 2 xor XOR_j (1 - b_j)
+#pragma unroll
+        for (int v = 0; v < 4; v++) u[v] |= __ballot_sync(FULL, ((syn[v] >> 31) ^ dp) != 0u);
+    }
+}
+
+template <int CH, typename LocT, bool FIRST, bool EARLY>
+__global__ void __launch_bounds__(CTA, 2)
+    k_cn_pipe(Graph g, StreamState w, int k, int rows_per_cta, int literal, const int *kdev) {
+    if (kdev) k = *kdev;  // body index supplied by the graph-driven loop
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __shared__ uint32_t s_u[4];
+    const int cnt = w.tcount[k & 1];
+    if (blockIdx.x == 0 && threadIdx.x == 0) w.tcount[(k + 1) & 1] = 0;  // rebuilt by k_bn of body k
+    if ((int)blockIdx.y >= cnt) return;  // active tiles are compacted to the front of the list
+    const int t = w.tlist[(size_t)(k & 1) * w.T + blockIdx.y];
+    if (EARLY) {
+        if (threadIdx.x < 4) s_u[threadIdx.x] = 0;
+        __syncthreads();
+    }
+    const int m = g.m, n = g.n;
+    const float *__restrict__ Sl = w.s + (size_t)t * n * TILE + 4 * lane;
+    uint32_t *__restrict__ SGl = w.sgn + (size_t)t * m * 32 + lane;  // wr == 1
+    float *__restrict__ M0l = w.min0 + (size_t)t * m * TILE + 4 * lane;
+    float *__restrict__ M1l = w.min1 + (size_t)t * m * TILE + 4 * lane;
+    LocT *__restrict__ LCl = reinterpret_cast<LocT *>(w.loc) + (size_t)t * m * TILE + 4 * lane;
+    const int i0 = blockIdx.x * rows_per_cta + warp, i1 = min(m, blockIdx.x * rows_per_cta + rows_per_cta);
+    const int nr = i0 < i1 ? (i1 - i0 + 7) / 8 : 0;  // rows of this warp (<= 32)
+    if (nr == 0) return;
+    int ra = 0, rb = 0;  // lane q: row_ptr of the warp's row q
+    if (lane < nr) {
+        ra = __ldg(g.row_ptr + i0 + 8 * lane);
+        rb = __ldg(g.row_ptr + i0 + 8 * lane + 1);
+    }
+    auto row_of = [&](int q) { return i0 + 8 * min(q, nr - 1); };
+    auto deg_of = [&](int q) { return __shfl_sync(FULL, rb, q & 31) - __shfl_sync(FULL, ra, q & 31); };
+    auto cols_of = [&](int q) {  // lane p: column of edge p of row q (0 past the degree / past the rows)
+        const int a = __shfl_sync(FULL, ra, q & 31), d = __shfl_sync(FULL, rb, q & 31) - a;
+        return (q < nr && lane < d) ? __ldg(g.col_idx + a + lane) : 0;
+    };
+    uint32_t u[4] = {0u, 0u, 0u, 0u};
+    CnRow<CH, LocT> A, B;
+    int cjA = cols_of(0), cjB = cols_of(1);
+    cn_fetch<CH, LocT, FIRST>(A, cjA, row_of(0), Sl, SGl, M0l, M1l, LCl);
+    cjA = cols_of(2);
+    for (int q = 0; q < nr; q += 2) {
+        cn_fetch<CH, LocT, FIRST>(B, cjB, row_of(q + 1), Sl, SGl, M0l, M1l, LCl);
+        cjB = cols_of(q + 3);
+        cn_compute<CH, LocT, FIRST, EARLY>(A, row_of(q), deg_of(q), literal, SGl, M0l, M1l, LCl, u);
+        if (q + 1 >= nr) break;
+        cn_fetch<CH, LocT, FIRST>(A, cjA, row_of(q + 2), Sl, SGl, M0l, M1l, LCl);
+        cjA = cols_of(q + 4);
+        cn_compute<CH, LocT, FIRST, EARLY>(B, row_of(q + 1), deg_of(q + 1), literal, SGl, M0l, M1l, LCl, u);
     }
     if (EARLY) {
         if (lane == 0) {
-            if (u0) atomicOr(&s_u[0], u0);
-            if (u1) atomicOr(&s_u[1], u1);
-            if (u2) atomicOr(&s_u[2], u2);
-            if (u3) atomicOr(&s_u[3], u3);
+#pragma unroll
+            for (int v = 0; v < 4; v++)
+                if (u[v]) atomicOr(&s_u[v], u[v]);
         }
         __syncthreads();
         if (threadIdx.x < 4 && s_u[threadIdx.x])
@@ -444,19 +458,20 @@ __global__ void __launch_bounds__(CTA) k_cn_tma(Graph g, StreamState w, int k, i
 
 // ------------------------------------------------------------------------------------------------
 // a5/a6: bit-node sweep of loop body k; stops frames whose b^(k-1) satisfied every check.
-// Column edges in chunks of BN_U with all loads of a chunk in flight before the (ordered) sum.
+// A warp owns columns j0 + warp + 8q; lane q holds edge q of the column ({row, position}, prefetched
+// one column ahead), and the row-state gathers of BN_CHUNK edges are all in flight before the
+// (ordered) sum.
 // ------------------------------------------------------------------------------------------------
-template <typename LocT, bool EARLY, int BN_U>
-__global__ void __launch_bounds__(CTA, BN_U <= 1 ? 6 : MinBlocks<BN_U>::value)
+template <typename LocT, bool EARLY>
+__global__ void __launch_bounds__(CTA, BN_MINB)
     k_bn(Graph g, StreamState w, int k, int cols_per_cta, int literal, const int *kdev, int check_every) {
-    using L4 = typename Vec4<LocT>::type;
+    using LO = LocOps<LocT>;
     if (kdev) k = *kdev;
     (void)literal;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
     const int T = w.T;
     const int cnt = w.tcount[k & 1];
     if ((int)blockIdx.y >= cnt) return;
-    {
     const int t = w.tlist[(size_t)(k & 1) * T + blockIdx.y];
     const int cblk = blockIdx.x;
     uint4 act = make_uint4(FULL, FULL, FULL, FULL);
@@ -490,83 +505,452 @@ __global__ void __launch_bounds__(CTA, BN_U <= 1 ? 6 : MinBlocks<BN_U>::value)
     }
     const unsigned mine = ((act.x >> lane) & 1u) | (((act.y >> lane) & 1u) << 1) | (((act.z >> lane) & 1u) << 2) |
                           (((act.w >> lane) & 1u) << 3);
-    const int *__restrict__ col_ptr = g.col_ptr;
-    const int4 *__restrict__ bn_edge = g.bn_edge;
-    const float *__restrict__ M0 = w.min0;
-    const float *__restrict__ M1 = w.min1;
-    const LocT *__restrict__ LC = reinterpret_cast<const LocT *>(w.loc);
-    const uint32_t *__restrict__ SG = w.sgn;
-    const float *__restrict__ R = w.r;
-    float *__restrict__ Sv = w.s;
-    const int m = g.m, n = g.n, E = g.E;
-    const size_t tm = (size_t)t * m, tn = (size_t)t * n, tE = (size_t)t * E;
-    const int sh = 4 * (lane & 7), wsel = lane >> 3;
-    const int j0 = cblk * cols_per_cta, j1 = min(n, j0 + cols_per_cta);
-    for (int j = j0 + warp; j < j1; j += CTA / 32) {
-        const int c0 = __ldg(col_ptr + j), dv = __ldg(col_ptr + j + 1) - c0;
-        const size_t sj = (tn + j) * TILE + 4 * lane;
-        const float4 rv = ld4(R + sj);
+    const int m = g.m, n = g.n, wr = g.wr;
+    const float *__restrict__ M0l = w.min0 + (size_t)t * m * TILE + 4 * lane;
+    const float *__restrict__ M1l = w.min1 + (size_t)t * m * TILE + 4 * lane;
+    const LocT *__restrict__ LCl = reinterpret_cast<const LocT *>(w.loc) + (size_t)t * m * TILE + 4 * lane;
+    const uint32_t *__restrict__ SGl = w.sgn + (size_t)t * m * wr * 32 + lane;
+    const float *__restrict__ Rl = w.r + (size_t)t * n * TILE + 4 * lane;
+    float *__restrict__ Sl = w.s + (size_t)t * n * TILE + 4 * lane;
+    const int warp = threadIdx.x >> 5;
+    const int j0 = cblk * cols_per_cta + warp, j1 = min(n, cblk * cols_per_cta + cols_per_cta);
+    const int nc = j0 < j1 ? (j1 - j0 + 7) / 8 : 0;  // columns of this warp (<= 32)
+    int ca = 0, cb = 0;
+    if (lane < nc) {
+        ca = __ldg(g.col_ptr + j0 + 8 * lane);
+        cb = __ldg(g.col_ptr + j0 + 8 * lane + 1);
+    }
+    int c0 = __shfl_sync(FULL, ca, 0), dv = __shfl_sync(FULL, cb, 0) - c0;
+    int ei = 0, ep = 0;  // lane q: {row, position in the row} of edge q of the column
+    if (nc > 0 && lane < dv) {
+        const int4 ed = __ldg(g.bn_edge + c0 + lane);
+        ei = ed.y;
+        ep = ed.z;
+    }
+    for (int q = 0; q < nc; q++) {
+        const int j = j0 + 8 * q;
+        const int cn = __shfl_sync(FULL, ca, (q + 1) & 31), dn = __shfl_sync(FULL, cb, (q + 1) & 31) - cn;
+        const float4 rv = ld4(Rl + (size_t)j * TILE);
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
-        if (BN_U <= 1) {
-            for (int q = 0; q < dv; q++) {
-                const int4 ed = __ldg(bn_edge + c0 + q);  // {e, i, p, -}, ascending i
-                const size_t st = (tm + ed.y) * TILE + 4 * lane;
-                const float4 m0 = ld4(M0 + st);
-                const float4 m1 = ld4(M1 + st);
-                const L4 lc = *reinterpret_cast<const L4 *>(LC + st);
-                const unsigned sw = SG[(tE + ed.x) * 4 + wsel] >> sh;
-#pragma unroll
-                for (int v = 0; v < 4; v++) {
-                    const float m0v = comp(m0, v);
-                    const float mag = (ed.z == compl4(lc, v)) ? comp(m1, v) : fabsf(m0v);  // Obs. 1
-                    const unsigned neg = ((sw >> v) & 1u) ^ (__float_as_uint(m0v) >> 31);   // Obs. 2
-                    acc[v] = acc[v] + (neg ? -mag : mag);  // ascending rows from +0.0 (A14)
+        for (int q0 = 0; q0 < dv; q0 += BN_CHUNK) {
+            if (q0 > 0 && (q0 & 31) == 0) {
+                ei = ep = 0;
+                if (lane < dv - q0) {
+                    const int4 ed = __ldg(g.bn_edge + c0 + q0 + lane);
+                    ei = ed.y;
+                    ep = ed.z;
                 }
             }
-        } else {
-            for (int q0 = 0; q0 < dv; q0 += BN_U) {
-                int4 ed[BN_U];
-                float4 m0[BN_U], m1[BN_U];
-                L4 lc[BN_U];
-                unsigned sw[BN_U];
+            float4 m0[BN_CHUNK], m1[BN_CHUNK];
+            typename LO::W lc[BN_CHUNK];
+            uint32_t W[BN_CHUNK];
+            int pe[BN_CHUNK];
 #pragma unroll
-                for (int u = 0; u < BN_U; u++)
-                    if (q0 + u < dv) ed[u] = __ldg(bn_edge + c0 + q0 + u);
-#pragma unroll
-                for (int u = 0; u < BN_U; u++) {
-                    if (q0 + u < dv) {
-                        const size_t st = (tm + ed[u].y) * TILE + 4 * lane;
-                        m0[u] = ld4(M0 + st);
-                        m1[u] = ld4(M1 + st);
-                        lc[u] = *reinterpret_cast<const L4 *>(LC + st);
-                        sw[u] = SG[(tE + ed[u].x) * 4 + wsel] >> sh;
-                    }
+            for (int u = 0; u < BN_CHUNK; u++) {
+                const int i = __shfl_sync(FULL, ei, (q0 + u) & 31);
+                pe[u] = __shfl_sync(FULL, ep, (q0 + u) & 31);
+                if (q0 + u < dv) {
+                    const size_t ro = (size_t)i * TILE;
+                    m0[u] = ld4(M0l + ro);
+                    m1[u] = ld4(M1l + ro);
+                    lc[u] = LO::load(LCl + ro);
+                    W[u] = SGl[((size_t)i * wr + (pe[u] >> 3)) * 32];
                 }
+            }
 #pragma unroll
-                for (int u = 0; u < BN_U; u++) {
-                    if (q0 + u >= dv) break;
+            for (int u = 0; u < BN_CHUNK; u++) {
+                if (q0 + u < dv) {
+                    const typename LO::W key = LO::key(lc[u], pe[u]);
+                    const uint32_t ws = W[u] << (28 - 4 * (pe[u] & 7));  // bit 4(p%8)+v -> bit 28+v
 #pragma unroll
                     for (int v = 0; v < 4; v++) {
-                        const float m0v = comp(m0[u], v);
-                        const float mag = (ed[u].z == compl4(lc[u], v)) ? comp(m1[u], v) : fabsf(m0v);
-                        const unsigned neg = ((sw[u] >> v) & 1u) ^ (__float_as_uint(m0v) >> 31);
-                        acc[v] = acc[v] + (neg ? -mag : mag);
+                        const float mag = LO::hit(key, v) ? comp(m1[u], v) : comp(m0[u], v);  // Obs. 1
+                        acc[v] = acc[v] + flip31(mag, ws << (3 - v));  // ascending rows from +0.0 (A14)
                     }
                 }
             }
         }
+        // prefetch the next column's edges
+        ei = ep = 0;
+        if (q + 1 < nc && lane < dn) {
+            const int4 ed = __ldg(g.bn_edge + cn + lane);
+            ei = ed.y;
+            ep = ed.z;
+        }
         float4 out = make_float4(acc[0] + rv.x, acc[1] + rv.y, acc[2] + rv.z, acc[3] + rv.w);
+        float *sp = Sl + (size_t)j * TILE;
         if (mine == 0xFu) {
-            st4(Sv + sj, out);
+            st4(sp, out);
         } else if (mine) {
-            const float4 old = ld4(Sv + sj);
+            const float4 old = ld4(sp);
             out.x = (mine & 1u) ? out.x : old.x;
             out.y = (mine & 2u) ? out.y : old.y;
             out.z = (mine & 4u) ? out.z : old.z;
             out.w = (mine & 8u) ? out.w : old.w;
-            st4(Sv + sj, out);
+            st4(sp, out);
         }
+        c0 = cn;
+        dv = dn;
     }
+}
+
+// ------------------------------------------------------------------------------------------------
+// Software-pipelined bit-node sweep.  A warp's columns j0 + warp + 8q are cut into chunks of 3
+// edges; two chunk buffers in registers hold every load of a chunk (row state, sign word, r), and the
+// loads of the next chunk (same column or the next one) are in flight while the current one is
+// summed.  Lane q holds edge q ({row, position}) of the fetch column and the next two columns.
+// Loads are unconditional (edges past d_j read row 0), sums are over the real edges in ascending
+// row order (A14).
+// ------------------------------------------------------------------------------------------------
+constexpr int BC = 3;  // edges per chunk
+#ifndef BN_NS
+#define BN_NS 4
+#endif
+
+template <typename LocT>
+struct BnChunk {
+    float4 m0[BC], m1[BC];
+    typename LocOps<LocT>::W lc[BC];
+    uint32_t w[BC];
+    int p[BC];
+    float4 r;
+};
+
+template <typename LocT, bool EARLY>
+__global__ void __launch_bounds__(CTA, 2)
+    k_bn_pipe(Graph g, StreamState w, int k, int cols_per_cta, int literal, const int *kdev, int check_every) {
+    using LO = LocOps<LocT>;
+    if (kdev) k = *kdev;
+    (void)literal;
+    const int lane = threadIdx.x & 31;
+    const int T = w.T;
+    const int cnt = w.tcount[k & 1];
+    if ((int)blockIdx.y >= cnt) return;
+    const int t = w.tlist[(size_t)(k & 1) * T + blockIdx.y];
+    const int cblk = blockIdx.x;
+    uint4 act = make_uint4(FULL, FULL, FULL, FULL);
+    if (EARLY) {
+        // the syndrome of k_cn(k) tests b^(k-1); it may stop frames only at a check point (k-1) % T == 0
+        const bool check = ((k - 1) % check_every) == 0;
+        const uint4 ua = check ? ldu4(w.unsat + ((size_t)(k & 1) * T + t) * 4) : make_uint4(FULL, FULL, FULL, FULL);
+        const uint4 dw = ldu4(w.done + (size_t)t * 4);
+        const uint4 newly = make_uint4(~ua.x & ~dw.x, ~ua.y & ~dw.y, ~ua.z & ~dw.z, ~ua.w & ~dw.w);
+        act = make_uint4(ua.x & ~dw.x, ua.y & ~dw.y, ua.z & ~dw.z, ua.w & ~dw.w);
+        // every thread must read `done` before the tile's bookkeeping item rewrites it (other items of
+        // the tile may see either value: act is the same for both, since newly and ua are disjoint)
+        __syncthreads();
+        if (cblk == 0) {
+            const int tid = threadIdx.x;
+            if (tid < 4) {
+                w.done[(size_t)t * 4 + tid] = comp(dw, tid) | comp(newly, tid);
+                w.unsat[((size_t)((k + 1) & 1) * T + t) * 4 + tid] = 0;  // buffer of body k+1
+            }
+            if (tid < TILE && ((comp(newly, tid & 3) >> (tid >> 2)) & 1u))
+                w.iters[(size_t)t * TILE + tid] = k - 1;  // stopped after k-1 bodies
+            if (tid == 0 && (act.x | act.y | act.z | act.w)) {  // tile still runs in body k+1
+                const int pos = atomicAdd(w.tcount + ((k + 1) & 1), 1);
+                w.tlist[(size_t)((k + 1) & 1) * T + pos] = t;
+            }
+        }
+        if ((act.x | act.y | act.z | act.w) == 0) return;
+    } else if (cblk == 0 && threadIdx.x == 0) {
+        const int pos = atomicAdd(w.tcount + ((k + 1) & 1), 1);
+        w.tlist[(size_t)((k + 1) & 1) * T + pos] = t;
+    }
+    const unsigned mine = ((act.x >> lane) & 1u) | (((act.y >> lane) & 1u) << 1) | (((act.z >> lane) & 1u) << 2) |
+                          (((act.w >> lane) & 1u) << 3);
+    const int m = g.m, n = g.n, wr = g.wr;
+    const float *__restrict__ M0l = w.min0 + (size_t)t * m * TILE + 4 * lane;
+    const float *__restrict__ M1l = w.min1 + (size_t)t * m * TILE + 4 * lane;
+    const LocT *__restrict__ LCl = reinterpret_cast<const LocT *>(w.loc) + (size_t)t * m * TILE + 4 * lane;
+    const uint32_t *__restrict__ SGl = w.sgn + (size_t)t * m * wr * 32 + lane;
+    const float *__restrict__ Rl = w.r + (size_t)t * n * TILE + 4 * lane;
+    float *__restrict__ Sl = w.s + (size_t)t * n * TILE + 4 * lane;
+    const int warp = threadIdx.x >> 5;
+    const int j0 = cblk * cols_per_cta + warp, j1 = min(n, cblk * cols_per_cta + cols_per_cta);
+    const int nc = j0 < j1 ? (j1 - j0 + 7) / 8 : 0;  // columns of this warp (<= 32)
+    if (nc == 0) return;
+    int ca = 0, cb = 0;
+    if (lane < nc) {
+        ca = __ldg(g.col_ptr + j0 + 8 * lane);
+        cb = __ldg(g.col_ptr + j0 + 8 * lane + 1);
+    }
+    auto deg_of = [&](int q) { return q < nc ? __shfl_sync(FULL, cb, q & 31) - __shfl_sync(FULL, ca, q & 31) : 0; };
+    auto col_of = [&](int q) { return j0 + 8 * min(q, nc - 1); };
+    auto list_of = [&](int q, int &ei, int &ep) {  // lane e: {row, position} of edge e of column q
+        const int c0 = __shfl_sync(FULL, ca, q & 31), dv = __shfl_sync(FULL, cb, q & 31) - c0;
+        ei = 0;
+        ep = 0;
+        if (q < nc && lane < dv) {
+            const int4 ed = __ldg(g.bn_edge + c0 + lane);
+            ei = ed.y;
+            ep = ed.z;
+        }
+    };
+    auto fetch = [&](BnChunk<LocT> &B, int q, int c, int ei, int ep) {
+#pragma unroll
+        for (int u = 0; u < BC; u++) {
+            const int i = __shfl_sync(FULL, ei, (BC * c + u) & 31);
+            const int pp = __shfl_sync(FULL, ep, (BC * c + u) & 31);
+            const size_t ro = (size_t)i * TILE;
+            B.m0[u] = ld4(M0l + ro);
+            B.m1[u] = ld4(M1l + ro);
+            B.lc[u] = LO::load(LCl + ro);
+            B.w[u] = SGl[((size_t)i * wr + (pp >> 3)) * 32];
+            B.p[u] = pp;
+        }
+        B.r = ld4(Rl + (size_t)col_of(q) * TILE);
+    };
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    auto compute = [&](const BnChunk<LocT> &B, int q, int c) {
+        const int dv = deg_of(q);
+#pragma unroll
+        for (int u = 0; u < BC; u++) {
+            if (BC * c + u < dv) {
+                const typename LO::W key = LO::key(B.lc[u], B.p[u]);
+                const uint32_t ws = B.w[u] << (28 - 4 * (B.p[u] & 7));  // bit 4(p%8)+v -> bit 28+v
+#pragma unroll
+                for (int v = 0; v < 4; v++) {
+                    const float mag = LO::hit(key, v) ? comp(B.m1[u], v) : comp(B.m0[u], v);  // Obs. 1
+                    acc[v] = acc[v] + flip31(mag, ws << (3 - v));  // ascending rows from +0.0 (A14)
+                }
+            }
+        }
+        if (BC * (c + 1) >= dv) {  // last chunk of column q: s_j = sum + r_j (frozen frames keep s)
+            float4 out = make_float4(acc[0] + B.r.x, acc[1] + B.r.y, acc[2] + B.r.z, acc[3] + B.r.w);
+            float *sp = Sl + (size_t)col_of(q) * TILE;
+            if (mine == 0xFu) {
+                st4(sp, out);
+            } else if (mine) {
+                const float4 old = ld4(sp);
+                out.x = (mine & 1u) ? out.x : old.x;
+                out.y = (mine & 2u) ? out.y : old.y;
+                out.z = (mine & 4u) ? out.z : old.z;
+                out.w = (mine & 8u) ? out.w : old.w;
+                st4(sp, out);
+            }
+            acc[0] = acc[1] = acc[2] = acc[3] = 0.f;
+        }
+    };
+    // fetch cursor (fq, fc) with the edge lists of columns fq, fq+1, fq+2; compute cursor (cq, cc)
+    int e0i, e0p, e1i, e1p, e2i, e2p;
+    list_of(0, e0i, e0p);
+    list_of(1, e1i, e1p);
+    list_of(2, e2i, e2p);
+    int fq = 0, fc = 0, cq = 0, cc = 0;
+    auto advance_fetch = [&]() {
+        if (BC * (fc + 1) < deg_of(fq)) {
+            fc++;
+        } else {
+            fq++;
+            fc = 0;
+            e0i = e1i; e0p = e1p;
+            e1i = e2i; e1p = e2p;
+            list_of(fq + 2, e2i, e2p);
+        }
+    };
+    auto advance_compute = [&]() {
+        if (BC * (cc + 1) < deg_of(cq)) {
+            cc++;
+        } else {
+            cq++;
+            cc = 0;
+        }
+    };
+    BnChunk<LocT> A, B;
+    fetch(A, fq, fc, e0i, e0p);
+    advance_fetch();
+    while (true) {
+        fetch(B, fq, fc, e0i, e0p);
+        advance_fetch();
+        compute(A, cq, cc);
+        advance_compute();
+        if (cq >= nc) break;
+        fetch(A, fq, fc, e0i, e0p);
+        advance_fetch();
+        compute(B, cq, cc);
+        advance_compute();
+        if (cq >= nc) break;
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// Bit-node sweep with a per-warp cp.async ring in shared memory.  The bit node has little arithmetic
+// per edge (3 ALU ops per frame-edge), so its speed is the number of bytes in flight; registers cannot
+// hold enough of them.  Each warp owns a contiguous run of columns, i.e. a contiguous run of edges in
+// column order, and streams them through a ring of NS slots: lane l copies ITS OWN 16/16/4/4 bytes
+// of the edge's row state (min0, min1, loc, sign word) -- plus r_j with the column's last edge -- with
+// cp.async, and later reads back only those bytes, so no barrier or warp sync is needed (per-thread
+// cp.async groups).  NS - 1 edges are always in flight per warp.  Frozen frames are skipped with
+// per-component stores instead of a read-modify-write of s.
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void cp16(uint32_t dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp4(uint32_t dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp8(uint32_t dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+constexpr int BA_SLOT = 32 * (16 + 16 + 8 + 4 + 16);  // m0, m1, loc (<= 8 B), sign word, r per lane
+
+template <typename LocT>
+__device__ __forceinline__ void cp_loc(uint32_t dst, const LocT *src) {
+    if (sizeof(LocT) == 1) cp4(dst, src);
+    else cp8(dst, src);
+}
+
+template <typename LocT, bool EARLY, int NS>
+__global__ void __launch_bounds__(CTA, 1)
+    k_bn_async(Graph g, StreamState w, int k, int cols_per_cta, int literal, const int *kdev, int check_every) {
+    using LO = LocOps<LocT>;
+    extern __shared__ __align__(16) unsigned char bsm[];
+    if (kdev) k = *kdev;
+    (void)literal;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int T = w.T;
+    const int cnt = w.tcount[k & 1];
+    if ((int)blockIdx.y >= cnt) return;
+    const int t = w.tlist[(size_t)(k & 1) * T + blockIdx.y];
+    const int cblk = blockIdx.x;
+    uint4 act = make_uint4(FULL, FULL, FULL, FULL);
+    if (EARLY) {
+        // the syndrome of k_cn(k) tests b^(k-1); it may stop frames only at a check point (k-1) % T == 0
+        const bool check = ((k - 1) % check_every) == 0;
+        const uint4 ua = check ? ldu4(w.unsat + ((size_t)(k & 1) * T + t) * 4) : make_uint4(FULL, FULL, FULL, FULL);
+        const uint4 dw = ldu4(w.done + (size_t)t * 4);
+        const uint4 newly = make_uint4(~ua.x & ~dw.x, ~ua.y & ~dw.y, ~ua.z & ~dw.z, ~ua.w & ~dw.w);
+        act = make_uint4(ua.x & ~dw.x, ua.y & ~dw.y, ua.z & ~dw.z, ua.w & ~dw.w);
+        __syncthreads();
+        if (cblk == 0) {
+            const int tid = threadIdx.x;
+            if (tid < 4) {
+                w.done[(size_t)t * 4 + tid] = comp(dw, tid) | comp(newly, tid);
+                w.unsat[((size_t)((k + 1) & 1) * T + t) * 4 + tid] = 0;  // buffer of body k+1
+            }
+            if (tid < TILE && ((comp(newly, tid & 3) >> (tid >> 2)) & 1u))
+                w.iters[(size_t)t * TILE + tid] = k - 1;  // stopped after k-1 bodies
+            if (tid == 0 && (act.x | act.y | act.z | act.w)) {  // tile still runs in body k+1
+                const int pos = atomicAdd(w.tcount + ((k + 1) & 1), 1);
+                w.tlist[(size_t)((k + 1) & 1) * T + pos] = t;
+            }
+        }
+        if ((act.x | act.y | act.z | act.w) == 0) return;
+    } else if (cblk == 0 && threadIdx.x == 0) {
+        const int pos = atomicAdd(w.tcount + ((k + 1) & 1), 1);
+        w.tlist[(size_t)((k + 1) & 1) * T + pos] = t;
+    }
+    const unsigned mine = ((act.x >> lane) & 1u) | (((act.y >> lane) & 1u) << 1) | (((act.z >> lane) & 1u) << 2) |
+                          (((act.w >> lane) & 1u) << 3);
+    const int m = g.m, n = g.n, wr = g.wr;
+    const float *M0l = w.min0 + (size_t)t * m * TILE + 4 * lane;
+    const float *M1l = w.min1 + (size_t)t * m * TILE + 4 * lane;
+    const LocT *LCl = reinterpret_cast<const LocT *>(w.loc) + (size_t)t * m * TILE + 4 * lane;
+    const uint32_t *SGl = w.sgn + (size_t)t * m * wr * 32 + lane;
+    const float *Rl = w.r + (size_t)t * n * TILE + 4 * lane;
+    float *Sl = w.s + (size_t)t * n * TILE + 4 * lane;
+    // this warp's columns [ja, jb) and edges [ea, eb) (contiguous in column order)
+    const int cpw = (cols_per_cta + 7) / 8;
+    // the CTA's edge records {row, position} in shared memory (one coalesced pass)
+    int2 *rec = reinterpret_cast<int2 *>(bsm + (size_t)(CTA / 32) * NS * BA_SLOT);
+    const int cja = min(n, cblk * cols_per_cta), cjb = min(n, cblk * cols_per_cta + cols_per_cta);
+    const int cea = __ldg(g.col_ptr + cja), ceb = __ldg(g.col_ptr + cjb);
+    for (int q = threadIdx.x; q < ceb - cea; q += CTA) {
+        const int4 ed = __ldg(g.bn_edge + cea + q);
+        rec[q] = make_int2(ed.y, ed.z);
+    }
+    __syncthreads();
+    const int ja = min(n, cblk * cols_per_cta + warp * cpw), jb = min(cjb, ja + cpw);
+    if (ja >= jb) return;
+    int cpl = 0;  // lane q: col_ptr[ja + q] (q <= jb - ja <= 31)
+    if (lane <= jb - ja) cpl = __ldg(g.col_ptr + ja + lane);
+    const int ea = __shfl_sync(FULL, cpl, 0), eb = __shfl_sync(FULL, cpl, (jb - ja) & 31);
+    const int ne = eb - ea;
+    unsigned char *ring = bsm + (size_t)warp * NS * BA_SLOT;
+    const uint32_t ring_s = smem_u32(ring);
+    // producer: issue the copies of edge number te (column cursor pj / its end pe)
+    int pj = 0, pe = __shfl_sync(FULL, cpl, 1);
+    auto issue = [&](int te) {
+        if (te < ne) {
+            const int e = ea + te;
+            while (e >= pe) {  // advance the producer's column cursor (warp-uniform)
+                pj++;
+                pe = __shfl_sync(FULL, cpl, (pj + 1) & 31);
+            }
+            const int2 ed = rec[e - cea];  // {i, p}
+            const size_t ro = (size_t)ed.x * TILE;
+            const uint32_t sl = ring_s + (uint32_t)((te % NS) * BA_SLOT);
+            cp16(sl + lane * 16, M0l + ro);
+            cp16(sl + 512 + lane * 16, M1l + ro);
+            cp_loc<LocT>(sl + 1024 + lane * 8, LCl + ro);
+            cp4(sl + 1280 + lane * 4, SGl + ((size_t)ed.x * wr + (ed.y >> 3)) * 32);
+            if (e + 1 == pe) cp16(sl + 1408 + lane * 16, Rl + (size_t)(ja + pj) * TILE);  // r_j with the last edge
+        }
+        cp_commit();
+    };
+#pragma unroll 1
+    for (int te = 0; te < NS - 1; te++) issue(te);
+    const int nq = jb - ja;
+    int cj = 0;
+    while (cj < nq && __shfl_sync(FULL, cpl, (cj + 1) & 31) == __shfl_sync(FULL, cpl, cj)) cj++;  // first non-empty
+    int ce = __shfl_sync(FULL, cpl, (cj + 1) & 31);
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 1
+    for (int te = 0; te < ne; te++) {
+        cp_wait<NS - 2>();  // edge te has landed (this lane's copies)
+        const int e = ea + te;
+        const int pos = rec[e - cea].y;
+        const unsigned char *sp = ring + (te % NS) * BA_SLOT;
+        const float4 m0 = *reinterpret_cast<const float4 *>(sp + lane * 16);
+        const float4 m1 = *reinterpret_cast<const float4 *>(sp + 512 + lane * 16);
+        const typename LO::W lc = *reinterpret_cast<const typename LO::W *>(sp + 1024 + lane * 8);
+        const uint32_t wd = *reinterpret_cast<const uint32_t *>(sp + 1280 + lane * 4);
+        const typename LO::W key = LO::key(lc, pos);
+        const uint32_t ws = wd << (28 - 4 * (pos & 7));  // bit 4(p%8)+v -> bit 28+v
+#pragma unroll
+        for (int v = 0; v < 4; v++) {
+            const float mag = LO::hit(key, v) ? comp(m1, v) : comp(m0, v);  // Obs. 1
+            acc[v] = acc[v] + flip31(mag, ws << (3 - v));                   // ascending rows from +0.0 (A14)
+        }
+        if (e + 1 == ce) {  // last edge of column ja + cj: s_j = sum + r_j
+            const float4 rv = *reinterpret_cast<const float4 *>(sp + 1408 + lane * 16);
+            float *o = Sl + (size_t)(ja + cj) * TILE;
+            if (mine == 0xFu) {
+                st4(o, make_float4(acc[0] + rv.x, acc[1] + rv.y, acc[2] + rv.z, acc[3] + rv.w));
+            } else if (mine) {  // frozen frames keep their s
+                if (mine & 1u) o[0] = acc[0] + rv.x;
+                if (mine & 2u) o[1] = acc[1] + rv.y;
+                if (mine & 4u) o[2] = acc[2] + rv.z;
+                if (mine & 8u) o[3] = acc[3] + rv.w;
+            }
+            acc[0] = acc[1] = acc[2] = acc[3] = 0.f;
+            do {  // next column with an edge (columns of degree 0 are written below)
+                cj++;
+                ce = __shfl_sync(FULL, cpl, (cj + 1) & 31);
+            } while (cj < nq && ce == e + 1);
+        }
+        issue(te + NS - 1);  // refills the slot just read (its values are consumed above)
+    }
+    cp_wait<0>();
+    // columns of degree 0 (no edge): s_j = r_j
+    for (int q = 0; q < jb - ja; q++) {
+        const int c0 = __shfl_sync(FULL, cpl, q), c1 = __shfl_sync(FULL, cpl, (q + 1) & 31);
+        if (c0 == c1) {
+            const float4 rv = ld4(Rl + (size_t)(ja + q) * TILE);
+            float *o = Sl + (size_t)(ja + q) * TILE;
+            if (mine & 1u) o[0] = 0.f + rv.x;
+            if (mine & 2u) o[1] = 0.f + rv.y;
+            if (mine & 4u) o[2] = 0.f + rv.z;
+            if (mine & 8u) o[3] = 0.f + rv.w;
+        }
     }
 }
 
@@ -725,44 +1109,32 @@ int launch_stage_in(const Graph &g, const StreamState &w, const float *llr, int6
 template <typename LT, bool F, bool EA>
 void cn_launch(dim3 grid, cudaStream_t st, const Graph &g, const StreamState &w, int k, int rpc, int lit, int u,
                const int *kdev) {
-    if (u >= 4) k_cn<LT, F, EA, 4><<<grid, CTA, 0, st>>>(g, w, k, rpc, lit, kdev);
-    else if (u == 2) k_cn<LT, F, EA, 2><<<grid, CTA, 0, st>>>(g, w, k, rpc, lit, kdev);
-    else k_cn<LT, F, EA, 1><<<grid, CTA, 0, st>>>(g, w, k, rpc, lit, kdev);
+    // u: 0 = automatic (pipelined kernel when every row has degree <= 8), 1 = generic kernel
+    if (u != 1 && g.dmax <= 4) k_cn_pipe<4, LT, F, EA><<<grid, CTA, 0, st>>>(g, w, k, rpc, lit, kdev);
+    else if (u != 1 && g.dmax <= 6) k_cn_pipe<6, LT, F, EA><<<grid, CTA, 0, st>>>(g, w, k, rpc, lit, kdev);
+    else if (u != 1 && g.dmax <= 8) k_cn_pipe<8, LT, F, EA><<<grid, CTA, 0, st>>>(g, w, k, rpc, lit, kdev);
+    else k_cn<LT, F, EA><<<grid, CTA, 0, st>>>(g, w, k, rpc, lit, kdev);
 }
 
 template <typename LT, bool EA>
 void bn_launch(dim3 grid, cudaStream_t st, const Graph &g, const StreamState &w, int k, int cpc, int lit, int u,
                const int *kdev, int te) {
-    if (u >= 2) k_bn<LT, EA, 2><<<grid, CTA, 0, st>>>(g, w, k, cpc, lit, kdev, te);
-    else k_bn<LT, EA, 1><<<grid, CTA, 0, st>>>(g, w, k, cpc, lit, kdev, te);
-}
-
-template <typename LT, bool F, bool EA>
-void cn_tma_launch(const Graph &g, const StreamState &w, int k, int dm, int lit, const int *kdev, cudaStream_t st) {
-    const int rpc = (CTA / 32) * ROWS_PER_WARP;
-    const dim3 grid = grid2((g.m + rpc - 1) / rpc, w.T);
-    const size_t smem = (size_t)(CTA / 32) * 2 * cn_stage_bytes(dm, (int)sizeof(LT));
-    cudaFuncSetAttribute(k_cn_tma<LT, F, EA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_cn_tma<LT, F, EA><<<grid, CTA, smem, st>>>(g, w, k, dm, lit, kdev);
+    // u: 0 = automatic (pipelined kernel; column degrees <= 32), 1 = generic kernel
+    if (u == 0) {  // cp.async ring (default): 248 columns per CTA, 31 per warp
+        constexpr int NS = BN_NS;
+        const size_t smem = (size_t)(CTA / 32) * NS * BA_SLOT + (size_t)248 * g.dvmax * 8;
+        cudaFuncSetAttribute(k_bn_async<LT, EA, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const dim3 gr = grid2((g.n + 247) / 248, w.T);
+        k_bn_async<LT, EA, NS><<<gr, CTA, smem, st>>>(g, w, k, 248, lit, kdev, te);
+    } else if (u == 2 && g.dvmax <= 32) {
+        k_bn_pipe<LT, EA><<<grid, CTA, 0, st>>>(g, w, k, cpc, lit, kdev, te);
+    } else {
+        k_bn<LT, EA><<<grid, CTA, 0, st>>>(g, w, k, cpc, lit, kdev, te);
+    }
 }
 
 int launch_check_node(const Graph &g, const StreamState &w, int k, bool first, bool early, bool literal, bool loc16,
                       const StreamLaunch &cfg, cudaStream_t st, const int *kdev) {
-    if (cfg.cn_tma_dm > 0) {  // bulk-copy staged variant
-        const int dm = cfg.cn_tma_dm, lit = literal ? 1 : 0;
-        if (loc16) {
-            if (first) { if (early) cn_tma_launch<uint16_t, true, true>(g, w, k, dm, lit, kdev, st);
-                         else cn_tma_launch<uint16_t, true, false>(g, w, k, dm, lit, kdev, st); }
-            else { if (early) cn_tma_launch<uint16_t, false, true>(g, w, k, dm, lit, kdev, st);
-                   else cn_tma_launch<uint16_t, false, false>(g, w, k, dm, lit, kdev, st); }
-        } else {
-            if (first) { if (early) cn_tma_launch<uint8_t, true, true>(g, w, k, dm, lit, kdev, st);
-                         else cn_tma_launch<uint8_t, true, false>(g, w, k, dm, lit, kdev, st); }
-            else { if (early) cn_tma_launch<uint8_t, false, true>(g, w, k, dm, lit, kdev, st);
-                   else cn_tma_launch<uint8_t, false, false>(g, w, k, dm, lit, kdev, st); }
-        }
-        return 1;
-    }
     const dim3 grid = grid2((g.m + cfg.rows_per_cta - 1) / cfg.rows_per_cta, w.T);
     const int lit = literal ? 1 : 0, rpc = cfg.rows_per_cta, u = cfg.cn_unroll;
     if (loc16) {

@@ -23,14 +23,18 @@ struct Graph {
     const int *col_idx;  // [E]     ascending within a row
     const int *col_ptr;  // [n+1]   M_j = bn_edge[col_ptr[j] .. col_ptr[j+1])
     const int4 *bn_edge; // [E]     {edge id e (row-list position), row i, position p in N_i, d_i & 1}
+    int wr;              // sign words per row and lane in the streaming layout: ceil(max row degree / 8)
+    int dmax;            // max row degree
+    int dvmax;           // max column degree
 };
 
 // Per-chunk decode state of the streaming schedule, frame-interleaved in tiles of 128:
 //   r, s   [T][n][128] fp32          channel values and current soft vector (Eq. sCalculation)
 //   min0   [T][m][128] fp32          |lambda| minimum of the row; SIGN BIT = row sign parity (Obs. 2)
-//   min1   [T][m][128] fp32          second minimum (Obs. 1)
+//   min1   [T][m][128] fp32          second minimum (Obs. 1); same sign bit as min0
 //   loc    [T][m][128] u8 / u16      min0Location as the position inside N_i
-//   sgn    [T][E][4]   u32           sign bit of lambda_e per frame (bit `lane` of word v = frame 4*lane+v)
+//   sgn    [T][m][wr][32] u32        sign bits of lambda_e, row-transposed: word (i, p/8, lane l) holds bit
+//                                    4*(p%8) + v = sign for edge p of row i, frame 4l+v (one coalesced word per lane)
 //   unsat  [2][T][4]   u32           per-frame "some check unsatisfied" bits (double-buffered by iteration)
 //   done   [T][4]      u32           per-frame "stopped" bits
 //   iters  [T*128]     i32           k at which a frame stopped (early stop)
@@ -56,18 +60,17 @@ struct HostGraph {  // device allocations owned by the plan
     int *row_ptr = nullptr, *col_idx = nullptr, *col_ptr = nullptr, *col_edge = nullptr;
     int4 *bn_edge = nullptr;
     int64_t launches = 0;
-    Graph view() const { return Graph{m, n, E, row_ptr, col_idx, col_ptr, bn_edge}; }
+    Graph view() const { return Graph{m, n, E, row_ptr, col_idx, col_ptr, bn_edge, (max_row_deg + 7) / 8, max_row_deg, max_col_deg}; }
     void free_all();
 };
 
 // ---- streaming schedule (decode_stream.cu) ----
 struct StreamLaunch {
-    int rows_per_cta = 32;
-    int cols_per_cta = 32;
-    int cn_unroll = 1;  // check-node edges per load batch (1, 2, 4)
-    int bn_unroll = 1;  // bit-node edges per load batch (1, 2)
+    int rows_per_cta = 64;  // <= 256 (a warp owns <= 32 rows)
+    int cols_per_cta = 64;  // <= 256
+    int cn_unroll = 0;  // check-node kernel: 0 = automatic (pipelined when max row degree <= 8), 1 = generic
+    int bn_unroll = 0;  // bit-node kernel: 0 = automatic, 1 = generic
     int check_every = 1;  // codeword test after body k when k % T == 0 (and after body L)
-    int cn_tma_dm = 0;   // > 0: bulk-copy staged check node for rows of degree <= this
     int cn_ctas = 4736;  // grid caps of the (tile x block) work loops: a few waves of resident CTAs
     int bn_ctas = 7104;
 };

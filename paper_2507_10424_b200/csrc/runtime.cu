@@ -98,12 +98,12 @@ void launch(ldpc_plan *h, int cls, cudaStream_t st, F &&fn) {
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 size_t tile_bytes(const HostGraph &g, bool loc16) {
-    const size_t m = g.m, n = g.n, E = g.E;
+    const size_t m = g.m, n = g.n;
     size_t b = 0;
     b += 2 * align256(n * TILE * 4);                 // r, s
     b += 2 * align256(m * TILE * 4);                 // min0, min1
     b += align256(m * TILE * (loc16 ? 2 : 1));       // loc
-    b += align256(E * 16);                           // sgn
+    b += align256(m * (size_t)((g.max_row_deg + 7) / 8) * 128);  // sgn
     b += 3 * 256;                                    // unsat x2, done
     b += 4 * align256(TILE * 4);                     // iters, fbe, fraw, fnz
     b += 3 * 4 + 256;                                // tcount, tlist
@@ -112,7 +112,7 @@ size_t tile_bytes(const HostGraph &g, bool loc16) {
 
 // carve the workspace into per-array regions of T tiles each
 StreamState carve(void *base, int T, const HostGraph &g, bool loc16) {
-    const size_t m = g.m, n = g.n, E = g.E;
+    const size_t m = g.m, n = g.n;
     char *p = static_cast<char *>(base);
     auto take = [&](size_t bytes) {
         char *q = p;
@@ -126,7 +126,7 @@ StreamState carve(void *base, int T, const HostGraph &g, bool loc16) {
     w.min0 = reinterpret_cast<float *>(take((size_t)T * m * TILE * 4));
     w.min1 = reinterpret_cast<float *>(take((size_t)T * m * TILE * 4));
     w.loc = take((size_t)T * m * TILE * (loc16 ? 2 : 1));
-    w.sgn = reinterpret_cast<uint32_t *>(take((size_t)T * E * 16));
+    w.sgn = reinterpret_cast<uint32_t *>(take((size_t)T * m * ((g.max_row_deg + 7) / 8) * 128));
     w.unsat = reinterpret_cast<uint32_t *>(take((size_t)2 * T * 16));
     w.done = reinterpret_cast<uint32_t *>(take((size_t)T * 16));
     w.iters = reinterpret_cast<int *>(take((size_t)T * TILE * 4));
@@ -151,9 +151,9 @@ int ensure_ws(ldpc_plan *h, int T, bool loc16) {
     // size for the full per-array layout of T tiles
     size_t need = 0;
     {
-        const size_t m = h->g.m, n = h->g.n, E = h->g.E;
+        const size_t m = h->g.m, n = h->g.n;
         need = 2 * align256((size_t)T * n * TILE * 4) + 2 * align256((size_t)T * m * TILE * 4) +
-               align256((size_t)T * m * TILE * (loc16 ? 2 : 1)) + align256((size_t)T * E * 16) +
+               align256((size_t)T * m * TILE * (loc16 ? 2 : 1)) + align256((size_t)T * m * ((h->g.max_row_deg + 7) / 8) * 128) +
                align256((size_t)2 * T * 16) + align256((size_t)T * 16) + 4 * align256((size_t)T * TILE * 4) +
                align256(8) + align256((size_t)2 * T * 4) + align256(4);
     }
@@ -371,22 +371,17 @@ int finish_prepare(ldpc_plan *p, int rc, uint32_t flags, ldpc_handle_t *out) {
     p->launches = p->g.launches;
     cudaGetDevice(&p->device);
     p->rp = plan_resident(p->g, p->g.max_row_deg > 255, p->device);
-    if (const char *s = getenv("LDPC_ROWS_PER_CTA")) p->cfg.rows_per_cta = std::max(8, atoi(s));
-    if (const char *s = getenv("LDPC_COLS_PER_CTA")) p->cfg.cols_per_cta = std::max(8, atoi(s));
+    if (const char *s = getenv("LDPC_ROWS_PER_CTA")) p->cfg.rows_per_cta = std::min(256, std::max(8, atoi(s)));
+    if (const char *s = getenv("LDPC_COLS_PER_CTA")) p->cfg.cols_per_cta = std::min(256, std::max(8, atoi(s)));
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
     p->cfg.cn_ctas = sms * 4 * 2;  // 4 resident CTAs per SM (64-register kernel), two waves
     p->cfg.bn_ctas = sms * 6 * 2;
     if (const char *s = getenv("LDPC_CN_CTAS")) p->cfg.cn_ctas = std::max(1, atoi(s));
     if (const char *s = getenv("LDPC_BN_CTAS")) p->cfg.bn_ctas = std::max(1, atoi(s));
-    if (const char *s = getenv("LDPC_CN_UNROLL")) p->cfg.cn_unroll = std::max(1, atoi(s));
+    if (const char *s = getenv("LDPC_CN_UNROLL")) p->cfg.cn_unroll = std::max(0, atoi(s));
     if (const char *s = getenv("LDPC_NO_GRAPHS")) p->use_graphs = atoi(s) == 0;
-    // bulk-copy (cp.async.bulk + mbarrier) staged check node: opt-in (LDPC_CN_TMA=1).  Measured on
-    // B200 it is not faster than the register path (C4 915 vs 927 us, C3 2.78 vs 2.39 ms per sweep).
-    if (const char *s = getenv("LDPC_CN_TMA")) {
-        if (atoi(s) != 0 && p->g.max_row_deg <= 32) p->cfg.cn_tma_dm = p->g.max_row_deg;
-    }
-    if (const char *s = getenv("LDPC_BN_UNROLL")) p->cfg.bn_unroll = std::max(1, atoi(s));
+    if (const char *s = getenv("LDPC_BN_UNROLL")) p->cfg.bn_unroll = std::max(0, atoi(s));
     *out = p;
     return LDPC_OK;
 }

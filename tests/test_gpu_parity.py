@@ -58,6 +58,9 @@ def compare(code, llr, L, flags=0, h=None, exact=True, check_every=1):
     assert np.allclose(gp, op, rtol=TOL, atol=TOL)
     if exact:
         assert np.array_equal(gp.view(np.uint32), op.view(np.uint32)), "posterior not bit-exact"
+    else:  # bit-exact up to the sign of zero (the decoders keep s canonical, reading A12)
+        z = np.float32(0.0)
+        assert np.array_equal((gp + z).view(np.uint32), (op + z).view(np.uint32)), "posterior differs"
     assert np.array_equal(gs, oracle.stats(llr, ob, oi, oc, op))
     return gb, gi, gc, gp
 
@@ -204,18 +207,36 @@ def test_graph_loop_equals_plain_launches(cfg_name, frames):
             assert np.array_equal(a, b)
 
 
-def test_bulk_copy_check_node_variant(monkeypatch):
-    """The opt-in cp.async.bulk/mbarrier-staged check node (LDPC_CN_TMA=1) is bit-identical."""
-    monkeypatch.setenv("LDPC_CN_TMA", "1")
+@pytest.mark.parametrize("cu,bu", [(1, 1), (2, 2), (4, 3), (2, 3)])
+def test_stream_unroll_variants(monkeypatch, cu, bu):
+    """Every load-batching variant of the streaming check-node / bit-node sweeps is bit-identical
+    (LDPC_CN_UNROLL edges per check-node batch, LDPC_BN_UNROLL per bit-node batch)."""
+    monkeypatch.setenv("LDPC_CN_UNROLL", str(cu))
+    monkeypatch.setenv("LDPC_BN_UNROLL", str(bu))
     cfg = codes.CONFIGS["c2"]
     code = cfg["code"]()
     parts = [channel.bpsk_awgn(code.n, code.rate, e, cfg["seed"], p, 100, 300).numpy() for p, e in enumerate(cfg["ebn0"])]
     llr = np.concatenate(parts)
     for flags in (FORCE_STREAM, FORCE_STREAM | 16, FORCE_STREAM | NOES | LIT):
         compare(code, llr, cfg["max_iter"], flags, h=handle(code, flags))
-    code3 = codes.random_small(37, 70, 2, 2, 9)
+    code3 = codes.random_small(37, 70, 2, 2, 9)  # irregular, rows of degree 2..
     llr3 = (np.random.default_rng(3).standard_normal((300, code3.n)) - 0.5).astype(np.float32)
     compare(code3, llr3, 12, h=handle(code3, FORCE_STREAM))
+
+
+@pytest.mark.parametrize("flags", [FORCE_STREAM, FORCE_RESIDENT, FORCE_STREAM | LIT])
+def test_signed_zeros_and_ties(flags):
+    """Channel values with many exact +0 / -0 entries and exact magnitude ties (reading A12: sign(-0) =
+    sign(+0) = +1, slice(+-0) = 0; A13: ties).  The decoders keep s canonical (+0), so the posterior is
+    compared numerically for zeros (the sign of a zero posterior is not a decision)."""
+    code = codes.regular(504, 1008, 3, 6, 1008)
+    rng = np.random.default_rng(12)
+    y = np.round(rng.normal(-0.6, 1.0, size=(700, code.n)) * 2.0) / 2.0  # half-integer grid: ties, zeros
+    y = y.astype(np.float32)
+    zero = y == 0
+    y[zero & (rng.random(y.shape) < 0.5)] = np.float32(-0.0)
+    y[:50] = np.where(rng.random((50, code.n)) < 0.3, np.float32(-0.0), y[:50])
+    compare(code, y, 20, flags, h=handle(code, flags), exact=False)
 
 
 def test_nonzero_codewords_and_symmetry():
