@@ -4,12 +4,16 @@
 //
 // Per CTA, frame-interleaved over S slots (a lane owns 4 consecutive slots of one row or column):
 //   s    [n][S]  fp32          soft vector (Eq. sCalculation)
-//   min0 [m][S]  fp32          Observation 1's minimum
-//   min1 [m][S]  fp32          Observation 1's second minimum
+//   min0 [m][S]  fp32          Observation 1's minimum; SIGN BIT = the row's sign parity
+//                              (Obs. 2) x (-1)^{d_i} (reading A1)
+//   min1 [m][S]  fp32          Observation 1's second minimum, same sign bit
 //   lc   [m][S]  u8            min0Location as the position p inside row i's list (0xff = none)
 //   sgb  [m/G][dmax] 4 x u32   sign of lambda_e = s_j - eta_e, kept as the warp ballots of the check
 //                              node (bit (i % G) * LR + l of component v = row i, slot 4l + v)
-//   parb [m/G]   4 x u32       the rows' sign parity (Obs. 2) x (-1)^{d_i} (reading A1), same bits
+// eta_e = (loc == p ? min1 : min0) with its sign bit XORed with the ballot bit: one FSEL and one LOP3
+// per slot-edge (the ballot bit is moved to bit 31 by an integer multiply, on the FMA pipe).
+// Zeros of s are kept as -0.0 (same slice and sign() under reading A12), so the decision of a slot is
+// the complement of the IEEE sign bit of s and the syndrome is a XOR of sign bits.
 // plus the Tanner graph itself as 16-bit lists (N_i, M_j).  r lives in a global scratch
 // [CTA][n][S] (L2-resident) read once per column per body.  Loop per round:
 //   A  finish stopped slots (k, isCodeword, counters) and refill empty slots from a global counter
@@ -33,8 +37,8 @@ constexpr unsigned FULLM = 0xffffffffu;
 
 
 struct Layout {
-    size_t s, m0, m1, lc, sgb, parb, rp, cp, col, rec, rec2, meta, total;
-    size_t sgb_half, parb_half;  // words per buffer (sign words are double-buffered by loop pass)
+    size_t s, m0, m1, lc, sgb, rp, cp, col, rec, rec2, meta, total;
+    size_t sgb_half;  // words per buffer (sign words are double-buffered by loop pass)
 };
 
 constexpr size_t a16(size_t x) { return (x + 15) & ~(size_t)15; }
@@ -55,14 +59,12 @@ Layout layout_for(int S, int m, int n, int E, int dm) {
     L.m1 = o;   o = a16(o + (size_t)m * S * 4);
     L.lc = o;   o = a16(o + (size_t)m * S);
     L.sgb_half = nrg * dm;
-    L.parb_half = nrg;
     L.sgb = o;  o = a16(o + 2 * nrg * dm * 16);
-    L.parb = o; o = a16(o + 2 * nrg * 16);
     L.rp = o;   o = a16(o + (size_t)(m + 1) * 2);
     L.cp = o;   o = a16(o + (size_t)(n + 1) * 2);
     L.col = o;  o = a16(o + (size_t)E * 2);
     L.rec = o;  o = a16(o + (size_t)E * 4);
-    L.rec2 = o; o = a16(o + (size_t)E * 2);
+    L.rec2 = o; o = a16(o + (size_t)E * 4);
     L.meta = o; o = a16(o + (size_t)META_INTS * 4 + 8 * 8);
     L.total = o;
     return L;
@@ -84,6 +86,7 @@ struct ResArgs {
 };
 
 __device__ __forceinline__ float f4c(const float4 &a, int v) { return v == 0 ? a.x : v == 1 ? a.y : v == 2 ? a.z : a.w; }
+__device__ __forceinline__ uint32_t f4c(const uint4 &a, int v) { return v == 0 ? a.x : v == 1 ? a.y : v == 2 ? a.z : a.w; }
 __device__ __forceinline__ void f4s(float4 &a, int v, float x) {
     if (v == 0) a.x = x;
     else if (v == 1) a.y = x;
@@ -93,14 +96,18 @@ __device__ __forceinline__ void f4s(float4 &a, int v, float x) {
 
 // Check-node update of G rows (one per row group of the warp) for the 4 slots of this lane.
 // HAS: rows of the warp may have different degrees (irregular H), lanes past their degree idle.
-// fm: this lane's fresh slots (eta^prev = 0).  sgi/pai: the ballot words of this row block from
-// the previous body, sgo/pao: where this body's go (the other buffer, so no lane waits for the others).
+// fm: this lane's fresh slots (eta^prev = 0: their stored min0 = min1 = +0, so eta^prev = +-0 and
+// lambda = s - (+-0) has the magnitude and sign() of s, s being -0 rather than +0 for zero).
+// sgi: the ballot words of this row block from the previous body, sgo: where this body's go.
+__device__ __forceinline__ float flip31(float mag, uint32_t bit31) {
+    return __uint_as_float(__float_as_uint(mag) ^ (bit31 & 0x80000000u));
+}
+
 template <int S, bool HAS>
 __device__ __forceinline__ void cn_rows(const float *__restrict__ s, float *mn0, float *mn1, uint8_t *lc,
-                                        const uint4 *__restrict__ sgi, const uint4 *__restrict__ pai,
-                                        uint4 *__restrict__ sgo, uint4 *__restrict__ pao,
-                                        const uint16_t *col, int i, bool valid, int ra, int d, int dmax, int l,
-                                        int lane, unsigned fm, uint32_t fmb, bool corr, unsigned &syn_acc) {
+                                        const uint4 *__restrict__ sgi, uint4 *__restrict__ sgo, const uint16_t *col,
+                                        int i, bool valid, int ra, int d, int dmax, int l, int lane, unsigned fm,
+                                        uint32_t fmb, bool corr, unsigned &syn_acc) {
     const float INF = __int_as_float(0x7f800000);
     const int q0 = 4 * l;
     float4 om0 = make_float4(0.f, 0.f, 0.f, 0.f), om1 = om0;
@@ -117,15 +124,11 @@ __device__ __forceinline__ void cn_rows(const float *__restrict__ s, float *mn0,
             if (fm & 8u) { om0.w = 0.f; om1.w = 0.f; }
         }
     }
-    const uint4 P = *pai;  // row sign parities x (-1)^{d_i} of the previous body, one bit per lane
-    const unsigned lm = 1u << lane;
-    unsigned mk[4];  // this lane's bit, cleared for fresh slots (their eta^prev is +0)
-#pragma unroll
-    for (int v = 0; v < 4; v++) mk[v] = ((fm >> v) & 1u) ? 0u : lm;
+    const uint32_t mul = 1u << (31 - lane);  // moves this lane's ballot bit to bit 31
     float nm0[4] = {INF, INF, INF, INF}, nm1[4] = {INF, INF, INF, INF};
     int nloc[4] = {0xff, 0xff, 0xff, 0xff};
     unsigned parw[4] = {0, 0, 0, 0};
-    unsigned syn = 0;
+    uint32_t synw[4] = {0u, 0u, 0u, 0u};  // XOR of the sign bits of s over the row: bit 31 = XOR of (1 - b_j)
 #pragma unroll 2
     for (int p = 0; p < dmax; p++) {
         const bool has = HAS ? (p < d) : true;
@@ -136,36 +139,43 @@ __device__ __forceinline__ void cn_rows(const float *__restrict__ s, float *mn0,
         const uint4 W = sgi[p];  // own sign of lambda^prev per component (Obs. 2)
         const float mg[4] = {((olc ^ pp) & 0xffu) ? om0.x : om1.x, ((olc ^ pp) & 0xff00u) ? om0.y : om1.y,
                              ((olc ^ pp) & 0xff0000u) ? om0.z : om1.z,
-                             ((olc ^ pp) & 0xff000000u) ? om0.w : om1.w};  // Obs. 1
-        const bool ng[4] = {((W.x ^ P.x) & mk[0]) != 0u, ((W.y ^ P.y) & mk[1]) != 0u, ((W.z ^ P.z) & mk[2]) != 0u,
-                            ((W.w ^ P.w) & mk[3]) != 0u};
+                             ((olc ^ pp) & 0xff000000u) ? om0.w : om1.w};  // Obs. 1 (+ row parity)
         unsigned bal[4];
 #pragma unroll
         for (int v = 0; v < 4; v++) {
             const float sj = f4c(sv, v);
-            const float x = sj - (ng[v] ? -mg[v] : mg[v]);  // lambda - eta^prev
+            const float x = sj - flip31(mg[v], f4c(W, v) * mul);  // lambda - eta^prev
             const float ax = HAS ? (has ? fabsf(x) : INF) : fabsf(x);
             const bool lt = ax < nm0[v];  // first strict minimum (A13)
             nm1[v] = fminf(nm1[v], fmaxf(nm0[v], ax));
             nm0[v] = fminf(nm0[v], ax);
             nloc[v] = lt ? p : nloc[v];
             bal[v] = __ballot_sync(FULLM, (HAS ? has : true) && x < 0.f);  // sign(0) = +1
-            syn ^= (unsigned)((HAS ? has : true) && sj > 0.f) << v;        // b_j = slice(s_j)
+            synw[v] ^= (HAS ? has : true) ? __float_as_uint(sj) : 0u;      // slice(s_j) = 0 iff sign bit
         }
 #pragma unroll
         for (int v = 0; v < 4; v++) parw[v] ^= bal[v];
         if (lane == 0) sgo[p] = make_uint4(bal[0], bal[1], bal[2], bal[3]);
     }
-    // row parity words of this block; rows of odd degree flip under the CORRECTED rule (reading A1)
-    const unsigned flip = __ballot_sync(FULLM, valid && corr && (d & 1));
     if (valid) {
-        *reinterpret_cast<float4 *>(mn0 + ca) = make_float4(nm0[0], nm0[1], nm0[2], nm0[3]);
-        *reinterpret_cast<float4 *>(mn1 + ca) = make_float4(nm1[0], nm1[1], nm1[2], nm1[3]);
+        // this lane's row sign parity per slot, times (-1)^{d_i} under the CORRECTED rule (reading A1)
+        const uint32_t c = (corr && (d & 1)) ? 1u : 0u;
+        uint32_t sb[4];
+#pragma unroll
+        for (int v = 0; v < 4; v++) sb[v] = (((parw[v] >> lane) & 1u) ^ c) << 31;
+        *reinterpret_cast<float4 *>(mn0 + ca) =
+            make_float4(__uint_as_float(__float_as_uint(nm0[0]) | sb[0]), __uint_as_float(__float_as_uint(nm0[1]) | sb[1]),
+                        __uint_as_float(__float_as_uint(nm0[2]) | sb[2]), __uint_as_float(__float_as_uint(nm0[3]) | sb[3]));
+        *reinterpret_cast<float4 *>(mn1 + ca) =
+            make_float4(__uint_as_float(__float_as_uint(nm1[0]) | sb[0]), __uint_as_float(__float_as_uint(nm1[1]) | sb[1]),
+                        __uint_as_float(__float_as_uint(nm1[2]) | sb[2]), __uint_as_float(__float_as_uint(nm1[3]) | sb[3]));
         *reinterpret_cast<uint32_t *>(lc + ca) =
             (uint32_t)nloc[0] | ((uint32_t)nloc[1] << 8) | ((uint32_t)nloc[2] << 16) | ((uint32_t)nloc[3] << 24);
-        syn_acc |= syn;
+        // row unsatisfied iff XOR_j b_j = 1, with XOR_j b_j = d_i mod 2 xor XOR_j (1 - b_j)
+        const uint32_t dp = (uint32_t)(d & 1);
+        syn_acc |= (((synw[0] >> 31) ^ dp) | (((synw[1] >> 31) ^ dp) << 1) | (((synw[2] >> 31) ^ dp) << 2) |
+                    (((synw[3] >> 31) ^ dp) << 3));
     }
-    if (lane == 0) *pao = make_uint4(parw[0] ^ flip, parw[1] ^ flip, parw[2] ^ flip, parw[3] ^ flip);
 }
 
 // Lane layout: a lane owns 4 consecutive slots (float4) of one row or column; LR = S/4 lanes cover a
@@ -182,12 +192,11 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
     float *mn1 = reinterpret_cast<float *>(sm + a.lay.m1);
     uint8_t *lc = reinterpret_cast<uint8_t *>(sm + a.lay.lc);
     uint4 *sgb = reinterpret_cast<uint4 *>(sm + a.lay.sgb);
-    uint4 *parb = reinterpret_cast<uint4 *>(sm + a.lay.parb);
     uint16_t *rp = reinterpret_cast<uint16_t *>(sm + a.lay.rp);
     uint16_t *cp = reinterpret_cast<uint16_t *>(sm + a.lay.cp);
     uint16_t *col = reinterpret_cast<uint16_t *>(sm + a.lay.col);
     uint32_t *rec = reinterpret_cast<uint32_t *>(sm + a.lay.rec);
-    uint16_t *rec2 = reinterpret_cast<uint16_t *>(sm + a.lay.rec2);
+    uint32_t *rec2 = reinterpret_cast<uint32_t *>(sm + a.lay.rec2);
     int *meta = reinterpret_cast<int *>(sm + a.lay.meta);
     int *slot_f = meta;            // frame index of the slot, -1 = empty
     int *slot_k = meta + 32;       // completed loop bodies
@@ -210,7 +219,8 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
         col[e] = (uint16_t)__ldg(a.g.col_idx + e);
         const int4 be = __ldg(a.g.bn_edge + e);  // {edge id, row, pos, parity}
         rec[e] = ((uint32_t)be.z << 16) | (uint32_t)be.y;  // {pos p in row i, row i}
-        rec2[e] = (uint16_t)((be.y / G) * dm + be.z);  // ballot-word index of the edge
+        // ballot-word index of the edge | bit offset of row i inside the word (the lane adds l)
+        rec2[e] = (uint32_t)((be.y / G) * dm + be.z) | ((uint32_t)((be.y % G) * LR) << 16);
     }
     if (tid < 32) {
         slot_f[tid] = -1;
@@ -230,8 +240,8 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
 
     for (int pass = 0;; pass++) {
         const int cur = pass & 1;  // sign words of the previous body are in buffer cur, this body's in cur ^ 1
-        const uint4 *sgi = sgb + (cur ? a.lay.sgb_half : 0), *pai = parb + (cur ? a.lay.parb_half : 0);
-        uint4 *sgo = sgb + (cur ? 0 : a.lay.sgb_half), *pao = parb + (cur ? 0 : a.lay.parb_half);
+        const uint4 *sgi = sgb + (cur ? a.lay.sgb_half : 0);
+        uint4 *sgo = sgb + (cur ? 0 : a.lay.sgb_half);
         // ---------------- A: finish stopped slots, advance continuing ones, refill (warp 0)
         if (warp == 0) {
             const unsigned uns_all = ctl[0];
@@ -312,7 +322,7 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
                 for (int v = 0; v < 4; v++) {
                     if ((fm >> v) & 1u) {
                         const float x = __ldg(a.llr + (int64_t)fr[v] * n + j);
-                        f4s(o, v, x);
+                        f4s(o, v, x == 0.f ? -0.f : x);  // zeros of s are kept as -0 (A12)
                         rs[(size_t)j * S + q0 + v] = x;
                         raw[v] += x > 0.f;
                     }
@@ -340,11 +350,11 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
                 const int dmax = __reduce_max_sync(FULLM, d);
                 const size_t rg = (size_t)(rb / G);
                 if (__all_sync(FULLM, d == dmax))
-                    cn_rows<S, false>(s, mn0, mn1, lc, sgi + rg * dm, pai + rg, sgo + rg * dm, pao + rg, col, i,
-                                      valid, ra, d, dmax, l, lane, fm, fmb, corr, syn_acc);
+                    cn_rows<S, false>(s, mn0, mn1, lc, sgi + rg * dm, sgo + rg * dm, col, i, valid, ra, d, dmax, l,
+                                      lane, fm, fmb, corr, syn_acc);
                 else
-                    cn_rows<S, true>(s, mn0, mn1, lc, sgi + rg * dm, pai + rg, sgo + rg * dm, pao + rg, col, i,
-                                     valid, ra, d, dmax, l, lane, fm, fmb, corr, syn_acc);
+                    cn_rows<S, true>(s, mn0, mn1, lc, sgi + rg * dm, sgo + rg * dm, col, i, valid, ra, d, dmax, l,
+                                     lane, fm, fmb, corr, syn_acc);
             }
             const unsigned mine = (syn_acc << q0) & active;
             const unsigned wmask = __reduce_or_sync(FULLM, mine);
@@ -394,30 +404,34 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
                         const float4 rj = *reinterpret_cast<const float4 *>(rs + (size_t)j * S + q0);
                         const int c0 = cp[j], dv = (int)cp[j + 1] - c0;
                         float acc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 2
-                        for (int qq = 0; qq < dv; qq++) {
-                            const uint32_t rc = rec[c0 + qq];
-                            const int i = (int)(rc & 0xffffu);
-                            const uint32_t pp = (rc >> 16) * 0x01010101u;  // position of the edge in row i
-                            const int ca = i * S + q0;
-                            const float4 m0 = *reinterpret_cast<const float4 *>(mn0 + ca);
-                            const float4 m1 = *reinterpret_cast<const float4 *>(mn1 + ca);
-                            const uint32_t lv = *reinterpret_cast<const uint32_t *>(lc + ca) ^ pp;
-                            const uint4 W = sgo[rec2[c0 + qq]];
-                            const uint4 Pw = pao[i / G];
-                            const unsigned bm = 1u << ((i % G) * LR + l);  // this lane's bit of row i
-                            const float mg[4] = {(lv & 0xffu) ? m0.x : m1.x, (lv & 0xff00u) ? m0.y : m1.y,
-                                                 (lv & 0xff0000u) ? m0.z : m1.z, (lv & 0xff000000u) ? m0.w : m1.w};
-                            const bool ng[4] = {((W.x ^ Pw.x) & bm) != 0u, ((W.y ^ Pw.y) & bm) != 0u,
-                                                ((W.z ^ Pw.z) & bm) != 0u, ((W.w ^ Pw.w) & bm) != 0u};
+                        for (int q3 = 0; q3 < dv; q3 += 3) {  // chunks of 3 edges: no remainder loop for d_v = 3
 #pragma unroll
-                            for (int v = 0; v < 4; v++)
-                                acc[v] = acc[v] + (ng[v] ? -mg[v] : mg[v]);  // ascending rows from +0.0 (A14)
+                            for (int u = 0; u < 3; u++) {
+                                if (q3 + u < dv) {
+                                    const uint32_t rc = rec[c0 + q3 + u];
+                                    const uint32_t r2 = rec2[c0 + q3 + u];
+                                    const int i = (int)(rc & 0xffffu);
+                                    const uint32_t pp = (rc >> 16) * 0x01010101u;  // position of the edge in row i
+                                    const int ca = i * S + q0;
+                                    const float4 m0 = *reinterpret_cast<const float4 *>(mn0 + ca);
+                                    const float4 m1 = *reinterpret_cast<const float4 *>(mn1 + ca);
+                                    const uint32_t lv = *reinterpret_cast<const uint32_t *>(lc + ca) ^ pp;
+                                    const uint4 W = sgo[r2 & 0xffffu];
+                                    const uint32_t mul = 0x80000000u >> ((r2 >> 16) + l);  // this lane's bit of row i
+                                    const float mg[4] = {(lv & 0xffu) ? m0.x : m1.x, (lv & 0xff00u) ? m0.y : m1.y,
+                                                         (lv & 0xff0000u) ? m0.z : m1.z,
+                                                         (lv & 0xff000000u) ? m0.w : m1.w};  // Obs. 1
+#pragma unroll
+                                    for (int v = 0; v < 4; v++)  // ascending rows from +0.0 (A14)
+                                        acc[v] = acc[v] + flip31(mg[v], f4c(W, v) * mul);
+                                }
+                            }
                         }
-                        if (cm & 1u) o.x = acc[0] + rj.x;
-                        if (cm & 2u) o.y = acc[1] + rj.y;
-                        if (cm & 4u) o.z = acc[2] + rj.z;
-                        if (cm & 8u) o.w = acc[3] + rj.w;
+                        const float n0 = acc[0] + rj.x, n1 = acc[1] + rj.y, n2 = acc[2] + rj.z, n3 = acc[3] + rj.w;
+                        if (cm & 1u) o.x = n0 == 0.f ? -0.f : n0;  // zeros of s are kept as -0 (A12)
+                        if (cm & 2u) o.y = n1 == 0.f ? -0.f : n1;
+                        if (cm & 4u) o.z = n2 == 0.f ? -0.f : n2;
+                        if (cm & 8u) o.w = n3 == 0.f ? -0.f : n3;
                         *reinterpret_cast<float4 *>(sp) = o;
                     }
                 }

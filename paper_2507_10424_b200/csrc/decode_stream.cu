@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "ldpc_internal.cuh"
 
@@ -48,6 +49,39 @@ __device__ __forceinline__ int compl4(const V &a, int v) {
 __device__ __forceinline__ float4 ld4(const float *p) { return *reinterpret_cast<const float4 *>(p); }
 __device__ __forceinline__ void st4(float *p, float4 v) { *reinterpret_cast<float4 *>(p) = v; }
 __device__ __forceinline__ uint4 ldu4(const uint32_t *p) { return *reinterpret_cast<const uint4 *>(p); }
+
+// L2 cache-policy hints: data that is streamed once (r, the state rows a check node reads back, the
+// posterior stores) is marked evict_first so that it does not push out the gathered working set
+// (the s segments the check node reads d_v times, the row state the bit node reads d_i times).
+#ifndef LDPC_NO_L2_HINTS
+__device__ __forceinline__ uint64_t pol_evict_first() {
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ float4 ld4_pol(const float *a, uint64_t pol) {
+    float4 v;
+    asm("ld.global.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+        : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+        : "l"(a), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ uint32_t ld1_pol(const uint32_t *a, uint64_t pol) {
+    uint32_t v;
+    asm("ld.global.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void st4_pol(float *a, float4 v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(a), "f"(v.x), "f"(v.y), "f"(v.z),
+                 "f"(v.w), "l"(pol)
+                 : "memory");
+}
+#else
+__device__ __forceinline__ uint64_t pol_evict_first() { return 0; }
+__device__ __forceinline__ float4 ld4_pol(const float *a, uint64_t) { return *reinterpret_cast<const float4 *>(a); }
+__device__ __forceinline__ uint32_t ld1_pol(const uint32_t *a, uint64_t) { return *a; }
+__device__ __forceinline__ void st4_pol(float *a, float4 v, uint64_t) { *reinterpret_cast<float4 *>(a) = v; }
+#endif
 
 // ------------------------------------------------------------------------------------------------
 // a2: stage-in.  llr [F][n] -> r, s [T][n][128] (s = r), init per-tile flags.
@@ -794,6 +828,14 @@ __device__ __forceinline__ void cp4(uint32_t dst, const void *src) {
 __device__ __forceinline__ void cp8(uint32_t dst, const void *src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
 }
+__device__ __forceinline__ void cp16_pol(uint32_t dst, const void *src, uint64_t pol) {
+#ifndef LDPC_NO_L2_HINTS
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "l"(pol) : "memory");
+#else
+    (void)pol;
+    cp16(dst, src);
+#endif
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() {
@@ -874,6 +916,7 @@ __global__ void __launch_bounds__(CTA, 1)
     if (lane <= jb - ja) cpl = __ldg(g.col_ptr + ja + lane);
     const int ea = __shfl_sync(FULL, cpl, 0), eb = __shfl_sync(FULL, cpl, (jb - ja) & 31);
     const int ne = eb - ea;
+    const uint64_t pol = pol_evict_first();
     unsigned char *ring = bsm + (size_t)warp * NS * BA_SLOT;
     const uint32_t ring_s = smem_u32(ring);
     // producer: issue the copies of edge number te (column cursor pj / its end pe)
@@ -892,7 +935,7 @@ __global__ void __launch_bounds__(CTA, 1)
             cp16(sl + 512 + lane * 16, M1l + ro);
             cp_loc<LocT>(sl + 1024 + lane * 8, LCl + ro);
             cp4(sl + 1280 + lane * 4, SGl + ((size_t)ed.x * wr + (ed.y >> 3)) * 32);
-            if (e + 1 == pe) cp16(sl + 1408 + lane * 16, Rl + (size_t)(ja + pj) * TILE);  // r_j with the last edge
+            if (e + 1 == pe) cp16_pol(sl + 1408 + lane * 16, Rl + (size_t)(ja + pj) * TILE, pol);  // r_j, last edge
         }
         cp_commit();
     };
@@ -924,7 +967,7 @@ __global__ void __launch_bounds__(CTA, 1)
             const float4 rv = *reinterpret_cast<const float4 *>(sp + 1408 + lane * 16);
             float *o = Sl + (size_t)(ja + cj) * TILE;
             if (mine == 0xFu) {
-                st4(o, make_float4(acc[0] + rv.x, acc[1] + rv.y, acc[2] + rv.z, acc[3] + rv.w));
+                st4_pol(o, make_float4(acc[0] + rv.x, acc[1] + rv.y, acc[2] + rv.z, acc[3] + rv.w), pol);
             } else if (mine) {  // frozen frames keep their s
                 if (mine & 1u) o[0] = acc[0] + rv.x;
                 if (mine & 2u) o[1] = acc[1] + rv.y;
@@ -1116,16 +1159,25 @@ void cn_launch(dim3 grid, cudaStream_t st, const Graph &g, const StreamState &w,
     else k_cn<LT, F, EA><<<grid, CTA, 0, st>>>(g, w, k, rpc, lit, kdev);
 }
 
+// columns per CTA of the cp.async bit node (<= 248: a warp owns <= 31 columns); LDPC_BN_COLS overrides
+inline int bn_async_cols(int n) {
+    (void)n;
+    const char *e = getenv("LDPC_BN_COLS");
+    const int x = e ? atoi(e) : 248;
+    return std::max(8, std::min(248, (x + 7) & ~7));
+}
+
 template <typename LT, bool EA>
 void bn_launch(dim3 grid, cudaStream_t st, const Graph &g, const StreamState &w, int k, int cpc, int lit, int u,
                const int *kdev, int te) {
     // u: 0 = automatic (pipelined kernel; column degrees <= 32), 1 = generic kernel
     if (u == 0) {  // cp.async ring (default): 248 columns per CTA, 31 per warp
         constexpr int NS = BN_NS;
-        const size_t smem = (size_t)(CTA / 32) * NS * BA_SLOT + (size_t)248 * g.dvmax * 8;
+        const size_t smem = (size_t)(CTA / 32) * NS * BA_SLOT + (size_t)bn_async_cols(g.n) * g.dvmax * 8;
         cudaFuncSetAttribute(k_bn_async<LT, EA, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        const dim3 gr = grid2((g.n + 247) / 248, w.T);
-        k_bn_async<LT, EA, NS><<<gr, CTA, smem, st>>>(g, w, k, 248, lit, kdev, te);
+        const int cols = bn_async_cols(g.n);
+        const dim3 gr = grid2((g.n + cols - 1) / cols, w.T);
+        k_bn_async<LT, EA, NS><<<gr, CTA, smem, st>>>(g, w, k, cols, lit, kdev, te);
     } else if (u == 2 && g.dvmax <= 32) {
         k_bn_pipe<LT, EA><<<grid, CTA, 0, st>>>(g, w, k, cpc, lit, kdev, te);
     } else {
