@@ -185,6 +185,10 @@ def algorithmic_bytes(code, iters: np.ndarray, L: int, early: bool):
 # does subtract, compare + two min updates + argmin select, sign parity, eta^prev rebuild (magnitude
 # select, sign) and the syndrome bit = 9 lane operations; the bit node rebuilds eta (2) and adds (1).
 OPS_CN, OPS_BN = 9, 3
+# Of those, the ones that run on the ALU pipe (compare / min / select / logic; the subtract and the add
+# run on the FMA pipe): 8 and 2.  The ALU pipe issues one warp instruction every 2 cycles per SM
+# sub-partition (B300_MICROARCH.md "Pipe rates": alu rt_SMSP = 2), i.e. half the issue rate.
+ALU_CN, ALU_BN = 8, 2
 
 
 # ------------------------------------------------------------------ our arm ------------------
@@ -274,9 +278,14 @@ def run_ours(args):
             issue_peak = 148 * 4 * 32 * sm_mhz * 1e6 / 1e12  # lane-instructions per s, T
             ops = (float(cu.sum()) * OPS_CN + float(bu.sum()) * OPS_BN) * code.nnz * args.steps
             ach = ops / (kms / 1e3) / 1e12
+            alu_peak = issue_peak / 2  # 16 lanes per cycle per sub-partition
+            alu = (float(cu.sum()) * ALU_CN + float(bu.sum()) * ALU_BN) * code.nnz * args.steps / (kms / 1e3) / 1e12
             roof["issue_roofline"] = {"bound": "alu", "achieved": round(ach, 3), "peak": round(issue_peak, 2),
                                       "unit": "T lane-ops/s", "frac": round(ach / issue_peak, 4),
-                                      "ops_per_frame_edge": {"check_node": OPS_CN, "bit_node": OPS_BN}}
+                                      "ops_per_frame_edge": {"check_node": OPS_CN, "bit_node": OPS_BN},
+                                      "alu_pipe": {"achieved": round(alu, 3), "peak": round(alu_peak, 2),
+                                                   "frac": round(alu / alu_peak, 4),
+                                                   "ops_per_frame_edge": {"check_node": ALU_CN, "bit_node": ALU_BN}}}
     total_bits = float(world) * F * n * args.steps
     value = total_bits / (ms / 1e3) / 1e9
 

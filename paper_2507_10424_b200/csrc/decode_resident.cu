@@ -218,9 +218,9 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
     for (int e = tid; e < E; e += RT) {
         col[e] = (uint16_t)__ldg(a.g.col_idx + e);
         const int4 be = __ldg(a.g.bn_edge + e);  // {edge id, row, pos, parity}
-        rec[e] = ((uint32_t)be.z << 16) | (uint32_t)be.y;  // {pos p in row i, row i}
-        // ballot-word index of the edge | bit offset of row i inside the word (the lane adds l)
-        rec2[e] = (uint32_t)((be.y / G) * dm + be.z) | ((uint32_t)((be.y % G) * LR) << 16);
+        rec[e] = (uint32_t)be.y * S;  // first state element of row i (the lane adds its slot offset)
+        // ballot-word index of the edge | position p in row i << 16 | bit offset of row i in the word << 24
+        rec2[e] = (uint32_t)((be.y / G) * dm + be.z) | ((uint32_t)be.z << 16) | ((uint32_t)((be.y % G) * LR) << 24);
     }
     if (tid < 32) {
         slot_f[tid] = -1;
@@ -408,16 +408,14 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
 #pragma unroll
                             for (int u = 0; u < 3; u++) {
                                 if (q3 + u < dv) {
-                                    const uint32_t rc = rec[c0 + q3 + u];
+                                    const int ca = (int)rec[c0 + q3 + u] + q0;
                                     const uint32_t r2 = rec2[c0 + q3 + u];
-                                    const int i = (int)(rc & 0xffffu);
-                                    const uint32_t pp = (rc >> 16) * 0x01010101u;  // position of the edge in row i
-                                    const int ca = i * S + q0;
+                                    const uint32_t pp = __byte_perm(r2, 0u, 0x2222u);  // position p in every byte
                                     const float4 m0 = *reinterpret_cast<const float4 *>(mn0 + ca);
                                     const float4 m1 = *reinterpret_cast<const float4 *>(mn1 + ca);
                                     const uint32_t lv = *reinterpret_cast<const uint32_t *>(lc + ca) ^ pp;
                                     const uint4 W = sgo[r2 & 0xffffu];
-                                    const uint32_t mul = 0x80000000u >> ((r2 >> 16) + l);  // this lane's bit of row i
+                                    const uint32_t mul = 0x80000000u >> ((r2 >> 24) + l);  // this lane's bit of row i
                                     const float mg[4] = {(lv & 0xffu) ? m0.x : m1.x, (lv & 0xff00u) ? m0.y : m1.y,
                                                          (lv & 0xff0000u) ? m0.z : m1.z,
                                                          (lv & 0xff000000u) ? m0.w : m1.w};  // Obs. 1
