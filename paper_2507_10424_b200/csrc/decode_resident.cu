@@ -75,6 +75,7 @@ struct ResArgs {
     const float *llr;
     int64_t frames;
     int L, T, early, literal, dm;
+    int dc, dv;  // > 0: every row has degree dc and every column degree dv (regular code)
     float *post;
     uint8_t *bits;
     int32_t *iters;
@@ -103,7 +104,7 @@ __device__ __forceinline__ float flip31(float mag, uint32_t bit31) {
     return __uint_as_float(__float_as_uint(mag) ^ (bit31 & 0x80000000u));
 }
 
-template <int S, bool HAS>
+template <int S, bool HAS, int DC>
 __device__ __forceinline__ void cn_rows(const float *__restrict__ s, float *mn0, float *mn1, uint8_t *lc,
                                         const uint4 *__restrict__ sgi, uint4 *__restrict__ sgo, const uint16_t *col,
                                         int i, bool valid, int ra, int d, int dmax, int l, int lane, unsigned fm,
@@ -129,8 +130,9 @@ __device__ __forceinline__ void cn_rows(const float *__restrict__ s, float *mn0,
     int nloc[4] = {0xff, 0xff, 0xff, 0xff};
     unsigned parw[4] = {0, 0, 0, 0};
     uint32_t synw[4] = {0u, 0u, 0u, 0u};  // XOR of the sign bits of s over the row: bit 31 = XOR of (1 - b_j)
-#pragma unroll 2
-    for (int p = 0; p < dmax; p++) {
+    // DC > 0: every row has degree DC (regular code) -- the edge loop is fully unrolled
+#pragma unroll(DC > 0 ? DC : 2)
+    for (int p = 0; p < (DC > 0 ? DC : dmax); p++) {
         const bool has = HAS ? (p < d) : true;
         const int e = ra + p;
         const int j = has ? col[e] : 0;
@@ -180,7 +182,7 @@ __device__ __forceinline__ void cn_rows(const float *__restrict__ s, float *mn0,
 
 // Lane layout: a lane owns 4 consecutive slots (float4) of one row or column; LR = S/4 lanes cover a
 // row, G = 32/LR rows per warp.  Bit of slot q = 4*l + v inside an S-bit sign word: v*LR + l.
-template <int S, int RT>
+template <int S, int RT, int DC, int DV>
 __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 2) : RT == 384 ? 2 : 1) k_resident(ResArgs a) {
     constexpr int NWARP = RT / 32;
     constexpr int LR = S / 4;
@@ -345,16 +347,19 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
             for (int rb = warp * G; rb < m; rb += NWARP * G) {
                 const int i = rb + sub;
                 const bool valid = i < m;
-                const int ra = valid ? rp[i] : 0;
-                const int d = valid ? (int)rp[i + 1] - ra : 0;
-                const int dmax = __reduce_max_sync(FULLM, d);
+                const int ra = DC > 0 ? i * DC : (valid ? rp[i] : 0);
+                const int d = DC > 0 ? (valid ? DC : 0) : (valid ? (int)rp[i + 1] - ra : 0);
+                const int dmax = DC > 0 ? DC : __reduce_max_sync(FULLM, d);
                 const size_t rg = (size_t)(rb / G);
-                if (__all_sync(FULLM, d == dmax))
-                    cn_rows<S, false>(s, mn0, mn1, lc, sgi + rg * dm, sgo + rg * dm, col, i, valid, ra, d, dmax, l,
-                                      lane, fm, fmb, corr, syn_acc);
+                if (DC > 0 && rb + G <= m)
+                    cn_rows<S, false, DC>(s, mn0, mn1, lc, sgi + rg * dm, sgo + rg * dm, col, i, valid, ra, d, dmax, l,
+                                          lane, fm, fmb, corr, syn_acc);
+                else if (__all_sync(FULLM, d == dmax))
+                    cn_rows<S, false, 0>(s, mn0, mn1, lc, sgi + rg * dm, sgo + rg * dm, col, i, valid, ra, d, dmax, l,
+                                         lane, fm, fmb, corr, syn_acc);
                 else
-                    cn_rows<S, true>(s, mn0, mn1, lc, sgi + rg * dm, sgo + rg * dm, col, i, valid, ra, d, dmax, l,
-                                     lane, fm, fmb, corr, syn_acc);
+                    cn_rows<S, true, 0>(s, mn0, mn1, lc, sgi + rg * dm, sgo + rg * dm, col, i, valid, ra, d, dmax, l,
+                                        lane, fm, fmb, corr, syn_acc);
             }
             const unsigned mine = (syn_acc << q0) & active;
             const unsigned wmask = __reduce_or_sync(FULLM, mine);
@@ -402,7 +407,7 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
                     }
                     if (cm) {
                         const float4 rj = *reinterpret_cast<const float4 *>(rs + (size_t)j * S + q0);
-                        const int c0 = cp[j], dv = (int)cp[j + 1] - c0;
+                        const int c0 = DV > 0 ? j * DV : cp[j], dv = DV > 0 ? DV : (int)cp[j + 1] - c0;
                         float acc[4] = {0.f, 0.f, 0.f, 0.f};
                         for (int q3 = 0; q3 < dv; q3 += 3) {  // chunks of 3 edges: no remainder loop for d_v = 3
 #pragma unroll
@@ -471,8 +476,14 @@ int max_smem_optin(int device) {
 
 template <int S, int RT>
 void launch_s(const ResArgs &args, int ctas, size_t smem, cudaStream_t st) {
-    cudaFuncSetAttribute(k_resident<S, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_resident<S, RT><<<ctas, RT, smem, st>>>(args);
+    // regular (3,6) codes (C1, C2, C5): degree-specialised kernel (fully unrolled row and column loops)
+    if (args.dc == 6 && args.dv == 3) {
+        cudaFuncSetAttribute(k_resident<S, RT, 6, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_resident<S, RT, 6, 3><<<ctas, RT, smem, st>>>(args);
+        return;
+    }
+    cudaFuncSetAttribute(k_resident<S, RT, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_resident<S, RT, 0, 0><<<ctas, RT, smem, st>>>(args);
 }
 
 template <int S>
@@ -511,6 +522,8 @@ ResidentPlan plan_resident(const HostGraph &g, bool loc16, int device) {
             rp.ok = true;
             rp.slots = S;
             rp.dm = dm;
+            rp.dv = g.max_col_deg;
+            rp.regular = (int64_t)g.E == (int64_t)g.m * dm && (int64_t)g.E == (int64_t)g.n * g.max_col_deg;
             rp.smem = L.total;
             rp.threads = per_sm >= 2 ? 256 : 512;
             if (force_t == 128 || force_t == 256 || force_t == 384 || force_t == 512 || force_t == 1024)
@@ -547,6 +560,9 @@ int launch_resident(const Graph &g, const ResidentPlan &rp, const float *llr, in
     a.counter = work_counter;
     a.rs = reinterpret_cast<float *>(reinterpret_cast<char *>(work_counter) + 256);
     a.dm = rp.dm;
+    a.dc = rp.regular ? rp.dm : 0;
+    a.dv = rp.regular ? rp.dv : 0;
+    if (getenv("LDPC_RES_GENERIC")) a.dc = a.dv = 0;
     a.lay = layout_for(rp.slots, g.m, g.n, g.E, rp.dm);
     cudaMemsetAsync(work_counter, 0, sizeof(int), st);
     switch (rp.slots) {

@@ -96,6 +96,8 @@ struct ResidentPlan {
     size_t smem = 0;     // dynamic shared memory bytes
     int ctas = 0;        // persistent grid size
     int dm = 0;          // max row degree (ballot-word rows)
+    int dv = 0;          // max column degree
+    bool regular = false;  // every row has degree dm and every column degree dv
 };
 ResidentPlan plan_resident(const HostGraph &g, bool loc16, int device);
 size_t resident_scratch_bytes(const HostGraph &g, const ResidentPlan &rp);  // work counter + r scratch
