@@ -836,6 +836,23 @@ __device__ __forceinline__ void cp16_pol(uint32_t dst, const void *src, uint64_t
     cp16(dst, src);
 #endif
 }
+__device__ __forceinline__ uint64_t pol_gather() {
+#if defined(BN_GATHER_EVICT_LAST)
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+#else
+    return 0;
+#endif
+}
+__device__ __forceinline__ void cp16_g(uint32_t dst, const void *src, uint64_t pol) {
+#if defined(BN_GATHER_EVICT_LAST)
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "l"(pol) : "memory");
+#else
+    (void)pol;
+    cp16(dst, src);
+#endif
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() {
@@ -916,7 +933,7 @@ __global__ void __launch_bounds__(CTA, 1)
     if (lane <= jb - ja) cpl = __ldg(g.col_ptr + ja + lane);
     const int ea = __shfl_sync(FULL, cpl, 0), eb = __shfl_sync(FULL, cpl, (jb - ja) & 31);
     const int ne = eb - ea;
-    const uint64_t pol = pol_evict_first();
+    const uint64_t pol = pol_evict_first(), gpol = pol_gather();
     unsigned char *ring = bsm + (size_t)warp * NS * BA_SLOT;
     const uint32_t ring_s = smem_u32(ring);
     // producer: issue the copies of edge number te (column cursor pj / its end pe)
@@ -931,8 +948,8 @@ __global__ void __launch_bounds__(CTA, 1)
             const int2 ed = rec[e - cea];  // {i, p}
             const size_t ro = (size_t)ed.x * TILE;
             const uint32_t sl = ring_s + (uint32_t)((te % NS) * BA_SLOT);
-            cp16(sl + lane * 16, M0l + ro);
-            cp16(sl + 512 + lane * 16, M1l + ro);
+            cp16_g(sl + lane * 16, M0l + ro, gpol);
+            cp16_g(sl + 512 + lane * 16, M1l + ro, gpol);
             cp_loc<LocT>(sl + 1024 + lane * 8, LCl + ro);
             cp4(sl + 1280 + lane * 4, SGl + ((size_t)ed.x * wr + (ed.y >> 3)) * 32);
             if (e + 1 == pe) cp16_pol(sl + 1408 + lane * 16, Rl + (size_t)(ja + pj) * TILE, pol);  // r_j, last edge

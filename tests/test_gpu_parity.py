@@ -205,10 +205,11 @@ def test_graph_loop_equals_plain_launches(cfg_name, frames):
             assert np.array_equal(a, b)
 
 
-@pytest.mark.parametrize("cu,bu", [(1, 1), (2, 2), (4, 3), (2, 3)])
+@pytest.mark.parametrize("cu,bu", [(0, 0), (1, 1), (0, 2), (1, 0)])
 def test_stream_unroll_variants(monkeypatch, cu, bu):
-    """Every load-batching variant of the streaming check-node / bit-node sweeps is bit-identical
-    (LDPC_CN_UNROLL edges per check-node batch, LDPC_BN_UNROLL per bit-node batch)."""
+    """Every kernel variant of the streaming sweeps is bit-identical: check node LDPC_CN_UNROLL = 0
+    (software-pipelined, rows of degree <= 8) / 1 (generic); bit node LDPC_BN_UNROLL = 0 (cp.async
+    ring) / 1 (generic) / 2 (register-pipelined)."""
     monkeypatch.setenv("LDPC_CN_UNROLL", str(cu))
     monkeypatch.setenv("LDPC_BN_UNROLL", str(bu))
     cfg = codes.CONFIGS["c2"]
@@ -220,6 +221,20 @@ def test_stream_unroll_variants(monkeypatch, cu, bu):
     code3 = codes.random_small(37, 70, 2, 2, 9)  # irregular, rows of degree 2..
     llr3 = (np.random.default_rng(3).standard_normal((300, code3.n)) - 0.5).astype(np.float32)
     compare(code3, llr3, 12, h=handle(code3, FORCE_STREAM))
+
+
+def test_resident_generic_equals_regular_instance(monkeypatch):
+    """The degree-specialised resident kernel for regular (3,6) codes and the generic one agree
+    (LDPC_RES_GENERIC=1 forces the generic instance), and both match the oracle."""
+    cfg = codes.CONFIGS["c2"]
+    code = cfg["code"]()
+    parts = [channel.bpsk_awgn(code.n, code.rate, e, cfg["seed"], p, 500, 300).numpy() for p, e in enumerate(cfg["ebn0"])]
+    llr = np.concatenate(parts)
+    ref = compare(code, llr, cfg["max_iter"], FORCE_RESIDENT, h=handle(code, FORCE_RESIDENT))
+    monkeypatch.setenv("LDPC_RES_GENERIC", "1")
+    got = compare(code, llr, cfg["max_iter"], FORCE_RESIDENT, h=handle(code, FORCE_RESIDENT))
+    for a, b in zip(ref, got):
+        assert np.array_equal(a, b)
 
 
 @pytest.mark.parametrize("flags", [FORCE_STREAM, FORCE_RESIDENT, FORCE_STREAM | LIT])

@@ -16,6 +16,7 @@ ap.add_argument("--frames", type=int, default=0, help="0 = the config's block si
 ap.add_argument("--flags", type=int, default=0)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--max-iter", type=int, default=0)
+ap.add_argument("--chunk", type=int, default=0, help="frames per chunk (0 = automatic)")
 args = ap.parse_args()
 cfg = codes.CONFIGS[args.config]
 code = cfg["code"]()
@@ -27,6 +28,8 @@ llr = channel.bpsk_awgn(code.n, code.rate, cfg["ebn0"][args.point], cfg["seed"],
 rr, cc = code.coo()
 h = P.Handle.from_coo(torch.from_numpy(rr).cuda(), torch.from_numpy(cc).cuda(), code.m, code.n, flags=args.flags)
 print("schedule", h.schedule, "frames", F)
+if args.chunk:
+    h.set_chunk(args.chunk)
 st = torch.zeros(8, dtype=torch.int64, device="cuda")
 h.profile(True)
 for _ in range(args.reps):
