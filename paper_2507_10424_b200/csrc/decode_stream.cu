@@ -196,6 +196,12 @@ constexpr int BN_CHUNK = 4;  // column edges per batch of row-state gathers
 #ifndef BN_MINB
 #define BN_MINB 3
 #endif
+#ifndef BNL_MINB
+#define BNL_MINB 6
+#endif
+#ifndef BNL_COLS
+#define BNL_COLS 32
+#endif
 
 // ------------------------------------------------------------------------------------------------
 // a3/a4/a6: check-node sweep of loop body k (k = 1..L), fused syndrome of b^(k-1).
@@ -497,7 +503,7 @@ __global__ void __launch_bounds__(CTA, 2)
 // (ordered) sum.
 // ------------------------------------------------------------------------------------------------
 template <typename LocT, bool EARLY>
-__global__ void __launch_bounds__(CTA, BN_MINB)
+__global__ void __launch_bounds__(CTA, BNL_MINB)
     k_bn(Graph g, StreamState w, int k, int cols_per_cta, int literal, const int *kdev, int check_every) {
     using LO = LocOps<LocT>;
     if (kdev) k = *kdev;
@@ -547,84 +553,34 @@ __global__ void __launch_bounds__(CTA, BN_MINB)
     const float *__restrict__ Rl = w.r + (size_t)t * n * TILE + 4 * lane;
     float *__restrict__ Sl = w.s + (size_t)t * n * TILE + 4 * lane;
     const int warp = threadIdx.x >> 5;
-    const int j0 = cblk * cols_per_cta + warp, j1 = min(n, cblk * cols_per_cta + cols_per_cta);
-    const int nc = j0 < j1 ? (j1 - j0 + 7) / 8 : 0;  // columns of this warp (<= 32)
-    int ca = 0, cb = 0;
-    if (lane < nc) {
-        ca = __ldg(g.col_ptr + j0 + 8 * lane);
-        cb = __ldg(g.col_ptr + j0 + 8 * lane + 1);
-    }
-    int c0 = __shfl_sync(FULL, ca, 0), dv = __shfl_sync(FULL, cb, 0) - c0;
-    int ei = 0, ep = 0;  // lane q: {row, position in the row} of edge q of the column
-    if (nc > 0 && lane < dv) {
-        const int4 ed = __ldg(g.bn_edge + c0 + lane);
-        ei = ed.y;
-        ep = ed.z;
-    }
-    for (int q = 0; q < nc; q++) {
-        const int j = j0 + 8 * q;
-        const int cn = __shfl_sync(FULL, ca, (q + 1) & 31), dn = __shfl_sync(FULL, cb, (q + 1) & 31) - cn;
+    const int j1 = min(n, cblk * cols_per_cta + cols_per_cta);
+    // one edge at a time, few registers, many warps (6 CTAs per SM): the loads of an edge depend only
+    // on its (broadcast) record, and the warps of the SM keep enough of them in flight
+    for (int j = cblk * cols_per_cta + warp; j < j1; j += CTA / 32) {
+        const int c0 = __ldg(g.col_ptr + j), dv = __ldg(g.col_ptr + j + 1) - c0;
         const float4 rv = ld4(Rl + (size_t)j * TILE);
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
-        for (int q0 = 0; q0 < dv; q0 += BN_CHUNK) {
-            if (q0 > 0 && (q0 & 31) == 0) {
-                ei = ep = 0;
-                if (lane < dv - q0) {
-                    const int4 ed = __ldg(g.bn_edge + c0 + q0 + lane);
-                    ei = ed.y;
-                    ep = ed.z;
-                }
-            }
-            float4 m0[BN_CHUNK], m1[BN_CHUNK];
-            typename LO::W lc[BN_CHUNK];
-            uint32_t W[BN_CHUNK];
-            int pe[BN_CHUNK];
+        for (int q = 0; q < dv; q++) {
+            const int4 ed = __ldg(g.bn_edge + c0 + q);  // {e, i, p, -}, ascending i
+            const size_t ro = (size_t)ed.y * TILE;
+            const float4 m0 = ld4(M0l + ro), m1 = ld4(M1l + ro);
+            const typename LO::W key = LO::key(LO::load(LCl + ro), ed.z);
+            const uint32_t ws = SGl[((size_t)ed.y * wr + (ed.z >> 3)) * 32] << (28 - 4 * (ed.z & 7));
 #pragma unroll
-            for (int u = 0; u < BN_CHUNK; u++) {
-                const int i = __shfl_sync(FULL, ei, (q0 + u) & 31);
-                pe[u] = __shfl_sync(FULL, ep, (q0 + u) & 31);
-                if (q0 + u < dv) {
-                    const size_t ro = (size_t)i * TILE;
-                    m0[u] = ld4(M0l + ro);
-                    m1[u] = ld4(M1l + ro);
-                    lc[u] = LO::load(LCl + ro);
-                    W[u] = SGl[((size_t)i * wr + (pe[u] >> 3)) * 32];
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < BN_CHUNK; u++) {
-                if (q0 + u < dv) {
-                    const typename LO::W key = LO::key(lc[u], pe[u]);
-                    const uint32_t ws = W[u] << (28 - 4 * (pe[u] & 7));  // bit 4(p%8)+v -> bit 28+v
-#pragma unroll
-                    for (int v = 0; v < 4; v++) {
-                        const float mag = LO::hit(key, v) ? comp(m1[u], v) : comp(m0[u], v);  // Obs. 1
-                        acc[v] = acc[v] + flip31(mag, ws << (3 - v));  // ascending rows from +0.0 (A14)
-                    }
-                }
+            for (int v = 0; v < 4; v++) {
+                const float mag = LO::hit(key, v) ? comp(m1, v) : comp(m0, v);  // Obs. 1
+                acc[v] = acc[v] + flip31(mag, ws << (3 - v));                   // ascending rows from +0.0 (A14)
             }
         }
-        // prefetch the next column's edges
-        ei = ep = 0;
-        if (q + 1 < nc && lane < dn) {
-            const int4 ed = __ldg(g.bn_edge + cn + lane);
-            ei = ed.y;
-            ep = ed.z;
-        }
-        float4 out = make_float4(acc[0] + rv.x, acc[1] + rv.y, acc[2] + rv.z, acc[3] + rv.w);
-        float *sp = Sl + (size_t)j * TILE;
+        float *o = Sl + (size_t)j * TILE;
         if (mine == 0xFu) {
-            st4(sp, out);
-        } else if (mine) {
-            const float4 old = ld4(sp);
-            out.x = (mine & 1u) ? out.x : old.x;
-            out.y = (mine & 2u) ? out.y : old.y;
-            out.z = (mine & 4u) ? out.z : old.z;
-            out.w = (mine & 8u) ? out.w : old.w;
-            st4(sp, out);
+            st4(o, make_float4(acc[0] + rv.x, acc[1] + rv.y, acc[2] + rv.z, acc[3] + rv.w));
+        } else if (mine) {  // frozen frames keep their s
+            if (mine & 1u) o[0] = acc[0] + rv.x;
+            if (mine & 2u) o[1] = acc[1] + rv.y;
+            if (mine & 4u) o[2] = acc[2] + rv.z;
+            if (mine & 8u) o[3] = acc[3] + rv.w;
         }
-        c0 = cn;
-        dv = dn;
     }
 }
 
@@ -1187,8 +1143,9 @@ inline int bn_async_cols(int n) {
 template <typename LT, bool EA>
 void bn_launch(dim3 grid, cudaStream_t st, const Graph &g, const StreamState &w, int k, int cpc, int lit, int u,
                const int *kdev, int te) {
-    // u: 0 = automatic (pipelined kernel; column degrees <= 32), 1 = generic kernel
-    if (u == 0) {  // cp.async ring (default): 248 columns per CTA, 31 per warp
+    // u: 0 / 1 = one edge at a time, many warps (default; best on C3, equal on C4), 2 = register-
+    //    pipelined chunks, 3 = cp.async ring
+    if (u == 3) {  // cp.async ring: 248 columns per CTA, 31 per warp
         constexpr int NS = BN_NS;
         const size_t smem = (size_t)(CTA / 32) * NS * BA_SLOT + (size_t)bn_async_cols(g.n) * g.dvmax * 8;
         cudaFuncSetAttribute(k_bn_async<LT, EA, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1198,7 +1155,7 @@ void bn_launch(dim3 grid, cudaStream_t st, const Graph &g, const StreamState &w,
     } else if (u == 2 && g.dvmax <= 32) {
         k_bn_pipe<LT, EA><<<grid, CTA, 0, st>>>(g, w, k, cpc, lit, kdev, te);
     } else {
-        k_bn<LT, EA><<<grid, CTA, 0, st>>>(g, w, k, cpc, lit, kdev, te);
+        k_bn<LT, EA><<<grid2((g.n + BNL_COLS - 1) / BNL_COLS, w.T), CTA, 0, st>>>(g, w, k, BNL_COLS, lit, kdev, te);
     }
 }
 

@@ -205,11 +205,11 @@ def test_graph_loop_equals_plain_launches(cfg_name, frames):
             assert np.array_equal(a, b)
 
 
-@pytest.mark.parametrize("cu,bu", [(0, 0), (1, 1), (0, 2), (1, 0)])
+@pytest.mark.parametrize("cu,bu", [(0, 0), (1, 1), (0, 2), (1, 3)])
 def test_stream_unroll_variants(monkeypatch, cu, bu):
     """Every kernel variant of the streaming sweeps is bit-identical: check node LDPC_CN_UNROLL = 0
-    (software-pipelined, rows of degree <= 8) / 1 (generic); bit node LDPC_BN_UNROLL = 0 (cp.async
-    ring) / 1 (generic) / 2 (register-pipelined)."""
+    (software-pipelined, rows of degree <= 8) / 1 (generic); bit node LDPC_BN_UNROLL = 0 or 1 (one edge
+    at a time, the default) / 2 (register-pipelined) / 3 (cp.async ring)."""
     monkeypatch.setenv("LDPC_CN_UNROLL", str(cu))
     monkeypatch.setenv("LDPC_BN_UNROLL", str(bu))
     cfg = codes.CONFIGS["c2"]
