@@ -196,6 +196,9 @@ constexpr int BN_CHUNK = 4;  // column edges per batch of row-state gathers
 #ifndef BN_MINB
 #define BN_MINB 3
 #endif
+#ifndef CN1_MINB
+#define CN1_MINB 3
+#endif
 #ifndef BNL_MINB
 #define BNL_MINB 6
 #endif
@@ -393,7 +396,7 @@ __device__ __forceinline__ void cn_compute(const CnRow<CH, LocT> &R, int i, int 
     const float om0[4] = {R.m0.x, R.m0.y, R.m0.z, R.m0.w}, om1[4] = {R.m1.x, R.m1.y, R.m1.z, R.m1.w};
     float nm0[4] = {INF, INF, INF, INF}, nm1[4] = {INF, INF, INF, INF};
     int nloc[4] = {0, 0, 0, 0};
-    uint32_t par[4] = {0u, 0u, 0u, 0u}, syn[4] = {0u, 0u, 0u, 0u}, wnew = 0;
+    uint32_t syn[4] = {0u, 0u, 0u, 0u}, wnew = 0;
 #pragma unroll
     for (int p = 0; p < CH; p++) {
         if (p < d) {
@@ -412,16 +415,19 @@ __device__ __forceinline__ void cn_compute(const CnRow<CH, LocT> &R, int i, int 
                 nm1[v] = fminf(nm1[v], fmaxf(nm0[v], ax));
                 nm0[v] = fminf(nm0[v], ax);
                 nloc[v] = lt ? p : nloc[v];
-                par[v] ^= __float_as_uint(x);                       // sign parity (Obs. 2)
                 if (EARLY) syn[v] ^= __float_as_uint(sj) - 1u;      // bit 31: slice(s_j) == 0
                 wnew |= (__float_as_uint(x) >> 31) << (4 * p + v);  // sign(0) = +1
             }
         }
     }
     SGl[(size_t)i * 32] = wnew;
-    const uint32_t c31 = corr << 31;
-    const uint32_t s0 = (par[0] & 0x80000000u) ^ c31, s1 = (par[1] & 0x80000000u) ^ c31;
-    const uint32_t s2 = (par[2] & 0x80000000u) ^ c31, s3 = (par[3] & 0x80000000u) ^ c31;
+    // sign parity per frame (Obs. 2): XOR of bits v, v+4, ..., of the new sign word, times (-1)^{d_i}
+    uint32_t pw = wnew ^ (wnew >> 16);
+    pw ^= pw >> 8;
+    pw ^= pw >> 4;
+    pw ^= corr ? 0xfu : 0u;
+    const uint32_t s0 = pw << 31, s1 = (pw << 30) & 0x80000000u, s2 = (pw << 29) & 0x80000000u,
+                   s3 = (pw << 28) & 0x80000000u;
     st4(M0l + (size_t)i * TILE,
         make_float4(__uint_as_float(__float_as_uint(nm0[0]) | s0), __uint_as_float(__float_as_uint(nm0[1]) | s1),
                     __uint_as_float(__float_as_uint(nm0[2]) | s2), __uint_as_float(__float_as_uint(nm0[3]) | s3)));
@@ -436,8 +442,8 @@ __device__ __forceinline__ void cn_compute(const CnRow<CH, LocT> &R, int i, int 
     }
 }
 
-template <int CH, typename LocT, bool FIRST, bool EARLY>
-__global__ void __launch_bounds__(CTA, 2)
+template <int CH, typename LocT, bool FIRST, bool EARLY, bool DB>
+__global__ void __launch_bounds__(CTA, DB ? 2 : CN1_MINB)
     k_cn_pipe(Graph g, StreamState w, int k, int rows_per_cta, int literal, const int *kdev) {
     if (kdev) k = *kdev;  // body index supplied by the graph-driven loop
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -471,6 +477,15 @@ __global__ void __launch_bounds__(CTA, 2)
         return (q < nr && lane < d) ? __ldg(g.col_idx + a + lane) : 0;
     };
     uint32_t u[4] = {0u, 0u, 0u, 0u};
+    if (!DB) {  // one row buffer: all loads of a row in flight together, more warps per SM
+        CnRow<CH, LocT> A;
+        int cj = cols_of(0);
+        for (int q = 0; q < nr; q++) {
+            cn_fetch<CH, LocT, FIRST>(A, cj, row_of(q), Sl, SGl, M0l, M1l, LCl);
+            cj = cols_of(q + 1);
+            cn_compute<CH, LocT, FIRST, EARLY>(A, row_of(q), deg_of(q), literal, SGl, M0l, M1l, LCl, u);
+        }
+    } else {
     CnRow<CH, LocT> A, B;
     int cjA = cols_of(0), cjB = cols_of(1);
     cn_fetch<CH, LocT, FIRST>(A, cjA, row_of(0), Sl, SGl, M0l, M1l, LCl);
@@ -483,6 +498,7 @@ __global__ void __launch_bounds__(CTA, 2)
         cn_fetch<CH, LocT, FIRST>(A, cjA, row_of(q + 2), Sl, SGl, M0l, M1l, LCl);
         cjA = cols_of(q + 4);
         cn_compute<CH, LocT, FIRST, EARLY>(B, row_of(q + 1), deg_of(q + 1), literal, SGl, M0l, M1l, LCl, u);
+    }
     }
     if (EARLY) {
         if (lane == 0) {
@@ -1125,10 +1141,14 @@ int launch_stage_in(const Graph &g, const StreamState &w, const float *llr, int6
 template <typename LT, bool F, bool EA>
 void cn_launch(dim3 grid, cudaStream_t st, const Graph &g, const StreamState &w, int k, int rpc, int lit, int u,
                const int *kdev) {
-    // u: 0 = automatic (pipelined kernel when every row has degree <= 8), 1 = generic kernel
-    if (u != 1 && g.dmax <= 4) k_cn_pipe<4, LT, F, EA><<<grid, CTA, 0, st>>>(g, w, k, rpc, lit, kdev);
-    else if (u != 1 && g.dmax <= 6) k_cn_pipe<6, LT, F, EA><<<grid, CTA, 0, st>>>(g, w, k, rpc, lit, kdev);
-    else if (u != 1 && g.dmax <= 8) k_cn_pipe<8, LT, F, EA><<<grid, CTA, 0, st>>>(g, w, k, rpc, lit, kdev);
+    // u: 0 = single row buffer (default), 2 = two row buffers, 1 = generic kernel
+    if (u != 1 && u != 2 && g.dmax <= 8) {
+        if (g.dmax <= 4) k_cn_pipe<4, LT, F, EA, false><<<grid, CTA, 0, st>>>(g, w, k, rpc, lit, kdev);
+        else if (g.dmax <= 6) k_cn_pipe<6, LT, F, EA, false><<<grid, CTA, 0, st>>>(g, w, k, rpc, lit, kdev);
+        else if (g.dmax == 7) k_cn_pipe<7, LT, F, EA, false><<<grid, CTA, 0, st>>>(g, w, k, rpc, lit, kdev);
+        else k_cn_pipe<8, LT, F, EA, false><<<grid, CTA, 0, st>>>(g, w, k, rpc, lit, kdev);
+    } else if (u == 2 && g.dmax <= 6) k_cn_pipe<6, LT, F, EA, true><<<grid, CTA, 0, st>>>(g, w, k, rpc, lit, kdev);
+    else if (u == 2 && g.dmax <= 8) k_cn_pipe<8, LT, F, EA, true><<<grid, CTA, 0, st>>>(g, w, k, rpc, lit, kdev);
     else k_cn<LT, F, EA><<<grid, CTA, 0, st>>>(g, w, k, rpc, lit, kdev);
 }
 
