@@ -262,6 +262,7 @@ def run_ours(args):
         achieved = per_launch_bytes / per_launch_s / 1e9
         roof = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic_from_profiles(args.config, dom),
+                "traffic_vs_algorithmic_in_capture": traffic_ratio_from_profiles(args.config, dom),
                 "algorithmic_bytes_per_launch": round(per_launch_bytes), "avg_launch_us": round(per_launch_s * 1e6, 2),
                 "share_of_step": round(kms / ms_local, 4), "peak_source": peak_src,
                 "kernel_ms": {k: round(v[1], 3) for k, v in prof.items() if v[0]},
@@ -325,6 +326,17 @@ def run_ours(args):
         import torch.distributed as dist
 
         dist.destroy_process_group()
+
+
+def traffic_ratio_from_profiles(cfg_name, kernel):
+    """DRAM bytes / algorithmic bytes of the captured launch (a full-work launch), if recorded."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            e = json.load(f)[cfg_name][kernel]
+        return round(e["dram_bytes_per_launch"] / e["algorithmic_bytes_this_launch"], 3)
+    except Exception:
+        return None
 
 
 def traffic_from_profiles(cfg_name, kernel):

@@ -448,8 +448,12 @@ int ldpc_decode_host(ldpc_handle_t h, const float *llr, int64_t frames, int32_t 
     if (h->poisoned) return LDPC_ERR_CUDA;
     if (frames == 0) return LDPC_OK;
     const int64_t n = h->g.n;
-    // chunk of frames per pipeline stage
-    int64_t chunk = std::max<int64_t>(TILE, std::min<int64_t>(frames, (int64_t)(96u << 20) / (n * 4)));
+    // chunk of frames per pipeline stage: LDPC_HOST_CHUNK_MB of LLRs (default 384 MB for the streaming
+    // schedule -- enough tiles per launch to fill the GPU -- and 96 MB for the resident one, whose
+    // persistent CTAs are full at any size; measured e2e on C2-C4)
+    const char *cm = getenv("LDPC_HOST_CHUNK_MB");
+    const int64_t chunk_mb = cm ? std::max(1, atoi(cm)) : (use_resident(h) ? 96 : 384);
+    int64_t chunk = std::max<int64_t>(TILE, std::min<int64_t>(frames, (chunk_mb << 20) / (n * 4)));
     chunk = (chunk + TILE - 1) / TILE * TILE;
     const size_t per_frame = n * 4 + (bits_out ? n : 0) + (posterior_out ? n * 4 : 0) + 4 + 1;
     const size_t set_bytes = align256(chunk * n * 4) + align256(chunk * n) + align256(chunk * n * 4) +
