@@ -50,39 +50,6 @@ __device__ __forceinline__ float4 ld4(const float *p) { return *reinterpret_cast
 __device__ __forceinline__ void st4(float *p, float4 v) { *reinterpret_cast<float4 *>(p) = v; }
 __device__ __forceinline__ uint4 ldu4(const uint32_t *p) { return *reinterpret_cast<const uint4 *>(p); }
 
-// L2 cache-policy hints: data that is streamed once (r, the state rows a check node reads back, the
-// posterior stores) is marked evict_first so that it does not push out the gathered working set
-// (the s segments the check node reads d_v times, the row state the bit node reads d_i times).
-#ifndef LDPC_NO_L2_HINTS
-__device__ __forceinline__ uint64_t pol_evict_first() {
-    uint64_t p;
-    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-__device__ __forceinline__ float4 ld4_pol(const float *a, uint64_t pol) {
-    float4 v;
-    asm("ld.global.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
-        : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-        : "l"(a), "l"(pol));
-    return v;
-}
-__device__ __forceinline__ uint32_t ld1_pol(const uint32_t *a, uint64_t pol) {
-    uint32_t v;
-    asm("ld.global.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
-    return v;
-}
-__device__ __forceinline__ void st4_pol(float *a, float4 v, uint64_t pol) {
-    asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(a), "f"(v.x), "f"(v.y), "f"(v.z),
-                 "f"(v.w), "l"(pol)
-                 : "memory");
-}
-#else
-__device__ __forceinline__ uint64_t pol_evict_first() { return 0; }
-__device__ __forceinline__ float4 ld4_pol(const float *a, uint64_t) { return *reinterpret_cast<const float4 *>(a); }
-__device__ __forceinline__ uint32_t ld1_pol(const uint32_t *a, uint64_t) { return *a; }
-__device__ __forceinline__ void st4_pol(float *a, float4 v, uint64_t) { *reinterpret_cast<float4 *>(a) = v; }
-#endif
-
 // ------------------------------------------------------------------------------------------------
 // a2: stage-in.  llr [F][n] -> r, s [T][n][128] (s = r), init per-tile flags.
 // s is stored canonically (-0 -> +0; same slice and same sign() under reading A12), so that the later
@@ -189,12 +156,8 @@ __device__ __forceinline__ float flip31(float mag, uint32_t bit31) {
 }
 
 constexpr int CN_CHUNK = 8;  // edges per sign word and per batch of gathers (4 frames x 8 edges = 32 bits)
-constexpr int BN_CHUNK = 4;  // column edges per batch of row-state gathers
 #ifndef CN_MINB
 #define CN_MINB 2
-#endif
-#ifndef BN_MINB
-#define BN_MINB 3
 #endif
 #ifndef CN1_MINB
 #define CN1_MINB 3
@@ -514,9 +477,8 @@ __global__ void __launch_bounds__(CTA, DB ? 2 : CN1_MINB)
 
 // ------------------------------------------------------------------------------------------------
 // a5/a6: bit-node sweep of loop body k; stops frames whose b^(k-1) satisfied every check.
-// A warp owns columns j0 + warp + 8q; lane q holds edge q of the column ({row, position}, prefetched
-// one column ahead), and the row-state gathers of BN_CHUNK edges are all in flight before the
-// (ordered) sum.
+// One edge at a time with few registers and many warps (6 CTAs per SM): the loads of an edge depend
+// only on its broadcast record, and the warps of the SM keep enough of them in flight.
 // ------------------------------------------------------------------------------------------------
 template <typename LocT, bool EARLY>
 __global__ void __launch_bounds__(CTA, BNL_MINB)
@@ -596,392 +558,6 @@ __global__ void __launch_bounds__(CTA, BNL_MINB)
             if (mine & 2u) o[1] = acc[1] + rv.y;
             if (mine & 4u) o[2] = acc[2] + rv.z;
             if (mine & 8u) o[3] = acc[3] + rv.w;
-        }
-    }
-}
-
-// ------------------------------------------------------------------------------------------------
-// Software-pipelined bit-node sweep.  A warp's columns j0 + warp + 8q are cut into chunks of 3
-// edges; two chunk buffers in registers hold every load of a chunk (row state, sign word, r), and the
-// loads of the next chunk (same column or the next one) are in flight while the current one is
-// summed.  Lane q holds edge q ({row, position}) of the fetch column and the next two columns.
-// Loads are unconditional (edges past d_j read row 0), sums are over the real edges in ascending
-// row order (A14).
-// ------------------------------------------------------------------------------------------------
-constexpr int BC = 3;  // edges per chunk
-#ifndef BN_NS
-#define BN_NS 4
-#endif
-
-template <typename LocT>
-struct BnChunk {
-    float4 m0[BC], m1[BC];
-    typename LocOps<LocT>::W lc[BC];
-    uint32_t w[BC];
-    int p[BC];
-    float4 r;
-};
-
-template <typename LocT, bool EARLY>
-__global__ void __launch_bounds__(CTA, 2)
-    k_bn_pipe(Graph g, StreamState w, int k, int cols_per_cta, int literal, const int *kdev, int check_every) {
-    using LO = LocOps<LocT>;
-    if (kdev) k = *kdev;
-    (void)literal;
-    const int lane = threadIdx.x & 31;
-    const int T = w.T;
-    const int cnt = w.tcount[k & 1];
-    if ((int)blockIdx.y >= cnt) return;
-    const int t = w.tlist[(size_t)(k & 1) * T + blockIdx.y];
-    const int cblk = blockIdx.x;
-    uint4 act = make_uint4(FULL, FULL, FULL, FULL);
-    if (EARLY) {
-        // the syndrome of k_cn(k) tests b^(k-1); it may stop frames only at a check point (k-1) % T == 0
-        const bool check = ((k - 1) % check_every) == 0;
-        const uint4 ua = check ? ldu4(w.unsat + ((size_t)(k & 1) * T + t) * 4) : make_uint4(FULL, FULL, FULL, FULL);
-        const uint4 dw = ldu4(w.done + (size_t)t * 4);
-        const uint4 newly = make_uint4(~ua.x & ~dw.x, ~ua.y & ~dw.y, ~ua.z & ~dw.z, ~ua.w & ~dw.w);
-        act = make_uint4(ua.x & ~dw.x, ua.y & ~dw.y, ua.z & ~dw.z, ua.w & ~dw.w);
-        // every thread must read `done` before the tile's bookkeeping item rewrites it (other items of
-        // the tile may see either value: act is the same for both, since newly and ua are disjoint)
-        __syncthreads();
-        if (cblk == 0) {
-            const int tid = threadIdx.x;
-            if (tid < 4) {
-                w.done[(size_t)t * 4 + tid] = comp(dw, tid) | comp(newly, tid);
-                w.unsat[((size_t)((k + 1) & 1) * T + t) * 4 + tid] = 0;  // buffer of body k+1
-            }
-            if (tid < TILE && ((comp(newly, tid & 3) >> (tid >> 2)) & 1u))
-                w.iters[(size_t)t * TILE + tid] = k - 1;  // stopped after k-1 bodies
-            if (tid == 0 && (act.x | act.y | act.z | act.w)) {  // tile still runs in body k+1
-                const int pos = atomicAdd(w.tcount + ((k + 1) & 1), 1);
-                w.tlist[(size_t)((k + 1) & 1) * T + pos] = t;
-            }
-        }
-        if ((act.x | act.y | act.z | act.w) == 0) return;
-    } else if (cblk == 0 && threadIdx.x == 0) {
-        const int pos = atomicAdd(w.tcount + ((k + 1) & 1), 1);
-        w.tlist[(size_t)((k + 1) & 1) * T + pos] = t;
-    }
-    const unsigned mine = ((act.x >> lane) & 1u) | (((act.y >> lane) & 1u) << 1) | (((act.z >> lane) & 1u) << 2) |
-                          (((act.w >> lane) & 1u) << 3);
-    const int m = g.m, n = g.n, wr = g.wr;
-    const float *__restrict__ M0l = w.min0 + (size_t)t * m * TILE + 4 * lane;
-    const float *__restrict__ M1l = w.min1 + (size_t)t * m * TILE + 4 * lane;
-    const LocT *__restrict__ LCl = reinterpret_cast<const LocT *>(w.loc) + (size_t)t * m * TILE + 4 * lane;
-    const uint32_t *__restrict__ SGl = w.sgn + (size_t)t * m * wr * 32 + lane;
-    const float *__restrict__ Rl = w.r + (size_t)t * n * TILE + 4 * lane;
-    float *__restrict__ Sl = w.s + (size_t)t * n * TILE + 4 * lane;
-    const int warp = threadIdx.x >> 5;
-    const int j0 = cblk * cols_per_cta + warp, j1 = min(n, cblk * cols_per_cta + cols_per_cta);
-    const int nc = j0 < j1 ? (j1 - j0 + 7) / 8 : 0;  // columns of this warp (<= 32)
-    if (nc == 0) return;
-    int ca = 0, cb = 0;
-    if (lane < nc) {
-        ca = __ldg(g.col_ptr + j0 + 8 * lane);
-        cb = __ldg(g.col_ptr + j0 + 8 * lane + 1);
-    }
-    auto deg_of = [&](int q) { return q < nc ? __shfl_sync(FULL, cb, q & 31) - __shfl_sync(FULL, ca, q & 31) : 0; };
-    auto col_of = [&](int q) { return j0 + 8 * min(q, nc - 1); };
-    auto list_of = [&](int q, int &ei, int &ep) {  // lane e: {row, position} of edge e of column q
-        const int c0 = __shfl_sync(FULL, ca, q & 31), dv = __shfl_sync(FULL, cb, q & 31) - c0;
-        ei = 0;
-        ep = 0;
-        if (q < nc && lane < dv) {
-            const int4 ed = __ldg(g.bn_edge + c0 + lane);
-            ei = ed.y;
-            ep = ed.z;
-        }
-    };
-    auto fetch = [&](BnChunk<LocT> &B, int q, int c, int ei, int ep) {
-#pragma unroll
-        for (int u = 0; u < BC; u++) {
-            const int i = __shfl_sync(FULL, ei, (BC * c + u) & 31);
-            const int pp = __shfl_sync(FULL, ep, (BC * c + u) & 31);
-            const size_t ro = (size_t)i * TILE;
-            B.m0[u] = ld4(M0l + ro);
-            B.m1[u] = ld4(M1l + ro);
-            B.lc[u] = LO::load(LCl + ro);
-            B.w[u] = SGl[((size_t)i * wr + (pp >> 3)) * 32];
-            B.p[u] = pp;
-        }
-        B.r = ld4(Rl + (size_t)col_of(q) * TILE);
-    };
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    auto compute = [&](const BnChunk<LocT> &B, int q, int c) {
-        const int dv = deg_of(q);
-#pragma unroll
-        for (int u = 0; u < BC; u++) {
-            if (BC * c + u < dv) {
-                const typename LO::W key = LO::key(B.lc[u], B.p[u]);
-                const uint32_t ws = B.w[u] << (28 - 4 * (B.p[u] & 7));  // bit 4(p%8)+v -> bit 28+v
-#pragma unroll
-                for (int v = 0; v < 4; v++) {
-                    const float mag = LO::hit(key, v) ? comp(B.m1[u], v) : comp(B.m0[u], v);  // Obs. 1
-                    acc[v] = acc[v] + flip31(mag, ws << (3 - v));  // ascending rows from +0.0 (A14)
-                }
-            }
-        }
-        if (BC * (c + 1) >= dv) {  // last chunk of column q: s_j = sum + r_j (frozen frames keep s)
-            float4 out = make_float4(acc[0] + B.r.x, acc[1] + B.r.y, acc[2] + B.r.z, acc[3] + B.r.w);
-            float *sp = Sl + (size_t)col_of(q) * TILE;
-            if (mine == 0xFu) {
-                st4(sp, out);
-            } else if (mine) {
-                const float4 old = ld4(sp);
-                out.x = (mine & 1u) ? out.x : old.x;
-                out.y = (mine & 2u) ? out.y : old.y;
-                out.z = (mine & 4u) ? out.z : old.z;
-                out.w = (mine & 8u) ? out.w : old.w;
-                st4(sp, out);
-            }
-            acc[0] = acc[1] = acc[2] = acc[3] = 0.f;
-        }
-    };
-    // fetch cursor (fq, fc) with the edge lists of columns fq, fq+1, fq+2; compute cursor (cq, cc)
-    int e0i, e0p, e1i, e1p, e2i, e2p;
-    list_of(0, e0i, e0p);
-    list_of(1, e1i, e1p);
-    list_of(2, e2i, e2p);
-    int fq = 0, fc = 0, cq = 0, cc = 0;
-    auto advance_fetch = [&]() {
-        if (BC * (fc + 1) < deg_of(fq)) {
-            fc++;
-        } else {
-            fq++;
-            fc = 0;
-            e0i = e1i; e0p = e1p;
-            e1i = e2i; e1p = e2p;
-            list_of(fq + 2, e2i, e2p);
-        }
-    };
-    auto advance_compute = [&]() {
-        if (BC * (cc + 1) < deg_of(cq)) {
-            cc++;
-        } else {
-            cq++;
-            cc = 0;
-        }
-    };
-    BnChunk<LocT> A, B;
-    fetch(A, fq, fc, e0i, e0p);
-    advance_fetch();
-    while (true) {
-        fetch(B, fq, fc, e0i, e0p);
-        advance_fetch();
-        compute(A, cq, cc);
-        advance_compute();
-        if (cq >= nc) break;
-        fetch(A, fq, fc, e0i, e0p);
-        advance_fetch();
-        compute(B, cq, cc);
-        advance_compute();
-        if (cq >= nc) break;
-    }
-}
-
-// ------------------------------------------------------------------------------------------------
-// Bit-node sweep with a per-warp cp.async ring in shared memory.  The bit node has little arithmetic
-// per edge (3 ALU ops per frame-edge), so its speed is the number of bytes in flight; registers cannot
-// hold enough of them.  Each warp owns a contiguous run of columns, i.e. a contiguous run of edges in
-// column order, and streams them through a ring of NS slots: lane l copies ITS OWN 16/16/4/4 bytes
-// of the edge's row state (min0, min1, loc, sign word) -- plus r_j with the column's last edge -- with
-// cp.async, and later reads back only those bytes, so no barrier or warp sync is needed (per-thread
-// cp.async groups).  NS - 1 edges are always in flight per warp.  Frozen frames are skipped with
-// per-component stores instead of a read-modify-write of s.
-// ------------------------------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void cp16(uint32_t dst, const void *src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp4(uint32_t dst, const void *src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp8(uint32_t dst, const void *src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp16_pol(uint32_t dst, const void *src, uint64_t pol) {
-#ifndef LDPC_NO_L2_HINTS
-    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "l"(pol) : "memory");
-#else
-    (void)pol;
-    cp16(dst, src);
-#endif
-}
-__device__ __forceinline__ uint64_t pol_gather() {
-#if defined(BN_GATHER_EVICT_LAST)
-    uint64_t p;
-    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-    return p;
-#else
-    return 0;
-#endif
-}
-__device__ __forceinline__ void cp16_g(uint32_t dst, const void *src, uint64_t pol) {
-#if defined(BN_GATHER_EVICT_LAST)
-    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "l"(pol) : "memory");
-#else
-    (void)pol;
-    cp16(dst, src);
-#endif
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-constexpr int BA_SLOT = 32 * (16 + 16 + 8 + 4 + 16);  // m0, m1, loc (<= 8 B), sign word, r per lane
-
-template <typename LocT>
-__device__ __forceinline__ void cp_loc(uint32_t dst, const LocT *src) {
-    if (sizeof(LocT) == 1) cp4(dst, src);
-    else cp8(dst, src);
-}
-
-template <typename LocT, bool EARLY, int NS>
-__global__ void __launch_bounds__(CTA, 1)
-    k_bn_async(Graph g, StreamState w, int k, int cols_per_cta, int literal, const int *kdev, int check_every) {
-    using LO = LocOps<LocT>;
-    extern __shared__ __align__(16) unsigned char bsm[];
-    if (kdev) k = *kdev;
-    (void)literal;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int T = w.T;
-    const int cnt = w.tcount[k & 1];
-    if ((int)blockIdx.y >= cnt) return;
-    const int t = w.tlist[(size_t)(k & 1) * T + blockIdx.y];
-    const int cblk = blockIdx.x;
-    uint4 act = make_uint4(FULL, FULL, FULL, FULL);
-    if (EARLY) {
-        // the syndrome of k_cn(k) tests b^(k-1); it may stop frames only at a check point (k-1) % T == 0
-        const bool check = ((k - 1) % check_every) == 0;
-        const uint4 ua = check ? ldu4(w.unsat + ((size_t)(k & 1) * T + t) * 4) : make_uint4(FULL, FULL, FULL, FULL);
-        const uint4 dw = ldu4(w.done + (size_t)t * 4);
-        const uint4 newly = make_uint4(~ua.x & ~dw.x, ~ua.y & ~dw.y, ~ua.z & ~dw.z, ~ua.w & ~dw.w);
-        act = make_uint4(ua.x & ~dw.x, ua.y & ~dw.y, ua.z & ~dw.z, ua.w & ~dw.w);
-        __syncthreads();
-        if (cblk == 0) {
-            const int tid = threadIdx.x;
-            if (tid < 4) {
-                w.done[(size_t)t * 4 + tid] = comp(dw, tid) | comp(newly, tid);
-                w.unsat[((size_t)((k + 1) & 1) * T + t) * 4 + tid] = 0;  // buffer of body k+1
-            }
-            if (tid < TILE && ((comp(newly, tid & 3) >> (tid >> 2)) & 1u))
-                w.iters[(size_t)t * TILE + tid] = k - 1;  // stopped after k-1 bodies
-            if (tid == 0 && (act.x | act.y | act.z | act.w)) {  // tile still runs in body k+1
-                const int pos = atomicAdd(w.tcount + ((k + 1) & 1), 1);
-                w.tlist[(size_t)((k + 1) & 1) * T + pos] = t;
-            }
-        }
-        if ((act.x | act.y | act.z | act.w) == 0) return;
-    } else if (cblk == 0 && threadIdx.x == 0) {
-        const int pos = atomicAdd(w.tcount + ((k + 1) & 1), 1);
-        w.tlist[(size_t)((k + 1) & 1) * T + pos] = t;
-    }
-    const unsigned mine = ((act.x >> lane) & 1u) | (((act.y >> lane) & 1u) << 1) | (((act.z >> lane) & 1u) << 2) |
-                          (((act.w >> lane) & 1u) << 3);
-    const int m = g.m, n = g.n, wr = g.wr;
-    const float *M0l = w.min0 + (size_t)t * m * TILE + 4 * lane;
-    const float *M1l = w.min1 + (size_t)t * m * TILE + 4 * lane;
-    const LocT *LCl = reinterpret_cast<const LocT *>(w.loc) + (size_t)t * m * TILE + 4 * lane;
-    const uint32_t *SGl = w.sgn + (size_t)t * m * wr * 32 + lane;
-    const float *Rl = w.r + (size_t)t * n * TILE + 4 * lane;
-    float *Sl = w.s + (size_t)t * n * TILE + 4 * lane;
-    // this warp's columns [ja, jb) and edges [ea, eb) (contiguous in column order)
-    const int cpw = (cols_per_cta + 7) / 8;
-    // the CTA's edge records {row, position} in shared memory (one coalesced pass)
-    int2 *rec = reinterpret_cast<int2 *>(bsm + (size_t)(CTA / 32) * NS * BA_SLOT);
-    const int cja = min(n, cblk * cols_per_cta), cjb = min(n, cblk * cols_per_cta + cols_per_cta);
-    const int cea = __ldg(g.col_ptr + cja), ceb = __ldg(g.col_ptr + cjb);
-    for (int q = threadIdx.x; q < ceb - cea; q += CTA) {
-        const int4 ed = __ldg(g.bn_edge + cea + q);
-        rec[q] = make_int2(ed.y, ed.z);
-    }
-    __syncthreads();
-    const int ja = min(n, cblk * cols_per_cta + warp * cpw), jb = min(cjb, ja + cpw);
-    if (ja >= jb) return;
-    int cpl = 0;  // lane q: col_ptr[ja + q] (q <= jb - ja <= 31)
-    if (lane <= jb - ja) cpl = __ldg(g.col_ptr + ja + lane);
-    const int ea = __shfl_sync(FULL, cpl, 0), eb = __shfl_sync(FULL, cpl, (jb - ja) & 31);
-    const int ne = eb - ea;
-    const uint64_t pol = pol_evict_first(), gpol = pol_gather();
-    unsigned char *ring = bsm + (size_t)warp * NS * BA_SLOT;
-    const uint32_t ring_s = smem_u32(ring);
-    // producer: issue the copies of edge number te (column cursor pj / its end pe)
-    int pj = 0, pe = __shfl_sync(FULL, cpl, 1);
-    auto issue = [&](int te) {
-        if (te < ne) {
-            const int e = ea + te;
-            while (e >= pe) {  // advance the producer's column cursor (warp-uniform)
-                pj++;
-                pe = __shfl_sync(FULL, cpl, (pj + 1) & 31);
-            }
-            const int2 ed = rec[e - cea];  // {i, p}
-            const size_t ro = (size_t)ed.x * TILE;
-            const uint32_t sl = ring_s + (uint32_t)((te % NS) * BA_SLOT);
-            cp16_g(sl + lane * 16, M0l + ro, gpol);
-            cp16_g(sl + 512 + lane * 16, M1l + ro, gpol);
-            cp_loc<LocT>(sl + 1024 + lane * 8, LCl + ro);
-            cp4(sl + 1280 + lane * 4, SGl + ((size_t)ed.x * wr + (ed.y >> 3)) * 32);
-            if (e + 1 == pe) cp16_pol(sl + 1408 + lane * 16, Rl + (size_t)(ja + pj) * TILE, pol);  // r_j, last edge
-        }
-        cp_commit();
-    };
-#pragma unroll 1
-    for (int te = 0; te < NS - 1; te++) issue(te);
-    const int nq = jb - ja;
-    int cj = 0;
-    while (cj < nq && __shfl_sync(FULL, cpl, (cj + 1) & 31) == __shfl_sync(FULL, cpl, cj)) cj++;  // first non-empty
-    int ce = __shfl_sync(FULL, cpl, (cj + 1) & 31);
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 1
-    for (int te = 0; te < ne; te++) {
-        cp_wait<NS - 2>();  // edge te has landed (this lane's copies)
-        const int e = ea + te;
-        const int pos = rec[e - cea].y;
-        const unsigned char *sp = ring + (te % NS) * BA_SLOT;
-        const float4 m0 = *reinterpret_cast<const float4 *>(sp + lane * 16);
-        const float4 m1 = *reinterpret_cast<const float4 *>(sp + 512 + lane * 16);
-        const typename LO::W lc = *reinterpret_cast<const typename LO::W *>(sp + 1024 + lane * 8);
-        const uint32_t wd = *reinterpret_cast<const uint32_t *>(sp + 1280 + lane * 4);
-        const typename LO::W key = LO::key(lc, pos);
-        const uint32_t ws = wd << (28 - 4 * (pos & 7));  // bit 4(p%8)+v -> bit 28+v
-#pragma unroll
-        for (int v = 0; v < 4; v++) {
-            const float mag = LO::hit(key, v) ? comp(m1, v) : comp(m0, v);  // Obs. 1
-            acc[v] = acc[v] + flip31(mag, ws << (3 - v));                   // ascending rows from +0.0 (A14)
-        }
-        if (e + 1 == ce) {  // last edge of column ja + cj: s_j = sum + r_j
-            const float4 rv = *reinterpret_cast<const float4 *>(sp + 1408 + lane * 16);
-            float *o = Sl + (size_t)(ja + cj) * TILE;
-            if (mine == 0xFu) {
-                st4_pol(o, make_float4(acc[0] + rv.x, acc[1] + rv.y, acc[2] + rv.z, acc[3] + rv.w), pol);
-            } else if (mine) {  // frozen frames keep their s
-                if (mine & 1u) o[0] = acc[0] + rv.x;
-                if (mine & 2u) o[1] = acc[1] + rv.y;
-                if (mine & 4u) o[2] = acc[2] + rv.z;
-                if (mine & 8u) o[3] = acc[3] + rv.w;
-            }
-            acc[0] = acc[1] = acc[2] = acc[3] = 0.f;
-            do {  // next column with an edge (columns of degree 0 are written below)
-                cj++;
-                ce = __shfl_sync(FULL, cpl, (cj + 1) & 31);
-            } while (cj < nq && ce == e + 1);
-        }
-        issue(te + NS - 1);  // refills the slot just read (its values are consumed above)
-    }
-    cp_wait<0>();
-    // columns of degree 0 (no edge): s_j = r_j
-    for (int q = 0; q < jb - ja; q++) {
-        const int c0 = __shfl_sync(FULL, cpl, q), c1 = __shfl_sync(FULL, cpl, (q + 1) & 31);
-        if (c0 == c1) {
-            const float4 rv = ld4(Rl + (size_t)(ja + q) * TILE);
-            float *o = Sl + (size_t)(ja + q) * TILE;
-            if (mine & 1u) o[0] = 0.f + rv.x;
-            if (mine & 2u) o[1] = 0.f + rv.y;
-            if (mine & 4u) o[2] = 0.f + rv.z;
-            if (mine & 8u) o[3] = 0.f + rv.w;
         }
     }
 }
@@ -1152,31 +728,13 @@ void cn_launch(dim3 grid, cudaStream_t st, const Graph &g, const StreamState &w,
     else k_cn<LT, F, EA><<<grid, CTA, 0, st>>>(g, w, k, rpc, lit, kdev);
 }
 
-// columns per CTA of the cp.async bit node (<= 248: a warp owns <= 31 columns); LDPC_BN_COLS overrides
-inline int bn_async_cols(int n) {
-    (void)n;
-    const char *e = getenv("LDPC_BN_COLS");
-    const int x = e ? atoi(e) : 248;
-    return std::max(8, std::min(248, (x + 7) & ~7));
-}
-
 template <typename LT, bool EA>
 void bn_launch(dim3 grid, cudaStream_t st, const Graph &g, const StreamState &w, int k, int cpc, int lit, int u,
                const int *kdev, int te) {
-    // u: 0 / 1 = one edge at a time, many warps (default; best on C3, equal on C4), 2 = register-
-    //    pipelined chunks, 3 = cp.async ring
-    if (u == 3) {  // cp.async ring: 248 columns per CTA, 31 per warp
-        constexpr int NS = BN_NS;
-        const size_t smem = (size_t)(CTA / 32) * NS * BA_SLOT + (size_t)bn_async_cols(g.n) * g.dvmax * 8;
-        cudaFuncSetAttribute(k_bn_async<LT, EA, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        const int cols = bn_async_cols(g.n);
-        const dim3 gr = grid2((g.n + cols - 1) / cols, w.T);
-        k_bn_async<LT, EA, NS><<<gr, CTA, smem, st>>>(g, w, k, cols, lit, kdev, te);
-    } else if (u == 2 && g.dvmax <= 32) {
-        k_bn_pipe<LT, EA><<<grid, CTA, 0, st>>>(g, w, k, cpc, lit, kdev, te);
-    } else {
-        k_bn<LT, EA><<<grid2((g.n + BNL_COLS - 1) / BNL_COLS, w.T), CTA, 0, st>>>(g, w, k, BNL_COLS, lit, kdev, te);
-    }
+    (void)grid;
+    (void)cpc;
+    (void)u;
+    k_bn<LT, EA><<<grid2((g.n + BNL_COLS - 1) / BNL_COLS, w.T), CTA, 0, st>>>(g, w, k, BNL_COLS, lit, kdev, te);
 }
 
 int launch_check_node(const Graph &g, const StreamState &w, int k, bool first, bool early, bool literal, bool loc16,
