@@ -198,10 +198,13 @@ __global__ void __launch_bounds__(CTA, CN_MINB)
     }
     const int m = g.m, n = g.n, wr = g.wr;
     const float *__restrict__ Sl = w.s + (size_t)t * n * TILE + 4 * lane;
-    uint32_t *__restrict__ SGl = w.sgn + (size_t)t * m * wr * 32 + lane;
-    float *__restrict__ M0l = w.min0 + (size_t)t * m * TILE + 4 * lane;
-    float *__restrict__ M1l = w.min1 + (size_t)t * m * TILE + 4 * lane;
-    LocT *__restrict__ LCl = reinterpret_cast<LocT *>(w.loc) + (size_t)t * m * TILE + 4 * lane;
+    // the tile's row records: [min0 512 B][min1 512 B][loc 128 x sizeof(LocT)][sign words 128 x wr]
+    unsigned char *RB = w.rst + (size_t)t * m * w.rs;
+    const size_t RSW = (size_t)w.rs / 4, RSL = (size_t)w.rs / sizeof(LocT);  // row strides
+    float *__restrict__ M0l = reinterpret_cast<float *>(RB) + 4 * lane;
+    float *__restrict__ M1l = reinterpret_cast<float *>(RB) + 128 + 4 * lane;
+    LocT *__restrict__ LCl = reinterpret_cast<LocT *>(RB + 1024) + 4 * lane;
+    uint32_t *__restrict__ SGl = reinterpret_cast<uint32_t *>(RB + 1024 + 128 * sizeof(LocT)) + lane;
     const float INF = __int_as_float(0x7f800000);
     const int i0 = blockIdx.x * rows_per_cta + warp, i1 = min(m, blockIdx.x * rows_per_cta + rows_per_cta);
     const int nr = i0 < i1 ? (i1 - i0 + 7) / 8 : 0;  // rows of this warp (<= 32)
@@ -220,17 +223,17 @@ __global__ void __launch_bounds__(CTA, CN_MINB)
         float om0[4] = {0.f, 0.f, 0.f, 0.f}, om1[4] = {0.f, 0.f, 0.f, 0.f};
         typename LO::W olc{};
         if (!FIRST) {
-            const float4 A = ld4(M0l + (size_t)i * TILE), B = ld4(M1l + (size_t)i * TILE);
+            const float4 A = ld4(M0l + (size_t)i * RSW), B = ld4(M1l + (size_t)i * RSW);
             om0[0] = A.x; om0[1] = A.y; om0[2] = A.z; om0[3] = A.w;
             om1[0] = B.x; om1[1] = B.y; om1[2] = B.z; om1[3] = B.w;
-            olc = LO::load(LCl + (size_t)i * TILE);
+            olc = LO::load(LCl + (size_t)i * RSL);
         }
         float nm0[4] = {INF, INF, INF, INF}, nm1[4] = {INF, INF, INF, INF};
         int nloc[4] = {0, 0, 0, 0};
         uint32_t par[4] = {0u, 0u, 0u, 0u}, syn[4] = {0u, 0u, 0u, 0u};
         for (int p0 = 0; p0 < d; p0 += CN_CHUNK) {
             if (p0 > 0 && (p0 & 31) == 0) cj = (lane < d - p0) ? __ldg(g.col_idx + a + p0 + lane) : 0;
-            uint32_t *sgp = SGl + ((size_t)i * wr + (p0 >> 3)) * 32;
+            uint32_t *sgp = SGl + (size_t)i * RSW + (p0 >> 3) * 32;
             float4 sv[CN_CHUNK];
 #pragma unroll
             for (int u = 0; u < CN_CHUNK; u++) {
@@ -290,9 +293,9 @@ __global__ void __launch_bounds__(CTA, CN_MINB)
             o1 = make_float4(__uint_as_float(__float_as_uint(nm1[0]) | s0), __uint_as_float(__float_as_uint(nm1[1]) | s1),
                              __uint_as_float(__float_as_uint(nm1[2]) | s2), __uint_as_float(__float_as_uint(nm1[3]) | s3));
         }
-        st4(M0l + (size_t)i * TILE, o0);
-        st4(M1l + (size_t)i * TILE, o1);
-        LO::store(LCl + (size_t)i * TILE, nloc);
+        st4(M0l + (size_t)i * RSW, o0);
+        st4(M1l + (size_t)i * RSW, o1);
+        LO::store(LCl + (size_t)i * RSL, nloc);
         if (EARLY) {
             const uint32_t dp = (uint32_t)(d & 1);  // XOR_j b_j = d_i mod 2 xor XOR_j (1 - b_j)
             u0 |= __ballot_sync(FULL, ((syn[0] >> 31) ^ dp) != 0u);
@@ -335,12 +338,13 @@ struct CnRow {
 template <int CH, typename LocT, bool FIRST>
 __device__ __forceinline__ void cn_fetch(CnRow<CH, LocT> &R, int cj, int i, const float *__restrict__ Sl,
                                          const uint32_t *__restrict__ SGl, const float *__restrict__ M0l,
-                                         const float *__restrict__ M1l, const LocT *__restrict__ LCl) {
+                                         const float *__restrict__ M1l, const LocT *__restrict__ LCl, size_t RSW,
+                                         size_t RSL) {
     if (!FIRST) {
-        R.wold = SGl[(size_t)i * 32];
-        R.m0 = ld4(M0l + (size_t)i * TILE);
-        R.m1 = ld4(M1l + (size_t)i * TILE);
-        R.lc = LocOps<LocT>::load(LCl + (size_t)i * TILE);
+        R.wold = SGl[(size_t)i * RSW];
+        R.m0 = ld4(M0l + (size_t)i * RSW);
+        R.m1 = ld4(M1l + (size_t)i * RSW);
+        R.lc = LocOps<LocT>::load(LCl + (size_t)i * RSL);
     }
 #pragma unroll
     for (int u = 0; u < CH; u++) {
@@ -352,7 +356,8 @@ __device__ __forceinline__ void cn_fetch(CnRow<CH, LocT> &R, int cj, int i, cons
 template <int CH, typename LocT, bool FIRST, bool EARLY>
 __device__ __forceinline__ void cn_compute(const CnRow<CH, LocT> &R, int i, int d, int literal,
                                            uint32_t *__restrict__ SGl, float *__restrict__ M0l,
-                                           float *__restrict__ M1l, LocT *__restrict__ LCl, uint32_t (&u)[4]) {
+                                           float *__restrict__ M1l, LocT *__restrict__ LCl, size_t RSW, size_t RSL,
+                                           uint32_t (&u)[4]) {
     using LO = LocOps<LocT>;
     const float INF = __int_as_float(0x7f800000);
     const uint32_t corr = (uint32_t)(d & 1) & (uint32_t)(!literal);  // (-1)^{d_i}, reading A1
@@ -383,7 +388,7 @@ __device__ __forceinline__ void cn_compute(const CnRow<CH, LocT> &R, int i, int 
             }
         }
     }
-    SGl[(size_t)i * 32] = wnew;
+    SGl[(size_t)i * RSW] = wnew;
     // sign parity per frame (Obs. 2): XOR of bits v, v+4, ..., of the new sign word, times (-1)^{d_i}
     uint32_t pw = wnew ^ (wnew >> 16);
     pw ^= pw >> 8;
@@ -391,13 +396,13 @@ __device__ __forceinline__ void cn_compute(const CnRow<CH, LocT> &R, int i, int 
     pw ^= corr ? 0xfu : 0u;
     const uint32_t s0 = pw << 31, s1 = (pw << 30) & 0x80000000u, s2 = (pw << 29) & 0x80000000u,
                    s3 = (pw << 28) & 0x80000000u;
-    st4(M0l + (size_t)i * TILE,
+    st4(M0l + (size_t)i * RSW,
         make_float4(__uint_as_float(__float_as_uint(nm0[0]) | s0), __uint_as_float(__float_as_uint(nm0[1]) | s1),
                     __uint_as_float(__float_as_uint(nm0[2]) | s2), __uint_as_float(__float_as_uint(nm0[3]) | s3)));
-    st4(M1l + (size_t)i * TILE,
+    st4(M1l + (size_t)i * RSW,
         make_float4(__uint_as_float(__float_as_uint(nm1[0]) | s0), __uint_as_float(__float_as_uint(nm1[1]) | s1),
                     __uint_as_float(__float_as_uint(nm1[2]) | s2), __uint_as_float(__float_as_uint(nm1[3]) | s3)));
-    LO::store(LCl + (size_t)i * TILE, nloc);
+    LO::store(LCl + (size_t)i * RSL, nloc);
     if (EARLY) {
         const uint32_t dp = (uint32_t)(d & 1);  // XOR_j b_j = d_i mod 2 xor XOR_j (1 - b_j)
 #pragma unroll
@@ -421,10 +426,13 @@ __global__ void __launch_bounds__(CTA, DB ? 2 : CN1_MINB)
     }
     const int m = g.m, n = g.n;
     const float *__restrict__ Sl = w.s + (size_t)t * n * TILE + 4 * lane;
-    uint32_t *__restrict__ SGl = w.sgn + (size_t)t * m * 32 + lane;  // wr == 1
-    float *__restrict__ M0l = w.min0 + (size_t)t * m * TILE + 4 * lane;
-    float *__restrict__ M1l = w.min1 + (size_t)t * m * TILE + 4 * lane;
-    LocT *__restrict__ LCl = reinterpret_cast<LocT *>(w.loc) + (size_t)t * m * TILE + 4 * lane;
+    // the tile's row records: [min0 512 B][min1 512 B][loc 128 x sizeof(LocT)][sign words 128 x wr]
+    unsigned char *RB = w.rst + (size_t)t * m * w.rs;
+    const size_t RSW = (size_t)w.rs / 4, RSL = (size_t)w.rs / sizeof(LocT);  // row strides
+    float *__restrict__ M0l = reinterpret_cast<float *>(RB) + 4 * lane;
+    float *__restrict__ M1l = reinterpret_cast<float *>(RB) + 128 + 4 * lane;
+    LocT *__restrict__ LCl = reinterpret_cast<LocT *>(RB + 1024) + 4 * lane;
+    uint32_t *__restrict__ SGl = reinterpret_cast<uint32_t *>(RB + 1024 + 128 * sizeof(LocT)) + lane;
     const int i0 = blockIdx.x * rows_per_cta + warp, i1 = min(m, blockIdx.x * rows_per_cta + rows_per_cta);
     const int nr = i0 < i1 ? (i1 - i0 + 7) / 8 : 0;  // rows of this warp (<= 32)
     if (nr == 0) return;
@@ -444,23 +452,23 @@ __global__ void __launch_bounds__(CTA, DB ? 2 : CN1_MINB)
         CnRow<CH, LocT> A;
         int cj = cols_of(0);
         for (int q = 0; q < nr; q++) {
-            cn_fetch<CH, LocT, FIRST>(A, cj, row_of(q), Sl, SGl, M0l, M1l, LCl);
+            cn_fetch<CH, LocT, FIRST>(A, cj, row_of(q), Sl, SGl, M0l, M1l, LCl, RSW, RSL);
             cj = cols_of(q + 1);
-            cn_compute<CH, LocT, FIRST, EARLY>(A, row_of(q), deg_of(q), literal, SGl, M0l, M1l, LCl, u);
+            cn_compute<CH, LocT, FIRST, EARLY>(A, row_of(q), deg_of(q), literal, SGl, M0l, M1l, LCl, RSW, RSL, u);
         }
     } else {
     CnRow<CH, LocT> A, B;
     int cjA = cols_of(0), cjB = cols_of(1);
-    cn_fetch<CH, LocT, FIRST>(A, cjA, row_of(0), Sl, SGl, M0l, M1l, LCl);
+    cn_fetch<CH, LocT, FIRST>(A, cjA, row_of(0), Sl, SGl, M0l, M1l, LCl, RSW, RSL);
     cjA = cols_of(2);
     for (int q = 0; q < nr; q += 2) {
-        cn_fetch<CH, LocT, FIRST>(B, cjB, row_of(q + 1), Sl, SGl, M0l, M1l, LCl);
+        cn_fetch<CH, LocT, FIRST>(B, cjB, row_of(q + 1), Sl, SGl, M0l, M1l, LCl, RSW, RSL);
         cjB = cols_of(q + 3);
-        cn_compute<CH, LocT, FIRST, EARLY>(A, row_of(q), deg_of(q), literal, SGl, M0l, M1l, LCl, u);
+        cn_compute<CH, LocT, FIRST, EARLY>(A, row_of(q), deg_of(q), literal, SGl, M0l, M1l, LCl, RSW, RSL, u);
         if (q + 1 >= nr) break;
-        cn_fetch<CH, LocT, FIRST>(A, cjA, row_of(q + 2), Sl, SGl, M0l, M1l, LCl);
+        cn_fetch<CH, LocT, FIRST>(A, cjA, row_of(q + 2), Sl, SGl, M0l, M1l, LCl, RSW, RSL);
         cjA = cols_of(q + 4);
-        cn_compute<CH, LocT, FIRST, EARLY>(B, row_of(q + 1), deg_of(q + 1), literal, SGl, M0l, M1l, LCl, u);
+        cn_compute<CH, LocT, FIRST, EARLY>(B, row_of(q + 1), deg_of(q + 1), literal, SGl, M0l, M1l, LCl, RSW, RSL, u);
     }
     }
     if (EARLY) {
@@ -524,10 +532,13 @@ __global__ void __launch_bounds__(CTA, BNL_MINB)
     const unsigned mine = ((act.x >> lane) & 1u) | (((act.y >> lane) & 1u) << 1) | (((act.z >> lane) & 1u) << 2) |
                           (((act.w >> lane) & 1u) << 3);
     const int m = g.m, n = g.n, wr = g.wr;
-    const float *__restrict__ M0l = w.min0 + (size_t)t * m * TILE + 4 * lane;
-    const float *__restrict__ M1l = w.min1 + (size_t)t * m * TILE + 4 * lane;
-    const LocT *__restrict__ LCl = reinterpret_cast<const LocT *>(w.loc) + (size_t)t * m * TILE + 4 * lane;
-    const uint32_t *__restrict__ SGl = w.sgn + (size_t)t * m * wr * 32 + lane;
+    // the tile's row records: [min0 512 B][min1 512 B][loc 128 x sizeof(LocT)][sign words 128 x wr]
+    unsigned char *RB = w.rst + (size_t)t * m * w.rs;
+    const size_t RSW = (size_t)w.rs / 4, RSL = (size_t)w.rs / sizeof(LocT);  // row strides
+    const float *__restrict__ M0l = reinterpret_cast<float *>(RB) + 4 * lane;
+    const float *__restrict__ M1l = reinterpret_cast<float *>(RB) + 128 + 4 * lane;
+    const LocT *__restrict__ LCl = reinterpret_cast<LocT *>(RB + 1024) + 4 * lane;
+    const uint32_t *__restrict__ SGl = reinterpret_cast<uint32_t *>(RB + 1024 + 128 * sizeof(LocT)) + lane;
     const float *__restrict__ Rl = w.r + (size_t)t * n * TILE + 4 * lane;
     float *__restrict__ Sl = w.s + (size_t)t * n * TILE + 4 * lane;
     const int warp = threadIdx.x >> 5;
@@ -540,10 +551,10 @@ __global__ void __launch_bounds__(CTA, BNL_MINB)
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
         for (int q = 0; q < dv; q++) {
             const int4 ed = __ldg(g.bn_edge + c0 + q);  // {e, i, p, -}, ascending i
-            const size_t ro = (size_t)ed.y * TILE;
+            const size_t ro = (size_t)ed.y * RSW;  // row record of row i
             const float4 m0 = ld4(M0l + ro), m1 = ld4(M1l + ro);
-            const typename LO::W key = LO::key(LO::load(LCl + ro), ed.z);
-            const uint32_t ws = SGl[((size_t)ed.y * wr + (ed.z >> 3)) * 32] << (28 - 4 * (ed.z & 7));
+            const typename LO::W key = LO::key(LO::load(LCl + (size_t)ed.y * RSL), ed.z);
+            const uint32_t ws = SGl[ro + (ed.z >> 3) * 32] << (28 - 4 * (ed.z & 7));
 #pragma unroll
             for (int v = 0; v < 4; v++) {
                 const float mag = LO::hit(key, v) ? comp(m1, v) : comp(m0, v);  // Obs. 1

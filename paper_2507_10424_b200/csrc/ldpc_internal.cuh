@@ -30,20 +30,23 @@ struct Graph {
 
 // Per-chunk decode state of the streaming schedule, frame-interleaved in tiles of 128:
 //   r, s   [T][n][128] fp32          channel values and current soft vector (Eq. sCalculation)
-//   min0   [T][m][128] fp32          |lambda| minimum of the row; SIGN BIT = row sign parity (Obs. 2)
-//   min1   [T][m][128] fp32          second minimum (Obs. 1); same sign bit as min0
-//   loc    [T][m][128] u8 / u16      min0Location as the position inside N_i
-//   sgn    [T][m][wr][32] u32        sign bits of lambda_e, row-transposed: word (i, p/8, lane l) holds bit
-//                                    4*(p%8) + v = sign for edge p of row i, frame 4l+v (one coalesced word per lane)
+//   rst    [T][m] row records of rs bytes: the check-node state of row i for the tile's 128 frames,
+//          contiguous so that a gather of one row touches one DRAM page:
+//            min0 [128] fp32   |lambda| minimum of the row; SIGN BIT = row sign parity (Obs. 2)
+//            min1 [128] fp32   second minimum (Obs. 1); same sign bit as min0
+//            loc  [128] u8/u16 min0Location as the position inside N_i
+//            sgn  [wr][32] u32 sign bits of lambda_e, row-transposed: word (p/8, lane l) holds bit
+//                              4*(p%8) + v = sign for edge p of the row, frame 4l+v
 //   unsat  [2][T][4]   u32           per-frame "some check unsatisfied" bits (double-buffered by iteration)
 //   done   [T][4]      u32           per-frame "stopped" bits
 //   iters  [T*128]     i32           k at which a frame stopped (early stop)
 //   fbe/fraw/fnz [T*128] i32         per-frame bit errors, raw errors, near-zero flag
 struct StreamState {
     int T;
-    float *r, *s, *min0, *min1;
-    void *loc;
-    uint32_t *sgn, *unsat, *done;
+    float *r, *s;
+    unsigned char *rst;  // row records
+    int rs;              // bytes per row record: 1024 + 128 sizeof(loc) + 128 wr
+    uint32_t *unsat, *done;
     int *iters, *fbe, *fraw, *fnz;
     int *tcount;  // [2]     number of tiles with a running frame, per body parity
     int *tlist;   // [2][T]  those tiles

@@ -97,13 +97,15 @@ void launch(ldpc_plan *h, int cls, cudaStream_t st, F &&fn) {
 
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
+// bytes of one row record of the streaming schedule: min0, min1 (128 fp32 each), loc (128 u8/u16),
+// sign words (32 u32 per 8 edges of the longest row)
+int row_record_bytes(const HostGraph &g, bool loc16) { return 1024 + 128 * (loc16 ? 2 : 1) + 128 * ((g.max_row_deg + 7) / 8); }
+
 size_t tile_bytes(const HostGraph &g, bool loc16) {
     const size_t m = g.m, n = g.n;
     size_t b = 0;
     b += 2 * align256(n * TILE * 4);                 // r, s
-    b += 2 * align256(m * TILE * 4);                 // min0, min1
-    b += align256(m * TILE * (loc16 ? 2 : 1));       // loc
-    b += align256(m * (size_t)((g.max_row_deg + 7) / 8) * 128);  // sgn
+    b += align256(m * (size_t)row_record_bytes(g, loc16));  // row records (min0, min1, loc, signs)
     b += 3 * 256;                                    // unsat x2, done
     b += 4 * align256(TILE * 4);                     // iters, fbe, fraw, fnz
     b += 3 * 4 + 256;                                // tcount, tlist
@@ -123,10 +125,8 @@ StreamState carve(void *base, int T, const HostGraph &g, bool loc16) {
     w.T = T;
     w.r = reinterpret_cast<float *>(take((size_t)T * n * TILE * 4));
     w.s = reinterpret_cast<float *>(take((size_t)T * n * TILE * 4));
-    w.min0 = reinterpret_cast<float *>(take((size_t)T * m * TILE * 4));
-    w.min1 = reinterpret_cast<float *>(take((size_t)T * m * TILE * 4));
-    w.loc = take((size_t)T * m * TILE * (loc16 ? 2 : 1));
-    w.sgn = reinterpret_cast<uint32_t *>(take((size_t)T * m * ((g.max_row_deg + 7) / 8) * 128));
+    w.rs = row_record_bytes(g, loc16);
+    w.rst = reinterpret_cast<unsigned char *>(take((size_t)T * m * w.rs));
     w.unsat = reinterpret_cast<uint32_t *>(take((size_t)2 * T * 16));
     w.done = reinterpret_cast<uint32_t *>(take((size_t)T * 16));
     w.iters = reinterpret_cast<int *>(take((size_t)T * TILE * 4));
@@ -152,8 +152,7 @@ int ensure_ws(ldpc_plan *h, int T, bool loc16) {
     size_t need = 0;
     {
         const size_t m = h->g.m, n = h->g.n;
-        need = 2 * align256((size_t)T * n * TILE * 4) + 2 * align256((size_t)T * m * TILE * 4) +
-               align256((size_t)T * m * TILE * (loc16 ? 2 : 1)) + align256((size_t)T * m * ((h->g.max_row_deg + 7) / 8) * 128) +
+        need = 2 * align256((size_t)T * n * TILE * 4) + align256((size_t)T * m * row_record_bytes(h->g, loc16)) +
                align256((size_t)2 * T * 16) + align256((size_t)T * 16) + 4 * align256((size_t)T * TILE * 4) +
                align256(8) + align256((size_t)2 * T * 4) + align256(4);
     }
