@@ -238,25 +238,13 @@ __global__ void __launch_bounds__(CTA, CN_MINB)
 #pragma unroll
             for (int u = 0; u < CN_CHUNK; u++) {
                 const int j = __shfl_sync(FULL, cj, (p0 + u) & 31);
-#if defined(CN_PROBE) && CN_PROBE == 2
-                if (p0 + u < d) sv[u] = ld4(Sl + (size_t)(j & 7) * TILE);  // probe: gathers served by L1
-#else
-                if (p0 + u < d) sv[u] = ld4(Sl + (size_t)j * TILE);
-#endif
+                sv[u] = ld4(Sl + (size_t)j * TILE);  // unconditional: edges past d_i read column 0
             }
             const uint32_t wold = FIRST ? 0u : *sgp;
             uint32_t wnew = 0;
 #pragma unroll
             for (int u = 0; u < CN_CHUNK; u++) {
-#if defined(CN_PROBE) && CN_PROBE == 1
-                if (p0 + u < d) {  // probe: memory traffic only
-                    nm0[0] = fminf(nm0[0], sv[u].x + sv[u].y + sv[u].z + sv[u].w + om0[u & 3] + om1[u & 3]);
-                    wnew ^= __float_as_uint(sv[u].x) ^ wold;
-                }
-                if (false) {
-#else
                 if (p0 + u < d) {
-#endif
                     const int p = p0 + u;
                     typename LO::W key{};
                     if (!FIRST) key = LO::key(olc, p);
