@@ -204,8 +204,11 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
     int *slot_k = meta + 32;       // completed loop bodies
     int *slot_be = meta + 64;      // ones of b (bit errors vs the all-zero codeword)
     int *slot_raw = meta + 96;     // r_j > 0 count
-    int *slot_nz = meta + 128;     // some |s_j| <= 1e-4
-    unsigned *ctl = reinterpret_cast<unsigned *>(meta + 256);  // [0] unsat, [1] new, [2] active, [3] exhausted
+    int *slot_nz = meta + 128;     // some |s_j| <= 1e-4 (frame that stopped in the last pass)
+    int *slot_fout = meta + 160;   // frame index of the slot's stopping frame (outputs of this pass)
+    int *slot_pend = meta + 192;   // 1 + isCodeword of a stopped frame whose error counts are pending
+    // ctl: [0] unsat, [1] fresh, [2] active (continuing | fresh), [3] exhausted, [4] stopping, [5] continuing
+    unsigned *ctl = reinterpret_cast<unsigned *>(meta + 256);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int sub = lane / LR, l = lane % LR;  // row group inside the warp, lane inside the row
@@ -230,119 +233,28 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
         slot_be[tid] = 0;
         slot_raw[tid] = 0;
         slot_nz[tid] = 0;
+        slot_fout[tid] = -1;
+        slot_pend[tid] = 0;
     }
-    if (tid == 0) {
-        ctl[0] = 0;
-        ctl[1] = 0;
-        ctl[2] = 0;
-        ctl[3] = 0;
-    }
+    if (tid < 8) ctl[tid] = 0;
     unsigned long long acc_stats[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // warp 0, lane = slot
     __syncthreads();
 
+    // Per pass: C (check node + syndrome), then A (warp 0: stop / continue / refill the slots), then one
+    // column sweep D that writes the outputs of the stopping frames, runs the bit node of the continuing
+    // ones and stages the new frames (s = r) -- so a refill costs no extra sweep and no extra barrier.
+    // The first A and D (before the first C) only stage the first frames.
+    unsigned active = 0;
     for (int pass = 0;; pass++) {
         const int cur = pass & 1;  // sign words of the previous body are in buffer cur, this body's in cur ^ 1
         const uint4 *sgi = sgb + (cur ? a.lay.sgb_half : 0);
         uint4 *sgo = sgb + (cur ? 0 : a.lay.sgb_half);
-        // ---------------- A: finish stopped slots, advance continuing ones, refill (warp 0)
-        if (warp == 0) {
-            const unsigned uns_all = ctl[0];
-            const unsigned act_all = ctl[2];
-            const bool mine = lane < S;
-            int f = mine ? slot_f[lane] : 0;
-            if (mine && ((act_all >> lane) & 1u)) {
-                const int k = slot_k[lane];
-                const bool uns = (uns_all >> lane) & 1u;
-                // a clean syndrome stops the frame only at a check point k % T == 0 (P:498; S:226)
-                const bool fin = a.early ? ((!uns && k % a.T == 0) || k == a.L) : (k == a.L);
-                if (fin) {
-                    const int conv = !uns;
-                    if (a.iters) a.iters[f] = k;
-                    if (a.conv) a.conv[f] = (uint8_t)conv;
-                    const int be = slot_be[lane];
-                    acc_stats[0] += 1;
-                    acc_stats[1] += (unsigned long long)be;
-                    acc_stats[2] += be > 0;
-                    acc_stats[3] += (be > 0) && conv;
-                    acc_stats[4] += (unsigned long long)k;
-                    acc_stats[5] += conv;
-                    acc_stats[6] += slot_nz[lane] != 0;
-                    acc_stats[7] += (unsigned long long)slot_raw[lane];
-                    f = -1;
-                } else {
-                    slot_k[lane] = k + 1;
-                }
-            }
-            // refill: the free slots take consecutive frames from the global counter
-            const bool exhausted = ctl[3] != 0;
-            const unsigned freem = __ballot_sync(FULLM, mine && f < 0);
-            long long base = 0;
-            if (lane == 0 && freem && !exhausted) base = atomicAdd(a.counter, __popc(freem));
-            base = __shfl_sync(FULLM, base, 0);
-            unsigned fresh = 0;
-            if (freem && !exhausted) {
-                const long long mine_f = base + __popc(freem & ((1u << lane) - 1u));
-                const bool take = mine && f < 0 && mine_f < a.frames;
-                if (take) {
-                    f = (int)mine_f;
-                    slot_k[lane] = 0;
-                    slot_be[lane] = 0;
-                    slot_raw[lane] = 0;
-                    slot_nz[lane] = 0;
-                }
-                fresh = __ballot_sync(FULLM, take);
-                __syncwarp();  // every lane has read ctl[3] before lane 0 sets it
-                if (lane == 0 && base + __popc(freem) >= a.frames) ctl[3] = 1;
-            }
-            if (mine) slot_f[lane] = f;
-            const unsigned active = __ballot_sync(FULLM, mine && f >= 0);
-            __syncwarp();  // every lane has read ctl[] before lane 0 rewrites it
-            if (lane == 0) {
-                ctl[0] = 0;
-                ctl[1] = fresh;
-                ctl[2] = active;
-            }
-        }
-        __syncthreads();
-        const unsigned active = ctl[2], fresh_new = ctl[1];
-        if (!active) break;
-        const unsigned fm = (fresh_new >> q0) & 0xfu;  // this lane's fresh slots
-        const uint32_t fmb = (fm & 1u) * 0xffu | (fm & 2u) * 0x7f80u | (fm & 4u) * 0x3fc000u | (fm & 8u) * 0x1fe00000u;
-
-        // ---------------- B: stage new frames, s = r: column sweep in the float4 layout
-        if (fresh_new) {
-            int fr[4];
-#pragma unroll
-            for (int v = 0; v < 4; v++) fr[v] = slot_f[q0 + v];
-            int raw[4] = {0, 0, 0, 0};
-            for (int cb = warp * G; cb < n && fm; cb += NWARP * G) {
-                const int j = cb + sub;
-                if (j >= n) continue;
-                float *sp = s + j * S + q0;
-                float4 o = *reinterpret_cast<const float4 *>(sp);
-#pragma unroll
-                for (int v = 0; v < 4; v++) {
-                    if ((fm >> v) & 1u) {
-                        const float x = __ldg(a.llr + (int64_t)fr[v] * n + j);
-                        f4s(o, v, x == 0.f ? -0.f : x);  // zeros of s are kept as -0 (A12)
-                        rs[(size_t)j * S + q0 + v] = x;
-                        raw[v] += x > 0.f;
-                    }
-                }
-                *reinterpret_cast<float4 *>(sp) = o;
-            }
-            // per-slot counts: reduce over the row groups of the warp, then one atomic per slot
-#pragma unroll
-            for (int v = 0; v < 4; v++) {
-                int x = raw[v];
-                for (int o = LR; o < 32; o <<= 1) x += __shfl_xor_sync(FULLM, x, o);
-                if (sub == 0 && x) atomicAdd(&slot_raw[q0 + v], x);
-            }
-            __syncthreads();
-        }
-
-        // ---------------- C: check-node pass + syndrome of b = slice(s)
-        {
+        if (pass > 0) {
+            const unsigned fresh_prev = ctl[1];
+            const unsigned fm = (fresh_prev >> q0) & 0xfu;  // this lane's fresh slots (eta^prev = 0)
+            const uint32_t fmb =
+                (fm & 1u) * 0xffu | (fm & 2u) * 0x7f80u | (fm & 4u) * 0x3fc000u | (fm & 8u) * 0x1fe00000u;
+            // ---------------- C: check-node pass + syndrome of b = slice(s)
             unsigned syn_acc = 0;  // bit v: slot q0+v has an unsatisfied check
             for (int rb = warp * G; rb < m; rb += NWARP * G) {
                 const int i = rb + sub;
@@ -364,97 +276,185 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
             const unsigned mine = (syn_acc << q0) & active;
             const unsigned wmask = __reduce_or_sync(FULLM, mine);
             if (lane == 0 && wmask) atomicOr(&ctl[0], wmask);
+            __syncthreads();
         }
-        __syncthreads();
-
-        // ---------------- D: per-slot decision; outputs of stopping slots and bit-node update of the
-        //                     continuing ones in one column sweep
-        {
+        // ---------------- A: stop / continue / refill (warp 0)
+        if (warp == 0) {
             const unsigned uns_all = ctl[0];
+            const bool own = lane < S;
+            // error counts of the frames that stopped in the previous pass (written by that pass's D)
+            if (own && slot_pend[lane]) {
+                const int be = slot_be[lane], conv = slot_pend[lane] - 1;
+                acc_stats[1] += (unsigned long long)be;
+                acc_stats[2] += be > 0;
+                acc_stats[3] += (be > 0) && conv;
+                acc_stats[6] += slot_nz[lane] != 0;
+                slot_be[lane] = 0;
+                slot_nz[lane] = 0;
+                slot_pend[lane] = 0;
+            }
+            int f = own ? slot_f[lane] : 0;
             bool fin = false, cont = false;
-            if (lane < S && ((active >> lane) & 1u)) {
+            if (own && f >= 0 && pass > 0) {
                 const int k = slot_k[lane];
                 const bool uns = (uns_all >> lane) & 1u;
+                // a clean syndrome stops the frame only at a check point k % T == 0 (P:498; S:226)
                 fin = a.early ? ((!uns && k % a.T == 0) || k == a.L) : (k == a.L);
-                cont = !fin;
+                if (fin) {
+                    const int conv = !uns;
+                    if (a.iters) a.iters[f] = k;
+                    if (a.conv) a.conv[f] = (uint8_t)conv;
+                    acc_stats[0] += 1;
+                    acc_stats[4] += (unsigned long long)k;
+                    acc_stats[5] += conv;
+                    acc_stats[7] += (unsigned long long)slot_raw[lane];
+                    slot_fout[lane] = f;
+                    slot_pend[lane] = 1 + conv;
+                    f = -1;
+                } else {
+                    slot_k[lane] = k + 1;  // D runs body k + 1
+                    cont = true;
+                }
             }
-            const unsigned fin_mask = __ballot_sync(FULLM, fin), cont_mask = __ballot_sync(FULLM, cont);
-            const unsigned cm = (cont_mask >> q0) & 0xfu;  // continuing slots of this lane
-            const unsigned fk = (fin_mask >> q0) & 0xfu;   // stopping slots of this lane
-            if (fin_mask | cont_mask) {
-                int64_t fo[4];
-#pragma unroll
-                for (int v = 0; v < 4; v++) fo[v] = (int64_t)slot_f[q0 + v] * n;
-                int be[4] = {0, 0, 0, 0};
-                unsigned nz = 0;
-                for (int cb = warp * G; cb < n; cb += NWARP * G) {
-                    const int j = cb + sub;
-                    if (j >= n || !(cm | fk)) continue;
-                    float *sp = s + j * S + q0;
-                    float4 o = *reinterpret_cast<const float4 *>(sp);
-                    if (fk) {
-#pragma unroll
-                        for (int v = 0; v < 4; v++) {
-                            if ((fk >> v) & 1u) {
-                                const float x = f4c(o, v);
-                                const bool b = x > 0.f;  // Eq. slice
-                                if (a.post) a.post[fo[v] + j] = x;
-                                if (a.bits) a.bits[fo[v] + j] = (uint8_t)b;
-                                be[v] += b;
-                                nz |= (unsigned)(fabsf(x) <= 1e-4f) << v;
-                            }
-                        }
-                    }
-                    if (cm) {
-                        const float4 rj = *reinterpret_cast<const float4 *>(rs + (size_t)j * S + q0);
-                        const int c0 = DV > 0 ? j * DV : cp[j], dv = DV > 0 ? DV : (int)cp[j + 1] - c0;
-                        float acc[4] = {0.f, 0.f, 0.f, 0.f};
-                        for (int q3 = 0; q3 < dv; q3 += 3) {  // chunks of 3 edges: no remainder loop for d_v = 3
-#pragma unroll
-                            for (int u = 0; u < 3; u++) {
-                                if (q3 + u < dv) {
-                                    const int ca = (int)rec[c0 + q3 + u] + q0;
-                                    const uint32_t r2 = rec2[c0 + q3 + u];
-                                    const uint32_t pp = __byte_perm(r2, 0u, 0x2222u);  // position p in every byte
-                                    const float4 m0 = *reinterpret_cast<const float4 *>(mn0 + ca);
-                                    const float4 m1 = *reinterpret_cast<const float4 *>(mn1 + ca);
-                                    const uint32_t lv = *reinterpret_cast<const uint32_t *>(lc + ca) ^ pp;
-                                    const uint4 W = sgo[r2 & 0xffffu];
-                                    const uint32_t mul = 0x80000000u >> ((r2 >> 24) + l);  // this lane's bit of row i
-                                    const float mg[4] = {(lv & 0xffu) ? m0.x : m1.x, (lv & 0xff00u) ? m0.y : m1.y,
-                                                         (lv & 0xff0000u) ? m0.z : m1.z,
-                                                         (lv & 0xff000000u) ? m0.w : m1.w};  // Obs. 1
-#pragma unroll
-                                    for (int v = 0; v < 4; v++)  // ascending rows from +0.0 (A14)
-                                        acc[v] = acc[v] + flip31(mg[v], f4c(W, v) * mul);
-                                }
-                            }
-                        }
-                        const float n0 = acc[0] + rj.x, n1 = acc[1] + rj.y, n2 = acc[2] + rj.z, n3 = acc[3] + rj.w;
-                        if (cm & 1u) o.x = n0 == 0.f ? -0.f : n0;  // zeros of s are kept as -0 (A12)
-                        if (cm & 2u) o.y = n1 == 0.f ? -0.f : n1;
-                        if (cm & 4u) o.z = n2 == 0.f ? -0.f : n2;
-                        if (cm & 8u) o.w = n3 == 0.f ? -0.f : n3;
-                        *reinterpret_cast<float4 *>(sp) = o;
-                    }
+            // refill: the free slots take consecutive frames from the global counter
+            const bool exhausted = ctl[3] != 0;
+            const unsigned freem = __ballot_sync(FULLM, own && f < 0);
+            long long base = 0;
+            if (lane == 0 && freem && !exhausted) base = atomicAdd(a.counter, __popc(freem));
+            base = __shfl_sync(FULLM, base, 0);
+            bool take = false;
+            if (freem && !exhausted) {
+                const long long mine_f = base + __popc(freem & ((1u << lane) - 1u));
+                take = own && f < 0 && mine_f < a.frames;
+                if (take) {
+                    f = (int)mine_f;
+                    slot_k[lane] = 0;
+                    slot_raw[lane] = 0;
                 }
-                if (fin_mask) {
-#pragma unroll
-                    for (int v = 0; v < 4; v++) {
-                        int x = be[v];
-                        for (int o = LR; o < 32; o <<= 1) x += __shfl_xor_sync(FULLM, x, o);
-                        if (sub == 0 && x) atomicAdd(&slot_be[q0 + v], x);
-                    }
-                    unsigned z = nz;
-                    for (int o = LR; o < 32; o <<= 1) z |= __shfl_xor_sync(FULLM, z, o);
-                    if (sub == 0 && z)
-#pragma unroll
-                        for (int v = 0; v < 4; v++)
-                            if ((z >> v) & 1u) slot_nz[q0 + v] = 1;
-                }
+            }
+            if (own) slot_f[lane] = f;
+            const unsigned fresh = __ballot_sync(FULLM, take), fin_m = __ballot_sync(FULLM, fin),
+                           cont_m = __ballot_sync(FULLM, cont);
+            __syncwarp();  // every lane has read ctl[] before lane 0 rewrites it
+            if (lane == 0) {
+                if (freem && !exhausted && base + __popc(freem) >= a.frames) ctl[3] = 1;
+                ctl[0] = 0;
+                ctl[1] = fresh;
+                ctl[2] = fresh | cont_m;
+                ctl[4] = fin_m;
+                ctl[5] = cont_m;
             }
         }
         __syncthreads();
+        active = ctl[2];
+        const unsigned fin_mask = ctl[4], cont_mask = ctl[5], fresh_mask = ctl[1];
+        // ---------------- D: outputs of the stopping frames, bit node of the continuing ones, staging of
+        //                     the new ones (s = r), in one column sweep
+        if (fin_mask | active) {
+            const unsigned cm = (cont_mask >> q0) & 0xfu;   // continuing slots of this lane
+            const unsigned fk = (fin_mask >> q0) & 0xfu;    // stopping slots of this lane
+            const unsigned fw = (fresh_mask >> q0) & 0xfu;  // new frames of this lane
+            int64_t fo[4], fr[4];
+#pragma unroll
+            for (int v = 0; v < 4; v++) {
+                fo[v] = (int64_t)slot_fout[q0 + v] * n;
+                fr[v] = (int64_t)slot_f[q0 + v] * n;
+            }
+            int be[4] = {0, 0, 0, 0}, raw[4] = {0, 0, 0, 0};
+            unsigned nz = 0;
+            for (int cb = warp * G; cb < n; cb += NWARP * G) {
+                const int j = cb + sub;
+                if (j >= n || !(cm | fk | fw)) continue;
+                float *sp = s + j * S + q0;
+                float4 o = *reinterpret_cast<const float4 *>(sp);
+                if (fk) {
+#pragma unroll
+                    for (int v = 0; v < 4; v++) {
+                        if ((fk >> v) & 1u) {
+                            const float x = f4c(o, v);
+                            const bool b = x > 0.f;  // Eq. slice
+                            if (a.post) a.post[fo[v] + j] = x;
+                            if (a.bits) a.bits[fo[v] + j] = (uint8_t)b;
+                            be[v] += b;
+                            nz |= (unsigned)(fabsf(x) <= 1e-4f) << v;
+                        }
+                    }
+                }
+                if (cm) {
+                    const float4 rj = *reinterpret_cast<const float4 *>(rs + (size_t)j * S + q0);
+                    const int c0 = DV > 0 ? j * DV : cp[j], dv = DV > 0 ? DV : (int)cp[j + 1] - c0;
+                    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+                    for (int q3 = 0; q3 < dv; q3 += 3) {  // chunks of 3 edges: no remainder loop for d_v = 3
+#pragma unroll
+                        for (int u = 0; u < 3; u++) {
+                            if (q3 + u < dv) {
+                                const int ca = (int)rec[c0 + q3 + u] + q0;
+                                const uint32_t r2 = rec2[c0 + q3 + u];
+                                const uint32_t pp = __byte_perm(r2, 0u, 0x2222u);  // position p in every byte
+                                const float4 m0 = *reinterpret_cast<const float4 *>(mn0 + ca);
+                                const float4 m1 = *reinterpret_cast<const float4 *>(mn1 + ca);
+                                const uint32_t lv = *reinterpret_cast<const uint32_t *>(lc + ca) ^ pp;
+                                const uint4 W = sgo[r2 & 0xffffu];
+                                const uint32_t mul = 0x80000000u >> ((r2 >> 24) + l);  // this lane's bit of row i
+                                const float mg[4] = {(lv & 0xffu) ? m0.x : m1.x, (lv & 0xff00u) ? m0.y : m1.y,
+                                                     (lv & 0xff0000u) ? m0.z : m1.z,
+                                                     (lv & 0xff000000u) ? m0.w : m1.w};  // Obs. 1
+#pragma unroll
+                                for (int v = 0; v < 4; v++)  // ascending rows from +0.0 (A14)
+                                    acc[v] = acc[v] + flip31(mg[v], f4c(W, v) * mul);
+                            }
+                        }
+                    }
+                    const float n0 = acc[0] + rj.x, n1 = acc[1] + rj.y, n2 = acc[2] + rj.z, n3 = acc[3] + rj.w;
+                    if (cm & 1u) o.x = n0 == 0.f ? -0.f : n0;  // zeros of s are kept as -0 (A12)
+                    if (cm & 2u) o.y = n1 == 0.f ? -0.f : n1;
+                    if (cm & 4u) o.z = n2 == 0.f ? -0.f : n2;
+                    if (cm & 8u) o.w = n3 == 0.f ? -0.f : n3;
+                }
+                if (fw) {
+#pragma unroll
+                    for (int v = 0; v < 4; v++) {
+                        if ((fw >> v) & 1u) {
+                            const float x = __ldg(a.llr + fr[v] + j);
+                            f4s(o, v, x == 0.f ? -0.f : x);  // zeros of s are kept as -0 (A12)
+                            rs[(size_t)j * S + q0 + v] = x;
+                            raw[v] += x > 0.f;
+                        }
+                    }
+                }
+                if (cm | fw) *reinterpret_cast<float4 *>(sp) = o;
+            }
+            // per-slot counts: reduce over the row groups of the warp, then one atomic per slot (the
+            // condition is CTA-uniform: every lane of the warp takes part in the shuffles)
+            if (fin_mask | fresh_mask) {
+#pragma unroll
+                for (int v = 0; v < 4; v++) {
+                    int x = be[v], y = raw[v];
+                    for (int o = LR; o < 32; o <<= 1) {
+                        x += __shfl_xor_sync(FULLM, x, o);
+                        y += __shfl_xor_sync(FULLM, y, o);
+                    }
+                    if (sub == 0 && x) atomicAdd(&slot_be[q0 + v], x);
+                    if (sub == 0 && y) atomicAdd(&slot_raw[q0 + v], y);
+                }
+                unsigned z = nz;
+                for (int o = LR; o < 32; o <<= 1) z |= __shfl_xor_sync(FULLM, z, o);
+                if (sub == 0 && z)
+#pragma unroll
+                    for (int v = 0; v < 4; v++)
+                        if ((z >> v) & 1u) slot_nz[q0 + v] = 1;
+            }
+        }
+        __syncthreads();
+        if (!active) break;
+    }
+    // error counts of the frames that stopped in the last pass
+    if (warp == 0 && lane < S && slot_pend[lane]) {
+        const int be = slot_be[lane], conv = slot_pend[lane] - 1;
+        acc_stats[1] += (unsigned long long)be;
+        acc_stats[2] += be > 0;
+        acc_stats[3] += (be > 0) && conv;
+        acc_stats[6] += slot_nz[lane] != 0;
     }
 
     // ---- counters: warp 0 holds them per slot
