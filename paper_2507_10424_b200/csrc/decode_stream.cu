@@ -756,8 +756,8 @@ int launch_check_node(const Graph &g, const StreamState &w, int k, bool first, b
 
 int launch_bit_node(const Graph &g, const StreamState &w, int k, bool early, bool literal, bool loc16,
                     const StreamLaunch &cfg, cudaStream_t st, const int *kdev) {
-    const dim3 grid = grid2((g.n + cfg.cols_per_cta - 1) / cfg.cols_per_cta, w.T);
-    const int lit = literal ? 1 : 0, cpc = cfg.cols_per_cta, u = cfg.bn_unroll;
+    const dim3 grid = grid2((g.n + BNL_COLS - 1) / BNL_COLS, w.T);
+    const int lit = literal ? 1 : 0, cpc = BNL_COLS, u = 0;
     if (loc16) {
         if (early) bn_launch<uint16_t, true>(grid, st, g, w, k, cpc, lit, u, kdev, cfg.check_every);
         else bn_launch<uint16_t, false>(grid, st, g, w, k, cpc, lit, u, kdev, cfg.check_every);

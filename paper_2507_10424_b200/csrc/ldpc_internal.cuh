@@ -69,13 +69,9 @@ struct HostGraph {  // device allocations owned by the plan
 
 // ---- streaming schedule (decode_stream.cu) ----
 struct StreamLaunch {
-    int rows_per_cta = 64;  // <= 256 (a warp owns <= 32 rows)
-    int cols_per_cta = 64;  // <= 256
-    int cn_unroll = 0;  // check-node kernel: 0 = automatic (pipelined when max row degree <= 8), 1 = generic
-    int bn_unroll = 0;  // bit-node kernel: 0 = automatic, 1 = generic
-    int check_every = 1;  // codeword test after body k when k % T == 0 (and after body L)
-    int cn_ctas = 4736;  // grid caps of the (tile x block) work loops: a few waves of resident CTAs
-    int bn_ctas = 7104;
+    int rows_per_cta = 64;  // check-node rows per CTA, <= 256 (a warp owns <= 32 rows)
+    int cn_unroll = 0;      // check-node kernel: 0 = one row buffer (default), 1 = generic, 2 = two row buffers
+    int check_every = 1;    // codeword test after body k when k % T == 0 (and after body L)
 };
 // Launch helpers; each returns the number of kernels launched.
 int launch_stage_in(const Graph &g, const StreamState &w, const float *llr, int64_t frames, cudaStream_t st);

@@ -371,16 +371,8 @@ int finish_prepare(ldpc_plan *p, int rc, uint32_t flags, ldpc_handle_t *out) {
     cudaGetDevice(&p->device);
     p->rp = plan_resident(p->g, p->g.max_row_deg > 255, p->device);
     if (const char *s = getenv("LDPC_ROWS_PER_CTA")) p->cfg.rows_per_cta = std::min(256, std::max(8, atoi(s)));
-    if (const char *s = getenv("LDPC_COLS_PER_CTA")) p->cfg.cols_per_cta = std::min(256, std::max(8, atoi(s)));
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
-    p->cfg.cn_ctas = sms * 4 * 2;  // 4 resident CTAs per SM (64-register kernel), two waves
-    p->cfg.bn_ctas = sms * 6 * 2;
-    if (const char *s = getenv("LDPC_CN_CTAS")) p->cfg.cn_ctas = std::max(1, atoi(s));
-    if (const char *s = getenv("LDPC_BN_CTAS")) p->cfg.bn_ctas = std::max(1, atoi(s));
     if (const char *s = getenv("LDPC_CN_UNROLL")) p->cfg.cn_unroll = std::max(0, atoi(s));
     if (const char *s = getenv("LDPC_NO_GRAPHS")) p->use_graphs = atoi(s) == 0;
-    if (const char *s = getenv("LDPC_BN_UNROLL")) p->cfg.bn_unroll = std::max(0, atoi(s));
     *out = p;
     return LDPC_OK;
 }
