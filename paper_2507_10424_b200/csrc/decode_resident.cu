@@ -49,7 +49,9 @@ constexpr int META_INTS = 8 * 32 + 16;
 // together (rg = i / G), position p of the rows and slot component v, one u32 whose bit
 // (i % G) * LR + l is the sign of lambda for row i, slot 4l + v.  The writer stores four words per
 // edge position with one 16-byte store; readers test a lane bit.
-Layout layout_for(int S, int m, int n, int E, int dm) {
+// compact: the bit node's per-edge records are a u16 row offset and a u8 position (3 B per edge instead
+// of 8: the ballot word and bit are recomputed from them), for codes that fit no other way (C5 size)
+Layout layout_for(int S, int m, int n, int E, int dm, bool compact = false) {
     Layout L{};
     const int G = 128 / S;
     const size_t nrg = (size_t)(m + G - 1) / G;
@@ -63,8 +65,8 @@ Layout layout_for(int S, int m, int n, int E, int dm) {
     L.rp = o;   o = a16(o + (size_t)(m + 1) * 2);
     L.cp = o;   o = a16(o + (size_t)(n + 1) * 2);
     L.col = o;  o = a16(o + (size_t)E * 2);
-    L.rec = o;  o = a16(o + (size_t)E * 4);
-    L.rec2 = o; o = a16(o + (size_t)E * 4);
+    L.rec = o;  o = a16(o + (size_t)E * (compact ? 2 : 4));
+    L.rec2 = o; o = a16(o + (size_t)E * (compact ? 1 : 4));
     L.meta = o; o = a16(o + (size_t)META_INTS * 4 + 8 * 8);
     L.total = o;
     return L;
@@ -76,6 +78,7 @@ struct ResArgs {
     int64_t frames;
     int L, T, early, literal, dm;
     int dc, dv;  // > 0: every row has degree dc and every column degree dv (regular code)
+    int compact;  // bit-node records in the compact form (see layout_for)
     float *post;
     uint8_t *bits;
     int32_t *iters;
@@ -182,7 +185,7 @@ __device__ __forceinline__ void cn_rows(const float *__restrict__ s, float *mn0,
 
 // Lane layout: a lane owns 4 consecutive slots (float4) of one row or column; LR = S/4 lanes cover a
 // row, G = 32/LR rows per warp.  Bit of slot q = 4*l + v inside an S-bit sign word: v*LR + l.
-template <int S, int RT, int DC, int DV>
+template <int S, int RT, int DC, int DV, bool CMP>
 __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 2) : RT == 384 ? 2 : 1) k_resident(ResArgs a) {
     constexpr int NWARP = RT / 32;
     constexpr int LR = S / 4;
@@ -223,6 +226,11 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
     for (int e = tid; e < E; e += RT) {
         col[e] = (uint16_t)__ldg(a.g.col_idx + e);
         const int4 be = __ldg(a.g.bn_edge + e);  // {edge id, row, pos, parity}
+        if (CMP) {  // u16 row offset, u8 position
+            reinterpret_cast<uint16_t *>(rec)[e] = (uint16_t)(be.y * S);
+            reinterpret_cast<uint8_t *>(rec2)[e] = (uint8_t)be.z;
+            continue;
+        }
         rec[e] = (uint32_t)be.y * S;  // first state element of row i (the lane adds its slot offset)
         // ballot-word index of the edge | position p in row i << 16 | bit offset of row i in the word << 24
         rec2[e] = (uint32_t)((be.y / G) * dm + be.z) | ((uint32_t)be.z << 16) | ((uint32_t)((be.y % G) * LR) << 24);
@@ -388,14 +396,28 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
 #pragma unroll
                         for (int u = 0; u < 3; u++) {
                             if (q3 + u < dv) {
-                                const int ca = (int)rec[c0 + q3 + u] + q0;
-                                const uint32_t r2 = rec2[c0 + q3 + u];
-                                const uint32_t pp = __byte_perm(r2, 0u, 0x2222u);  // position p in every byte
+                                int ca;
+                                uint32_t pp, word, bit;
+                                if (CMP) {
+                                    const int ro = reinterpret_cast<const uint16_t *>(rec)[c0 + q3 + u];
+                                    const int pq = reinterpret_cast<const uint8_t *>(rec2)[c0 + q3 + u];
+                                    const int i = ro / S;
+                                    ca = ro + q0;
+                                    pp = (uint32_t)pq * 0x01010101u;
+                                    word = (uint32_t)((i / G) * dm + pq);
+                                    bit = (uint32_t)((i % G) * LR);
+                                } else {
+                                    ca = (int)rec[c0 + q3 + u] + q0;
+                                    const uint32_t r2 = rec2[c0 + q3 + u];
+                                    pp = __byte_perm(r2, 0u, 0x2222u);  // position p in every byte
+                                    word = r2 & 0xffffu;
+                                    bit = r2 >> 24;
+                                }
                                 const float4 m0 = *reinterpret_cast<const float4 *>(mn0 + ca);
                                 const float4 m1 = *reinterpret_cast<const float4 *>(mn1 + ca);
                                 const uint32_t lv = *reinterpret_cast<const uint32_t *>(lc + ca) ^ pp;
-                                const uint4 W = sgo[r2 & 0xffffu];
-                                const uint32_t mul = 0x80000000u >> ((r2 >> 24) + l);  // this lane's bit of row i
+                                const uint4 W = sgo[word];
+                                const uint32_t mul = 0x80000000u >> (bit + l);  // this lane's bit of row i
                                 const float mg[4] = {(lv & 0xffu) ? m0.x : m1.x, (lv & 0xff00u) ? m0.y : m1.y,
                                                      (lv & 0xff0000u) ? m0.z : m1.z,
                                                      (lv & 0xff000000u) ? m0.w : m1.w};  // Obs. 1
@@ -474,16 +496,27 @@ int max_smem_optin(int device) {
     return v;
 }
 
-template <int S, int RT>
-void launch_s(const ResArgs &args, int ctas, size_t smem, cudaStream_t st) {
+template <int S, int RT, bool CMP>
+void launch_c(const ResArgs &args, int ctas, size_t smem, cudaStream_t st) {
     // regular (3,6) codes (C1, C2, C5): degree-specialised kernel (fully unrolled row and column loops)
     if (args.dc == 6 && args.dv == 3) {
-        cudaFuncSetAttribute(k_resident<S, RT, 6, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_resident<S, RT, 6, 3><<<ctas, RT, smem, st>>>(args);
+        cudaFuncSetAttribute(k_resident<S, RT, 6, 3, CMP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_resident<S, RT, 6, 3, CMP><<<ctas, RT, smem, st>>>(args);
         return;
     }
-    cudaFuncSetAttribute(k_resident<S, RT, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_resident<S, RT, 0, 0><<<ctas, RT, smem, st>>>(args);
+    cudaFuncSetAttribute(k_resident<S, RT, 0, 0, CMP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_resident<S, RT, 0, 0, CMP><<<ctas, RT, smem, st>>>(args);
+}
+
+template <int S, int RT>
+void launch_s(const ResArgs &args, int ctas, size_t smem, cudaStream_t st) {
+    if constexpr (S <= 8 && (RT == 256 || RT == 512)) {
+        if (args.compact) {
+            launch_c<S, RT, true>(args, ctas, smem, st);
+            return;
+        }
+    }
+    launch_c<S, RT, false>(args, ctas, smem, st);
 }
 
 template <int S>
@@ -512,14 +545,19 @@ ResidentPlan plan_resident(const HostGraph &g, bool loc16, int device) {
     if (const char *e = getenv("LDPC_RES_THREADS")) force_t = atoi(e);
     // Prefer the largest S with two CTAs per SM (their phases interleave: measured 3-12 % faster on
     // the C2 code than one CTA of 2S slots), else the largest S with one CTA per SM.
-    for (int pass = 0; pass < 2 && !rp.ok; pass++) {
+    // A third pass tries the compact bit-node records (codes of the C5 size: 2048 x 4096 with S = 4).
+    for (int pass = 0; pass < 3 && !rp.ok; pass++) {
+        const bool compact = pass == 2;
+        if (compact && getenv("LDPC_RES_NO_COMPACT")) break;
         for (int S : {32, 16, 8, 4}) {
             if (force_s && S != force_s) continue;
-            const Layout L = layout_for(S, g.m, g.n, g.E, dm);
+            if (compact && (S > 8 || (int64_t)g.m * S > 65535)) continue;
+            const Layout L = layout_for(S, g.m, g.n, g.E, dm, compact);
             if (L.total > (size_t)cap) continue;
             const int per_sm = std::max(1, std::min(S == 4 ? 3 : 2, sm_smem / (int)(L.total + 1024)));
             if (pass == 0 && per_sm < 2 && !force_s) continue;
             rp.ok = true;
+            rp.compact = compact;
             rp.slots = S;
             rp.dm = dm;
             rp.dv = g.max_col_deg;
@@ -563,7 +601,8 @@ int launch_resident(const Graph &g, const ResidentPlan &rp, const float *llr, in
     a.dc = rp.regular ? rp.dm : 0;
     a.dv = rp.regular ? rp.dv : 0;
     if (getenv("LDPC_RES_GENERIC")) a.dc = a.dv = 0;
-    a.lay = layout_for(rp.slots, g.m, g.n, g.E, rp.dm);
+    a.compact = rp.compact ? 1 : 0;
+    a.lay = layout_for(rp.slots, g.m, g.n, g.E, rp.dm, rp.compact);
     cudaMemsetAsync(work_counter, 0, sizeof(int), st);
     switch (rp.slots) {
         case 32: launch_t<32>(a, rp.threads, rp.ctas, rp.smem, st); break;

@@ -97,6 +97,7 @@ struct ResidentPlan {
     int dm = 0;          // max row degree (ballot-word rows)
     int dv = 0;          // max column degree
     bool regular = false;  // every row has degree dm and every column degree dv
+    bool compact = false;  // compact bit-node records (larger codes, see layout_for)
 };
 ResidentPlan plan_resident(const HostGraph &g, bool loc16, int device);
 size_t resident_scratch_bytes(const HostGraph &g, const ResidentPlan &rp);  // work counter + r scratch

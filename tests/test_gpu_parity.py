@@ -347,7 +347,13 @@ def test_c5_sixteen_handles():
             continue
         parts = [channel.bpsk_awgn(code.n, code.rate, e, cfg["seed"] + hidx, p, 0, 80).numpy()
                  for p, e in enumerate(cfg["ebn0"])]
-        compare(code, np.concatenate(parts), cfg["max_iter"])
+        llr = np.concatenate(parts)
+        h = handle(code)
+        assert h.schedule == "resident"  # compact bit-node records make the 2048 x 4096 state fit
+        res = compare(code, llr, cfg["max_iter"], h=h)
+        got = compare(code, llr, cfg["max_iter"], FORCE_STREAM, h=handle(code, FORCE_STREAM))
+        for a, b in zip(res, got):
+            assert np.array_equal(a, b)
 
 
 def test_generator_device_independent():
