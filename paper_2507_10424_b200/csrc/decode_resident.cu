@@ -546,7 +546,8 @@ ResidentPlan plan_resident(const HostGraph &g, bool loc16, int device) {
     // Prefer the largest S with two CTAs per SM (their phases interleave: measured 3-12 % faster on
     // the C2 code than one CTA of 2S slots), else the largest S with one CTA per SM.
     // A third pass tries the compact bit-node records (codes of the C5 size: 2048 x 4096 with S = 4).
-    for (int pass = 0; pass < 3 && !rp.ok; pass++) {
+    // LDPC_RES_COMPACT=1 forces the compact records (tests; they are bit-identical).
+    for (int pass = getenv("LDPC_RES_COMPACT") ? 2 : 0; pass < 3 && !rp.ok; pass++) {
         const bool compact = pass == 2;
         if (compact && getenv("LDPC_RES_NO_COMPACT")) break;
         for (int S : {32, 16, 8, 4}) {

@@ -222,6 +222,20 @@ def test_stream_unroll_variants(monkeypatch, cu):
     compare(code3, llr3, 12, h=handle(code3, FORCE_STREAM))
 
 
+@pytest.mark.parametrize("which", ["paper", "reg", "small"])
+def test_resident_compact_records(monkeypatch, which):
+    """The compact bit-node records (u16 row offset + u8 position, recomputed ballot word and bit) are
+    bit-identical to the oracle on regular and irregular codes (LDPC_RES_COMPACT=1 forces them)."""
+    monkeypatch.setenv("LDPC_RES_COMPACT", "1")
+    code = {"paper": codes.paper_5x10, "reg": lambda: codes.regular(504, 1008, 3, 6, 1008),
+            "small": lambda: codes.random_small(37, 70, 2, 2, 9)}[which]()
+    h = handle(code, FORCE_RESIDENT)
+    assert h.schedule == "resident"
+    rng = np.random.default_rng(8)
+    llr = (rng.standard_normal((700, code.n)) * 1.2 - 0.9).astype(np.float32)
+    compare(code, llr, 25, h=h)
+
+
 def test_resident_generic_equals_regular_instance(monkeypatch):
     """The degree-specialised resident kernel for regular (3,6) codes and the generic one agree
     (LDPC_RES_GENERIC=1 forces the generic instance), and both match the oracle."""
