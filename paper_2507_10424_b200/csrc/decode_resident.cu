@@ -8,10 +8,12 @@
 //                              (Obs. 2) x (-1)^{d_i} (reading A1)
 //   min1 [m][S]  fp32          Observation 1's second minimum, same sign bit
 //   lc   [m][S]  u8            min0Location as the position p inside row i's list (0xff = none)
-//   sgb  [m/G][dmax] 4 x u32   sign of lambda_e = s_j - eta_e, kept as the warp ballots of the check
-//                              node (bit (i % G) * LR + l of component v = row i, slot 4l + v)
-// eta_e = (loc == p ? min1 : min0) with its sign bit XORed with the ballot bit: one FSEL and one LOP3
-// per slot-edge (the ballot bit is moved to bit 31 by an integer multiply, on the FMA pipe).
+//   sgr  [m][WR][LR] u32       sign of lambda_e = s_j - eta_e, row-transposed: the lane that owns slots
+//                              4l..4l+3 of row i owns word (i, p/8, l), whose bit 4(p%8) + v is the sign
+//                              for edge p and slot 4l + v (WR = ceil(dmax / 8), LR = S / 4)
+// eta_e = (loc == p ? min1 : min0) with its sign bit XORed with the stored bit: one FSEL and one LOP3
+// per slot-edge (the bit is moved to bit 31 by a constant shift when the row degree is a template
+// constant).
 // Zeros of s are kept as -0.0 (same slice and sign() under reading A12), so the decision of a slot is
 // the complement of the IEEE sign bit of s and the syndrome is a XOR of sign bits.
 // plus the Tanner graph itself as 16-bit lists (N_i, M_j).  r lives in a global scratch
@@ -37,8 +39,7 @@ constexpr unsigned FULLM = 0xffffffffu;
 
 
 struct Layout {
-    size_t s, m0, m1, lc, sgb, rp, cp, col, rec, rec2, meta, total;
-    size_t sgb_half;  // words per buffer (sign words are double-buffered by loop pass)
+    size_t s, m0, m1, lc, sgr, rp, cp, col, rec, rec2, meta, total;
 };
 
 constexpr size_t a16(size_t x) { return (x + 15) & ~(size_t)15; }
@@ -54,14 +55,12 @@ constexpr int META_INTS = 8 * 32 + 16;
 Layout layout_for(int S, int m, int n, int E, int dm, bool compact = false) {
     Layout L{};
     const int G = 128 / S;
-    const size_t nrg = (size_t)(m + G - 1) / G;
     size_t o = 0;
     L.s = o;    o = a16(o + (size_t)n * S * 4);
     L.m0 = o;   o = a16(o + (size_t)m * S * 4);
     L.m1 = o;   o = a16(o + (size_t)m * S * 4);
     L.lc = o;   o = a16(o + (size_t)m * S);
-    L.sgb_half = nrg * dm;
-    L.sgb = o;  o = a16(o + 2 * nrg * dm * 16);
+    L.sgr = o;  o = a16(o + (size_t)m * ((dm + 7) / 8) * (S / 4) * 4);
     L.rp = o;   o = a16(o + (size_t)(m + 1) * 2);
     L.cp = o;   o = a16(o + (size_t)(n + 1) * 2);
     L.col = o;  o = a16(o + (size_t)E * 2);
@@ -102,16 +101,18 @@ __device__ __forceinline__ void f4s(float4 &a, int v, float x) {
 // HAS: rows of the warp may have different degrees (irregular H), lanes past their degree idle.
 // fm: this lane's fresh slots (eta^prev = 0: their stored min0 = min1 = +0, so eta^prev = +-0 and
 // lambda = s - (+-0) has the magnitude and sign() of s, s being -0 rather than +0 for zero).
-// sgi: the ballot words of this row block from the previous body, sgo: where this body's go.
+// sgw: this lane's sign words of row i (sgw[q * LR] = edges 8q..8q+7): read as eta^prev's signs and
+// overwritten with the new ones (each lane owns its words: no ballot, no synchronisation).
 __device__ __forceinline__ float flip31(float mag, uint32_t bit31) {
     return __uint_as_float(__float_as_uint(mag) ^ (bit31 & 0x80000000u));
 }
 
 template <int S, bool HAS, int DC>
 __device__ __forceinline__ void cn_rows(const float *__restrict__ s, float *mn0, float *mn1, uint8_t *lc,
-                                        const uint4 *__restrict__ sgi, uint4 *__restrict__ sgo, const uint16_t *col,
-                                        int i, bool valid, int ra, int d, int dmax, int l, int lane, unsigned fm,
-                                        uint32_t fmb, bool corr, unsigned &syn_acc) {
+                                        uint32_t *__restrict__ sgw, const uint16_t *col, int i, bool valid, int ra,
+                                        int d, int dmax, int l, unsigned fm, uint32_t fmb, bool corr,
+                                        unsigned &syn_acc) {
+    constexpr int LR = S / 4;
     const float INF = __int_as_float(0x7f800000);
     const int q0 = 4 * l;
     float4 om0 = make_float4(0.f, 0.f, 0.f, 0.f), om1 = om0;
@@ -128,46 +129,53 @@ __device__ __forceinline__ void cn_rows(const float *__restrict__ s, float *mn0,
             if (fm & 8u) { om0.w = 0.f; om1.w = 0.f; }
         }
     }
-    const uint32_t mul = 1u << (31 - lane);  // moves this lane's ballot bit to bit 31
     float nm0[4] = {INF, INF, INF, INF}, nm1[4] = {INF, INF, INF, INF};
     int nloc[4] = {0xff, 0xff, 0xff, 0xff};
-    unsigned parw[4] = {0, 0, 0, 0};
     uint32_t synw[4] = {0u, 0u, 0u, 0u};  // XOR of the sign bits of s over the row: bit 31 = XOR of (1 - b_j)
+    uint32_t wo = valid ? sgw[0] : 0u, wn = 0u, pf = 0u;  // old / new sign word of the current 8 edges
+    const int pe = DC > 0 ? DC : dmax;
     // DC > 0: every row has degree DC (regular code) -- the edge loop is fully unrolled
 #pragma unroll(DC > 0 ? DC : 2)
-    for (int p = 0; p < (DC > 0 ? DC : dmax); p++) {
+    for (int p = 0; p < pe; p++) {
+        if ((DC == 0 || DC > 8) && p > 0 && (p & 7) == 0) {  // next sign word of the row
+            if (valid) sgw[((p >> 3) - 1) * LR] = wn;
+            pf ^= wn;
+            wn = 0u;
+            wo = valid ? sgw[(p >> 3) * LR] : 0u;
+        }
         const bool has = HAS ? (p < d) : true;
         const int e = ra + p;
         const int j = has ? col[e] : 0;
         const uint32_t pp = (uint32_t)p * 0x01010101u;
         const float4 sv = *reinterpret_cast<const float4 *>(s + j * S + q0);
-        const uint4 W = sgi[p];  // own sign of lambda^prev per component (Obs. 2)
         const float mg[4] = {((olc ^ pp) & 0xffu) ? om0.x : om1.x, ((olc ^ pp) & 0xff00u) ? om0.y : om1.y,
                              ((olc ^ pp) & 0xff0000u) ? om0.z : om1.z,
                              ((olc ^ pp) & 0xff000000u) ? om0.w : om1.w};  // Obs. 1 (+ row parity)
-        unsigned bal[4];
 #pragma unroll
         for (int v = 0; v < 4; v++) {
+            const int sh = 4 * (p & 7) + v;
             const float sj = f4c(sv, v);
-            const float x = sj - flip31(mg[v], f4c(W, v) * mul);  // lambda - eta^prev
+            const float x = sj - flip31(mg[v], wo << (31 - sh));  // lambda - eta^prev (Obs. 2 sign)
             const float ax = HAS ? (has ? fabsf(x) : INF) : fabsf(x);
             const bool lt = ax < nm0[v];  // first strict minimum (A13)
             nm1[v] = fminf(nm1[v], fmaxf(nm0[v], ax));
             nm0[v] = fminf(nm0[v], ax);
             nloc[v] = lt ? p : nloc[v];
-            bal[v] = __ballot_sync(FULLM, (HAS ? has : true) && x < 0.f);  // sign(0) = +1
-            synw[v] ^= (HAS ? has : true) ? __float_as_uint(sj) : 0u;      // slice(s_j) = 0 iff sign bit
+            if ((HAS ? has : true) && x < 0.f) wn |= 1u << sh;          // sign(0) = +1
+            synw[v] ^= (HAS ? has : true) ? __float_as_uint(sj) : 0u;  // slice(s_j) = 0 iff sign bit
         }
-#pragma unroll
-        for (int v = 0; v < 4; v++) parw[v] ^= bal[v];
-        if (lane == 0) sgo[p] = make_uint4(bal[0], bal[1], bal[2], bal[3]);
     }
+    if (valid) sgw[((pe - 1) >> 3) * LR] = wn;
+    pf ^= wn;
     if (valid) {
-        // this lane's row sign parity per slot, times (-1)^{d_i} under the CORRECTED rule (reading A1)
-        const uint32_t c = (corr && (d & 1)) ? 1u : 0u;
-        uint32_t sb[4];
-#pragma unroll
-        for (int v = 0; v < 4; v++) sb[v] = (((parw[v] >> lane) & 1u) ^ c) << 31;
+        // this lane's row sign parity per slot (XOR of bits v, v+4, ... of the sign words), times
+        // (-1)^{d_i} under the CORRECTED rule (reading A1)
+        uint32_t pw = pf ^ (pf >> 16);
+        pw ^= pw >> 8;
+        pw ^= pw >> 4;
+        pw ^= (corr && (d & 1)) ? 0xfu : 0u;
+        const uint32_t sb[4] = {pw << 31, (pw << 30) & 0x80000000u, (pw << 29) & 0x80000000u,
+                                (pw << 28) & 0x80000000u};
         *reinterpret_cast<float4 *>(mn0 + ca) =
             make_float4(__uint_as_float(__float_as_uint(nm0[0]) | sb[0]), __uint_as_float(__float_as_uint(nm0[1]) | sb[1]),
                         __uint_as_float(__float_as_uint(nm0[2]) | sb[2]), __uint_as_float(__float_as_uint(nm0[3]) | sb[3]));
@@ -196,7 +204,8 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
     float *mn0 = reinterpret_cast<float *>(sm + a.lay.m0);
     float *mn1 = reinterpret_cast<float *>(sm + a.lay.m1);
     uint8_t *lc = reinterpret_cast<uint8_t *>(sm + a.lay.lc);
-    uint4 *sgb = reinterpret_cast<uint4 *>(sm + a.lay.sgb);
+    uint32_t *sgr = reinterpret_cast<uint32_t *>(sm + a.lay.sgr);
+    const int WR = (a.dm + 7) / 8;  // sign words per lane and row
     uint16_t *rp = reinterpret_cast<uint16_t *>(sm + a.lay.rp);
     uint16_t *cp = reinterpret_cast<uint16_t *>(sm + a.lay.cp);
     uint16_t *col = reinterpret_cast<uint16_t *>(sm + a.lay.col);
@@ -231,9 +240,10 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
             reinterpret_cast<uint8_t *>(rec2)[e] = (uint8_t)be.z;
             continue;
         }
-        rec[e] = (uint32_t)be.y * S;  // first state element of row i (the lane adds its slot offset)
-        // ballot-word index of the edge | position p in row i << 16 | bit offset of row i in the word << 24
-        rec2[e] = (uint32_t)((be.y / G) * dm + be.z) | ((uint32_t)be.z << 16) | ((uint32_t)((be.y % G) * LR) << 24);
+        // first state element of row i (the lane adds its slot offset) | position p in row i << 24
+        rec[e] = (uint32_t)be.y * S | ((uint32_t)be.z << 24);
+        // the edge's sign word (the lane adds l) | the shift that brings its bits to 28..31 << 24
+        rec2[e] = (uint32_t)((be.y * WR + (be.z >> 3)) * LR) | ((uint32_t)(28 - 4 * (be.z & 7)) << 24);
     }
     if (tid < 32) {
         slot_f[tid] = -1;
@@ -254,9 +264,6 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
     // The first A and D (before the first C) only stage the first frames.
     unsigned active = 0;
     for (int pass = 0;; pass++) {
-        const int cur = pass & 1;  // sign words of the previous body are in buffer cur, this body's in cur ^ 1
-        const uint4 *sgi = sgb + (cur ? a.lay.sgb_half : 0);
-        uint4 *sgo = sgb + (cur ? 0 : a.lay.sgb_half);
         if (pass > 0) {
             const unsigned fresh_prev = ctl[1];
             const unsigned fm = (fresh_prev >> q0) & 0xfu;  // this lane's fresh slots (eta^prev = 0)
@@ -270,16 +277,13 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
                 const int ra = DC > 0 ? i * DC : (valid ? rp[i] : 0);
                 const int d = DC > 0 ? (valid ? DC : 0) : (valid ? (int)rp[i + 1] - ra : 0);
                 const int dmax = DC > 0 ? DC : __reduce_max_sync(FULLM, d);
-                const size_t rg = (size_t)(rb / G);
+                uint32_t *sgw = sgr + (size_t)(valid ? i : 0) * WR * LR + l;
                 if (DC > 0 && rb + G <= m)
-                    cn_rows<S, false, DC>(s, mn0, mn1, lc, sgi + rg * dm, sgo + rg * dm, col, i, valid, ra, d, dmax, l,
-                                          lane, fm, fmb, corr, syn_acc);
+                    cn_rows<S, false, DC>(s, mn0, mn1, lc, sgw, col, i, valid, ra, d, dmax, l, fm, fmb, corr, syn_acc);
                 else if (__all_sync(FULLM, d == dmax))
-                    cn_rows<S, false, 0>(s, mn0, mn1, lc, sgi + rg * dm, sgo + rg * dm, col, i, valid, ra, d, dmax, l,
-                                         lane, fm, fmb, corr, syn_acc);
+                    cn_rows<S, false, 0>(s, mn0, mn1, lc, sgw, col, i, valid, ra, d, dmax, l, fm, fmb, corr, syn_acc);
                 else
-                    cn_rows<S, true, 0>(s, mn0, mn1, lc, sgi + rg * dm, sgo + rg * dm, col, i, valid, ra, d, dmax, l,
-                                        lane, fm, fmb, corr, syn_acc);
+                    cn_rows<S, true, 0>(s, mn0, mn1, lc, sgw, col, i, valid, ra, d, dmax, l, fm, fmb, corr, syn_acc);
             }
             const unsigned mine = (syn_acc << q0) & active;
             const unsigned wmask = __reduce_or_sync(FULLM, mine);
@@ -397,33 +401,32 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
                         for (int u = 0; u < 3; u++) {
                             if (q3 + u < dv) {
                                 int ca;
-                                uint32_t pp, word, bit;
+                                uint32_t pp, widx, shift;
                                 if (CMP) {
                                     const int ro = reinterpret_cast<const uint16_t *>(rec)[c0 + q3 + u];
                                     const int pq = reinterpret_cast<const uint8_t *>(rec2)[c0 + q3 + u];
                                     const int i = ro / S;
                                     ca = ro + q0;
                                     pp = (uint32_t)pq * 0x01010101u;
-                                    word = (uint32_t)((i / G) * dm + pq);
-                                    bit = (uint32_t)((i % G) * LR);
+                                    widx = (uint32_t)((i * WR + (pq >> 3)) * LR);
+                                    shift = (uint32_t)(28 - 4 * (pq & 7));
                                 } else {
-                                    ca = (int)rec[c0 + q3 + u] + q0;
-                                    const uint32_t r2 = rec2[c0 + q3 + u];
-                                    pp = __byte_perm(r2, 0u, 0x2222u);  // position p in every byte
-                                    word = r2 & 0xffffu;
-                                    bit = r2 >> 24;
+                                    const uint32_t r1 = rec[c0 + q3 + u], r2 = rec2[c0 + q3 + u];
+                                    ca = (int)(r1 & 0xffffffu) + q0;
+                                    pp = __byte_perm(r1, 0u, 0x3333u);  // position p in every byte
+                                    widx = r2 & 0xffffffu;
+                                    shift = r2 >> 24;
                                 }
                                 const float4 m0 = *reinterpret_cast<const float4 *>(mn0 + ca);
                                 const float4 m1 = *reinterpret_cast<const float4 *>(mn1 + ca);
                                 const uint32_t lv = *reinterpret_cast<const uint32_t *>(lc + ca) ^ pp;
-                                const uint4 W = sgo[word];
-                                const uint32_t mul = 0x80000000u >> (bit + l);  // this lane's bit of row i
+                                const uint32_t ws = sgr[widx + l] << shift;  // bits of edge p -> 28..31
                                 const float mg[4] = {(lv & 0xffu) ? m0.x : m1.x, (lv & 0xff00u) ? m0.y : m1.y,
                                                      (lv & 0xff0000u) ? m0.z : m1.z,
                                                      (lv & 0xff000000u) ? m0.w : m1.w};  // Obs. 1
 #pragma unroll
                                 for (int v = 0; v < 4; v++)  // ascending rows from +0.0 (A14)
-                                    acc[v] = acc[v] + flip31(mg[v], f4c(W, v) * mul);
+                                    acc[v] = acc[v] + flip31(mg[v], ws << (3 - v));
                             }
                         }
                     }
