@@ -366,9 +366,9 @@ def run_e2e(h, llr_dev, pts, L, args, world, dev):
     st = torch.zeros(8, dtype=torch.int64)
 
     def step():
-        for lo, hi in pts:
-            sub = P.DecodeResult(outs.bits[lo:hi], outs.iters[lo:hi], outs.converged[lo:hi], None)
-            h.decode_host(host_llr[lo:hi], L, posterior=False, stats=st, out=sub)
+        # one call over the whole batch: the Eb/N0 blocks are just frames (each frame's outputs do not
+        # depend on its batch, A19), and the chunked copy / decode pipeline drains once per step
+        h.decode_host(host_llr, L, posterior=False, stats=st, out=outs)
 
     step()  # warm (pipeline buffers, graphs)
     barrier(world)
@@ -382,8 +382,8 @@ def run_e2e(h, llr_dev, pts, L, args, world, dev):
     bits = float(world) * F * n * steps
     return {"value": round(bits / secs / 1e9, 4), "unit": "Gbit/s", "steps": steps,
             "h2d_bytes_per_step": int(F * n * 4), "d2h_bytes_per_step": int(F * n + F * 4 + F),
-            "api": "ldpc_decode_host (pinned host buffers; chunked H2D / decode / D2H overlap; returns b, k, "
-                   "isCodeword and the counters)"}
+            "api": "ldpc_decode_host over the step's batch (pinned host buffers; chunked H2D / decode / D2H "
+                   "overlap; returns b, k, isCodeword and the counters)"}
 
 
 # ------------------------------------------------------------------ CPU oracle ---------------
