@@ -69,7 +69,7 @@ struct HostGraph {  // device allocations owned by the plan
 
 // ---- streaming schedule (decode_stream.cu) ----
 struct StreamLaunch {
-    int rows_per_cta = 64;  // check-node rows per CTA, <= 256 (a warp owns <= 32 rows)
+    int rows_per_cta = 128;  // check-node rows per CTA, <= 256 (a warp owns <= 32 rows); 128 measured best
     int cn_unroll = 0;      // check-node kernel: 0 = one row buffer (default), 1 = generic, 2 = two row buffers
     int check_every = 1;    // codeword test after body k when k % T == 0 (and after body L)
 };
