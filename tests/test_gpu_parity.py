@@ -236,6 +236,21 @@ def test_resident_compact_records(monkeypatch, which):
     compare(code, llr, 25, h=h)
 
 
+@pytest.mark.parametrize("shape", [(60, 200, 2, 20), (300, 900, 3, 17), (120, 128, 9, 16)])
+@pytest.mark.parametrize("flags", [FORCE_STREAM, FORCE_RESIDENT])
+def test_high_degree_irregular_rows(shape, flags):
+    """Irregular codes with rows of degree up to 20 (several sign words per row and lane in both
+    schedules; the generic streaming check node), early stop on, against the oracle."""
+    m, n, dmin, dmax = shape
+    code = codes.random_small(m, n, 31 + m, dmin, dmax)
+    h = handle(code, flags)
+    if flags == FORCE_RESIDENT:
+        assert h.schedule == "resident"
+    rng = np.random.default_rng(m)
+    llr = (rng.standard_normal((500, code.n)) * 0.8 - 1.1).astype(np.float32)
+    compare(code, llr, 15, h=h)
+
+
 def test_resident_generic_equals_regular_instance(monkeypatch):
     """The degree-specialised resident kernel for regular (3,6) codes and the generic one agree
     (LDPC_RES_GENERIC=1 forces the generic instance), and both match the oracle."""
