@@ -378,7 +378,9 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
                 const int j = cb + sub;
                 if (j >= n || !(cm | fk | fw)) continue;
                 float *sp = s + j * S + q0;
-                float4 o = *reinterpret_cast<const float4 *>(sp);
+                // the old s is needed unless all four slots continue (their s is overwritten)
+                float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (cm != 0xfu) o = *reinterpret_cast<const float4 *>(sp);
                 if (fk) {
 #pragma unroll
                     for (int v = 0; v < 4; v++) {
