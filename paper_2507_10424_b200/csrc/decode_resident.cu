@@ -515,11 +515,9 @@ void launch_c(const ResArgs &args, int ctas, size_t smem, cudaStream_t st) {
 
 template <int S, int RT>
 void launch_s(const ResArgs &args, int ctas, size_t smem, cudaStream_t st) {
-    if constexpr (S <= 8 && (RT == 256 || RT == 512)) {
-        if (args.compact) {
-            launch_c<S, RT, true>(args, ctas, smem, st);
-            return;
-        }
+    if (args.compact) {  // the planner only picks compact records with S <= 8 and 256 / 512 threads
+        if constexpr (S <= 8 && (RT == 256 || RT == 512)) launch_c<S, RT, true>(args, ctas, smem, st);
+        return;
     }
     launch_c<S, RT, false>(args, ctas, smem, st);
 }
@@ -572,6 +570,7 @@ ResidentPlan plan_resident(const HostGraph &g, bool loc16, int device) {
             rp.threads = per_sm >= 2 ? 256 : 512;
             if (force_t == 128 || force_t == 256 || force_t == 384 || force_t == 512 || force_t == 1024)
                 rp.threads = force_t;
+            if (compact && rp.threads != 256) rp.threads = 512;  // compact records: 256- or 512-thread kernels only
             const int fit = rp.threads == 128   ? per_sm
                             : rp.threads == 256 ? std::min(per_sm, S == 4 ? 3 : 2)
                             : rp.threads == 384 ? std::min(per_sm, 2)

@@ -251,6 +251,20 @@ def test_high_degree_irregular_rows(shape, flags):
     compare(code, llr, 15, h=h)
 
 
+@pytest.mark.parametrize("threads", ["128", "384", "1024"])
+def test_resident_forced_threads(monkeypatch, threads):
+    """LDPC_RES_THREADS forces the CTA size; with compact records the planner falls back to a compact
+    kernel size (regression: a 384-thread request once launched the non-compact kernel on a compact
+    layout)."""
+    monkeypatch.setenv("LDPC_RES_THREADS", threads)
+    code = codes.regular(504, 1008, 3, 6, 1008)
+    rng = np.random.default_rng(int(threads))
+    llr = (rng.standard_normal((400, code.n)) * 1.2 - 0.9).astype(np.float32)
+    compare(code, llr, 25, h=handle(code, FORCE_RESIDENT))
+    monkeypatch.setenv("LDPC_RES_COMPACT", "1")
+    compare(code, llr, 25, h=handle(code, FORCE_RESIDENT))
+
+
 def test_resident_generic_equals_regular_instance(monkeypatch):
     """The degree-specialised resident kernel for regular (3,6) codes and the generic one agree
     (LDPC_RES_GENERIC=1 forces the generic instance), and both match the oracle."""
