@@ -265,6 +265,28 @@ def test_resident_forced_threads(monkeypatch, threads):
     compare(code, llr, 25, h=handle(code, FORCE_RESIDENT))
 
 
+@pytest.mark.parametrize("case", range(int(__import__("os").environ.get("LDPC_RAND_CASES", "12"))))
+def test_randomised_shapes_flags_and_check_points(case):
+    """Randomised sweep: code shape (rows of degree 2..14, columns of degree 0 allowed), sign rule,
+    early stop, checkEvery and batch size, both schedules, against the oracle."""
+    rng = np.random.default_rng(1000 + case)
+    m = int(rng.integers(8, 400))
+    n = int(rng.integers(m + 4, 3 * m + 40))
+    dmin = int(rng.integers(2, 5))
+    dmax = int(rng.integers(dmin, 15))
+    code = codes.random_small(m, n, 77 + case, dmin, dmax)
+    flags = int(rng.choice([0, LIT, NOES, LIT | NOES]))
+    T = int(rng.choice([1, 1, 2, 3, 6]))
+    L = int(rng.integers(1, 30))
+    F = int(rng.integers(1, 700))
+    llr = (rng.standard_normal((F, code.n)) * rng.uniform(0.5, 2.0) - rng.uniform(0.0, 2.0)).astype(np.float32)
+    for sched in (FORCE_STREAM, FORCE_RESIDENT):
+        h = handle(code, flags | sched)
+        if h.schedule == "unavailable":
+            continue
+        compare(code, llr, L, flags | sched, h=h, check_every=T)
+
+
 def test_resident_generic_equals_regular_instance(monkeypatch):
     """The degree-specialised resident kernel for regular (3,6) codes and the generic one agree
     (LDPC_RES_GENERIC=1 forces the generic instance), and both match the oracle."""
