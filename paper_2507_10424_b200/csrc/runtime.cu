@@ -484,8 +484,10 @@ int ldpc_decode_host(ldpc_handle_t h, const float *llr, int64_t frames, int32_t 
     int rc = LDPC_OK;
     int idx = 0;
     bool used[2] = {false, false};
-    for (int64_t c0 = 0; c0 < frames && rc == LDPC_OK; c0 += chunk, idx ^= 1) {
-        const int64_t fc = std::min(chunk, frames - c0);
+    // chunk sizes ramp up geometrically from chunk/16 (the first copy, which nothing overlaps, is short)
+    int64_t cur = std::max<int64_t>(TILE, (chunk / 16 + TILE - 1) / TILE * TILE);
+    for (int64_t c0 = 0, fc = 0; c0 < frames && rc == LDPC_OK; c0 += fc, idx ^= 1, cur = std::min(chunk, 2 * cur)) {
+        fc = std::min(cur, frames - c0);
         char *base = static_cast<char *>(h->hbuf[idx]);
         float *d_llr = reinterpret_cast<float *>(base);
         uint8_t *d_bits = reinterpret_cast<uint8_t *>(base + align256(chunk * n * 4));
