@@ -602,41 +602,62 @@ __global__ void __launch_bounds__(CTA) k_syndrome(Graph g, StreamState w, int sl
 // ------------------------------------------------------------------------------------------------
 // a7: stage-out.  s [T][n][128] -> posterior [F][n], bits = slice(s) [F][n]; per-frame counters.
 // ------------------------------------------------------------------------------------------------
+constexpr int FIN_SUB = 8;  // 32-column sub-blocks per finalize CTA
+
 __global__ void __launch_bounds__(CTA) k_finalize(StreamState w, int n, int64_t frames, float *__restrict__ post,
                                                   uint8_t *__restrict__ bits) {
     __shared__ float ts[32][TILE + 1];
     __shared__ float tr[32][TILE + 1];
-    const int t = blockIdx.y, j0 = blockIdx.x * 32;
+    const int t = blockIdx.y;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int jl = warp; jl < 32; jl += CTA / 32) {
-        const int j = j0 + jl;
-        if (j >= n) break;
-        const size_t base = ((size_t)t * n + j) * TILE;
+    // per-frame counters over the CTA's 256 columns: lane q holds frame warp + 8q (q < 16); one atomic
+    // per frame and CTA instead of one per 32 columns
+    int be_acc = 0, raw_acc = 0;
+    bool nz_acc = false;
+    for (int sb = 0; sb < FIN_SUB; sb++) {
+        const int j0 = (blockIdx.x * FIN_SUB + sb) * 32;
+        if (j0 >= n) break;
+        for (int jl = warp; jl < 32; jl += CTA / 32) {
+            const int j = j0 + jl;
+            if (j >= n) break;
+            const size_t base = ((size_t)t * n + j) * TILE;
 #pragma unroll
-        for (int q = 0; q < 4; q++) {
-            ts[jl][lane + 32 * q] = w.s[base + lane + 32 * q];
-            tr[jl][lane + 32 * q] = w.r[base + lane + 32 * q];
+            for (int q = 0; q < 4; q++) {
+                ts[jl][lane + 32 * q] = w.s[base + lane + 32 * q];
+                tr[jl][lane + 32 * q] = w.r[base + lane + 32 * q];
+            }
         }
+        __syncthreads();
+        const int j = j0 + lane;
+        const bool jv = j < n;
+#pragma unroll 4
+        for (int q = 0; q < TILE / (CTA / 32); q++) {
+            const int fl = warp + (CTA / 32) * q;
+            const int64_t f = (int64_t)t * TILE + fl;
+            if (f >= frames) break;
+            const float sv = ts[lane][fl];
+            const bool b = jv && sv > 0.f;  // Eq. slice
+            if (jv) {
+                if (post) post[f * n + j] = sv;
+                if (bits) bits[f * n + j] = (uint8_t)b;
+            }
+            const int be = __popc(__ballot_sync(FULL, b));
+            const int raw = __popc(__ballot_sync(FULL, jv && tr[lane][fl] > 0.f));
+            const bool nz = __any_sync(FULL, jv && fabsf(sv) <= 1e-4f);
+            if (lane == q) {
+                be_acc += be;
+                raw_acc += raw;
+                nz_acc = nz_acc || nz;
+            }
+        }
+        __syncthreads();  // the next sub-block overwrites ts / tr
     }
-    __syncthreads();
-    const int j = j0 + lane;
-    const bool jv = j < n;
-    for (int fl = warp; fl < TILE; fl += CTA / 32) {
-        const int64_t f = (int64_t)t * TILE + fl;
-        if (f >= frames) break;
-        const float sv = ts[lane][fl];
-        const bool b = jv && sv > 0.f;  // Eq. slice
-        if (jv) {
-            if (post) post[f * n + j] = sv;
-            if (bits) bits[f * n + j] = (uint8_t)b;
-        }
-        const int be = __popc(__ballot_sync(FULL, b));
-        const int raw = __popc(__ballot_sync(FULL, jv && tr[lane][fl] > 0.f));
-        const bool nz = __any_sync(FULL, jv && fabsf(sv) <= 1e-4f);
-        if (lane == 0) {
-            if (be) atomicAdd(w.fbe + (size_t)t * TILE + fl, be);
-            if (raw) atomicAdd(w.fraw + (size_t)t * TILE + fl, raw);
-            if (nz) w.fnz[(size_t)t * TILE + fl] = 1;
+    if (lane < TILE / (CTA / 32)) {
+        const int fl = warp + (CTA / 32) * lane;
+        if ((int64_t)t * TILE + fl < frames) {
+            if (be_acc) atomicAdd(w.fbe + (size_t)t * TILE + fl, be_acc);
+            if (raw_acc) atomicAdd(w.fraw + (size_t)t * TILE + fl, raw_acc);
+            if (nz_acc) w.fnz[(size_t)t * TILE + fl] = 1;
         }
     }
 }
@@ -786,7 +807,7 @@ int launch_loop_step(const StreamState &w, int L, cudaGraphConditionalHandle h, 
 
 int launch_finalize(const Graph &g, const StreamState &w, int64_t frames, float *posterior, uint8_t *bits,
                     cudaStream_t st) {
-    k_finalize<<<grid2((g.n + 31) / 32, w.T), CTA, 0, st>>>(w, g.n, frames, posterior, bits);
+    k_finalize<<<grid2((g.n + 32 * FIN_SUB - 1) / (32 * FIN_SUB), w.T), CTA, 0, st>>>(w, g.n, frames, posterior, bits);
     return 1;
 }
 
