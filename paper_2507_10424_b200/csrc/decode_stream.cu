@@ -165,6 +165,9 @@ constexpr int CN_CHUNK = 8;  // edges per sign word and per batch of gathers (4 
 #ifndef BNL_MINB
 #define BNL_MINB 6
 #endif
+#ifndef CN_T
+#define CN_T CTA
+#endif
 #ifndef BNL_T
 #define BNL_T 128  // bit-node CTA size: 128 threads x 12 CTAs per SM measured 1.5-2 % faster than 256 x 6
 #endif
@@ -402,7 +405,7 @@ __device__ __forceinline__ void cn_compute(const CnRow<CH, LocT> &R, int i, int 
 }
 
 template <int CH, typename LocT, bool FIRST, bool EARLY, bool DB>
-__global__ void __launch_bounds__(CTA, DB ? 2 : CN1_MINB)
+__global__ void __launch_bounds__(CN_T, (DB ? 2 : CN1_MINB) * CTA / CN_T)
     k_cn_pipe(Graph g, StreamState w, int k, int rows_per_cta, int literal, const int *kdev) {
     if (kdev) k = *kdev;  // body index supplied by the graph-driven loop
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -425,14 +428,15 @@ __global__ void __launch_bounds__(CTA, DB ? 2 : CN1_MINB)
     LocT *__restrict__ LCl = reinterpret_cast<LocT *>(RB + 1024) + 4 * lane;
     uint32_t *__restrict__ SGl = reinterpret_cast<uint32_t *>(RB + 1024 + 128 * sizeof(LocT)) + lane;
     const int i0 = blockIdx.x * rows_per_cta + warp, i1 = min(m, blockIdx.x * rows_per_cta + rows_per_cta);
-    const int nr = i0 < i1 ? (i1 - i0 + 7) / 8 : 0;  // rows of this warp (<= 32)
+    constexpr int NW = CN_T / 32;  // warps per CTA
+    const int nr = i0 < i1 ? (i1 - i0 + NW - 1) / NW : 0;  // rows of this warp (<= 32)
     if (nr == 0) return;
     int ra = 0, rb = 0;  // lane q: row_ptr of the warp's row q
     if (lane < nr) {
-        ra = __ldg(g.row_ptr + i0 + 8 * lane);
-        rb = __ldg(g.row_ptr + i0 + 8 * lane + 1);
+        ra = __ldg(g.row_ptr + i0 + NW * lane);
+        rb = __ldg(g.row_ptr + i0 + NW * lane + 1);
     }
-    auto row_of = [&](int q) { return i0 + 8 * min(q, nr - 1); };
+    auto row_of = [&](int q) { return i0 + NW * min(q, nr - 1); };
     auto deg_of = [&](int q) { return __shfl_sync(FULL, rb, q & 31) - __shfl_sync(FULL, ra, q & 31); };
     auto cols_of = [&](int q) {  // lane p: column of edge p of row q (0 past the degree / past the rows)
         const int a = __shfl_sync(FULL, ra, q & 31), d = __shfl_sync(FULL, rb, q & 31) - a;
@@ -742,12 +746,12 @@ void cn_launch(dim3 grid, cudaStream_t st, const Graph &g, const StreamState &w,
                const int *kdev) {
     // u: 0 = single row buffer (default), 2 = two row buffers, 1 = generic kernel
     if (u != 1 && u != 2 && g.dmax <= 8) {
-        if (g.dmax <= 4) k_cn_pipe<4, LT, F, EA, false><<<grid, CTA, 0, st>>>(g, w, k, rpc, lit, kdev);
-        else if (g.dmax <= 6) k_cn_pipe<6, LT, F, EA, false><<<grid, CTA, 0, st>>>(g, w, k, rpc, lit, kdev);
-        else if (g.dmax == 7) k_cn_pipe<7, LT, F, EA, false><<<grid, CTA, 0, st>>>(g, w, k, rpc, lit, kdev);
-        else k_cn_pipe<8, LT, F, EA, false><<<grid, CTA, 0, st>>>(g, w, k, rpc, lit, kdev);
-    } else if (u == 2 && g.dmax <= 6) k_cn_pipe<6, LT, F, EA, true><<<grid, CTA, 0, st>>>(g, w, k, rpc, lit, kdev);
-    else if (u == 2 && g.dmax <= 8) k_cn_pipe<8, LT, F, EA, true><<<grid, CTA, 0, st>>>(g, w, k, rpc, lit, kdev);
+        if (g.dmax <= 4) k_cn_pipe<4, LT, F, EA, false><<<grid, CN_T, 0, st>>>(g, w, k, rpc, lit, kdev);
+        else if (g.dmax <= 6) k_cn_pipe<6, LT, F, EA, false><<<grid, CN_T, 0, st>>>(g, w, k, rpc, lit, kdev);
+        else if (g.dmax == 7) k_cn_pipe<7, LT, F, EA, false><<<grid, CN_T, 0, st>>>(g, w, k, rpc, lit, kdev);
+        else k_cn_pipe<8, LT, F, EA, false><<<grid, CN_T, 0, st>>>(g, w, k, rpc, lit, kdev);
+    } else if (u == 2 && g.dmax <= 6) k_cn_pipe<6, LT, F, EA, true><<<grid, CN_T, 0, st>>>(g, w, k, rpc, lit, kdev);
+    else if (u == 2 && g.dmax <= 8) k_cn_pipe<8, LT, F, EA, true><<<grid, CN_T, 0, st>>>(g, w, k, rpc, lit, kdev);
     else k_cn<LT, F, EA><<<grid, CTA, 0, st>>>(g, w, k, rpc, lit, kdev);
 }
 
