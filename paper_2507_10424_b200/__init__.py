@@ -61,6 +61,28 @@ def _require_cuda(t: torch.Tensor, name: str, dtype: torch.dtype):
         raise ValueError(f"{name} must be contiguous")
 
 
+def _check_out(t, name: str, shape: tuple, dtype: torch.dtype, device):
+    """A caller-supplied output buffer: exact shape, dtype, contiguity and device (the C-ABI writes
+    frames x n elements through the raw pointer, so a mismatch would be an out-of-bounds write)."""
+    if t is None:
+        return
+    if tuple(t.shape) != shape:
+        raise ValueError(f"out.{name} must have shape {shape}, got {tuple(t.shape)}")
+    if t.dtype != dtype:
+        raise ValueError(f"out.{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"out.{name} must be contiguous")
+    if t.device != device:
+        raise ValueError(f"out.{name} must be on {device}, got {t.device}")
+
+
+def _check_result(out, F: int, n: int, device):
+    _check_out(out.bits, "bits", (F, n), torch.uint8, device)
+    _check_out(out.iters, "iters", (F,), torch.int32, device)
+    _check_out(out.converged, "converged", (F,), torch.uint8, device)
+    _check_out(out.posterior, "posterior", (F, n), torch.float32, device)
+
+
 @dataclass
 class DecodeResult:
     bits: torch.Tensor | None  # [F, n] uint8
@@ -120,7 +142,11 @@ class Handle:
             raise ValueError(f"llr must be [frames, {self.n}]")
         F = llr.shape[0]
         dev = llr.device
-        if out is None:
+        if dev != self.device:
+            raise ValueError(f"llr is on {dev}, the handle on {self.device}")
+        if out is not None:
+            _check_result(out, F, self.n, dev)
+        else:
             out = DecodeResult(
                 torch.empty((F, self.n), dtype=torch.uint8, device=dev) if bits else None,
                 torch.empty(F, dtype=torch.int32, device=dev) if iters else None,
@@ -130,6 +156,8 @@ class Handle:
             _require_cuda(stats, "stats", torch.int64)
             if stats.numel() != 8:
                 raise ValueError("stats must hold 8 int64 counters")
+            if stats.device != dev:
+                raise ValueError(f"stats must be on {dev}")
         with torch.cuda.device(dev):
             _check(self._lib.ldpc_decode(self._h, llr.data_ptr(), F, int(max_iter), _ptr(out.bits), _ptr(out.iters),
                                          _ptr(out.posterior), _ptr(out.converged), _ptr(stats), _stream(stream)),
@@ -141,16 +169,21 @@ class Handle:
         """ldpc_decode_host: llr and all outputs in HOST memory (pin them for copy/compute overlap)."""
         if llr.is_cuda or llr.dtype != torch.float32 or not llr.is_contiguous():
             raise ValueError("llr must be a contiguous float32 CPU tensor")
+        if llr.dim() != 2 or llr.shape[1] != self.n:
+            raise ValueError(f"llr must be [frames, {self.n}]")
         F = llr.shape[0]
-        if out is None:
+        if out is not None:
+            _check_result(out, F, self.n, torch.device("cpu"))
+        else:
             pin = llr.is_pinned()
             out = DecodeResult(
                 torch.empty((F, self.n), dtype=torch.uint8, pin_memory=pin) if bits else None,
                 torch.empty(F, dtype=torch.int32, pin_memory=pin) if iters else None,
                 torch.empty(F, dtype=torch.uint8, pin_memory=pin) if converged else None,
                 torch.empty((F, self.n), dtype=torch.float32, pin_memory=pin) if posterior else None)
-        if stats is not None and (stats.is_cuda or stats.dtype != torch.int64 or stats.numel() != 8):
-            raise ValueError("stats must be a CPU int64 tensor of 8 counters")
+        if stats is not None and (stats.is_cuda or stats.dtype != torch.int64 or stats.numel() != 8
+                                  or not stats.is_contiguous()):
+            raise ValueError("stats must be a contiguous CPU int64 tensor of 8 counters")
         with torch.cuda.device(self.device):
             _check(self._lib.ldpc_decode_host(self._h, llr.data_ptr(), F, int(max_iter), _ptr(out.bits),
                                               _ptr(out.iters), _ptr(out.posterior), _ptr(out.converged), _ptr(stats),

@@ -430,7 +430,9 @@ __global__ void __launch_bounds__(CN_T, (DB ? 2 : CN1_MINB) * CTA / CN_T)
     const int i0 = blockIdx.x * rows_per_cta + warp, i1 = min(m, blockIdx.x * rows_per_cta + rows_per_cta);
     constexpr int NW = CN_T / 32;  // warps per CTA
     const int nr = i0 < i1 ? (i1 - i0 + NW - 1) / NW : 0;  // rows of this warp (<= 32)
-    if (nr == 0) return;
+    uint32_t u[4] = {0u, 0u, 0u, 0u};
+    // a warp without rows must still reach the CTA barrier of the EARLY epilogue
+    if (nr > 0) {
     int ra = 0, rb = 0;  // lane q: row_ptr of the warp's row q
     if (lane < nr) {
         ra = __ldg(g.row_ptr + i0 + NW * lane);
@@ -442,7 +444,6 @@ __global__ void __launch_bounds__(CN_T, (DB ? 2 : CN1_MINB) * CTA / CN_T)
         const int a = __shfl_sync(FULL, ra, q & 31), d = __shfl_sync(FULL, rb, q & 31) - a;
         return (q < nr && lane < d) ? __ldg(g.col_idx + a + lane) : 0;
     };
-    uint32_t u[4] = {0u, 0u, 0u, 0u};
     if (!DB) {  // one row buffer: all loads of a row in flight together, more warps per SM
         CnRow<CH, LocT> A;
         int cj = cols_of(0);
@@ -466,6 +467,7 @@ __global__ void __launch_bounds__(CN_T, (DB ? 2 : CN1_MINB) * CTA / CN_T)
         cn_compute<CH, LocT, FIRST, EARLY>(B, row_of(q + 1), deg_of(q + 1), literal, SGl, M0l, M1l, LCl, RSW, RSL, u);
     }
     }
+    }  // nr > 0
     if (EARLY) {
         if (lane == 0) {
 #pragma unroll
@@ -719,6 +721,7 @@ __global__ void k_loop_pre(StreamState w, int L, cudaGraphConditionalHandle h) {
     const int k = 2;
     const bool run = k <= L && w.tcount[k & 1] > 0;
     *w.kdev = k;
+    if (run && w.nlaunch) *w.nlaunch += 3;  // check node, bit node, step of body k
     if (!run) w.tcount[(L + 1) & 1] = 0;
     cudaGraphSetConditional(h, run ? 1u : 0u);
 }
@@ -727,6 +730,7 @@ __global__ void k_loop_step(StreamState w, int L, cudaGraphConditionalHandle h) 
     const int k = *w.kdev + 1;
     const bool run = k <= L && w.tcount[k & 1] > 0;
     *w.kdev = k;
+    if (run && w.nlaunch) *w.nlaunch += 3;
     if (!run && k <= L) w.tcount[(L + 1) & 1] = 0;
     cudaGraphSetConditional(h, run ? 1u : 0u);
 }

@@ -51,6 +51,7 @@ struct StreamState {
     int *tcount;  // [2]     number of tiles with a running frame, per body parity
     int *tlist;   // [2][T]  those tiles
     int *kdev;    // body index of the graph-driven loop
+    unsigned long long *nlaunch;  // launches of graph-driven loop bodies (3 per body that ran), or null
 };
 
 // ---- ingest (ingest.cu) ----

@@ -58,6 +58,12 @@ struct ldpc_plan {
     cudaStream_t hs[3] = {nullptr, nullptr, nullptr};
     void *hbuf[2] = {nullptr, nullptr};
     size_t hbuf_bytes = 0;
+    unsigned long long *hstats = nullptr;  // device counters of ldpc_decode_host (64 B, allocated once)
+    // device-side accounting of graph-driven loop bodies (3 launches per body that ran)
+    unsigned long long *dev_launches = nullptr;
+    // completion of the handle's last enqueued work (ldpc_destroy waits for it, not for the device)
+    cudaEvent_t last = nullptr;
+    bool last_recorded = false;
 };
 
 namespace {
@@ -136,6 +142,7 @@ StreamState carve(void *base, int T, const HostGraph &g, bool loc16) {
     w.tcount = reinterpret_cast<int *>(take(2 * 4));
     w.tlist = reinterpret_cast<int *>(take((size_t)2 * T * 4));
     w.kdev = reinterpret_cast<int *>(take(4));
+    w.nlaunch = nullptr;  // set by the caller (a plan-owned counter that outlives the workspace)
     return w;
 }
 
@@ -183,6 +190,10 @@ int check_async(ldpc_plan *h) {
     return LDPC_OK;
 }
 
+// kernels of a chunk graph outside the WHILE node: stage-in, check + bit node of body 1, loop_pre,
+// final syndrome, finalize, frame stats.  Each WHILE iteration adds 3 (counted by the loop kernels).
+constexpr int GRAPH_STATIC_LAUNCHES = 7;
+
 // One chunk as a CUDA graph: stage-in, body 1, then a conditional WHILE node whose body (check node,
 // bit node, loop step) repeats while a frame is still running and k <= L, then the final syndrome
 // pass and stage-out.  No host round trip and no launch for bodies after the last frame stopped.
@@ -199,7 +210,7 @@ int run_graph(ldpc_plan *h, const Graph &g, const StreamState &w, const float *l
                 h->poisoned = true;
                 return LDPC_ERR_CUDA;
             }
-            h->launches += 4 + 3 + 3 * L;  // upper bound: stage-in, body 1, pre, bodies, tail
+            h->launches += GRAPH_STATIC_LAUNCHES;  // the loop bodies are counted on the device
             return LDPC_OK;
         }
     }
@@ -276,7 +287,7 @@ int run_graph(ldpc_plan *h, const Graph &g, const StreamState &w, const float *l
         h->poisoned = true;
         return LDPC_ERR_CUDA;
     }
-    h->launches += 4 + 3 + 3 * L;
+    h->launches += GRAPH_STATIC_LAUNCHES;
     return LDPC_OK;
 }
 
@@ -293,11 +304,19 @@ int decode_stream(ldpc_plan *h, const float *llr, int64_t frames, int L, uint8_t
     int rc = ensure_ws(h, T_max, loc16);
     if (rc) return rc;
     const int final_slot = (L + 1) & 1;
+    if (!h->dev_launches) {
+        if (cudaMalloc(&h->dev_launches, sizeof(unsigned long long)) != cudaSuccess) {
+            cudaGetLastError();
+            return LDPC_ERR_OOM;
+        }
+        if (cudaMemsetAsync(h->dev_launches, 0, sizeof(unsigned long long), st) != cudaSuccess) return LDPC_ERR_CUDA;
+    }
     const bool graphs = h->use_graphs && !h->prof && L >= 2 && !(h->flags & LDPC_FLAG_NO_GRAPH);
     for (int64_t c0 = 0; c0 < frames; c0 += (int64_t)T_max * TILE) {
         const int64_t fc = std::min<int64_t>((int64_t)T_max * TILE, frames - c0);
         const int T = (int)((fc + TILE - 1) / TILE);
-        const StreamState w = carve(h->ws, T, h->g, loc16);
+        StreamState w = carve(h->ws, T, h->g, loc16);
+        w.nlaunch = h->dev_launches;
         const float *cl = llr + c0 * g.n;
         float *cp = post ? post + c0 * g.n : nullptr;
         uint8_t *cb = bits ? bits + c0 * g.n : nullptr;
@@ -353,11 +372,28 @@ int decode_resident(ldpc_plan *h, const float *llr, int64_t frames, int L, uint8
         }
     }
     const Graph g = h->g.view();
-    launch(h, LDPC_K_RESIDENT, st, [&] {
-        return launch_resident(g, h->rp, llr, frames, L, h->check_every, early, literal, loc16, post, bits, iters,
-                               conv, reinterpret_cast<unsigned long long *>(stats), h->work_counter, st);
-    });
+    // the kernel's work counter and slot frame indices are 32-bit: at most 2^30 frames per launch
+    const int64_t n = g.n, cap = (int64_t)1 << 30;
+    for (int64_t c0 = 0; c0 < frames; c0 += cap) {
+        const int64_t fc = std::min(cap, frames - c0);
+        launch(h, LDPC_K_RESIDENT, st, [&] {
+            return launch_resident(g, h->rp, llr + c0 * n, fc, L, h->check_every, early, literal, loc16,
+                                   post ? post + c0 * n : nullptr, bits ? bits + c0 * n : nullptr,
+                                   iters ? iters + c0 : nullptr, conv ? conv + c0 : nullptr,
+                                   reinterpret_cast<unsigned long long *>(stats), h->work_counter, st);
+        });
+    }
     return check_async(h);
+}
+
+// remember the end of the handle's last enqueued work on `st` (ldpc_destroy waits for it)
+void mark_last(ldpc_plan *h, cudaStream_t st) {
+    if (!h->last && cudaEventCreateWithFlags(&h->last, cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        h->last = nullptr;
+        return;
+    }
+    h->last_recorded = cudaEventRecord(h->last, st) == cudaSuccess;
 }
 
 int finish_prepare(ldpc_plan *p, int rc, uint32_t flags, ldpc_handle_t *out) {
@@ -424,11 +460,12 @@ int ldpc_decode(ldpc_handle_t h, const float *llr, int64_t frames, int32_t max_i
     if (h->poisoned) return LDPC_ERR_CUDA;
     if (frames == 0) return LDPC_OK;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (use_resident(h))
-        return decode_resident(h, llr, frames, max_iter, bits_out, iters_out, posterior_out, converged_out,
-                               stats_inout, st);
-    return decode_stream(h, llr, frames, max_iter, bits_out, iters_out, posterior_out, converged_out, stats_inout,
-                         st);
+    const int rc = use_resident(h) ? decode_resident(h, llr, frames, max_iter, bits_out, iters_out, posterior_out,
+                                                     converged_out, stats_inout, st)
+                                   : decode_stream(h, llr, frames, max_iter, bits_out, iters_out, posterior_out,
+                                                   converged_out, stats_inout, st);
+    mark_last(h, st);
+    return rc;
 }
 
 int ldpc_decode_host(ldpc_handle_t h, const float *llr, int64_t frames, int32_t max_iter, uint8_t *bits_out,
@@ -468,6 +505,14 @@ int ldpc_decode_host(ldpc_handle_t h, const float *llr, int64_t frames, int32_t 
             }
         h->hbuf_bytes = set_bytes;
     }
+    if (stats_inout && !h->hstats) {
+        if (cudaMalloc(&h->hstats, 64) != cudaSuccess) {
+            cudaGetLastError();
+            h->hstats = nullptr;
+            return LDPC_ERR_OOM;
+        }
+    }
+    // every allocation is done: from here on, all paths return the events to the pool
     cudaStream_t user = static_cast<cudaStream_t>(stream);
     cudaStream_t s_in = h->hs[0], s_run = h->hs[1], s_out = h->hs[2];
     cudaEvent_t ev_start = get_event(h), ev_in[2] = {get_event(h), get_event(h)},
@@ -476,11 +521,8 @@ int ldpc_decode_host(ldpc_handle_t h, const float *llr, int64_t frames, int32_t 
     cudaStreamWaitEvent(s_in, ev_start, 0);
     cudaStreamWaitEvent(s_run, ev_start, 0);
     cudaStreamWaitEvent(s_out, ev_start, 0);
-    unsigned long long *d_stats = nullptr;
-    if (stats_inout) {
-        if (cudaMalloc(&d_stats, 64) != cudaSuccess) return LDPC_ERR_OOM;
-        cudaMemsetAsync(d_stats, 0, 64, s_run);
-    }
+    unsigned long long *d_stats = stats_inout ? h->hstats : nullptr;
+    if (d_stats) cudaMemsetAsync(d_stats, 0, 64, s_run);
     int rc = LDPC_OK;
     int idx = 0;
     bool used[2] = {false, false};
@@ -519,7 +561,6 @@ int ldpc_decode_host(ldpc_handle_t h, const float *llr, int64_t frames, int32_t 
     e = cudaStreamSynchronize(s_out);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s_run);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s_in);
-    if (d_stats) cudaFree(d_stats);
     h->pool.push_back(ev_start);
     for (int q = 0; q < 2; q++) {
         h->pool.push_back(ev_in[q]);
@@ -620,12 +661,33 @@ int ldpc_profile_reset(ldpc_handle_t h) {
     return rc;
 }
 
-int64_t ldpc_launch_count(ldpc_handle_t h) { return h ? h->launches : -1; }
+int64_t ldpc_launch_count(ldpc_handle_t h) {
+    if (!h) return -1;
+    unsigned long long dev = 0;
+    if (h->dev_launches) {  // loop bodies launched by graph conditional nodes (synchronises the device)
+        if (cudaDeviceSynchronize() != cudaSuccess ||
+            cudaMemcpy(&dev, h->dev_launches, sizeof(dev), cudaMemcpyDeviceToHost) != cudaSuccess) {
+            cudaGetLastError();
+            dev = 0;
+        }
+    }
+    return h->launches + (int64_t)dev;
+}
 
 void ldpc_destroy(ldpc_handle_t h) {
     if (!h) return;
-    cudaDeviceSynchronize();
+    // wait for this handle's own work only (its last decode and its internal streams), not the device
+    if (h->last) {
+        if (h->last_recorded) cudaEventSynchronize(h->last);
+        cudaEventDestroy(h->last);
+    }
+    for (int q = 0; q < 3; q++)
+        if (h->hs[q]) cudaStreamSynchronize(h->hs[q]);
+    for (int q = 0; q < 2; q++)
+        if (h->cap[q]) cudaStreamSynchronize(h->cap[q]);
     h->g.free_all();
+    cudaFree(h->hstats);
+    cudaFree(h->dev_launches);
     cudaFree(h->ws);
     cudaFree(h->work_counter);
     for (int q = 0; q < 2; q++) cudaFree(h->hbuf[q]);
