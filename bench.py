@@ -1,23 +1,35 @@
 #!/usr/bin/env python
 """Benchmark: decoded Gbps of batched Min-Sum LDPC decoding on B200 (BASELINE.json "metric").
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl reference]
-    torchrun --nproc-per-node N bench.py --gpus N ...      (one process per GPU, NCCL)
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl reference]
+    python -m torch.distributed.run --nproc-per-node N bench.py --gpus N ...   (one process per GPU)
 
-A step is one pass of the whole hot path (ingested H; stage-in, check-node / bit-node sweeps with
-fused syndrome and per-frame early stop, stage-out and counters) over this rank's batch: config C2 =
-2^20 frames of a random (3,6)-regular 504x1008 code split into 7 contiguous Eb/N0 blocks
-1.0..4.0 dB, max_iter 50, decoded by one ldpc_decode call (--per-block: one per Eb/N0 block).  Frames are keyed by global frame
-index, so rank r of N decodes its own 2^20 frames (weak scaling); the only collectives are the
-barrier, the MAX of the elapsed time and the SUM of the 8 counters.
+`--gpus N` without torchrun's environment re-launches itself through torch.distributed.run with N
+ranks (127.0.0.1 rendezvous), one process per GPU over NCCL.
 
-value = (frames decoded by all ranks) * n / (max-over-ranks device time), in Gbit/s.
+A step is one pass of the whole hot path over this rank's batch (steps a2-a7 of SURVEY 8(a) with H
+already ingested): stage-in, check-node / bit-node sweeps with the fused syndrome and per-frame early
+stop, stage-out and counters.  The default workload is config C3 (random H with 5G-NR BG1 lifted
+dimensions 17664 x 26112, 65,536 frames over Eb/N0 {2, 3, 3.5, 4, 5} dB, max_iter 20), the largest
+configuration of BASELINE.json that fits one GPU; C1-C6 are selectable (`--config`).  C5 decodes all
+16 codes (16 handles) per step.
+
+Scaling: frames are keyed by their global index, so a frame decodes identically on any rank.  Weak
+scaling (default): rank r of N decodes its own full batch (global frames r F .. (r+1) F).  Strong
+(`--strong`, default for C4 as SURVEY 8(d) specifies): the config's F frames are split over the N
+ranks.  The only collectives are the barrier, the MAX of the elapsed time and the SUM of the counters.
+
+value = (frames decoded by all ranks) * n / (max-over-ranks device time of the K timed steps), Gbit/s.
+The timed steps run the product path (CUDA-graph loop, no per-kernel events); the per-kernel split
+behind `roofline` comes from one separate profiled step (per-kernel CUDA events, plain launches).
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -34,34 +46,65 @@ from gen import channel, codes  # noqa: E402
 METRIC = "decoded Gbps (1/2/4/8 B200) at fixed max_iter; % of HBM roofline"
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
+DEFAULT_CONFIG = "c3"
+DEFAULT_SCALING = {"c4": "strong"}  # C4's 16,384 frames are sharded over the GPUs
 
 
-def hbm_peak():
+def peaks():
     try:
         with open(PEAKS_PATH) as f:
-            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+            d = json.load(f)
+        return float(d["hbm_gbs"]), float(d.get("sm_max_mhz", 1965.0)), "measured (MEASURED_PEAKS.json)"
     except Exception:
-        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+        return FALLBACK_HBM, 1965.0, "fallback (B200_PROFILING.md)"
 
 
-def describe(cfg_name, cfg, code):
-    te = cfg.get("check_every", 1)
-    return (f"{cfg_name}: {code.name} ({code.m}x{code.n}, nnz {code.nnz}), {cfg['frames']} frames per GPU over "
-            f"Eb/N0 {cfg['ebn0']} dB, max_iter {cfg['max_iter']}"
-            + (f", codeword test every {te} bodies" if te != 1 else "") + ", BPSK/AWGN all-zero codeword")
+# ------------------------------------------------------------------ launcher / distributed ---
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
 
 
-# ------------------------------------------------------------------ distributed plumbing -------
-def dist_setup(n_gpus):
+def relaunch_if_needed(args, argv):
+    """`--gpus N` (N > 1) outside torchrun: re-exec as N ranks through torch.distributed.run."""
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + argv
+        sys.stdout.flush()
+        sys.stderr.flush()
+        os.execv(sys.executable, cmd)
+
+
+def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    info = {"backend": None, "world": world}
     if world > 1:
         import torch.distributed as dist
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
-    return rank, world, local
+        cuda = torch.cuda.is_available() and not args.dry_run
+        backend = "nccl" if cuda else "gloo"
+        if cuda:
+            torch.cuda.set_device(local)
+            dist.init_process_group(backend, device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+        # NCCL builds its communicator lazily: force it now (outside any timed region) and log it
+        t = torch.ones(1, device=torch.device("cuda", local) if cuda else "cpu")
+        dist.all_reduce(t)
+        ver = ".".join(map(str, torch.cuda.nccl.version())) if cuda else None
+        info = {"backend": backend, "world": world, "nccl_version": ver, "all_reduce_check": int(t.item())}
+        print(f"[bench] rank {rank}/{world} local_rank {local}: {backend} process group up"
+              + (f" (NCCL {ver})" if ver else "") + f", all_reduce(1) = {int(t.item())}", file=sys.stderr, flush=True)
+    if args.gpus != world and rank == 0:
+        print(f"[bench] warning: --gpus {args.gpus} but WORLD_SIZE={world}; reporting n_gpus={world}",
+              file=sys.stderr)
+    return rank, world, local, info
 
 
 def barrier(world):
@@ -93,7 +136,7 @@ def reduce_sum_(t, world):
 class ClockSampler:
     FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
               "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
-              "clocks_event_reasons.sw_power_cap"]
+              "clocks_event_reasons.sw_power_cap", "power.draw"]
     NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
@@ -122,7 +165,7 @@ class ClockSampler:
             self.lines = [ln for ln in out.splitlines() if ln.strip()]
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
+        sm, mx, pw, reasons = [], [], [], set()
         for ln in getattr(self, "lines", []):
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 6:
@@ -135,26 +178,84 @@ class ClockSampler:
             for name, v in zip(self.NAMES, parts[2:6]):
                 if v.lower() == "active":
                     reasons.add(name)
+            try:
+                pw.append(float(parts[6]))
+            except (IndexError, ValueError):
+                pass
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+               "samples": len(sm)}
+        if pw:
+            out["power_w_median"] = statistics.median(pw)
+        return out
 
 
 # ------------------------------------------------------------------ workload -----------------
-def build_workload(cfg_name, rank, dev):
-    cfg = codes.CONFIGS[cfg_name]
-    code = cfg["code"]()
-    if isinstance(code, list):
-        code = code[0]
+def code_list(cfg):
+    c = cfg["code"]()
+    return c if isinstance(c, list) else [c]
+
+
+def scaling_of(args):
+    if args.strong:
+        return "strong"
+    if args.weak:
+        return "weak"
+    return DEFAULT_SCALING.get(args.config, "weak")
+
+
+def rank_shard(cfg, rank, world, scaling):
+    """(w0, count, goff): this rank decodes workload frames w0 .. w0+count of the config's batch (whose
+    index w sets the Eb/N0 block), generated at global frame index g = w + goff."""
     F = cfg["frames"]
-    pts = codes.point_ranges(F, len(cfg["ebn0"]))
-    llr = torch.empty((F, code.n), dtype=torch.float32, device=dev)
+    if scaling == "strong":
+        lo, hi = codes.shard_range(F, rank, world)
+        return lo, hi - lo, 0
+    return 0, F, rank * F
+
+
+def gen_frames(code, cfg, seed, w0, count, goff, device="cpu", out=None):
+    """LLRs of workload frames [w0, w0+count) (all-zero codeword, BPSK/AWGN, keyed by global index)
+    and the Eb/N0 block index of each."""
+    pts = codes.point_ranges(cfg["frames"], len(cfg["ebn0"]))
+    if out is None:
+        out = torch.empty((count, code.n), dtype=torch.float32, device=device)
+    pidx = np.zeros(count, np.int64)
     for p, (lo, hi) in enumerate(pts):
-        # global frame index of this rank's frames: rank * F + local (weak scaling)
-        channel.bpsk_awgn(code.n, code.rate, cfg["ebn0"][p], cfg["seed"], p, rank * F + lo, hi - lo, device=dev,
-                          out=llr[lo:hi])
-    return cfg, code, llr, pts
+        a, b = max(lo, w0), min(hi, w0 + count)
+        if a >= b:
+            continue
+        channel.bpsk_awgn(code.n, code.rate, cfg["ebn0"][p], seed, p, a + goff, b - a, device=device,
+                          out=out[a - w0:b - w0])
+        pidx[a - w0:b - w0] = p
+    return out, pidx
+
+
+def seed_of(cfg, h):
+    return cfg["seed"] + h  # C5: code h is decoded with its own frames (seeds 4096 + h)
+
+
+def describe(cfg_name, cfg, cl):
+    te = cfg.get("check_every", 1)
+    c = cl[0]
+    what = (f"{len(cl)} codes {c.m}x{c.n} (nnz {c.nnz} each)" if len(cl) > 1 else
+            f"{c.name} ({c.m}x{c.n}, nnz {c.nnz})")
+    return (f"{cfg_name}: {what}, {cfg['frames']} frames per code over Eb/N0 {cfg['ebn0']} dB, max_iter "
+            f"{cfg['max_iter']}" + (f", codeword test every {te} bodies" if te != 1 else "")
+            + ", BPSK/AWGN all-zero codeword")
+
+
+def config_dict(args, cfg, cl, world, scaling, frames_rank):
+    """The `config` object of both arms (identical for --impl ours / reference)."""
+    c = cl[0]
+    F = cfg["frames"]
+    gb = F * len(cl) * (world if scaling == "weak" else 1)
+    return {"workload": describe(args.config, cfg, cl), "global_batch": gb, "frames_per_gpu": frames_rank * len(cl),
+            "codes": len(cl), "m": c.m, "n": c.n, "nnz": c.nnz, "max_iter": cfg["max_iter"], "ebn0_db": cfg["ebn0"],
+            "check_every": cfg.get("check_every", 1), "flags": args.flags,
+            "parallelism": f"dp{world} (frame shards, {scaling} scaling, no data-path collective)",
+            "l2": f"inputs {frames_rank * len(cl) * c.n * 4 / 1e9:.2f} GB per GPU > 126 MB L2 (no flush needed)"}
 
 
 def units(iters: np.ndarray, L: int, early: bool):
@@ -191,43 +292,74 @@ OPS_CN, OPS_BN = 9, 3
 ALU_CN, ALU_BN = 8, 2
 
 
+def ncu_traffic(cfg_name, kernel):
+    """Per-launch DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of the kernel in the committed
+    ncu --set full capture (profiles/ncu_traffic.json), with that launch's algorithmic bytes."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            e = json.load(f)[cfg_name][kernel]
+        alg = e.get("algorithmic_bytes_this_launch")
+        return (e["dram_bytes_per_launch"], round(e["dram_bytes_per_launch"] / alg, 3) if alg else None,
+                e.get("source", "profiles/ncu_traffic.json"))
+    except Exception:
+        return None, None, None
+
+
 # ------------------------------------------------------------------ our arm ------------------
 def run_ours(args):
     import paper_2507_10424_b200 as P
 
-    rank, world, local = dist_setup(args.gpus)
+    rank, world, local, dinfo = dist_setup(args)
+    scaling = scaling_of(args)
+    cfg = codes.CONFIGS[args.config]
+    cl = code_list(cfg)
+    w0, Fr, goff = rank_shard(cfg, rank, world, scaling)
+    if args.dry_run:  # launcher / sharding check without a GPU: the rank's frames and their checksum
+        c = cl[0]
+        llr, _ = gen_frames(c, cfg, seed_of(cfg, 0), w0, Fr, goff)
+        print(json.dumps({"dry_run": True, "rank": rank, "world": world, "scaling": scaling,
+                          "workload_frames": [w0, w0 + Fr], "global_frames": [w0 + goff, w0 + goff + Fr],
+                          "llr_sha1": hashlib.sha1(llr.numpy().tobytes()).hexdigest(), "dist": dinfo}), flush=True)
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+            dist.destroy_process_group()
+        return
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    cfg, code, llr, pts = build_workload(args.config, rank, dev)
-    F, n, L = cfg["frames"], code.n, cfg["max_iter"]
-    rr, cc = code.coo()
-    h = P.Handle.from_coo(torch.from_numpy(rr).to(dev), torch.from_numpy(cc).to(dev), code.m, code.n,
-                          flags=args.flags)
+    L = cfg["max_iter"]
     T = cfg.get("check_every", 1)
-    if T != 1:
-        h.set_check_every(T)
-    out = P.DecodeResult(torch.empty((F, n), dtype=torch.uint8, device=dev),
-                         torch.empty(F, dtype=torch.int32, device=dev),
-                         torch.empty(F, dtype=torch.uint8, device=dev),
-                         torch.empty((F, n), dtype=torch.float32, device=dev))
-    stats = torch.zeros((len(pts), 8), dtype=torch.int64, device=dev)
+    n = cl[0].n
+    # ---- per code: H ingested once (not timed), this rank's frames resident in HBM, output buffers
+    jobs = []
+    for hi, code in enumerate(cl):
+        rr, cc = code.coo()
+        h = P.Handle.from_coo(torch.from_numpy(rr).to(dev), torch.from_numpy(cc).to(dev), code.m, code.n,
+                              flags=args.flags)
+        if T != 1:
+            h.set_check_every(T)
+        llr, pidx = gen_frames(code, cfg, seed_of(cfg, hi), w0, Fr, goff, device=dev)
+        out = P.DecodeResult(torch.empty((Fr, n), dtype=torch.uint8, device=dev),
+                             torch.empty(Fr, dtype=torch.int32, device=dev),
+                             torch.empty(Fr, dtype=torch.uint8, device=dev),
+                             torch.empty((Fr, n), dtype=torch.float32, device=dev))
+        jobs.append(dict(code=code, h=h, llr=llr, pidx=pidx, out=out,
+                         stats=torch.zeros(8, dtype=torch.int64, device=dev)))
     stream = torch.cuda.current_stream()
+    sched = jobs[0]["h"].schedule
 
     def step():
-        if args.per_block:  # one decode per Eb/N0 block
-            for p, (lo, hi) in enumerate(pts):
-                sub = P.DecodeResult(out.bits[lo:hi], out.iters[lo:hi], out.converged[lo:hi], out.posterior[lo:hi])
-                h.decode(llr[lo:hi], L, posterior=True, stats=stats[p], out=sub, stream=stream)
-        else:  # one decode over the batch (the blocks are just frames: outputs do not depend on the batch, A19)
-            h.decode(llr, L, posterior=True, stats=stats[0], out=out, stream=stream)
+        for j in jobs:  # one ldpc_decode per code over the rank's whole batch (the Eb/N0 blocks are just
+            # frames: each frame's outputs do not depend on its batch, A19)
+            j["h"].decode(j["llr"], L, posterior=True, stats=j["stats"], out=j["out"], stream=stream)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    stats.zero_()
-    h.profile(True)
-    h.profile_reset()
-    launches0 = h.launch_count
+    for j in jobs:
+        j["stats"].zero_()
+    launches0 = sum(j["h"].launch_count for j in jobs)  # synchronises (device-side loop counters)
     barrier(world)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -238,152 +370,195 @@ def run_ours(args):
         e1.record(stream)
         torch.cuda.synchronize()
     barrier(world)
-    launches = h.launch_count - launches0
     ms_local = e0.elapsed_time(e1)
-    prof = h.profile_read()
-    h.profile(False)
+    launches = sum(j["h"].launch_count for j in jobs) - launches0
     ms = reduce_max(ms_local, world, dev)
-    tot_stats = reduce_sum_(stats.sum(dim=0).clone(), world).cpu().numpy()
-    if args.per_block:
-        per_point = stats.cpu().numpy()
-    else:  # per-block counters of one step, from the outputs (same definitions as the decoder's stats)
-        rows = []
-        for lo, hi in pts:
-            be = out.bits[lo:hi].sum(dim=1, dtype=torch.int64)
-            it = out.iters[lo:hi].to(torch.int64)
-            cv = out.converged[lo:hi].to(torch.int64)
-            nz = (out.posterior[lo:hi].abs() <= 1e-4).any(dim=1)
-            raw = (llr[lo:hi] > 0).sum(dtype=torch.int64)
-            rows.append([hi - lo, int(be.sum()), int((be > 0).sum()), int(((be > 0) & (cv > 0)).sum()),
-                         int(it.sum()), int(cv.sum()), int(nz.sum()), int(raw)])
-        per_point = np.array(rows, dtype=np.int64)
+    tot_stats = reduce_sum_(sum(j["stats"] for j in jobs).clone(), world).cpu().numpy()
 
-    # ---- roofline of the dominant kernel (per-launch algorithmic bytes / per-launch device time)
-    iters_np = out.iters.cpu().numpy()
+    # ---- one profiled step (per-kernel CUDA events on the launching stream; plain launches, no graph):
+    # the per-kernel split and the roofline of the dominant kernel
+    for j in jobs:
+        j["h"].profile(True)
+        j["h"].profile_reset()
+    torch.cuda.synchronize()
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    step()
+    p1.record(stream)
+    torch.cuda.synchronize()
+    prof_step_ms = p0.elapsed_time(p1)
+    prof = {}
+    for j in jobs:
+        for k, (nl, kms) in j["h"].profile_read().items():
+            a = prof.setdefault(k, [0, 0.0])
+            a[0] += nl
+            a[1] += kms
+        j["h"].profile(False)
+
     early = not (args.flags & P.FLAG_NO_EARLY_STOP)
-    cn_b, bn_b, io_b = algorithmic_bytes(code, iters_np, L, early)
-    cu, bu = units(iters_np, L, early)
-    peak, peak_src = hbm_peak()
-    if h.schedule == "resident":
-        kern = {"resident": cn_b + bn_b + io_b}
-    else:
-        kern = {"check_node": cn_b, "bit_node": bn_b}
-    dom = max(kern, key=lambda c: prof[c][1])
-    n_launch, kms = prof[dom]
-    roof = None
-    if n_launch and kms > 0:
-        per_launch_bytes = kern[dom] * args.steps / n_launch
-        per_launch_s = kms / 1e3 / n_launch
-        achieved = per_launch_bytes / per_launch_s / 1e9
-        roof = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": traffic_from_profiles(args.config, dom),
-                "traffic_vs_algorithmic_in_capture": traffic_ratio_from_profiles(args.config, dom),
-                "algorithmic_bytes_per_launch": round(per_launch_bytes), "avg_launch_us": round(per_launch_s * 1e6, 2),
-                "share_of_step": round(kms / ms_local, 4), "peak_source": peak_src,
-                "kernel_ms": {k: round(v[1], 3) for k, v in prof.items() if v[0]},
-                "kernel_launches": {k: v[0] for k, v in prof.items() if v[0]}}
-        if dom == "resident":
-            roof["note"] = ("state is SMEM-resident: the algorithmic bytes (B_comp per frame-body, SURVEY 8(d)) "
-                            "stay on chip, DRAM carries only I/O (see traffic)")
-            sm_mhz = 1965.0
-            try:
-                with open(PEAKS_PATH) as f:
-                    sm_mhz = float(json.load(f).get("sm_max_mhz", sm_mhz))
-            except Exception:
-                pass
-            issue_peak = 148 * 4 * 32 * sm_mhz * 1e6 / 1e12  # lane-instructions per s, T
-            ops = (float(cu.sum()) * OPS_CN + float(bu.sum()) * OPS_BN) * code.nnz * args.steps
-            ach = ops / (kms / 1e3) / 1e12
-            alu_peak = issue_peak / 2  # 16 lanes per cycle per sub-partition
-            alu = (float(cu.sum()) * ALU_CN + float(bu.sum()) * ALU_BN) * code.nnz * args.steps / (kms / 1e3) / 1e12
-            roof["issue_roofline"] = {"bound": "alu", "achieved": round(ach, 3), "peak": round(issue_peak, 2),
-                                      "unit": "T lane-ops/s", "frac": round(ach / issue_peak, 4),
-                                      "ops_per_frame_edge": {"check_node": OPS_CN, "bit_node": OPS_BN},
-                                      "alu_pipe": {"achieved": round(alu, 3), "peak": round(alu_peak, 2),
-                                                   "frac": round(alu / alu_peak, 4),
-                                                   "ops_per_frame_edge": {"check_node": ALU_CN, "bit_node": ALU_BN}}}
-    total_bits = float(world) * F * n * args.steps
-    value = total_bits / (ms / 1e3) / 1e9
+    cn_b = bn_b = io_b = 0.0
+    cu_sum = bu_sum = 0.0
+    per_point, per_code_fer = [], []
+    for j in jobs:
+        it = j["out"].iters.cpu().numpy()
+        a, b, c = algorithmic_bytes(j["code"], it, L, early)
+        cn_b, bn_b, io_b = cn_b + a, bn_b + b, io_b + c
+        cu, bu = units(it, L, early)
+        cu_sum += float(cu.sum()) * j["code"].nnz
+        bu_sum += float(bu.sum()) * j["code"].nnz
+        rows = point_rows(j, cfg)
+        per_point.append(rows)
+        per_code_fer.append([r[2] / max(1, r[0]) for r in rows])
+    per_point = np.sum(np.array(per_point, dtype=np.int64), axis=0)
+    hbm, sm_mhz, peak_src = peaks()
+    roof = roofline(args, sched, prof, prof_step_ms, cn_b, bn_b, io_b, cu_sum, bu_sum, hbm, sm_mhz, peak_src, ms_local,
+                    args.steps)
+    value = float(reduce_sum_(torch.tensor([Fr * len(cl) * n], dtype=torch.float64, device=dev), world).item())
+    value = value * args.steps / (ms / 1e3) / 1e9
 
-    # ---- end to end through the host-buffer C-ABI call (copies inside the timed region)
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(h, llr, pts, L, args, world, dev)
+        e2e = run_e2e(jobs, L, args, world, dev)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(cfg, code, args)
+        cpu = cpu_baseline(args, cfg, cl)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 4), "unit": "Gbit/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": describe(args.config, cfg, code), "global_batch": world * F,
-                       "frames_per_gpu": F, "m": code.m, "n": code.n, "nnz": code.nnz, "max_iter": L,
-                       "ebn0_db": cfg["ebn0"], "check_every": T, "schedule": h.schedule, "flags": args.flags,
-                       "parallelism": f"dp{world} (frame shards, no data-path collective)",
-                       "l2": f"inputs {F * n * 4 / 1e9:.2f} GB per GPU > 126 MB L2 (no flush needed)"},
+            "scaling": scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": config_dict(args, cfg, cl, world, scaling, Fr),
+            "schedule": sched,
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
+            "dist": dinfo,
             "stats": {k: int(v) for k, v in zip(P.STATS_FIELDS, tot_stats)},
             "per_point": [{"ebn0_db": cfg["ebn0"][p], "frames": int(s[0]), "fer": s[2] / max(1, s[0]),
                            "ber": s[1] / max(1, s[0] * n), "raw_ber": s[7] / max(1, s[0] * n),
                            "avg_iters": s[4] / max(1, s[0]), "near_zero_frames": int(s[6])}
                           for p, s in enumerate(per_point)],
         }
+        if len(cl) > 1:  # C5: FER vs Eb/N0 of every code (the code-selection result)
+            line["fer_per_code"] = {cl[q].name: [round(x, 6) for x in per_code_fer[q]] for q in range(len(cl))}
         print(json.dumps(line), flush=True)
-    h.close()
+    for j in jobs:
+        j["h"].close()
     if world > 1:
         import torch.distributed as dist
 
         dist.destroy_process_group()
 
 
-def traffic_ratio_from_profiles(cfg_name, kernel):
-    """DRAM bytes / algorithmic bytes of the captured launch (a full-work launch), if recorded."""
-    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    try:
-        with open(path) as f:
-            e = json.load(f)[cfg_name][kernel]
-        return round(e["dram_bytes_per_launch"] / e["algorithmic_bytes_this_launch"], 3)
-    except Exception:
+def point_rows(j, cfg):
+    """Per Eb/N0 block counters of one step, from the outputs (same definitions as the decoder's stats)."""
+    out, llr, pidx = j["out"], j["llr"], j["pidx"]
+    rows = []
+    for p in range(len(cfg["ebn0"])):
+        sel = np.nonzero(pidx == p)[0]
+        if len(sel) == 0:
+            rows.append([0] * 8)
+            continue
+        lo, hi = int(sel[0]), int(sel[-1]) + 1  # blocks are contiguous
+        be = out.bits[lo:hi].sum(dim=1, dtype=torch.int64)
+        it = out.iters[lo:hi].to(torch.int64)
+        cv = out.converged[lo:hi].to(torch.int64)
+        nz = (out.posterior[lo:hi].abs() <= 1e-4).any(dim=1)
+        raw = (llr[lo:hi] > 0).sum(dtype=torch.int64)
+        rows.append([hi - lo, int(be.sum()), int((be > 0).sum()), int(((be > 0) & (cv > 0)).sum()),
+                     int(it.sum()), int(cv.sum()), int(nz.sum()), int(raw)])
+    return rows
+
+
+def roofline(args, sched, prof, prof_step_ms, cn_b, bn_b, io_b, cu_edges, bu_edges, hbm, sm_mhz, peak_src,
+             ms_local, steps):
+    """Roofline of the dominant kernel, from the profiled step (algorithmic bytes per step of that kernel
+    class / its summed CUDA-event time in that step), plus the whole-step fraction of the timed steps."""
+    kms = {k: v[1] for k, v in prof.items() if v[0]}
+    kl = {k: v[0] for k, v in prof.items() if v[0]}
+    step_ms = ms_local / steps
+    step_alg = cn_b + bn_b + io_b
+    whole = {"algorithmic_bytes_per_step": round(step_alg), "ideal_ms_at_peak": round(step_alg / hbm / 1e6, 3),
+             "ms_per_step": round(step_ms, 3), "frac": round(step_alg / (step_ms / 1e3) / 1e9 / hbm, 4),
+             "what": "SURVEY 8(d): (sum over frames of iters x B_comp + B_io) / peak, against the timed step"}
+    if sched == "resident":
+        t = kms.get("resident", 0.0)
+        if t <= 0:
+            return None
+        nl = kl["resident"]
+        issue_peak = 148 * 4 * 32 * sm_mhz * 1e6 / 1e12  # T lane-instructions per s
+        ops = cu_edges * OPS_CN + bu_edges * OPS_BN
+        ach = ops / (t / 1e3) / 1e12
+        alu = (cu_edges * ALU_CN + bu_edges * ALU_BN) / (t / 1e3) / 1e12
+        traffic, tratio, tsrc = ncu_traffic(args.config, "resident")
+        model = step_alg / (t / 1e3) / 1e9
+        return {"bound": "alu", "kernel": "resident", "achieved": round(ach, 3), "peak": round(issue_peak, 2),
+                "unit": "T lane-ops/s", "frac": round(ach / issue_peak, 4), "traffic": traffic,
+                "traffic_source": tsrc,
+                "what": ("SMEM-resident schedule: issue/ALU bound.  achieved = the method's minimum lane operations "
+                         f"({OPS_CN} per frame-edge per check-node pass, {OPS_BN} per bit-node pass) / kernel time; "
+                         "peak = 4 warp-instructions/clk/SM x 32 lanes x 148 SMs x sm_max_mhz"),
+                "alu_pipe": {"achieved": round(alu, 3), "peak": round(issue_peak / 2, 2),
+                             "frac": round(alu / (issue_peak / 2), 4),
+                             "ops_per_frame_edge": {"check_node": ALU_CN, "bit_node": ALU_BN}},
+                "dram": {"bytes_per_launch": round(io_b / nl), "achieved_gbs": round(io_b / (t / 1e3) / 1e9, 1),
+                         "frac_of_peak": round(io_b / (t / 1e3) / 1e9 / hbm, 4),
+                         "what": "the I/O (B_io per frame) is all the DRAM traffic; the state stays on chip"},
+                "hbm_model": {"achieved_gbs": round(model, 1), "peak": hbm, "frac": round(model / hbm, 4),
+                              "what": ("MODEL fraction: the B_comp bytes an HBM-streaming implementation of the same "
+                                       "method would move, per second of this kernel; they never leave the SM")},
+                "peak_source": peak_src, "avg_launch_us": round(t / nl * 1e3, 2), "kernel_launches": kl,
+                "kernel_ms_profiled_step": {k: round(v, 3) for k, v in kms.items()},
+                "share_of_step": round(t / prof_step_ms, 4), "whole_step": whole}
+    bytes_of = {"check_node": cn_b, "bit_node": bn_b}
+    sweeps = {}
+    for k, b in bytes_of.items():
+        if kms.get(k, 0) > 0:
+            ach = b / (kms[k] / 1e3) / 1e9
+            traffic, tratio, tsrc = ncu_traffic(args.config, k)
+            sweeps[k] = {"achieved": round(ach, 1), "frac": round(ach / hbm, 4),
+                         "algorithmic_bytes_per_launch": round(b / kl[k]), "avg_launch_us": round(kms[k] / kl[k] * 1e3, 2),
+                         "launches": kl[k], "share_of_step": round(kms[k] / prof_step_ms, 4),
+                         "traffic": traffic, "traffic_vs_algorithmic_in_capture": tratio}
+    if not sweeps:
         return None
+    dom = max(sweeps, key=lambda k: kms[k])
+    d = sweeps[dom]
+    traffic, tratio, tsrc = ncu_traffic(args.config, dom)
+    return {"bound": "hbm", "kernel": dom, "achieved": d["achieved"], "peak": hbm, "unit": "GB/s", "frac": d["frac"],
+            "traffic": traffic, "traffic_vs_algorithmic_in_capture": tratio, "traffic_source": tsrc,
+            "algorithmic_bytes_per_launch": d["algorithmic_bytes_per_launch"], "avg_launch_us": d["avg_launch_us"],
+            "share_of_step": d["share_of_step"], "peak_source": peak_src, "sweeps": sweeps,
+            "kernel_ms_profiled_step": {k: round(v, 3) for k, v in kms.items()}, "kernel_launches": kl,
+            "profiled_step_ms": round(prof_step_ms, 3), "whole_step": whole,
+            "what": ("achieved = algorithmic bytes of the kernel class in one step (SURVEY 8(d) B_comp split by "
+                     "sweep, per frame and body that frame ran) / its summed CUDA-event time in a separate "
+                     "profiled step (plain launches); the timed steps run the CUDA-graph loop")}
 
 
-def traffic_from_profiles(cfg_name, kernel):
-    """Per-launch DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of the kernel from the
-    committed ncu --set full summary, if one exists for this config."""
-    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    try:
-        with open(path) as f:
-            d = json.load(f)
-        return d[cfg_name][kernel]["dram_bytes_per_launch"]
-    except Exception:
-        return None
-
-
-def run_e2e(h, llr_dev, pts, L, args, world, dev):
+def run_e2e(jobs, L, args, world, dev):
     """The same workload through the host-buffer C-ABI call (ldpc_decode_host): every step copies the
     LLRs host->device from pinned memory and the decisions (bits, k, isCodeword) back, inside the timed
     region.  The soft output is not returned here, which keeps the pinned footprint per rank at
-    LLRs + bits (5.3 GB for C2) when eight ranks share one host."""
-    F, n = llr_dev.shape
-    host_llr = llr_dev.cpu().pin_memory()
+    LLRs + bits when eight ranks share one host."""
     import paper_2507_10424_b200 as P
 
-    outs = P.DecodeResult(torch.empty((F, n), dtype=torch.uint8).pin_memory(),
-                          torch.empty(F, dtype=torch.int32).pin_memory(),
-                          torch.empty(F, dtype=torch.uint8).pin_memory(), None)
-    st = torch.zeros(8, dtype=torch.int64)
+    hosts = []
+    for j in jobs:
+        F, n = j["llr"].shape
+        hosts.append((j["h"], j["llr"].cpu().pin_memory(),
+                      P.DecodeResult(torch.empty((F, n), dtype=torch.uint8).pin_memory(),
+                                     torch.empty(F, dtype=torch.int32).pin_memory(),
+                                     torch.empty(F, dtype=torch.uint8).pin_memory(), None),
+                      torch.zeros(8, dtype=torch.int64)))
 
     def step():
-        # one call over the whole batch: the Eb/N0 blocks are just frames (each frame's outputs do not
-        # depend on its batch, A19), and the chunked copy / decode pipeline drains once per step
-        h.decode_host(host_llr, L, posterior=False, stats=st, out=outs)
+        for h, hl, o, st in hosts:  # one call per code over the whole batch
+            h.decode_host(hl, L, posterior=False, stats=st, out=o)
 
     step()  # warm (pipeline buffers, graphs)
     barrier(world)
@@ -394,6 +569,8 @@ def run_e2e(h, llr_dev, pts, L, args, world, dev):
         step()
     t1 = time.perf_counter()
     secs = reduce_max(t1 - t0, world, dev)
+    F = sum(hl.shape[0] for _, hl, _, _ in hosts)
+    n = hosts[0][1].shape[1]
     bits = float(world) * F * n * steps
     return {"value": round(bits / secs / 1e9, 4), "unit": "Gbit/s", "steps": steps,
             "h2d_bytes_per_step": int(F * n * 4), "d2h_bytes_per_step": int(F * n + F * 4 + F),
@@ -402,106 +579,117 @@ def run_e2e(h, llr_dev, pts, L, args, world, dev):
 
 
 # ------------------------------------------------------------------ CPU oracle ---------------
-def cpu_baseline(cfg, code, args, budget_s: float = 15.0):
+def oracle_sample(cfg, cl, per_point, offset=0):
+    """A bounded, deterministic sample of the workload: per Eb/N0 block, `per_point` frames evenly spaced
+    over the block (C5: the codes taken round robin).  Returns [(code index, llr [k, n])]."""
+    F = cfg["frames"]
+    pts = codes.point_ranges(F, len(cfg["ebn0"]))
+    groups = {}
+    for p, (lo, hi) in enumerate(pts):
+        k = min(per_point, hi - lo)
+        idx = lo + (np.arange(k) * ((hi - lo) // k) + offset) % (hi - lo)
+        for q, w in enumerate(idx):
+            h = (q + p) % len(cl)
+            groups.setdefault(h, []).append(channel.bpsk_awgn(cl[h].n, cl[h].rate, cfg["ebn0"][p], seed_of(cfg, h), p,
+                                                              int(w), 1).numpy())
+    return [(h, np.concatenate(v)) for h, v in sorted(groups.items())]
+
+
+def time_oracle(cfg, cl, sample, threads):
+    import oracle
+
+    t0 = time.perf_counter()
+    nb = 0
+    for h, llr in sample:
+        oracle.decode(cl[h].oracle_h(), llr, cfg["max_iter"], threads=threads, check_every=cfg.get("check_every", 1))
+        nb += llr.shape[0] * cl[h].n
+    secs = time.perf_counter() - t0
+    return nb / secs / 1e9, secs, sum(x.shape[0] for _, x in sample)
+
+
+def cpu_baseline(args, cfg, cl, budget_s: float = 15.0):
+    """The oracle as it stands on the host cores (all threads, plus one thread on a smaller sample)."""
     import oracle
 
     oracle.build()
     threads = oracle.max_threads()
-    F = cfg["frames"]
-    pts = codes.point_ranges(F, len(cfg["ebn0"]))
-
-    def sample(per_point):
-        parts = []
-        for p, (lo, hi) in enumerate(pts):
-            idx = np.linspace(lo, hi - 1, per_point).astype(np.int64)
-            for i in idx:
-                parts.append(channel.bpsk_awgn(code.n, code.rate, cfg["ebn0"][p], cfg["seed"], p, int(i), 1).numpy())
-        return np.concatenate(parts)
-
-    # calibrate on a small sample, then size the timed sample for ~budget_s of CPU work
-    cal = sample(max(1, threads // len(pts) + 1))
-    t0 = time.perf_counter()
-    oracle.decode(code.oracle_h(), cal, cfg["max_iter"], threads=threads, check_every=cfg.get("check_every", 1))
-    t_cal = time.perf_counter() - t0
-    per_frame = t_cal / len(cal)
-    per_point = int(max(1, min(5000, budget_s / max(per_frame, 1e-6) / len(pts))))
-    llr = sample(per_point)
-    t0 = time.perf_counter()
-    oracle.decode(code.oracle_h(), llr, cfg["max_iter"], threads=threads, check_every=cfg.get("check_every", 1))
-    secs = time.perf_counter() - t0
-    gbps = len(llr) * code.n / secs / 1e9
+    npts = len(cfg["ebn0"])
+    g, _, nf = time_oracle(cfg, cl, oracle_sample(cfg, cl, max(1, threads // npts + 1), offset=7), threads)
+    per_frame = cl[0].n / (g * 1e9)
+    per_point = int(max(1, min(5000, budget_s / max(per_frame, 1e-7) / npts)))
+    gbps, secs, nf = time_oracle(cfg, cl, oracle_sample(cfg, cl, per_point), threads)
+    pp1 = max(1, int(per_point * 5.0 / budget_s / max(1, threads)))
+    g1, s1, nf1 = time_oracle(cfg, cl, oracle_sample(cfg, cl, pp1, offset=3), 1)
     return {"value": round(gbps, 6), "unit": "Gbit/s", "cores": threads, "kind": "oracle",
-            "sample": f"{per_point} frames per Eb/N0 block x {len(pts)} blocks = {len(llr)} frames, evenly "
-                      f"spaced over the {F}-frame batch; {secs:.1f} s on {threads} threads"}
+            "sample": f"{nf} frames ({per_point} per Eb/N0 block, evenly spaced over the {cfg['frames']}-frame batch"
+                      + (", codes round robin" if len(cl) > 1 else "") + f"); {secs:.1f} s on {threads} threads",
+            "single_thread": {"value": round(g1, 6), "unit": "Gbit/s", "cores": 1,
+                              "sample": f"{nf1} frames ({pp1} per block); {s1:.1f} s on 1 thread"}}
 
 
 def run_reference(args):
-    """--impl reference: the CPU oracle (the only reference this tier has) on the same workload."""
+    """--impl reference: the CPU oracle (the only reference this tier has) on the same workload, each step a
+    bounded sample of it (the same evenly spaced frames each step, shifted by the step index)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    cfg = codes.CONFIGS[args.config]
-    code = cfg["code"]()
-    if isinstance(code, list):
-        code = code[0]
     import oracle
 
     oracle.build()
     threads = oracle.max_threads()
-    F = cfg["frames"]
-    pts = codes.point_ranges(F, len(cfg["ebn0"]))
-    per_point = max(1, int(os.environ.get("REF_FRAMES_PER_POINT", "1024")))
-
-    def sample(step_idx):
-        parts = []
-        for p, (lo, hi) in enumerate(pts):
-            idx = lo + (np.arange(per_point) * ((hi - lo) // per_point) + step_idx) % (hi - lo)
-            for i in idx:
-                parts.append(channel.bpsk_awgn(code.n, code.rate, cfg["ebn0"][p], cfg["seed"], p, int(i), 1).numpy())
-        return np.concatenate(parts)
-
+    cfg = codes.CONFIGS[args.config]
+    cl = code_list(cfg)
+    npts = len(cfg["ebn0"])
+    per_point = int(os.environ.get("REF_FRAMES_PER_POINT", "0")) or int(
+        max(1, min(1024, 64e6 / (cl[0].n * npts))))  # about 64 Mbit of frames per step
     for w in range(args.warmup):
-        oracle.decode(code.oracle_h(), sample(1000 + w), cfg["max_iter"], threads=threads,
-                      check_every=cfg.get("check_every", 1))
-    tot_t, tot_frames = 0.0, 0
+        time_oracle(cfg, cl, oracle_sample(cfg, cl, max(1, per_point // 8), offset=1000 + w), threads)
+    tot_b, tot_t = 0.0, 0.0
+    nf = 0
     for s in range(args.steps):
-        llr = sample(s)
-        t0 = time.perf_counter()
-        oracle.decode(code.oracle_h(), llr, cfg["max_iter"], threads=threads, check_every=cfg.get("check_every", 1))
-        tot_t += time.perf_counter() - t0
-        tot_frames += len(llr)
-    value = tot_frames * code.n / tot_t / 1e9
-    desc = (f"{per_point} frames per Eb/N0 block x {len(pts)} blocks per step (every "
-            f"{F // len(pts) // per_point}-th frame of each block of the {F}-frame batch)")
+        g, secs, k = time_oracle(cfg, cl, oracle_sample(cfg, cl, per_point, offset=s), threads)
+        tot_b += g * 1e9 * secs
+        tot_t += secs
+        nf = k
+    value = tot_b / tot_t / 1e9
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    scaling = scaling_of(args)
+    w0, Fr, _ = rank_shard(cfg, 0, world, scaling)
+    desc = (f"{nf} frames per step ({per_point} per Eb/N0 block, evenly spaced over the {cfg['frames']}-frame batch"
+            + (", codes round robin" if len(cl) > 1 else "") + f"); {threads} host threads")
     line = {"impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "Gbit/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot_t / args.steps * 1e3, 3),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": describe(args.config, cfg, code), "global_batch": F, "max_iter": cfg["max_iter"],
-                       "ebn0_db": cfg["ebn0"], "parallelism": "host threads over frames"},
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": config_dict(args, cfg, cl, world, scaling, Fr),
             "cpu_baseline": {"value": round(value, 6), "unit": "Gbit/s", "cores": threads, "kind": "oracle",
                              "sample": desc},
             "e2e": {"value": round(value, 6), "unit": "Gbit/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def main():
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=sorted(codes.CONFIGS))
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(codes.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--flags", type=int, default=0)
+    ap.add_argument("--strong", action="store_true", help="split the config's frames over the ranks")
+    ap.add_argument("--weak", action="store_true", help="every rank decodes a full batch (default except C4)")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--per-block", action="store_true", help="one decode call per Eb/N0 block (default: one per step)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    args = ap.parse_args()
-    if args.warmup < 3 and args.impl == "ours":
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher / sharding check: print each rank's frame range and LLR checksum, no decode")
+    args = ap.parse_args(argv)
+    if args.warmup < 3 and args.impl == "ours" and not args.dry_run:
         print("warning: the timing rules require --warmup >= 3", file=sys.stderr)
     if args.impl == "reference":
         run_reference(args)
-    else:
-        run_ours(args)
+        return
+    relaunch_if_needed(args, argv)
+    run_ours(args)
 
 
 if __name__ == "__main__":

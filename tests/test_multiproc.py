@@ -79,3 +79,92 @@ def test_shards_partition_the_batch(world):
     assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
     sizes = [b - a for a, b in rs]
     assert max(sizes) - min(sizes) <= 1
+
+
+def _dry(args):
+    import json
+    import subprocess
+
+    r = subprocess.run([sys.executable, "bench.py", "--dry-run", "--config", "c1"] + args, cwd=ROOT,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    return sorted((json.loads(ln) for ln in r.stdout.splitlines() if ln.startswith("{")), key=lambda d: d["rank"])
+
+
+@pytest.mark.parametrize("mode", ["weak", "strong"])
+def test_bench_launcher_brings_up_ranks(mode):
+    """`bench.py --gpus 2` (no torchrun environment) re-launches itself as 2 ranks through
+    torch.distributed.run (gloo here, NCCL on GPUs); every rank logs its process group, and each rank's
+    frames are exactly the frames a 1-rank run generates for the same global indices."""
+    import hashlib
+
+    import bench
+    from gen import codes
+
+    extra = ["--strong"] if mode == "strong" else []
+    lines = _dry(["--gpus", "2"] + extra)
+    assert [d["rank"] for d in lines] == [0, 1]
+    assert all(d["world"] == 2 and d["dist"]["backend"] == "gloo" and d["dist"]["all_reduce_check"] == 2
+               for d in lines)
+    cfg = codes.CONFIGS["c1"]
+    code = codes.paper_5x10()
+    F = cfg["frames"]
+    if mode == "strong":
+        assert [d["global_frames"] for d in lines] == [[0, F // 2], [F // 2, F]]
+        one, _ = bench.gen_frames(code, cfg, cfg["seed"], 0, F, 0)
+        parts = [one[:F // 2], one[F // 2:]]
+    else:
+        assert [d["global_frames"] for d in lines] == [[0, F], [F, 2 * F]]
+        parts = [bench.gen_frames(code, cfg, cfg["seed"], 0, F, r * F)[0] for r in range(2)]
+        assert lines[0]["llr_sha1"] == _dry([])[0]["llr_sha1"]  # rank 0 of 2 == the 1-rank run
+    for d, p in zip(lines, parts):
+        assert d["llr_sha1"] == hashlib.sha1(p.numpy().tobytes()).hexdigest()
+
+
+def _strong_worker(rank, world, port, q):
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import bench
+    import oracle
+    from gen import codes
+
+    cfg = dict(codes.CONFIGS["c1"], frames=600)
+    code = codes.paper_5x10()
+    w0, cnt, goff = bench.rank_shard(cfg, rank, world, "strong")
+    llr, _ = bench.gen_frames(code, cfg, cfg["seed"], w0, cnt, goff)
+    bits, iters, conv, post = oracle.decode(code.oracle_h(), llr.numpy(), cfg["max_iter"], threads=1)
+    objs = [None] * world
+    dist.all_gather_object(objs, (w0, bits, iters, conv, post))
+    if rank == 0:
+        q.put(objs)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_strong_shards_give_the_one_rank_outputs_per_global_frame():
+    """bench.py's strong split over 3 gloo ranks: every global frame's (b, k, isCodeword, s) equals the
+    1-rank result for that frame (frames are independent of their batch and shard, A19)."""
+    import bench
+    import oracle
+    from gen import codes
+
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_strong_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    objs = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    cfg = dict(codes.CONFIGS["c1"], frames=600)
+    code = codes.paper_5x10()
+    llr, _ = bench.gen_frames(code, cfg, cfg["seed"], 0, 600, 0)
+    ref = oracle.decode(code.oracle_h(), llr.numpy(), cfg["max_iter"])
+    objs.sort(key=lambda o: o[0])
+    for k in range(4):
+        got = np.concatenate([o[1 + k] for o in objs])
+        assert np.array_equal(got, ref[k])
