@@ -174,13 +174,24 @@ enum ldpc_kernel_class {
     LDPC_K_SYNDROME = 4,
     LDPC_K_FINALIZE = 5,
     LDPC_K_RESIDENT = 6,
-    LDPC_K_NUM_CLASSES = 7
+    LDPC_K_COMPACT = 7, /* streaming schedule: compaction of tiles with few running frames (plan + move) */
+    LDPC_K_NUM_CLASSES = 8
 };
 LDPC_API int ldpc_profile_enable(ldpc_handle_t h, int enable);
 LDPC_API int ldpc_profile_read(ldpc_handle_t h, int64_t *launches /* [LDPC_K_NUM_CLASSES] */,
                       double *milliseconds /* [LDPC_K_NUM_CLASSES] */);
 LDPC_API int ldpc_profile_reset(ldpc_handle_t h);
+/* Kernels launched by the handle so far, including the loop bodies a CUDA-graph conditional node ran
+ * (counted on the device: this call synchronises the device). */
 LDPC_API int64_t ldpc_launch_count(ldpc_handle_t h);
+
+/*
+ * Compaction activity of the streaming schedule since the handle was created (tiles with
+ * fewer than half of their frames running have those frames moved into fresh dense tiles):
+ * counters[0] frames moved, [1] compactions, [2] source tiles retired.  Host output; synchronises the
+ * device.  Errors: INVALID_ARG, CUDA.
+ */
+LDPC_API int ldpc_stream_counters(ldpc_handle_t h, int64_t *counters /* [3] */);
 
 LDPC_API void ldpc_destroy(ldpc_handle_t h);
 LDPC_API const char *ldpc_status_string(int code);

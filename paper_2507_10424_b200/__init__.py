@@ -24,7 +24,7 @@ FLAG_FORCE_STREAM = 4
 FLAG_FORCE_RESIDENT = 8
 FLAG_NO_GRAPH = 16
 
-KERNEL_CLASSES = ("ingest", "stage_in", "check_node", "bit_node", "syndrome", "finalize", "resident")
+KERNEL_CLASSES = ("ingest", "stage_in", "check_node", "bit_node", "syndrome", "finalize", "resident", "compact")
 
 STATS_FIELDS = ("frames", "bit_errors", "frame_errors", "undetected", "sum_iters", "converged", "near_zero",
                 "raw_bit_errors")
@@ -231,6 +231,13 @@ class Handle:
     def profile_reset(self):
         with torch.cuda.device(self.device):
             _check(self._lib.ldpc_profile_reset(self._h), "ldpc_profile_reset")
+
+    def stream_counters(self) -> dict:
+        """Compaction activity of the streaming schedule (frames moved, compactions, tiles retired)."""
+        c = (ctypes.c_int64 * 3)()
+        with torch.cuda.device(self.device):
+            _check(self._lib.ldpc_stream_counters(self._h, c), "ldpc_stream_counters")
+        return {"frames_moved": int(c[0]), "compactions": int(c[1]), "tiles_retired": int(c[2])}
 
     @property
     def launch_count(self) -> int:

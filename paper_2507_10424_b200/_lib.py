@@ -28,6 +28,7 @@ SIGNATURES = {
     "ldpc_profile_read": (ctypes.c_int, [P, P, P]),
     "ldpc_profile_reset": (ctypes.c_int, [P]),
     "ldpc_launch_count": (I64, [P]),
+    "ldpc_stream_counters": (ctypes.c_int, [P, P]),
     "ldpc_destroy": (None, [P]),
     "ldpc_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "ldpc_abi_version": (ctypes.c_int, []),

@@ -13,8 +13,24 @@
 // freezes stopped frames and records k-1.  No host round trip anywhere.
 //
 // Layout: frames are interleaved in tiles of 128 ([tile][row-or-column][128 frames]); lane l of a
-// warp owns frames 4l..4l+3 of the tile, so every gather of s, r or row state is one 512-byte
-// contiguous float4 access per warp, and per-frame bits of 128 frames are four ballot words.
+// warp owns frames ("slots") 4l..4l+3, so every gather of s, r or row state is one 512-byte
+// contiguous float4 access per warp, and per-slot bits of 128 slots are four ballot words.
+//
+// Row record of row i in tile t (rs bytes, 32-byte aligned; see ldpc_internal.cuh):
+//   [0, 512)            min0 [128] fp32  |lambda| minimum; SIGN BIT = row sign parity x (-1)^{d_i} (A1)
+//   [512, 1024)         min1 [128] fp32  second minimum (Obs. 1), same sign bit
+//   [1024 + 32 p, +32)  edge p of N_i: byte l = sign nibble (bit v = sign of lambda_e for slot 4l+v)
+//                                      | isloc nibble << 4 (bit v: p == min0Location of slot 4l+v)
+// eta_e = (isloc ? min1 : min0) with its sign bit XORed with the stored sign: one SEL and one LOP3 per
+// frame-edge.  The bit node gathers per edge 512 + 512 + 32 bytes per warp (the edge's own 32-byte
+// block, not a whole row of locations and sign words).
+//
+// Sweeps are persistent grids that take (tile, block) items from a work counter, so a sweep over a
+// handful of still-running tiles costs no empty CTAs.  Early stop is exact per frame; the work is
+// per tile, and tiles whose running frames fall under half are COMPACTED: their
+// running frames are moved, with their whole state, into fresh dense tiles at the end of the
+// workspace, so a tile stops costing its slowest frame.  Every slot carries its frame index, and the
+// outputs are written through it at the end.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -28,317 +44,139 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 
-template <typename T>
-struct Vec4;
-template <>
-struct Vec4<uint8_t> {
-    using type = uchar4;
-};
-template <>
-struct Vec4<uint16_t> {
-    using type = ushort4;
-};
-
 __device__ __forceinline__ float comp(const float4 &a, int v) { return v == 0 ? a.x : v == 1 ? a.y : v == 2 ? a.z : a.w; }
 __device__ __forceinline__ unsigned comp(const uint4 &a, int v) { return v == 0 ? a.x : v == 1 ? a.y : v == 2 ? a.z : a.w; }
-template <typename V>
-__device__ __forceinline__ int compl4(const V &a, int v) {
-    return v == 0 ? (int)a.x : v == 1 ? (int)a.y : v == 2 ? (int)a.z : (int)a.w;
-}
-
 __device__ __forceinline__ float4 ld4(const float *p) { return *reinterpret_cast<const float4 *>(p); }
 __device__ __forceinline__ void st4(float *p, float4 v) { *reinterpret_cast<float4 *>(p) = v; }
 __device__ __forceinline__ uint4 ldu4(const uint32_t *p) { return *reinterpret_cast<const uint4 *>(p); }
-
-// ------------------------------------------------------------------------------------------------
-// a2: stage-in.  llr [F][n] -> r, s [T][n][128] (s = r), init per-tile flags.
-// s is stored canonically (-0 -> +0; same slice and same sign() under reading A12), so that the later
-// sweeps can read both the decision b = slice(s) and the sign of lambda = s - eta^prev straight from
-// IEEE bits: after this no s and no lambda is ever -0 (x - y = -0 only for x = -0 and y = +0, and a
-// bit-node sum started at +0.0 is never -0).
-// ------------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(CTA) k_stage_in(const float *__restrict__ llr, int64_t frames, int n, int T,
-                                                  float *__restrict__ r, float *__restrict__ s,
-                                                  uint32_t *__restrict__ unsat, uint32_t *__restrict__ done,
-                                                  int *__restrict__ fbe, int *__restrict__ fraw, int *__restrict__ fnz,
-                                                  int *__restrict__ tcount, int *__restrict__ tlist) {
-    __shared__ float tile[32][TILE + 1];
-    const int t = blockIdx.y, j0 = blockIdx.x * 32;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t f0 = (int64_t)t * TILE;
-    for (int fl = warp; fl < TILE; fl += CTA / 32) {
-        int64_t f = f0 + fl;
-        int j = j0 + lane;
-        tile[lane][fl] = (f < frames && j < n) ? __ldg(llr + f * n + j) : -1.0f;
-    }
-    __syncthreads();
-    for (int jl = warp; jl < 32; jl += CTA / 32) {
-        int j = j0 + jl;
-        if (j >= n) break;
-        size_t base = ((size_t)t * n + j) * TILE;
-#pragma unroll
-        for (int q = 0; q < 4; q++) {
-            float v = tile[jl][lane + 32 * q];
-            r[base + lane + 32 * q] = v;
-            s[base + lane + 32 * q] = __fadd_rn(v, 0.0f);  // canonical zero
-        }
-    }
-    if (blockIdx.x == 0) {
-        int tid = threadIdx.x;
-        if (tid < 4) {
-            // frame 4*lane+v of the tile is bit `lane` of word v; padding frames start "done"
-            uint32_t pad = 0;
-            for (int l = 0; l < 32; l++)
-                if (f0 + 4 * l + tid >= frames) pad |= 1u << l;
-            done[(size_t)t * 4 + tid] = pad;
-            unsat[(size_t)t * 4 + tid] = 0;
-            unsat[((size_t)T + t) * 4 + tid] = 0;
-        }
-        if (tid == 0) {
-            tlist[(size_t)T + t] = t;  // body 1 runs every tile
-            if (t == 0) {
-                tcount[0] = 0;
-                tcount[1] = T;
-            }
-        }
-        if (tid < TILE) {
-            fbe[(size_t)t * TILE + tid] = 0;
-            fraw[(size_t)t * TILE + tid] = 0;
-            fnz[(size_t)t * TILE + tid] = 0;
-        }
-    }
-}
-
-// ------------------------------------------------------------------------------------------------
-// Encoding of the check-node state (it IS eta: Obs. 1 and 2, reading A2):
-//   min0, min1   fp32, both with SIGN BIT = the row's sign parity x (-1)^{d_i} (reading A1), so the
-//                magnitude picked by Obs. 1 already carries the row factor of Obs. 2;
-//   loc          u8 / u16 min0Location (position inside N_i);
-//   sgn          per (tile, edge) four u32 in "ballot layout": bit l of word v is the sign of
-//                lambda_e for frame 4l + v -- exactly the four warp ballots the check node produces.
-// eta_e = (loc == p ? min1 : min0) with its sign bit XORed with sgn bit: one FSEL and one LOP3 per
-// frame-edge; a lane moves its ballot bit to bit 31 with one integer multiply by 2^(31-lane) (FMA
-// pipe), which keeps the ALU pipe -- the sweeps' real limiter -- for the min/argmin work.
-// ------------------------------------------------------------------------------------------------
-template <typename LocT>
-struct LocOps;
-template <>
-struct LocOps<uint8_t> {
-    using W = uint32_t;  // the 4 locations of a lane, one byte each
-    static __device__ __forceinline__ W load(const uint8_t *p) { return *reinterpret_cast<const uint32_t *>(p); }
-    static __device__ __forceinline__ void store(uint8_t *p, const int l[4]) {
-        *reinterpret_cast<uint32_t *>(p) =
-            (uint32_t)l[0] | ((uint32_t)l[1] << 8) | ((uint32_t)l[2] << 16) | ((uint32_t)l[3] << 24);
-    }
-    static __device__ __forceinline__ W key(W w, int p) { return w ^ ((uint32_t)p * 0x01010101u); }
-    static __device__ __forceinline__ bool hit(W x, int v) { return (x & (0xffu << (8 * v))) == 0u; }
-};
-template <>
-struct LocOps<uint16_t> {
-    using W = uint2;
-    static __device__ __forceinline__ W load(const uint16_t *p) { return *reinterpret_cast<const uint2 *>(p); }
-    static __device__ __forceinline__ void store(uint16_t *p, const int l[4]) {
-        *reinterpret_cast<uint2 *>(p) = make_uint2((uint32_t)l[0] | ((uint32_t)l[1] << 16),
-                                                   (uint32_t)l[2] | ((uint32_t)l[3] << 16));
-    }
-    static __device__ __forceinline__ W key(W w, int p) {
-        const uint32_t q = (uint32_t)p * 0x00010001u;
-        return make_uint2(w.x ^ q, w.y ^ q);
-    }
-    static __device__ __forceinline__ bool hit(W x, int v) {
-        return ((v < 2 ? x.x : x.y) & (0xffffu << (16 * (v & 1)))) == 0u;
-    }
-};
 
 // the sign of a magnitude picked by Obs. 1 flipped by one stored sign bit (already moved to bit 31)
 __device__ __forceinline__ float flip31(float mag, uint32_t bit31) {
     return __uint_as_float(__float_as_uint(mag) ^ (bit31 & 0x80000000u));
 }
 
-constexpr int CN_CHUNK = 8;  // edges per sign word and per batch of gathers (4 frames x 8 edges = 32 bits)
-#ifndef CN_MINB
-#define CN_MINB 2
-#endif
-#ifndef CN1_MINB
-#define CN1_MINB 3
-#endif
-#ifndef BNL_MINB
-#define BNL_MINB 6
-#endif
+// Take the next (tile, block) item of a persistent sweep from a work counter.  Two barriers: every
+// thread has finished the previous item (and read its index) before thread 0 overwrites s_item.
+__device__ __forceinline__ int next_item(int *ctr, int &s_item) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_item = atomicAdd(ctr, 1);
+    __syncthreads();
+    return s_item;
+}
+
 #ifndef CN_T
-#define CN_T CTA
+#define CN_T 256
 #endif
-#ifndef BNL_T
-#define BNL_T 128  // bit-node CTA size: 128 threads x 12 CTAs per SM measured 1.5-2 % faster than 256 x 6
+#ifndef CN_MINB
+#define CN_MINB 3
 #endif
-#ifndef BNL_COLS
-#define BNL_COLS 16
+#ifndef BN_T
+#define BN_T 128  // 128 threads x 12 CTAs per SM (48 warps): the bit node lives on loads in flight
 #endif
+#ifndef BN_MINB
+#define BN_MINB 12
+#endif
+constexpr int CN_ROWS = 128;  // rows per check-node item (16 per warp)
+constexpr int BN_COLS = 16;   // columns per bit-node item (4 per warp)
+constexpr int CN_NW = CN_T / 32;
 
 // ------------------------------------------------------------------------------------------------
-// a3/a4/a6: check-node sweep of loop body k (k = 1..L), fused syndrome of b^(k-1).
-// FIRST: eta^prev = 0, so no old state is read.
-// A warp owns rows i0 + warp + 8q.  Per row, every load -- the d gathers of s (512-byte float4
-// segments, lane = 4 frames), the row state and the lane's old sign word -- is issued before any
-// arithmetic, and the column indices of the next row are prefetched meanwhile, so each row costs one
-// memory latency, overlapped across the warps of the SM.  Per frame-edge: lambda = s_j - eta^prev
-// (SEL, LOP3, FADD), first-strict-minimum tracking (FSETP, 3 FMNMX, SEL; reading A13), sign parity
-// (LOP3 on the IEEE bits), the new sign bit into the lane's own word, and, when EARLY, the decision
-// parity (slice(s) = 0 iff bit 31 of bits(s) - 1 is set, s never -0).
+// a2: stage-in.  llr [F][n] -> r [t][n][128] (canonical zeros: -0 -> +0, same slice and sign() under
+// reading A12, so that no s and no lambda is ever -0 and IEEE sign bits can be read directly), the
+// per-slot frame index, per-tile flags, and the raw channel errors of every frame (r_j > 0) counted
+// where r is read anyway.  Body 1 reads r itself (s = r).
 // ------------------------------------------------------------------------------------------------
-template <typename LocT, bool FIRST, bool EARLY>
-__global__ void __launch_bounds__(CTA, CN_MINB)
-    k_cn(Graph g, StreamState w, int k, int rows_per_cta, int literal, const int *kdev) {
-    using LO = LocOps<LocT>;
-    if (kdev) k = *kdev;  // body index supplied by the graph-driven loop
+constexpr int SI_SUB = 8;  // 32-column sub-blocks per stage-in / finalize CTA
+
+__global__ void __launch_bounds__(CTA) k_stage_in(const float *__restrict__ llr, int64_t frames, int n,
+                                                  StreamState w) {
+    __shared__ float tile[32][TILE + 1];
+    const int t = blockIdx.y;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    __shared__ uint32_t s_u[4];
-    // the tiles of body k are the ones with a running frame (list rebuilt by k_bn of body k-1)
-    const int cnt = w.tcount[k & 1];
-    if (blockIdx.x == 0 && threadIdx.x == 0) w.tcount[(k + 1) & 1] = 0;  // rebuilt by k_bn of body k
-    if ((int)blockIdx.y >= cnt) return;  // active tiles are compacted to the front of the list
-    const int t = w.tlist[(size_t)(k & 1) * w.T + blockIdx.y];
-    if (EARLY) {
-        if (threadIdx.x < 4) s_u[threadIdx.x] = 0;
-        __syncthreads();
-    }
-    const int m = g.m, n = g.n, wr = g.wr;
-    const float *__restrict__ Sl = w.s + (size_t)t * n * TILE + 4 * lane;
-    // the tile's row records: [min0 512 B][min1 512 B][loc 128 x sizeof(LocT)][sign words 128 x wr]
-    unsigned char *RB = w.rst + (size_t)t * m * w.rs;
-    const size_t RSW = (size_t)w.rs / 4, RSL = (size_t)w.rs / sizeof(LocT);  // row strides
-    float *__restrict__ M0l = reinterpret_cast<float *>(RB) + 4 * lane;
-    float *__restrict__ M1l = reinterpret_cast<float *>(RB) + 128 + 4 * lane;
-    LocT *__restrict__ LCl = reinterpret_cast<LocT *>(RB + 1024) + 4 * lane;
-    uint32_t *__restrict__ SGl = reinterpret_cast<uint32_t *>(RB + 1024 + 128 * sizeof(LocT)) + lane;
-    const float INF = __int_as_float(0x7f800000);
-    const int i0 = blockIdx.x * rows_per_cta + warp, i1 = min(m, blockIdx.x * rows_per_cta + rows_per_cta);
-    const int nr = i0 < i1 ? (i1 - i0 + 7) / 8 : 0;  // rows of this warp (<= 32)
-    int ra = 0, rb = 0;  // lane q: row_ptr of the warp's row q
-    if (lane < nr) {
-        ra = __ldg(g.row_ptr + i0 + 8 * lane);
-        rb = __ldg(g.row_ptr + i0 + 8 * lane + 1);
-    }
-    int a = __shfl_sync(FULL, ra, 0), d = __shfl_sync(FULL, rb, 0) - a;
-    int cj = (nr > 0 && lane < d) ? __ldg(g.col_idx + a + lane) : 0;  // lane q: column of edge q
-    uint32_t u0 = 0, u1 = 0, u2 = 0, u3 = 0;
-    for (int q = 0; q < nr; q++) {
-        const int i = i0 + 8 * q;
-        const int an = __shfl_sync(FULL, ra, (q + 1) & 31), dn = __shfl_sync(FULL, rb, (q + 1) & 31) - an;
-        const uint32_t corr = (uint32_t)(d & 1) & (uint32_t)(!literal);  // (-1)^{d_i}, reading A1
-        float om0[4] = {0.f, 0.f, 0.f, 0.f}, om1[4] = {0.f, 0.f, 0.f, 0.f};
-        typename LO::W olc{};
-        if (!FIRST) {
-            const float4 A = ld4(M0l + (size_t)i * RSW), B = ld4(M1l + (size_t)i * RSW);
-            om0[0] = A.x; om0[1] = A.y; om0[2] = A.z; om0[3] = A.w;
-            om1[0] = B.x; om1[1] = B.y; om1[2] = B.z; om1[3] = B.w;
-            olc = LO::load(LCl + (size_t)i * RSL);
-        }
-        float nm0[4] = {INF, INF, INF, INF}, nm1[4] = {INF, INF, INF, INF};
-        int nloc[4] = {0, 0, 0, 0};
-        uint32_t par[4] = {0u, 0u, 0u, 0u}, syn[4] = {0u, 0u, 0u, 0u};
-        for (int p0 = 0; p0 < d; p0 += CN_CHUNK) {
-            if (p0 > 0 && (p0 & 31) == 0) cj = (lane < d - p0) ? __ldg(g.col_idx + a + p0 + lane) : 0;
-            uint32_t *sgp = SGl + (size_t)i * RSW + (p0 >> 3) * 32;
-            float4 sv[CN_CHUNK];
-#pragma unroll
-            for (int u = 0; u < CN_CHUNK; u++) {
-                const int j = __shfl_sync(FULL, cj, (p0 + u) & 31);
-                sv[u] = ld4(Sl + (size_t)j * TILE);  // unconditional: edges past d_i read column 0
-            }
-            const uint32_t wold = FIRST ? 0u : *sgp;
-            uint32_t wnew = 0;
-#pragma unroll
-            for (int u = 0; u < CN_CHUNK; u++) {
-                if (p0 + u < d) {
-                    const int p = p0 + u;
-                    typename LO::W key{};
-                    if (!FIRST) key = LO::key(olc, p);
-#pragma unroll
-                    for (int v = 0; v < 4; v++) {
-                        const float sj = comp(sv[u], v);
-                        float x = sj;
-                        if (!FIRST) {
-                            const float mag = LO::hit(key, v) ? om1[v] : om0[v];  // Obs. 1 (+ row parity)
-                            x = sj - flip31(mag, wold << (31 - 4 * u - v));        // lambda_k - eta^prev_{i,k}
-                        }
-                        const float ax = fabsf(x);
-                        const bool lt = ax < nm0[v];  // first strict minimum (A13)
-                        nm1[v] = fminf(nm1[v], fmaxf(nm0[v], ax));
-                        nm0[v] = fminf(nm0[v], ax);
-                        nloc[v] = lt ? p : nloc[v];
-                        par[v] ^= __float_as_uint(x);                          // sign parity (Obs. 2)
-                        if (EARLY) syn[v] ^= __float_as_uint(sj) - 1u;         // bit 31: slice(s_j) == 0
-                        wnew |= (__float_as_uint(x) >> 31) << (4 * u + v);     // sign(0) = +1
-                    }
-                }
-            }
-            *sgp = wnew;
-        }
-        // prefetch the next row's column indices (its state and gathers are issued at its start)
-        cj = (q + 1 < nr && lane < dn) ? __ldg(g.col_idx + an + lane) : 0;
-        float4 o0, o1;
-        {
-            const uint32_t c31 = corr << 31;
-            const uint32_t s0 = (par[0] & 0x80000000u) ^ c31, s1 = (par[1] & 0x80000000u) ^ c31;
-            const uint32_t s2 = (par[2] & 0x80000000u) ^ c31, s3 = (par[3] & 0x80000000u) ^ c31;
-            o0 = make_float4(__uint_as_float(__float_as_uint(nm0[0]) | s0), __uint_as_float(__float_as_uint(nm0[1]) | s1),
-                             __uint_as_float(__float_as_uint(nm0[2]) | s2), __uint_as_float(__float_as_uint(nm0[3]) | s3));
-            o1 = make_float4(__uint_as_float(__float_as_uint(nm1[0]) | s0), __uint_as_float(__float_as_uint(nm1[1]) | s1),
-                             __uint_as_float(__float_as_uint(nm1[2]) | s2), __uint_as_float(__float_as_uint(nm1[3]) | s3));
-        }
-        st4(M0l + (size_t)i * RSW, o0);
-        st4(M1l + (size_t)i * RSW, o1);
-        LO::store(LCl + (size_t)i * RSL, nloc);
-        if (EARLY) {
-            const uint32_t dp = (uint32_t)(d & 1);  // XOR_j b_j = d_i mod 2 xor XOR_j (1 - b_j)
-            u0 |= __ballot_sync(FULL, ((syn[0] >> 31) ^ dp) != 0u);
-            u1 |= __ballot_sync(FULL, ((syn[1] >> 31) ^ dp) != 0u);
-            u2 |= __ballot_sync(FULL, ((syn[2] >> 31) ^ dp) != 0u);
-            u3 |= __ballot_sync(FULL, ((syn[3] >> 31) ^ dp) != 0u);
-        }
-        a = an;
-        d = dn;
-    }
-    if (EARLY) {
-        if (lane == 0) {
-            if (u0) atomicOr(&s_u[0], u0);
-            if (u1) atomicOr(&s_u[1], u1);
-            if (u2) atomicOr(&s_u[2], u2);
-            if (u3) atomicOr(&s_u[3], u3);
+    const int64_t f0 = (int64_t)t * TILE;
+    int raw = 0;  // lane q < 16 of warp w counts frame w + 8q
+    for (int sb = 0; sb < SI_SUB; sb++) {
+        const int j0 = (blockIdx.x * SI_SUB + sb) * 32;
+        if (j0 >= n) break;
+        const int j = j0 + lane;
+        for (int fl = warp; fl < TILE; fl += CTA / 32) {
+            const int64_t f = f0 + fl;
+            const bool ok = f < frames && j < n;
+            const float v = ok ? __ldg(llr + f * n + j) : -1.0f;
+            tile[lane][fl] = v;
+            const int c = __popc(__ballot_sync(FULL, ok && v > 0.f));
+            if (lane == (fl >> 3)) raw += c;
         }
         __syncthreads();
-        if (threadIdx.x < 4 && s_u[threadIdx.x])
-            atomicOr(w.unsat + ((size_t)(k & 1) * w.T + t) * 4 + threadIdx.x, s_u[threadIdx.x]);
+        for (int jl = warp; jl < 32; jl += CTA / 32) {
+            const int jj = j0 + jl;
+            if (jj >= n) break;
+            const size_t base = ((size_t)t * n + jj) * TILE;
+#pragma unroll
+            for (int q = 0; q < 4; q++) w.r[base + lane + 32 * q] = __fadd_rn(tile[jl][lane + 32 * q], 0.0f);
+        }
+        __syncthreads();
+    }
+    if (lane < 16 && raw) {
+        const int64_t f = f0 + warp + 8 * lane;
+        if (f < frames) atomicAdd(w.fraw + f, raw);
+    }
+    if (blockIdx.x == 0) {
+        const int tid = threadIdx.x;
+        if (tid < 4) {
+            // slot 4*lane+v of the tile is bit `lane` of word v; padding slots start "done"
+            uint32_t pad = 0;
+            for (int l = 0; l < 32; l++)
+                if (f0 + 4 * l + tid >= frames) pad |= 1u << l;
+            w.done[(size_t)t * 4 + tid] = pad;
+            w.unsat[(size_t)t * 4 + tid] = 0;
+            w.unsat[((size_t)w.Tcap + t) * 4 + tid] = 0;
+        }
+        if (tid < TILE) w.fid[(size_t)t * TILE + tid] = (f0 + tid < frames) ? (int)(f0 + tid) : -1;
+        if (tid == 0) {
+            w.tlist[(size_t)w.Tcap + t] = t;  // body 1 runs every tile
+            if (t == 0) {
+                w.tcount[0] = 0;
+                w.tcount[1] = w.T;
+                w.work[WK_CN] = 0;
+                w.work[WK_BN] = 0;
+                w.work[WK_MOVE] = 0;
+                w.work[WK_SYN] = 0;
+                w.ctl[CT_TNEXT] = w.T;
+                w.ctl[CT_NSRC] = 0;
+                w.ctl[CT_NDST] = 0;
+            }
+        }
     }
 }
 
 // ------------------------------------------------------------------------------------------------
-// Software-pipelined check-node sweep for codes whose rows all have degree <= CH (<= 8: one sign
-// word per row and lane).  Two row buffers in registers: while a warp computes row q from buffer A,
-// every load of row q+1 -- its CH gathers of s, its state and its old sign word -- is already in
-// flight into buffer B, and the column indices of row q+2 are being fetched.  All loads are
-// unconditional (edges past d_i read column 0 of the tile, rows past the warp's last read its first
-// row), so the compiler issues them back to back instead of behind predicated moves.
+// a3/a4/a6: check-node sweep of loop body k (k = 1..L), fused syndrome of b^(k-1).
+// FIRST: eta^prev = 0, no old state is read, lambda = r.
+// A warp owns rows i0 + warp + 8q of its item.  Per row, every load -- the CH gathers of s (512-byte
+// float4 segments, lane = 4 slots), the row's min0/min1 and the lane's old edge bytes -- is issued
+// before any arithmetic, and the column indices of the next row are fetched meanwhile, so each row
+// costs one memory latency, overlapped across the warps of the SM.  All loads are unconditional
+// (edges past d_i read column 0 of the tile; the record holds CH edge blocks).
+// Per frame-edge: eta^prev = (isloc ? min1 : min0) ^ sign (SHF, ISETP, SEL, LOP3), lambda (FADD),
+// first-strict-minimum tracking (FSETP, 3 FMNMX, SEL; reading A13), the new sign bit, and, when
+// EARLY, the decision parity (slice(s) = 0 iff bit 31 of bits(s) - 1 is set, s never -0).
 // ------------------------------------------------------------------------------------------------
-template <int CH, typename LocT>
+template <int CH>
 struct CnRow {
     float4 sv[CH];
     float4 m0, m1;
-    typename LocOps<LocT>::W lc;
-    uint32_t wold;
+    uint32_t eb[CH];
 };
 
-template <int CH, typename LocT, bool FIRST>
-__device__ __forceinline__ void cn_fetch(CnRow<CH, LocT> &R, int cj, int i, const float *__restrict__ Sl,
-                                         const uint32_t *__restrict__ SGl, const float *__restrict__ M0l,
-                                         const float *__restrict__ M1l, const LocT *__restrict__ LCl, size_t RSW,
-                                         size_t RSL) {
+template <int CH, bool FIRST>
+__device__ __forceinline__ void cn_fetch(CnRow<CH> &R, int cj, const float *__restrict__ Sl,
+                                         const unsigned char *__restrict__ Ri, int lane) {
     if (!FIRST) {
-        R.wold = SGl[(size_t)i * RSW];
-        R.m0 = ld4(M0l + (size_t)i * RSW);
-        R.m1 = ld4(M1l + (size_t)i * RSW);
-        R.lc = LocOps<LocT>::load(LCl + (size_t)i * RSL);
+        R.m0 = ld4(reinterpret_cast<const float *>(Ri) + 4 * lane);
+        R.m1 = ld4(reinterpret_cast<const float *>(Ri) + 128 + 4 * lane);
+#pragma unroll
+        for (int p = 0; p < CH; p++) R.eb[p] = Ri[REC_EDGE0 + 32 * p + lane];
     }
 #pragma unroll
     for (int u = 0; u < CH; u++) {
@@ -347,56 +185,57 @@ __device__ __forceinline__ void cn_fetch(CnRow<CH, LocT> &R, int cj, int i, cons
     }
 }
 
-template <int CH, typename LocT, bool FIRST, bool EARLY>
-__device__ __forceinline__ void cn_compute(const CnRow<CH, LocT> &R, int i, int d, int literal,
-                                           uint32_t *__restrict__ SGl, float *__restrict__ M0l,
-                                           float *__restrict__ M1l, LocT *__restrict__ LCl, size_t RSW, size_t RSL,
-                                           uint32_t (&u)[4]) {
-    using LO = LocOps<LocT>;
+template <int CH, bool FIRST, bool EARLY>
+__device__ __forceinline__ void cn_compute(const CnRow<CH> &R, unsigned char *__restrict__ Ri, int d, int literal,
+                                           int lane, uint32_t (&u)[4]) {
     const float INF = __int_as_float(0x7f800000);
-    const uint32_t corr = (uint32_t)(d & 1) & (uint32_t)(!literal);  // (-1)^{d_i}, reading A1
     const float om0[4] = {R.m0.x, R.m0.y, R.m0.z, R.m0.w}, om1[4] = {R.m1.x, R.m1.y, R.m1.z, R.m1.w};
     float nm0[4] = {INF, INF, INF, INF}, nm1[4] = {INF, INF, INF, INF};
     int nloc[4] = {0, 0, 0, 0};
-    uint32_t syn[4] = {0u, 0u, 0u, 0u}, wnew = 0;
+    uint32_t syn[4] = {0u, 0u, 0u, 0u}, sw = 0;  // sw: sign nibble of edge p at bits 4p..4p+3
 #pragma unroll
     for (int p = 0; p < CH; p++) {
         if (p < d) {
-            typename LO::W key{};
-            if (!FIRST) key = LO::key(R.lc, p);
+            const uint32_t b = FIRST ? 0u : R.eb[p];
 #pragma unroll
             for (int v = 0; v < 4; v++) {
                 const float sj = comp(R.sv[p], v);
                 float x = sj;
                 if (!FIRST) {
-                    const float mag = LO::hit(key, v) ? om1[v] : om0[v];  // Obs. 1 (+ row parity)
-                    x = sj - flip31(mag, R.wold << (31 - 4 * p - v));     // lambda_k - eta^prev_{i,k}
+                    const float mag = (b & (16u << v)) ? om1[v] : om0[v];  // Obs. 1 (+ row parity)
+                    x = sj - flip31(mag, b << (31 - v));                      // lambda_k - eta^prev_{i,k}
                 }
                 const float ax = fabsf(x);
                 const bool lt = ax < nm0[v];  // first strict minimum (A13)
                 nm1[v] = fminf(nm1[v], fmaxf(nm0[v], ax));
                 nm0[v] = fminf(nm0[v], ax);
                 nloc[v] = lt ? p : nloc[v];
-                if (EARLY) syn[v] ^= __float_as_uint(sj) - 1u;      // bit 31: slice(s_j) == 0
-                wnew |= (__float_as_uint(x) >> 31) << (4 * p + v);  // sign(0) = +1
+                if (EARLY) syn[v] ^= __float_as_uint(sj) - 1u;     // bit 31: slice(s_j) == 0
+                sw |= (__float_as_uint(x) >> 31) << (4 * p + v);  // sign(0) = +1: x is never -0
             }
         }
     }
-    SGl[(size_t)i * RSW] = wnew;
-    // sign parity per frame (Obs. 2): XOR of bits v, v+4, ..., of the new sign word, times (-1)^{d_i}
-    uint32_t pw = wnew ^ (wnew >> 16);
+    // sign parity per slot (Obs. 2): XOR of bits v, v+4, ..., of sw, times (-1)^{d_i} (reading A1)
+    uint32_t pw = sw ^ (sw >> 16);
     pw ^= pw >> 8;
     pw ^= pw >> 4;
-    pw ^= corr ? 0xfu : 0u;
+    pw ^= ((uint32_t)(d & 1) & (uint32_t)(!literal)) ? 0xfu : 0u;
     const uint32_t s0 = pw << 31, s1 = (pw << 30) & 0x80000000u, s2 = (pw << 29) & 0x80000000u,
                    s3 = (pw << 28) & 0x80000000u;
-    st4(M0l + (size_t)i * RSW,
+    st4(reinterpret_cast<float *>(Ri) + 4 * lane,
         make_float4(__uint_as_float(__float_as_uint(nm0[0]) | s0), __uint_as_float(__float_as_uint(nm0[1]) | s1),
                     __uint_as_float(__float_as_uint(nm0[2]) | s2), __uint_as_float(__float_as_uint(nm0[3]) | s3)));
-    st4(M1l + (size_t)i * RSW,
+    st4(reinterpret_cast<float *>(Ri) + 128 + 4 * lane,
         make_float4(__uint_as_float(__float_as_uint(nm1[0]) | s0), __uint_as_float(__float_as_uint(nm1[1]) | s1),
                     __uint_as_float(__float_as_uint(nm1[2]) | s2), __uint_as_float(__float_as_uint(nm1[3]) | s3)));
-    LO::store(LCl + (size_t)i * RSL, nloc);
+#pragma unroll
+    for (int p = 0; p < CH; p++) {
+        if (p < d) {
+            const uint32_t il = (uint32_t)(nloc[0] == p) | ((uint32_t)(nloc[1] == p) << 1) |
+                                ((uint32_t)(nloc[2] == p) << 2) | ((uint32_t)(nloc[3] == p) << 3);
+            Ri[REC_EDGE0 + 32 * p + lane] = (unsigned char)(((sw >> (4 * p)) & 0xfu) | (il << 4));
+        }
+    }
     if (EARLY) {
         const uint32_t dp = (uint32_t)(d & 1);  // XOR_j b_j = d_i mod 2 xor XOR_j (1 - b_j)
 #pragma unroll
@@ -404,276 +243,576 @@ __device__ __forceinline__ void cn_compute(const CnRow<CH, LocT> &R, int i, int 
     }
 }
 
-template <int CH, typename LocT, bool FIRST, bool EARLY, bool DB>
-__global__ void __launch_bounds__(CN_T, (DB ? 2 : CN1_MINB) * CTA / CN_T)
-    k_cn_pipe(Graph g, StreamState w, int k, int rows_per_cta, int literal, const int *kdev) {
+// Rows of degree up to 8 (CH = the smallest instance >= the maximum row degree).
+template <int CH, bool FIRST, bool EARLY>
+__global__ void __launch_bounds__(CN_T, CN_MINB) k_cn(Graph g, StreamState w, int k, int literal, const int *kdev) {
     if (kdev) k = *kdev;  // body index supplied by the graph-driven loop
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     __shared__ uint32_t s_u[4];
+    __shared__ int s_item;
     const int cnt = w.tcount[k & 1];
-    if (blockIdx.x == 0 && threadIdx.x == 0) w.tcount[(k + 1) & 1] = 0;  // rebuilt by k_bn of body k
-    if ((int)blockIdx.y >= cnt) return;  // active tiles are compacted to the front of the list
-    const int t = w.tlist[(size_t)(k & 1) * w.T + blockIdx.y];
-    if (EARLY) {
-        if (threadIdx.x < 4) s_u[threadIdx.x] = 0;
-        __syncthreads();
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        w.tcount[(k + 1) & 1] = 0;  // rebuilt by k_bn of body k
+        w.work[WK_BN] = 0;
+        w.ctl[CT_NSRC] = 0;
     }
     const int m = g.m, n = g.n;
-    const float *__restrict__ Sl = w.s + (size_t)t * n * TILE + 4 * lane;
-    // the tile's row records: [min0 512 B][min1 512 B][loc 128 x sizeof(LocT)][sign words 128 x wr]
-    unsigned char *RB = w.rst + (size_t)t * m * w.rs;
-    const size_t RSW = (size_t)w.rs / 4, RSL = (size_t)w.rs / sizeof(LocT);  // row strides
-    float *__restrict__ M0l = reinterpret_cast<float *>(RB) + 4 * lane;
-    float *__restrict__ M1l = reinterpret_cast<float *>(RB) + 128 + 4 * lane;
-    LocT *__restrict__ LCl = reinterpret_cast<LocT *>(RB + 1024) + 4 * lane;
-    uint32_t *__restrict__ SGl = reinterpret_cast<uint32_t *>(RB + 1024 + 128 * sizeof(LocT)) + lane;
-    const int i0 = blockIdx.x * rows_per_cta + warp, i1 = min(m, blockIdx.x * rows_per_cta + rows_per_cta);
-    constexpr int NW = CN_T / 32;  // warps per CTA
-    const int nr = i0 < i1 ? (i1 - i0 + NW - 1) / NW : 0;  // rows of this warp (<= 32)
-    uint32_t u[4] = {0u, 0u, 0u, 0u};
-    // a warp without rows must still reach the CTA barrier of the EARLY epilogue
-    if (nr > 0) {
-    int ra = 0, rb = 0;  // lane q: row_ptr of the warp's row q
-    if (lane < nr) {
-        ra = __ldg(g.row_ptr + i0 + NW * lane);
-        rb = __ldg(g.row_ptr + i0 + NW * lane + 1);
-    }
-    auto row_of = [&](int q) { return i0 + NW * min(q, nr - 1); };
-    auto deg_of = [&](int q) { return __shfl_sync(FULL, rb, q & 31) - __shfl_sync(FULL, ra, q & 31); };
-    auto cols_of = [&](int q) {  // lane p: column of edge p of row q (0 past the degree / past the rows)
-        const int a = __shfl_sync(FULL, ra, q & 31), d = __shfl_sync(FULL, rb, q & 31) - a;
-        return (q < nr && lane < d) ? __ldg(g.col_idx + a + lane) : 0;
-    };
-    if (!DB) {  // one row buffer: all loads of a row in flight together, more warps per SM
-        CnRow<CH, LocT> A;
-        int cj = cols_of(0);
-        for (int q = 0; q < nr; q++) {
-            cn_fetch<CH, LocT, FIRST>(A, cj, row_of(q), Sl, SGl, M0l, M1l, LCl, RSW, RSL);
-            cj = cols_of(q + 1);
-            cn_compute<CH, LocT, FIRST, EARLY>(A, row_of(q), deg_of(q), literal, SGl, M0l, M1l, LCl, RSW, RSL, u);
+    const int nrb = (m + CN_ROWS - 1) / CN_ROWS;
+    const int items = cnt * nrb;
+    for (;;) {
+        if (EARLY && threadIdx.x < 4) s_u[threadIdx.x] = 0;
+        const int it = next_item(w.work + WK_CN, s_item);
+        if (it >= items) break;
+        const int y = it / nrb, x = it - y * nrb;
+        const int t = w.tlist[(size_t)(k & 1) * w.Tcap + y];
+        const float *__restrict__ Sl = (FIRST ? w.r : w.s) + (size_t)t * n * TILE + 4 * lane;
+        unsigned char *RB = w.rst + (size_t)t * m * w.rs;
+        const int i0 = x * CN_ROWS + warp, i1 = min(m, x * CN_ROWS + CN_ROWS);
+        const int nr = i0 < i1 ? (i1 - i0 + CN_NW - 1) / CN_NW : 0;  // rows of this warp (<= 16)
+        uint32_t u[4] = {0u, 0u, 0u, 0u};
+        if (nr > 0) {
+            int ra = 0, rb = 0;  // lane q: row_ptr of the warp's row q
+            if (lane < nr) {
+                ra = __ldg(g.row_ptr + i0 + CN_NW * lane);
+                rb = __ldg(g.row_ptr + i0 + CN_NW * lane + 1);
+            }
+            auto cols_of = [&](int q) {  // lane p: column of edge p of row q (0 past the degree / the rows)
+                const int a = __shfl_sync(FULL, ra, q & 31), d = __shfl_sync(FULL, rb, q & 31) - a;
+                return (q < nr && lane < d) ? __ldg(g.col_idx + a + lane) : 0;
+            };
+            CnRow<CH> A;
+            int cj = cols_of(0);
+            for (int q = 0; q < nr; q++) {
+                const int i = i0 + CN_NW * q;
+                unsigned char *Ri = RB + (size_t)i * w.rs;
+                cn_fetch<CH, FIRST>(A, cj, Sl, Ri, lane);
+                const int d = __shfl_sync(FULL, rb, q) - __shfl_sync(FULL, ra, q);
+                cj = cols_of(q + 1);
+                cn_compute<CH, FIRST, EARLY>(A, Ri, d, literal, lane, u);
+            }
         }
-    } else {
-    CnRow<CH, LocT> A, B;
-    int cjA = cols_of(0), cjB = cols_of(1);
-    cn_fetch<CH, LocT, FIRST>(A, cjA, row_of(0), Sl, SGl, M0l, M1l, LCl, RSW, RSL);
-    cjA = cols_of(2);
-    for (int q = 0; q < nr; q += 2) {
-        cn_fetch<CH, LocT, FIRST>(B, cjB, row_of(q + 1), Sl, SGl, M0l, M1l, LCl, RSW, RSL);
-        cjB = cols_of(q + 3);
-        cn_compute<CH, LocT, FIRST, EARLY>(A, row_of(q), deg_of(q), literal, SGl, M0l, M1l, LCl, RSW, RSL, u);
-        if (q + 1 >= nr) break;
-        cn_fetch<CH, LocT, FIRST>(A, cjA, row_of(q + 2), Sl, SGl, M0l, M1l, LCl, RSW, RSL);
-        cjA = cols_of(q + 4);
-        cn_compute<CH, LocT, FIRST, EARLY>(B, row_of(q + 1), deg_of(q + 1), literal, SGl, M0l, M1l, LCl, RSW, RSL, u);
-    }
-    }
-    }  // nr > 0
-    if (EARLY) {
-        if (lane == 0) {
+        if (EARLY) {
+            if (lane == 0) {
 #pragma unroll
-            for (int v = 0; v < 4; v++)
-                if (u[v]) atomicOr(&s_u[v], u[v]);
+                for (int v = 0; v < 4; v++)
+                    if (u[v]) atomicOr(&s_u[v], u[v]);
+            }
+            __syncthreads();
+            if (threadIdx.x < 4 && s_u[threadIdx.x])
+                atomicOr(w.unsat + ((size_t)(k & 1) * w.Tcap + t) * 4 + threadIdx.x, s_u[threadIdx.x]);
         }
-        __syncthreads();
-        if (threadIdx.x < 4 && s_u[threadIdx.x])
-            atomicOr(w.unsat + ((size_t)(k & 1) * w.T + t) * 4 + threadIdx.x, s_u[threadIdx.x]);
+    }
+}
+
+// Rows of any degree: edges in chunks of 8 (one gather batch); each edge byte is written with its
+// sign nibble during the sweep, and the isloc bits are OR-ed into the (at most 4) min0Location
+// bytes of the lane afterwards (each lane owns byte `lane` of every edge block: no conflicts).
+template <bool FIRST, bool EARLY>
+__global__ void __launch_bounds__(CN_T, 2) k_cn_generic(Graph g, StreamState w, int k, int literal, const int *kdev) {
+    if (kdev) k = *kdev;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __shared__ uint32_t s_u[4];
+    __shared__ int s_item;
+    const int cnt = w.tcount[k & 1];
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        w.tcount[(k + 1) & 1] = 0;
+        w.work[WK_BN] = 0;
+        w.ctl[CT_NSRC] = 0;
+    }
+    const int m = g.m, n = g.n;
+    const int nrb = (m + CN_ROWS - 1) / CN_ROWS;
+    const int items = cnt * nrb;
+    const float INF = __int_as_float(0x7f800000);
+    constexpr int C8 = 8;
+    for (;;) {
+        if (EARLY && threadIdx.x < 4) s_u[threadIdx.x] = 0;
+        const int it = next_item(w.work + WK_CN, s_item);
+        if (it >= items) break;
+        const int y = it / nrb, x = it - y * nrb;
+        const int t = w.tlist[(size_t)(k & 1) * w.Tcap + y];
+        const float *__restrict__ Sl = (FIRST ? w.r : w.s) + (size_t)t * n * TILE + 4 * lane;
+        unsigned char *RB = w.rst + (size_t)t * m * w.rs;
+        uint32_t u[4] = {0u, 0u, 0u, 0u};
+        for (int i = x * CN_ROWS + warp; i < min(m, x * CN_ROWS + CN_ROWS); i += CN_NW) {
+            const int a = __ldg(g.row_ptr + i), d = __ldg(g.row_ptr + i + 1) - a;
+            unsigned char *Ri = RB + (size_t)i * w.rs;
+            float om0[4] = {0.f, 0.f, 0.f, 0.f}, om1[4] = {0.f, 0.f, 0.f, 0.f};
+            if (!FIRST) {
+                const float4 A = ld4(reinterpret_cast<const float *>(Ri) + 4 * lane);
+                const float4 B = ld4(reinterpret_cast<const float *>(Ri) + 128 + 4 * lane);
+                om0[0] = A.x; om0[1] = A.y; om0[2] = A.z; om0[3] = A.w;
+                om1[0] = B.x; om1[1] = B.y; om1[2] = B.z; om1[3] = B.w;
+            }
+            float nm0[4] = {INF, INF, INF, INF}, nm1[4] = {INF, INF, INF, INF};
+            int nloc[4] = {0, 0, 0, 0};
+            uint32_t par[4] = {0u, 0u, 0u, 0u}, syn[4] = {0u, 0u, 0u, 0u};
+            int cj = 0;
+            for (int p0 = 0; p0 < d; p0 += C8) {
+                if ((p0 & 31) == 0) cj = (lane < d - p0) ? __ldg(g.col_idx + a + p0 + lane) : 0;
+                float4 sv[C8];
+                uint32_t eb[C8];
+#pragma unroll
+                for (int u8 = 0; u8 < C8; u8++) {
+                    const int j = __shfl_sync(FULL, cj, (p0 + u8) & 31);
+                    sv[u8] = ld4(Sl + (size_t)j * TILE);  // unconditional: edges past d_i read column 0
+                    eb[u8] = FIRST ? 0u : Ri[REC_EDGE0 + 32 * (p0 + u8) + lane];
+                }
+#pragma unroll
+                for (int u8 = 0; u8 < C8; u8++) {
+                    const int p = p0 + u8;
+                    if (p < d) {
+                        uint32_t nib = 0;
+#pragma unroll
+                        for (int v = 0; v < 4; v++) {
+                            const float sj = comp(sv[u8], v);
+                            float x = sj;
+                            if (!FIRST) {
+                                const float mag = (eb[u8] & (16u << v)) ? om1[v] : om0[v];
+                                x = sj - flip31(mag, eb[u8] << (31 - v));
+                            }
+                            const float ax = fabsf(x);
+                            const bool lt = ax < nm0[v];
+                            nm1[v] = fminf(nm1[v], fmaxf(nm0[v], ax));
+                            nm0[v] = fminf(nm0[v], ax);
+                            nloc[v] = lt ? p : nloc[v];
+                            par[v] ^= __float_as_uint(x);
+                            if (EARLY) syn[v] ^= __float_as_uint(sj) - 1u;
+                            nib |= (__float_as_uint(x) >> 31) << v;
+                        }
+                        Ri[REC_EDGE0 + 32 * p + lane] = (unsigned char)nib;  // sign nibble, isloc = 0
+                    }
+                }
+            }
+            // isloc bits into the min0Location bytes of this lane (same thread wrote them: ordered)
+#pragma unroll
+            for (int v = 0; v < 4; v++) {
+                unsigned char *bp = Ri + REC_EDGE0 + 32 * nloc[v] + lane;
+                *bp = (unsigned char)(*bp | (16u << v));
+            }
+            const uint32_t c31 = ((uint32_t)(d & 1) & (uint32_t)(!literal)) << 31;
+            float4 o0, o1;
+            uint32_t sb[4];
+#pragma unroll
+            for (int v = 0; v < 4; v++) sb[v] = (par[v] & 0x80000000u) ^ c31;
+            o0 = make_float4(__uint_as_float(__float_as_uint(nm0[0]) | sb[0]), __uint_as_float(__float_as_uint(nm0[1]) | sb[1]),
+                             __uint_as_float(__float_as_uint(nm0[2]) | sb[2]), __uint_as_float(__float_as_uint(nm0[3]) | sb[3]));
+            o1 = make_float4(__uint_as_float(__float_as_uint(nm1[0]) | sb[0]), __uint_as_float(__float_as_uint(nm1[1]) | sb[1]),
+                             __uint_as_float(__float_as_uint(nm1[2]) | sb[2]), __uint_as_float(__float_as_uint(nm1[3]) | sb[3]));
+            st4(reinterpret_cast<float *>(Ri) + 4 * lane, o0);
+            st4(reinterpret_cast<float *>(Ri) + 128 + 4 * lane, o1);
+            if (EARLY) {
+                const uint32_t dp = (uint32_t)(d & 1);
+#pragma unroll
+                for (int v = 0; v < 4; v++) u[v] |= __ballot_sync(FULL, ((syn[v] >> 31) ^ dp) != 0u);
+            }
+        }
+        if (EARLY) {
+            if (lane == 0) {
+#pragma unroll
+                for (int v = 0; v < 4; v++)
+                    if (u[v]) atomicOr(&s_u[v], u[v]);
+            }
+            __syncthreads();
+            if (threadIdx.x < 4 && s_u[threadIdx.x])
+                atomicOr(w.unsat + ((size_t)(k & 1) * w.Tcap + t) * 4 + threadIdx.x, s_u[threadIdx.x]);
+        }
     }
 }
 
 // ------------------------------------------------------------------------------------------------
 // a5/a6: bit-node sweep of loop body k; stops frames whose b^(k-1) satisfied every check.
-// One edge at a time with few registers and many warps (6 CTAs per SM): the loads of an edge depend
-// only on its broadcast record, and the warps of the SM keep enough of them in flight.
+// Item = 16 columns of one tile; a warp walks each of its columns' edges one at a time (broadcast edge
+// record, then three loads: min0, min1 -- 512 B each per warp -- and the lane's edge byte), with few
+// registers and 48 warps per SM to keep the loads in flight.
+// The item with block 0 of a tile does the tile's bookkeeping: newly stopped frames (k, isCodeword),
+// and the tile goes to the list of body k+1 -- or, when fewer than half of its slots still run and
+// at least two bodies remain, to the compaction sources.
 // ------------------------------------------------------------------------------------------------
-template <typename LocT, bool EARLY>
-__global__ void __launch_bounds__(BNL_T, BNL_MINB * CTA / BNL_T)
-    k_bn(Graph g, StreamState w, int k, int cols_per_cta, int literal, const int *kdev, int check_every) {
-    using LO = LocOps<LocT>;
+template <bool EARLY>
+__global__ void __launch_bounds__(BN_T, BN_MINB)
+    k_bn(Graph g, StreamState w, int k, int L, const int *kdev, int check_every, int compact) {
     if (kdev) k = *kdev;
-    (void)literal;
-    const int lane = threadIdx.x & 31;
-    const int T = w.T;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int Tc = w.Tcap;
+    __shared__ int s_item;
     const int cnt = w.tcount[k & 1];
-    if ((int)blockIdx.y >= cnt) return;
-    const int t = w.tlist[(size_t)(k & 1) * T + blockIdx.y];
-    const int cblk = blockIdx.x;
-    uint4 act = make_uint4(FULL, FULL, FULL, FULL);
-    if (EARLY) {
-        // the syndrome of k_cn(k) tests b^(k-1); it may stop frames only at a check point (k-1) % T == 0
-        const bool check = ((k - 1) % check_every) == 0;
-        const uint4 ua = check ? ldu4(w.unsat + ((size_t)(k & 1) * T + t) * 4) : make_uint4(FULL, FULL, FULL, FULL);
-        const uint4 dw = ldu4(w.done + (size_t)t * 4);
-        const uint4 newly = make_uint4(~ua.x & ~dw.x, ~ua.y & ~dw.y, ~ua.z & ~dw.z, ~ua.w & ~dw.w);
-        act = make_uint4(ua.x & ~dw.x, ua.y & ~dw.y, ua.z & ~dw.z, ua.w & ~dw.w);
-        // every thread must read `done` before the tile's bookkeeping item rewrites it (other items of
-        // the tile may see either value: act is the same for both, since newly and ua are disjoint)
-        __syncthreads();
-        if (cblk == 0) {
-            const int tid = threadIdx.x;
-            if (tid < 4) {
-                w.done[(size_t)t * 4 + tid] = comp(dw, tid) | comp(newly, tid);
-                w.unsat[((size_t)((k + 1) & 1) * T + t) * 4 + tid] = 0;  // buffer of body k+1
-            }
-            if (tid < TILE && ((comp(newly, tid & 3) >> (tid >> 2)) & 1u))
-                w.iters[(size_t)t * TILE + tid] = k - 1;  // stopped after k-1 bodies
-            if (tid == 0 && (act.x | act.y | act.z | act.w)) {  // tile still runs in body k+1
-                const int pos = atomicAdd(w.tcount + ((k + 1) & 1), 1);
-                w.tlist[(size_t)((k + 1) & 1) * T + pos] = t;
-            }
-        }
-        if ((act.x | act.y | act.z | act.w) == 0) return;
-    } else if (cblk == 0 && threadIdx.x == 0) {
-        const int pos = atomicAdd(w.tcount + ((k + 1) & 1), 1);
-        w.tlist[(size_t)((k + 1) & 1) * T + pos] = t;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        w.work[WK_CN] = 0;  // next check-node sweep
+        w.work[WK_MOVE] = 0;
+        w.work[WK_SYN] = 0;
     }
-    const unsigned mine = ((act.x >> lane) & 1u) | (((act.y >> lane) & 1u) << 1) | (((act.z >> lane) & 1u) << 2) |
-                          (((act.w >> lane) & 1u) << 3);
-    const int m = g.m, n = g.n, wr = g.wr;
-    // the tile's row records: [min0 512 B][min1 512 B][loc 128 x sizeof(LocT)][sign words 128 x wr]
-    unsigned char *RB = w.rst + (size_t)t * m * w.rs;
-    const size_t RSW = (size_t)w.rs / 4, RSL = (size_t)w.rs / sizeof(LocT);  // row strides
-    const float *__restrict__ M0l = reinterpret_cast<float *>(RB) + 4 * lane;
-    const float *__restrict__ M1l = reinterpret_cast<float *>(RB) + 128 + 4 * lane;
-    const LocT *__restrict__ LCl = reinterpret_cast<LocT *>(RB + 1024) + 4 * lane;
-    const uint32_t *__restrict__ SGl = reinterpret_cast<uint32_t *>(RB + 1024 + 128 * sizeof(LocT)) + lane;
-    const float *__restrict__ Rl = w.r + (size_t)t * n * TILE + 4 * lane;
-    float *__restrict__ Sl = w.s + (size_t)t * n * TILE + 4 * lane;
-    const int warp = threadIdx.x >> 5;
-    const int j1 = min(n, cblk * cols_per_cta + cols_per_cta);
-    // one edge at a time, few registers, many warps (6 CTAs per SM): the loads of an edge depend only
-    // on its (broadcast) record, and the warps of the SM keep enough of them in flight
-    for (int j = cblk * cols_per_cta + warp; j < j1; j += BNL_T / 32) {
-        const int c0 = __ldg(g.col_ptr + j), dv = __ldg(g.col_ptr + j + 1) - c0;
-        const float4 rv = ld4(Rl + (size_t)j * TILE);
-        float acc[4] = {0.f, 0.f, 0.f, 0.f};
-        for (int q = 0; q < dv; q++) {
-            const int4 ed = __ldg(g.bn_edge + c0 + q);  // {e, i, p, -}, ascending i
-            const size_t ro = (size_t)ed.y * RSW;  // row record of row i
-            const float4 m0 = ld4(M0l + ro), m1 = ld4(M1l + ro);
-            const typename LO::W key = LO::key(LO::load(LCl + (size_t)ed.y * RSL), ed.z);
-            const uint32_t ws = SGl[ro + (ed.z >> 3) * 32] << (28 - 4 * (ed.z & 7));
-#pragma unroll
-            for (int v = 0; v < 4; v++) {
-                const float mag = LO::hit(key, v) ? comp(m1, v) : comp(m0, v);  // Obs. 1
-                acc[v] = acc[v] + flip31(mag, ws << (3 - v));                   // ascending rows from +0.0 (A14)
+    const int m = g.m, n = g.n;
+    const int ncb = (n + BN_COLS - 1) / BN_COLS;
+    const int items = cnt * ncb;
+    const bool compact_ok = EARLY && compact && k + 2 <= L;
+    for (;;) {
+        const int it = next_item(w.work + WK_BN, s_item);
+        if (it >= items) break;
+        const int y = it / ncb, x = it - y * ncb;
+        const int t = w.tlist[(size_t)(k & 1) * Tc + y];
+        uint4 act = make_uint4(FULL, FULL, FULL, FULL);
+        if (EARLY) {
+            // the syndrome of k_cn(k) tests b^(k-1); it may stop frames only at a check point (k-1) % T == 0
+            const bool check = ((k - 1) % check_every) == 0;
+            const uint4 ua = check ? ldu4(w.unsat + ((size_t)(k & 1) * Tc + t) * 4) : make_uint4(FULL, FULL, FULL, FULL);
+            const uint4 dw = ldu4(w.done + (size_t)t * 4);
+            const uint4 newly = make_uint4(~ua.x & ~dw.x, ~ua.y & ~dw.y, ~ua.z & ~dw.z, ~ua.w & ~dw.w);
+            act = make_uint4(ua.x & ~dw.x, ua.y & ~dw.y, ua.z & ~dw.z, ua.w & ~dw.w);
+            // every thread has read `done` before the tile's bookkeeping item rewrites it (other items of
+            // the tile may see either value: act is the same for both, since newly and ua are disjoint)
+            __syncthreads();
+            if (x == 0) {
+                const int tid = threadIdx.x;
+                if (tid < 4) {
+                    w.done[(size_t)t * 4 + tid] = comp(dw, tid) | comp(newly, tid);
+                    w.unsat[((size_t)((k + 1) & 1) * Tc + t) * 4 + tid] = 0;  // buffer of body k+1
+                }
+                if (tid < TILE && ((comp(newly, tid & 3) >> (tid >> 2)) & 1u)) {
+                    const int f = w.fid[(size_t)t * TILE + tid];
+                    w.iters[f] = k - 1;  // stopped after k-1 bodies
+                    w.conv[f] = 1;
+                }
+                if (tid == 0) {
+                    const int run = __popc(act.x) + __popc(act.y) + __popc(act.z) + __popc(act.w);
+                    if (run > 0 && compact_ok && 2 * run < TILE) {  // compaction source
+                        const int pos = atomicAdd(w.ctl + CT_NSRC, 1);
+                        w.csrc[pos] = t;
+                        w.ccnt[pos] = run;
+                    } else if (run > 0) {  // the tile still runs in body k+1
+                        const int pos = atomicAdd(w.tcount + ((k + 1) & 1), 1);
+                        w.tlist[(size_t)((k + 1) & 1) * Tc + pos] = t;
+                    }
+                }
             }
+            if (k > 1 && (act.x | act.y | act.z | act.w) == 0) continue;
+        } else if (x == 0 && threadIdx.x == 0) {
+            const int pos = atomicAdd(w.tcount + ((k + 1) & 1), 1);
+            w.tlist[(size_t)((k + 1) & 1) * Tc + pos] = t;
         }
-        float *o = Sl + (size_t)j * TILE;
-        if (mine == 0xFu) {
-            st4(o, make_float4(acc[0] + rv.x, acc[1] + rv.y, acc[2] + rv.z, acc[3] + rv.w));
-        } else if (mine) {  // frozen frames keep their s
-            if (mine & 1u) o[0] = acc[0] + rv.x;
-            if (mine & 2u) o[1] = acc[1] + rv.y;
-            if (mine & 4u) o[2] = acc[2] + rv.z;
-            if (mine & 8u) o[3] = acc[3] + rv.w;
+        const unsigned mine = ((act.x >> lane) & 1u) | (((act.y >> lane) & 1u) << 1) | (((act.z >> lane) & 1u) << 2) |
+                              (((act.w >> lane) & 1u) << 3);
+        const unsigned char *RB = w.rst + (size_t)t * m * w.rs;
+        const float *__restrict__ Rl = w.r + (size_t)t * n * TILE + 4 * lane;
+        float *__restrict__ Sl = w.s + (size_t)t * n * TILE + 4 * lane;
+        const int j1 = min(n, x * BN_COLS + BN_COLS);
+        for (int j = x * BN_COLS + warp; j < j1; j += BN_T / 32) {
+            const int c0 = __ldg(g.col_ptr + j), dv = __ldg(g.col_ptr + j + 1) - c0;
+            const float4 rv = ld4(Rl + (size_t)j * TILE);
+            float acc[4] = {0.f, 0.f, 0.f, 0.f};
+            for (int q = 0; q < dv; q++) {
+                const int4 ed = __ldg(g.bn_edge + c0 + q);  // {e, i, p, -}, ascending i
+                const unsigned char *Ri = RB + (size_t)ed.y * w.rs;
+                const float4 m0 = ld4(reinterpret_cast<const float *>(Ri) + 4 * lane);
+                const float4 m1 = ld4(reinterpret_cast<const float *>(Ri) + 128 + 4 * lane);
+                const uint32_t b = Ri[REC_EDGE0 + 32 * ed.z + lane];
+#pragma unroll
+                for (int v = 0; v < 4; v++) {
+                    const float mag = (b & (16u << v)) ? comp(m1, v) : comp(m0, v);  // Obs. 1
+                    acc[v] = acc[v] + flip31(mag, b << (31 - v));                    // ascending rows from +0.0 (A14)
+                }
+            }
+            float *o = Sl + (size_t)j * TILE;
+            if (mine == 0xFu) {
+                st4(o, make_float4(acc[0] + rv.x, acc[1] + rv.y, acc[2] + rv.z, acc[3] + rv.w));
+            } else if (k == 1) {  // body 1: frames that stopped at the pre-check keep s = r
+                st4(o, make_float4((mine & 1u) ? acc[0] + rv.x : rv.x, (mine & 2u) ? acc[1] + rv.y : rv.y,
+                                   (mine & 4u) ? acc[2] + rv.z : rv.z, (mine & 8u) ? acc[3] + rv.w : rv.w));
+            } else if (mine) {  // frozen frames keep their s
+                if (mine & 1u) o[0] = acc[0] + rv.x;
+                if (mine & 2u) o[1] = acc[1] + rv.y;
+                if (mine & 4u) o[2] = acc[2] + rv.z;
+                if (mine & 8u) o[3] = acc[3] + rv.w;
+            }
         }
     }
 }
 
 // ------------------------------------------------------------------------------------------------
-// a6: syndrome of b^(L) (the test after the last body), into unsat[slot].
+// f1: compaction of the sources the bit node of body k collected (tiles with fewer than 64 running
+// frames).  Plan (one CTA): the running frames of the sources, in (source, slot) order, get the
+// slots of ceil(R/128) fresh tiles at the end of the workspace; the fresh tiles join the list of body
+// k+1, the sources are retired (their stopped frames stay in place for the stage-out).  If that would
+// not save a tile (or the workspace is full), the sources simply stay in the list.
 // ------------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(CTA) k_syndrome(Graph g, StreamState w, int slot, int rows_per_cta) {
+__global__ void __launch_bounds__(1024) k_compact_plan(StreamState w, int k, const int *kdev) {
+    if (kdev) k = *kdev;
+    __shared__ int s_part[1024];
+    __shared__ int s_tot;
+    const int tid = threadIdx.x, NT = blockDim.x, Tc = w.Tcap;
+    const int nsrc = w.ctl[CT_NSRC];
+    if (nsrc == 0) {
+        if (tid == 0) w.ctl[CT_NDST] = 0;
+        return;
+    }
+    // exclusive scan of the running counts (contiguous ranges per thread)
+    const int per = (nsrc + NT - 1) / NT, a = min(nsrc, tid * per), b = min(nsrc, a + per);
+    int sum = 0;
+    for (int q = a; q < b; q++) sum += w.ccnt[q];
+    s_part[tid] = sum;
+    __syncthreads();
+    if (tid == 0) {
+        int run = 0;
+        for (int q = 0; q < NT; q++) {
+            const int v = s_part[q];
+            s_part[q] = run;
+            run += v;
+        }
+        s_tot = run;
+    }
+    __syncthreads();
+    const int R = s_tot, ndst = (R + TILE - 1) / TILE, base = w.ctl[CT_TNEXT];
+    const int nxt = (k + 1) & 1;
+    if (ndst >= nsrc || base + ndst > Tc) {  // nothing to gain (or no room): the sources keep running
+        if (tid == 0) w.ctl[CT_NDST] = 0;
+        for (int q = tid; q < nsrc; q += NT) {
+            const int pos = atomicAdd(w.tcount + nxt, 1);
+            w.tlist[(size_t)nxt * Tc + pos] = w.csrc[q];
+        }
+        return;
+    }
+    int run = s_part[tid];
+    for (int q = a; q < b; q++) {
+        const int t = w.csrc[q];
+        const uint4 dw = ldu4(w.done + (size_t)t * 4);
+        for (int sl = 0; sl < TILE; sl++) {
+            if ((comp(dw, sl & 3) >> (sl >> 2)) & 1u) continue;  // stopped (or padding): stays
+            const int dt = run >> 7, ds = run & 127;
+            run++;
+            w.cmap[(size_t)dt * TILE + ds] = (t << 7) | sl;
+            w.fid[(size_t)(base + dt) * TILE + ds] = w.fid[(size_t)t * TILE + sl];
+            w.fid[(size_t)t * TILE + sl] = -1;  // moved: its outputs come from the fresh tile
+        }
+        w.done[(size_t)t * 4 + 0] = FULL;
+        w.done[(size_t)t * 4 + 1] = FULL;
+        w.done[(size_t)t * 4 + 2] = FULL;
+        w.done[(size_t)t * 4 + 3] = FULL;
+    }
+    // fresh tiles: padding slots past R in the last one
+    for (int q = tid; q < ndst * TILE; q += NT) {
+        if (q >= R) {
+            w.cmap[q] = -1;
+            w.fid[(size_t)base * TILE + q] = -1;
+        }
+    }
+    for (int dt = tid; dt < ndst; dt += NT) {
+        const int T2 = base + dt;
+        for (int v = 0; v < 4; v++) {
+            uint32_t pad = 0;
+            for (int l = 0; l < 32; l++)
+                if (dt * TILE + 4 * l + v >= R) pad |= 1u << l;
+            w.done[(size_t)T2 * 4 + v] = pad;
+            w.unsat[(size_t)T2 * 4 + v] = 0;
+            w.unsat[((size_t)Tc + T2) * 4 + v] = 0;
+        }
+        const int pos = atomicAdd(w.tcount + nxt, 1);
+        w.tlist[(size_t)nxt * Tc + pos] = T2;
+    }
+    if (tid == 0) {
+        w.ctl[CT_NDST] = ndst;
+        w.ctl[CT_DBASE] = base;
+        w.ctl[CT_TNEXT] = base + ndst;
+        if (w.nlaunch) {  // handle counters: [1] frames moved, [2] compactions, [3] source tiles retired
+            w.nlaunch[1] += (unsigned long long)R;
+            w.nlaunch[2] += 1;
+            w.nlaunch[3] += (unsigned long long)nsrc;
+        }
+    }
+}
+
+// Move (persistent): item = (fresh tile, 8 columns) -> s and r; or (fresh tile, 8 rows) -> min0, min1 and
+// the edge bytes.  Lane l assembles slots 4l..4l+3 from their sources (scalar loads that hit the few
+// source segments the tile draws from) and writes them with one 16-byte store / one byte per edge.
+constexpr int MV_T = 256;
+
+__global__ void __launch_bounds__(MV_T) k_compact_move(Graph g, StreamState w) {
+    __shared__ int s_map[TILE];
+    __shared__ int s_item;
+    const int ndst = w.ctl[CT_NDST];
+    if (ndst == 0) return;
+    const int base = w.ctl[CT_DBASE];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int m = g.m, n = g.n;
+    const int nc = (n + 7) / 8, nrw = (m + 7) / 8, per = nc + nrw;
+    const int items = ndst * per;
+    for (;;) {
+        const int it = next_item(w.work + WK_MOVE, s_item);
+        if (it >= items) break;
+        const int y = it / per, x = it - y * per;
+        if (threadIdx.x < TILE) s_map[threadIdx.x] = w.cmap[(size_t)y * TILE + threadIdx.x];
+        __syncthreads();
+        const int T2 = base + y;
+        int src[4];
+#pragma unroll
+        for (int v = 0; v < 4; v++) src[v] = s_map[4 * lane + v];
+        if (x < nc) {
+            const int j = x * 8 + warp;
+            if (j < n) {
+                float sv[4], rv[4];
+#pragma unroll
+                for (int v = 0; v < 4; v++) {
+                    if (src[v] >= 0) {
+                        const size_t o = ((size_t)(src[v] >> 7) * n + j) * TILE + (src[v] & 127);
+                        sv[v] = w.s[o];
+                        rv[v] = w.r[o];
+                    } else {
+                        sv[v] = rv[v] = -1.0f;
+                    }
+                }
+                const size_t o = ((size_t)T2 * n + j) * TILE + 4 * lane;
+                st4(w.s + o, make_float4(sv[0], sv[1], sv[2], sv[3]));
+                st4(w.r + o, make_float4(rv[0], rv[1], rv[2], rv[3]));
+            }
+        } else {
+            const int i = (x - nc) * 8 + warp;
+            if (i < m) {
+                const int d = __ldg(g.row_ptr + i + 1) - __ldg(g.row_ptr + i);
+                float a0[4], a1[4];
+#pragma unroll
+                for (int v = 0; v < 4; v++) {
+                    if (src[v] >= 0) {
+                        const float *Rs = reinterpret_cast<const float *>(w.rst + ((size_t)(src[v] >> 7) * m + i) * w.rs);
+                        a0[v] = Rs[src[v] & 127];
+                        a1[v] = Rs[128 + (src[v] & 127)];
+                    } else {
+                        a0[v] = a1[v] = 0.f;
+                    }
+                }
+                unsigned char *Rd = w.rst + ((size_t)T2 * m + i) * w.rs;
+                st4(reinterpret_cast<float *>(Rd) + 4 * lane, make_float4(a0[0], a0[1], a0[2], a0[3]));
+                st4(reinterpret_cast<float *>(Rd) + 128 + 4 * lane, make_float4(a1[0], a1[1], a1[2], a1[3]));
+                for (int p = 0; p < d; p++) {
+                    uint32_t byte = 0;
+#pragma unroll
+                    for (int v = 0; v < 4; v++) {
+                        if (src[v] >= 0) {
+                            const int sq = src[v] & 127;
+                            const uint32_t sb =
+                                w.rst[((size_t)(src[v] >> 7) * m + i) * w.rs + REC_EDGE0 + 32 * p + (sq >> 2)];
+                            byte |= ((sb >> (sq & 3)) & 1u) << v;             // sign
+                            byte |= ((sb >> (4 + (sq & 3))) & 1u) << (4 + v);  // isloc
+                        }
+                    }
+                    Rd[REC_EDGE0 + 32 * p + lane] = (unsigned char)byte;
+                }
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// a6: syndrome of b^(L) (the test after the last body), into unsat[slot], over the tiles still running.
+// ------------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(CTA) k_syndrome(Graph g, StreamState w, int slot, const float *__restrict__ sfin) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     __shared__ uint32_t s_u[4];
+    __shared__ int s_item;
     const int cnt = w.tcount[slot];  // tiles still running after the last body
-    if ((int)blockIdx.y >= cnt) return;
-    {
-    const int t = w.tlist[(size_t)slot * w.T + blockIdx.y];
-    const int rblk = blockIdx.x;
-    if (threadIdx.x < 4) s_u[threadIdx.x] = 0;
-    __syncthreads();
-    const size_t tn = (size_t)t * g.n;
-    const int i0 = rblk * rows_per_cta, i1 = min(g.m, i0 + rows_per_cta);
-    uint32_t u[4] = {0, 0, 0, 0};
-    for (int i = i0 + warp; i < i1; i += CTA / 32) {
-        const int a = __ldg(g.row_ptr + i), d = __ldg(g.row_ptr + i + 1) - a;
-        unsigned syn = 0;
-        for (int p = 0; p < d; p++) {
-            const int j = __ldg(g.col_idx + a + p);
-            const float4 sv = ld4(w.s + (tn + j) * TILE + 4 * lane);
-            syn ^= (unsigned)(sv.x > 0.f) | ((unsigned)(sv.y > 0.f) << 1) | ((unsigned)(sv.z > 0.f) << 2) |
-                   ((unsigned)(sv.w > 0.f) << 3);
+    const int nrb = (g.m + CN_ROWS - 1) / CN_ROWS;
+    const int items = cnt * nrb;
+    for (;;) {
+        if (threadIdx.x < 4) s_u[threadIdx.x] = 0;
+        const int it = next_item(w.work + WK_SYN, s_item);
+        if (it >= items) break;
+        const int y = it / nrb, x = it - y * nrb;
+        const int t = w.tlist[(size_t)slot * w.Tcap + y];
+        const size_t tn = (size_t)t * g.n;
+        const int i0 = x * CN_ROWS, i1 = min(g.m, i0 + CN_ROWS);
+        uint32_t u[4] = {0, 0, 0, 0};
+        for (int i = i0 + warp; i < i1; i += CTA / 32) {
+            const int a = __ldg(g.row_ptr + i), d = __ldg(g.row_ptr + i + 1) - a;
+            unsigned syn = 0;
+            for (int p = 0; p < d; p++) {
+                const int j = __ldg(g.col_idx + a + p);
+                const float4 sv = ld4(sfin + (tn + j) * TILE + 4 * lane);
+                syn ^= (unsigned)(sv.x > 0.f) | ((unsigned)(sv.y > 0.f) << 1) | ((unsigned)(sv.z > 0.f) << 2) |
+                       ((unsigned)(sv.w > 0.f) << 3);
+            }
+#pragma unroll
+            for (int v = 0; v < 4; v++) u[v] |= __ballot_sync(FULL, (syn >> v) & 1u);
         }
+        if (lane == 0)
 #pragma unroll
-        for (int v = 0; v < 4; v++) u[v] |= __ballot_sync(FULL, (syn >> v) & 1u);
-    }
-    if (lane == 0)
-#pragma unroll
-        for (int v = 0; v < 4; v++)
-            if (u[v]) atomicOr(&s_u[v], u[v]);
-    __syncthreads();
-    if (threadIdx.x < 4 && s_u[threadIdx.x])
-        atomicOr(w.unsat + ((size_t)slot * w.T + t) * 4 + threadIdx.x, s_u[threadIdx.x]);
+            for (int v = 0; v < 4; v++)
+                if (u[v]) atomicOr(&s_u[v], u[v]);
+        __syncthreads();
+        if (threadIdx.x < 4 && s_u[threadIdx.x])
+            atomicOr(w.unsat + ((size_t)slot * w.Tcap + t) * 4 + threadIdx.x, s_u[threadIdx.x]);
     }
 }
 
 // ------------------------------------------------------------------------------------------------
-// a7: stage-out.  s [T][n][128] -> posterior [F][n], bits = slice(s) [F][n]; per-frame counters.
+// a7: stage-out.  For every tile ever used and every slot holding a frame (fid >= 0): posterior
+// [F][n] = s, bits = slice(s) (transposed through shared memory: 128-byte rows per frame), the
+// per-frame bit errors and near-zero flag; block 0 of a tile also settles the frames that ran all L
+// bodies (k = L, isCodeword = the final syndrome).
 // ------------------------------------------------------------------------------------------------
-constexpr int FIN_SUB = 8;  // 32-column sub-blocks per finalize CTA
-
-__global__ void __launch_bounds__(CTA) k_finalize(StreamState w, int n, int64_t frames, float *__restrict__ post,
+__global__ void __launch_bounds__(CTA) k_finalize(StreamState w, int n, int L, int final_slot,
+                                                  const float *__restrict__ sfin, float *__restrict__ post,
                                                   uint8_t *__restrict__ bits) {
     __shared__ float ts[32][TILE + 1];
-    __shared__ float tr[32][TILE + 1];
+    __shared__ int s_fid[TILE];
     const int t = blockIdx.y;
+    if (t >= w.ctl[CT_TNEXT]) return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    // per-frame counters over the CTA's 256 columns: lane q holds frame warp + 8q (q < 16); one atomic
-    // per frame and CTA instead of one per 32 columns
-    int be_acc = 0, raw_acc = 0;
+    if (threadIdx.x < TILE) {
+        const int q = threadIdx.x, f = w.fid[(size_t)t * TILE + q];
+        s_fid[q] = f;
+        if (blockIdx.x == 0 && f >= 0) {
+            const uint32_t dn = w.done[(size_t)t * 4 + (q & 3)];
+            if (!((dn >> (q >> 2)) & 1u)) {  // still running after body L
+                w.iters[f] = L;
+                w.conv[f] = !((w.unsat[((size_t)final_slot * w.Tcap + t) * 4 + (q & 3)] >> (q >> 2)) & 1u);
+            }
+        }
+    }
+    __syncthreads();
+    int be_acc = 0;  // lane q < 16 of warp w: slot w + 8q
     bool nz_acc = false;
-    for (int sb = 0; sb < FIN_SUB; sb++) {
-        const int j0 = (blockIdx.x * FIN_SUB + sb) * 32;
+    for (int sb = 0; sb < SI_SUB; sb++) {
+        const int j0 = (blockIdx.x * SI_SUB + sb) * 32;
         if (j0 >= n) break;
         for (int jl = warp; jl < 32; jl += CTA / 32) {
             const int j = j0 + jl;
             if (j >= n) break;
             const size_t base = ((size_t)t * n + j) * TILE;
 #pragma unroll
-            for (int q = 0; q < 4; q++) {
-                ts[jl][lane + 32 * q] = w.s[base + lane + 32 * q];
-                tr[jl][lane + 32 * q] = w.r[base + lane + 32 * q];
-            }
+            for (int q = 0; q < 4; q++) ts[jl][lane + 32 * q] = sfin[base + lane + 32 * q];
         }
         __syncthreads();
         const int j = j0 + lane;
         const bool jv = j < n;
 #pragma unroll 4
         for (int q = 0; q < TILE / (CTA / 32); q++) {
-            const int fl = warp + (CTA / 32) * q;
-            const int64_t f = (int64_t)t * TILE + fl;
-            if (f >= frames) break;
-            const float sv = ts[lane][fl];
+            const int sl = warp + (CTA / 32) * q;
+            const int f = s_fid[sl];
+            if (f < 0) continue;  // warp-uniform
+            const float sv = ts[lane][sl];
             const bool b = jv && sv > 0.f;  // Eq. slice
             if (jv) {
-                if (post) post[f * n + j] = sv;
-                if (bits) bits[f * n + j] = (uint8_t)b;
+                if (post) post[(int64_t)f * n + j] = sv;
+                if (bits) bits[(int64_t)f * n + j] = (uint8_t)b;
             }
             const int be = __popc(__ballot_sync(FULL, b));
-            const int raw = __popc(__ballot_sync(FULL, jv && tr[lane][fl] > 0.f));
             const bool nz = __any_sync(FULL, jv && fabsf(sv) <= 1e-4f);
             if (lane == q) {
                 be_acc += be;
-                raw_acc += raw;
                 nz_acc = nz_acc || nz;
             }
         }
-        __syncthreads();  // the next sub-block overwrites ts / tr
+        __syncthreads();  // the next sub-block overwrites ts
     }
     if (lane < TILE / (CTA / 32)) {
-        const int fl = warp + (CTA / 32) * lane;
-        if ((int64_t)t * TILE + fl < frames) {
-            if (be_acc) atomicAdd(w.fbe + (size_t)t * TILE + fl, be_acc);
-            if (raw_acc) atomicAdd(w.fraw + (size_t)t * TILE + fl, raw_acc);
-            if (nz_acc) w.fnz[(size_t)t * TILE + fl] = 1;
+        const int f = s_fid[warp + (CTA / 32) * lane];
+        if (f >= 0) {
+            if (be_acc) atomicAdd(w.fbe + f, be_acc);
+            if (nz_acc) w.fnz[f] = 1;
         }
     }
 }
 
 // per-frame k, isCodeword and the 8 accumulated counters
-__global__ void __launch_bounds__(CTA) k_frame_stats(StreamState w, int64_t frames, int L, int early, int slot,
-                                                     int32_t *__restrict__ iters_out, uint8_t *__restrict__ conv_out,
+__global__ void __launch_bounds__(CTA) k_frame_stats(StreamState w, int64_t frames, int32_t *__restrict__ iters_out,
+                                                     uint8_t *__restrict__ conv_out,
                                                      unsigned long long *__restrict__ stats) {
     __shared__ unsigned long long s_acc[8];
     if (threadIdx.x < 8) s_acc[threadIdx.x] = 0;
@@ -681,16 +820,7 @@ __global__ void __launch_bounds__(CTA) k_frame_stats(StreamState w, int64_t fram
     const int64_t f = blockIdx.x * (int64_t)CTA + threadIdx.x;
     unsigned long long c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (f < frames) {
-        const int64_t t = f / TILE;
-        const int fl = (int)(f % TILE), ln = fl >> 2, v = fl & 3;
-        int it = L, conv;
-        const bool stopped = early && ((w.done[t * 4 + v] >> ln) & 1u);
-        if (stopped) {
-            it = w.iters[f];
-            conv = 1;
-        } else {
-            conv = !((w.unsat[((int64_t)slot * w.T + t) * 4 + v] >> ln) & 1u);
-        }
+        const int it = w.iters[f], conv = w.conv[f];
         if (iters_out) iters_out[f] = it;
         if (conv_out) conv_out[f] = (uint8_t)conv;
         const int be = w.fbe[f];
@@ -721,7 +851,7 @@ __global__ void k_loop_pre(StreamState w, int L, cudaGraphConditionalHandle h) {
     const int k = 2;
     const bool run = k <= L && w.tcount[k & 1] > 0;
     *w.kdev = k;
-    if (run && w.nlaunch) *w.nlaunch += 3;  // check node, bit node, step of body k
+    if (run && w.nlaunch) *w.nlaunch += BODY_LAUNCHES;
     if (!run) w.tcount[(L + 1) & 1] = 0;
     cudaGraphSetConditional(h, run ? 1u : 0u);
 }
@@ -730,79 +860,71 @@ __global__ void k_loop_step(StreamState w, int L, cudaGraphConditionalHandle h) 
     const int k = *w.kdev + 1;
     const bool run = k <= L && w.tcount[k & 1] > 0;
     *w.kdev = k;
-    if (run && w.nlaunch) *w.nlaunch += 3;
+    if (run && w.nlaunch) *w.nlaunch += BODY_LAUNCHES;
     if (!run && k <= L) w.tcount[(L + 1) & 1] = 0;
     cudaGraphSetConditional(h, run ? 1u : 0u);
 }
 
 inline dim3 grid2(int64_t x, int y) { return dim3((unsigned)std::max<int64_t>(1, x), (unsigned)y); }
 
+template <bool F, bool EA>
+void cn_launch(const Graph &g, const StreamState &w, int k, int lit, const StreamLaunch &cfg, cudaStream_t st,
+               const int *kdev) {
+    const dim3 grid(cfg.sms * CN_MINB), gridg(cfg.sms * 2);
+    if (!cfg.cn_generic && g.dmax <= 8) {
+        if (g.dmax <= 4) k_cn<4, F, EA><<<grid, CN_T, 0, st>>>(g, w, k, lit, kdev);
+        else if (g.dmax <= 6) k_cn<6, F, EA><<<grid, CN_T, 0, st>>>(g, w, k, lit, kdev);
+        else if (g.dmax == 7) k_cn<7, F, EA><<<grid, CN_T, 0, st>>>(g, w, k, lit, kdev);
+        else k_cn<8, F, EA><<<grid, CN_T, 0, st>>>(g, w, k, lit, kdev);
+    } else {
+        k_cn_generic<F, EA><<<gridg, CN_T, 0, st>>>(g, w, k, lit, kdev);
+    }
+}
+
 }  // namespace
 
+int edge_capacity(int dmax, bool generic) {
+    if (!generic && dmax <= 8) return dmax <= 4 ? 4 : dmax <= 6 ? 6 : dmax == 7 ? 7 : 8;
+    return (dmax + 7) / 8 * 8;
+}
+
 int launch_stage_in(const Graph &g, const StreamState &w, const float *llr, int64_t frames, cudaStream_t st) {
-    k_stage_in<<<grid2((g.n + 31) / 32, w.T), CTA, 0, st>>>(llr, frames, g.n, w.T, w.r, w.s, w.unsat, w.done, w.fbe,
-                                                           w.fraw, w.fnz, w.tcount, w.tlist);
+    cudaMemsetAsync(w.fcnt, 0, sizeof(int) * 3 * (size_t)w.T * TILE, st);  // fbe, fraw, fnz
+    k_stage_in<<<grid2((g.n + 32 * SI_SUB - 1) / (32 * SI_SUB), w.T), CTA, 0, st>>>(llr, frames, g.n, w);
     return 1;
 }
 
-template <typename LT, bool F, bool EA>
-void cn_launch(dim3 grid, cudaStream_t st, const Graph &g, const StreamState &w, int k, int rpc, int lit, int u,
-               const int *kdev) {
-    // u: 0 = single row buffer (default), 2 = two row buffers, 1 = generic kernel
-    if (u != 1 && u != 2 && g.dmax <= 8) {
-        if (g.dmax <= 4) k_cn_pipe<4, LT, F, EA, false><<<grid, CN_T, 0, st>>>(g, w, k, rpc, lit, kdev);
-        else if (g.dmax <= 6) k_cn_pipe<6, LT, F, EA, false><<<grid, CN_T, 0, st>>>(g, w, k, rpc, lit, kdev);
-        else if (g.dmax == 7) k_cn_pipe<7, LT, F, EA, false><<<grid, CN_T, 0, st>>>(g, w, k, rpc, lit, kdev);
-        else k_cn_pipe<8, LT, F, EA, false><<<grid, CN_T, 0, st>>>(g, w, k, rpc, lit, kdev);
-    } else if (u == 2 && g.dmax <= 6) k_cn_pipe<6, LT, F, EA, true><<<grid, CN_T, 0, st>>>(g, w, k, rpc, lit, kdev);
-    else if (u == 2 && g.dmax <= 8) k_cn_pipe<8, LT, F, EA, true><<<grid, CN_T, 0, st>>>(g, w, k, rpc, lit, kdev);
-    else k_cn<LT, F, EA><<<grid, CTA, 0, st>>>(g, w, k, rpc, lit, kdev);
-}
-
-template <typename LT, bool EA>
-void bn_launch(dim3 grid, cudaStream_t st, const Graph &g, const StreamState &w, int k, int cpc, int lit, int u,
-               const int *kdev, int te) {
-    (void)grid;
-    (void)cpc;
-    (void)u;
-    k_bn<LT, EA><<<grid2((g.n + BNL_COLS - 1) / BNL_COLS, w.T), BNL_T, 0, st>>>(g, w, k, BNL_COLS, lit, kdev, te);
-}
-
-int launch_check_node(const Graph &g, const StreamState &w, int k, bool first, bool early, bool literal, bool loc16,
+int launch_check_node(const Graph &g, const StreamState &w, int k, bool first, bool early, bool literal,
                       const StreamLaunch &cfg, cudaStream_t st, const int *kdev) {
-    const dim3 grid = grid2((g.m + cfg.rows_per_cta - 1) / cfg.rows_per_cta, w.T);
-    const int lit = literal ? 1 : 0, rpc = cfg.rows_per_cta, u = cfg.cn_unroll;
-    if (loc16) {
-        if (first) { if (early) cn_launch<uint16_t, true, true>(grid, st, g, w, k, rpc, lit, u, kdev);
-                     else cn_launch<uint16_t, true, false>(grid, st, g, w, k, rpc, lit, u, kdev); }
-        else { if (early) cn_launch<uint16_t, false, true>(grid, st, g, w, k, rpc, lit, u, kdev);
-               else cn_launch<uint16_t, false, false>(grid, st, g, w, k, rpc, lit, u, kdev); }
+    const int lit = literal ? 1 : 0;
+    if (first) {
+        if (early) cn_launch<true, true>(g, w, k, lit, cfg, st, kdev);
+        else cn_launch<true, false>(g, w, k, lit, cfg, st, kdev);
     } else {
-        if (first) { if (early) cn_launch<uint8_t, true, true>(grid, st, g, w, k, rpc, lit, u, kdev);
-                     else cn_launch<uint8_t, true, false>(grid, st, g, w, k, rpc, lit, u, kdev); }
-        else { if (early) cn_launch<uint8_t, false, true>(grid, st, g, w, k, rpc, lit, u, kdev);
-               else cn_launch<uint8_t, false, false>(grid, st, g, w, k, rpc, lit, u, kdev); }
+        if (early) cn_launch<false, true>(g, w, k, lit, cfg, st, kdev);
+        else cn_launch<false, false>(g, w, k, lit, cfg, st, kdev);
     }
     return 1;
 }
 
-int launch_bit_node(const Graph &g, const StreamState &w, int k, bool early, bool literal, bool loc16,
-                    const StreamLaunch &cfg, cudaStream_t st, const int *kdev) {
-    const dim3 grid = grid2((g.n + BNL_COLS - 1) / BNL_COLS, w.T);
-    const int lit = literal ? 1 : 0, cpc = BNL_COLS, u = 0;
-    if (loc16) {
-        if (early) bn_launch<uint16_t, true>(grid, st, g, w, k, cpc, lit, u, kdev, cfg.check_every);
-        else bn_launch<uint16_t, false>(grid, st, g, w, k, cpc, lit, u, kdev, cfg.check_every);
-    } else {
-        if (early) bn_launch<uint8_t, true>(grid, st, g, w, k, cpc, lit, u, kdev, cfg.check_every);
-        else bn_launch<uint8_t, false>(grid, st, g, w, k, cpc, lit, u, kdev, cfg.check_every);
-    }
+int launch_bit_node(const Graph &g, const StreamState &w, int k, int L, bool early, const StreamLaunch &cfg,
+                    cudaStream_t st, const int *kdev) {
+    const dim3 grid(cfg.sms * BN_MINB);
+    if (early) k_bn<true><<<grid, BN_T, 0, st>>>(g, w, k, L, kdev, cfg.check_every, cfg.compact ? 1 : 0);
+    else k_bn<false><<<grid, BN_T, 0, st>>>(g, w, k, L, kdev, cfg.check_every, 0);
     return 1;
 }
 
-int launch_syndrome(const Graph &g, const StreamState &w, int slot, const StreamLaunch &cfg, cudaStream_t st) {
-    k_syndrome<<<grid2((g.m + cfg.rows_per_cta - 1) / cfg.rows_per_cta, w.T), CTA, 0, st>>>(g, w, slot,
-                                                                                             cfg.rows_per_cta);
+int launch_compact(const Graph &g, const StreamState &w, int k, const StreamLaunch &cfg, cudaStream_t st,
+                   const int *kdev) {
+    k_compact_plan<<<1, 1024, 0, st>>>(w, k, kdev);
+    k_compact_move<<<cfg.sms * 4, MV_T, 0, st>>>(g, w);
+    return 2;
+}
+
+int launch_syndrome(const Graph &g, const StreamState &w, int slot, const float *sfin, const StreamLaunch &cfg,
+                    cudaStream_t st) {
+    k_syndrome<<<cfg.sms * 4, CTA, 0, st>>>(g, w, slot, sfin);
     return 1;
 }
 
@@ -816,17 +938,17 @@ int launch_loop_step(const StreamState &w, int L, cudaGraphConditionalHandle h, 
     return 1;
 }
 
-int launch_finalize(const Graph &g, const StreamState &w, int64_t frames, float *posterior, uint8_t *bits,
-                    cudaStream_t st) {
-    k_finalize<<<grid2((g.n + 32 * FIN_SUB - 1) / (32 * FIN_SUB), w.T), CTA, 0, st>>>(w, g.n, frames, posterior, bits);
+int launch_finalize(const Graph &g, const StreamState &w, int L, int final_slot, const float *sfin, float *posterior,
+                    uint8_t *bits, cudaStream_t st) {
+    k_finalize<<<grid2((g.n + 32 * SI_SUB - 1) / (32 * SI_SUB), w.Tcap), CTA, 0, st>>>(w, g.n, L, final_slot, sfin,
+                                                                                       posterior, bits);
     return 1;
 }
 
-int launch_frame_stats(const Graph &g, const StreamState &w, int64_t frames, int L, bool early, int final_slot,
-                       int32_t *iters_out, uint8_t *conv_out, unsigned long long *stats, cudaStream_t st) {
-    (void)g;
-    k_frame_stats<<<(unsigned)std::max<int64_t>(1, (frames + CTA - 1) / CTA), CTA, 0, st>>>(
-        w, frames, L, early ? 1 : 0, final_slot, iters_out, conv_out, stats);
+int launch_frame_stats(const StreamState &w, int64_t frames, int32_t *iters_out, uint8_t *conv_out,
+                       unsigned long long *stats, cudaStream_t st) {
+    k_frame_stats<<<(unsigned)std::max<int64_t>(1, (frames + CTA - 1) / CTA), CTA, 0, st>>>(w, frames, iters_out,
+                                                                                           conv_out, stats);
     return 1;
 }
 

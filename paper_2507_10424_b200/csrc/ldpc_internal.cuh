@@ -28,30 +28,45 @@ struct Graph {
     int dvmax;           // max column degree
 };
 
-// Per-chunk decode state of the streaming schedule, frame-interleaved in tiles of 128:
-//   r, s   [T][n][128] fp32          channel values and current soft vector (Eq. sCalculation)
-//   rst    [T][m] row records of rs bytes: the check-node state of row i for the tile's 128 frames,
+// Per-chunk decode state of the streaming schedule, frame-interleaved in tiles of 128 slots (T tiles
+// hold the chunk's frames; the workspace has Tcap >= T tiles, the extra ones receive compacted frames):
+//   r, s   [Tcap][n][128] fp32       channel values and current soft vector (Eq. sCalculation)
+//   rst    [Tcap][m] row records of rs bytes: the check-node state of row i for the tile's 128 slots,
 //          contiguous so that a gather of one row touches one DRAM page:
 //            min0 [128] fp32   |lambda| minimum of the row; SIGN BIT = row sign parity (Obs. 2)
 //            min1 [128] fp32   second minimum (Obs. 1); same sign bit as min0
-//            loc  [128] u8/u16 min0Location as the position inside N_i
-//            sgn  [wr][32] u32 sign bits of lambda_e, row-transposed: word (p/8, lane l) holds bit
-//                              4*(p%8) + v = sign for edge p of the row, frame 4l+v
-//   unsat  [2][T][4]   u32           per-frame "some check unsatisfied" bits (double-buffered by iteration)
-//   done   [T][4]      u32           per-frame "stopped" bits
-//   iters  [T*128]     i32           k at which a frame stopped (early stop)
-//   fbe/fraw/fnz [T*128] i32         per-frame bit errors, raw errors, near-zero flag
+//            edge blocks [ecap][32 B]: byte l of edge p = sign nibble (bit v: sign of lambda_e, slot
+//                              4l+v) | isloc nibble << 4 (bit v: p == min0Location of slot 4l+v)
+//   unsat  [2][Tcap][4] u32          per-slot "some check unsatisfied" bits (double-buffered by body)
+//   done   [Tcap][4]    u32          per-slot "stopped" bits (padding and moved-away slots are done)
+//   fid    [Tcap][128]  i32          chunk frame index held by the slot (-1: none)
+//   per chunk frame f < T*128: iters, conv (k and isCodeword), fcnt = fbe | fraw | fnz (bit errors,
+//   raw errors, near-zero flag)
+//   compaction: csrc/ccnt [Tcap] source tiles of this body and their running counts, cmap [Tcap][128]
+//   (fresh slot -> source tile << 7 | slot), ctl [8] counters, work [4] persistent-sweep item counters
+constexpr int REC_EDGE0 = 1024;  // byte offset of edge block 0 in a row record
+enum { WK_CN = 0, WK_BN = 1, WK_MOVE = 2, WK_SYN = 3 };
+enum { CT_TNEXT = 0, CT_NSRC = 1, CT_NDST = 2, CT_DBASE = 3 };
+// launches of one graph-driven loop body: check node, bit node, compaction plan + move, loop step
+constexpr int BODY_LAUNCHES = 5;
+
 struct StreamState {
-    int T;
+    int T, Tcap;
     float *r, *s;
     unsigned char *rst;  // row records
-    int rs;              // bytes per row record: 1024 + 128 sizeof(loc) + 128 wr
+    int rs;              // bytes per row record: 1024 + 32 ecap
     uint32_t *unsat, *done;
-    int *iters, *fbe, *fraw, *fnz;
+    int *fid;
+    int *iters, *conv;
+    int *fcnt, *fbe, *fraw, *fnz;
     int *tcount;  // [2]     number of tiles with a running frame, per body parity
-    int *tlist;   // [2][T]  those tiles
+    int *tlist;   // [2][Tcap]  those tiles
     int *kdev;    // body index of the graph-driven loop
-    unsigned long long *nlaunch;  // launches of graph-driven loop bodies (3 per body that ran), or null
+    int *work;    // [4]
+    int *ctl;     // [8]
+    int *csrc, *ccnt, *cmap;
+    unsigned long long *nlaunch;  // [4] handle counters: [0] graph-loop launches, [1] frames moved by
+                                  // compaction, [2] compactions, [3] tiles retired by them; or null
 };
 
 // ---- ingest (ingest.cu) ----
@@ -70,23 +85,29 @@ struct HostGraph {  // device allocations owned by the plan
 
 // ---- streaming schedule (decode_stream.cu) ----
 struct StreamLaunch {
-    int rows_per_cta = 128;  // check-node rows per CTA, <= 256 (a warp owns <= 32 rows); 128 measured best
-    int cn_unroll = 0;      // check-node kernel: 0 = one row buffer (default), 1 = generic, 2 = two row buffers
+    int sms = 148;          // persistent sweep grids are multiples of the SM count
+    bool cn_generic = false;  // force the any-degree check-node kernel (tests)
+    bool compact = true;    // f1: compaction of tiles with fewer than half of their frames running
     int check_every = 1;    // codeword test after body k when k % T == 0 (and after body L)
 };
+// edge blocks per row record for a maximum row degree (the check-node instance reads CH of them)
+int edge_capacity(int dmax, bool generic);
 // Launch helpers; each returns the number of kernels launched.
 int launch_stage_in(const Graph &g, const StreamState &w, const float *llr, int64_t frames, cudaStream_t st);
-int launch_check_node(const Graph &g, const StreamState &w, int k, bool first, bool early, bool literal, bool loc16,
+int launch_check_node(const Graph &g, const StreamState &w, int k, bool first, bool early, bool literal,
                       const StreamLaunch &cfg, cudaStream_t st, const int *kdev = nullptr);
-int launch_bit_node(const Graph &g, const StreamState &w, int k, bool early, bool literal, bool loc16,
-                    const StreamLaunch &cfg, cudaStream_t st, const int *kdev = nullptr);
+int launch_bit_node(const Graph &g, const StreamState &w, int k, int L, bool early, const StreamLaunch &cfg,
+                    cudaStream_t st, const int *kdev = nullptr);
+int launch_compact(const Graph &g, const StreamState &w, int k, const StreamLaunch &cfg, cudaStream_t st,
+                   const int *kdev = nullptr);
 int launch_loop_pre(const StreamState &w, int L, cudaGraphConditionalHandle h, cudaStream_t st);
 int launch_loop_step(const StreamState &w, int L, cudaGraphConditionalHandle h, cudaStream_t st);
-int launch_syndrome(const Graph &g, const StreamState &w, int slot, const StreamLaunch &cfg, cudaStream_t st);
-int launch_finalize(const Graph &g, const StreamState &w, int64_t frames, float *posterior, uint8_t *bits,
+int launch_syndrome(const Graph &g, const StreamState &w, int slot, const float *sfin, const StreamLaunch &cfg,
                     cudaStream_t st);
-int launch_frame_stats(const Graph &g, const StreamState &w, int64_t frames, int L, bool early, int final_slot,
-                       int32_t *iters_out, uint8_t *conv_out, unsigned long long *stats, cudaStream_t st);
+int launch_finalize(const Graph &g, const StreamState &w, int L, int final_slot, const float *sfin, float *posterior,
+                    uint8_t *bits, cudaStream_t st);
+int launch_frame_stats(const StreamState &w, int64_t frames, int32_t *iters_out, uint8_t *conv_out,
+                       unsigned long long *stats, cudaStream_t st);
 
 // ---- resident schedule (decode_resident.cu) ----
 struct ResidentPlan {

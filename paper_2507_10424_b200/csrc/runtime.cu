@@ -103,66 +103,74 @@ void launch(ldpc_plan *h, int cls, cudaStream_t st, F &&fn) {
 
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
-// bytes of one row record of the streaming schedule: min0, min1 (128 fp32 each), loc (128 u8/u16),
-// sign words (32 u32 per 8 edges of the longest row)
-int row_record_bytes(const HostGraph &g, bool loc16) { return 1024 + 128 * (loc16 ? 2 : 1) + 128 * ((g.max_row_deg + 7) / 8); }
-
-size_t tile_bytes(const HostGraph &g, bool loc16) {
-    const size_t m = g.m, n = g.n;
-    size_t b = 0;
-    b += 2 * align256(n * TILE * 4);                 // r, s
-    b += align256(m * (size_t)row_record_bytes(g, loc16));  // row records (min0, min1, loc, signs)
-    b += 3 * 256;                                    // unsat x2, done
-    b += 4 * align256(TILE * 4);                     // iters, fbe, fraw, fnz
-    b += 3 * 4 + 256;                                // tcount, tlist
-    return b;
+// bytes of one row record of the streaming schedule: min0, min1 (128 fp32 each) and one 32-byte edge
+// block per edge position the check-node instance reads
+int row_record_bytes(const ldpc_plan *h) {
+    return REC_EDGE0 + 32 * edge_capacity(h->g.max_row_deg, h->cfg.cn_generic);
 }
 
-// carve the workspace into per-array regions of T tiles each
-StreamState carve(void *base, int T, const HostGraph &g, bool loc16) {
-    const size_t m = g.m, n = g.n;
-    char *p = static_cast<char *>(base);
+// workspace tiles for a chunk of T tiles: room for the fresh tiles of the compactions (each one retires
+// more tiles than it creates; the plan kernel never exceeds the capacity)
+int tile_capacity(const ldpc_plan *h, int T) { return h->cfg.compact ? 2 * T : T; }
+
+// Carve the workspace into its arrays (base == nullptr: only the size).  Per tile: r, s, row records,
+// flags, slot frame indices, compaction map; per chunk frame: k, isCodeword, three counters.
+StreamState carve(void *base, int T, int Tcap, const ldpc_plan *h, size_t *total) {
+    const size_t m = h->g.m, n = h->g.n;
+    char *p0 = static_cast<char *>(base), *p = p0;
+    size_t off = 0;
     auto take = [&](size_t bytes) {
-        char *q = p;
-        p += align256(bytes);
+        char *q = p0 ? p0 + off : nullptr;
+        off += align256(bytes);
         return q;
     };
-    StreamState w;
+    (void)p;
+    StreamState w{};
     w.T = T;
-    w.r = reinterpret_cast<float *>(take((size_t)T * n * TILE * 4));
-    w.s = reinterpret_cast<float *>(take((size_t)T * n * TILE * 4));
-    w.rs = row_record_bytes(g, loc16);
-    w.rst = reinterpret_cast<unsigned char *>(take((size_t)T * m * w.rs));
-    w.unsat = reinterpret_cast<uint32_t *>(take((size_t)2 * T * 16));
-    w.done = reinterpret_cast<uint32_t *>(take((size_t)T * 16));
+    w.Tcap = Tcap;
+    w.rs = row_record_bytes(h);
+    w.r = reinterpret_cast<float *>(take((size_t)Tcap * n * TILE * 4));
+    w.s = reinterpret_cast<float *>(take((size_t)Tcap * n * TILE * 4));
+    w.rst = reinterpret_cast<unsigned char *>(take((size_t)Tcap * m * w.rs));
+    w.unsat = reinterpret_cast<uint32_t *>(take((size_t)2 * Tcap * 16));
+    w.done = reinterpret_cast<uint32_t *>(take((size_t)Tcap * 16));
+    w.fid = reinterpret_cast<int *>(take((size_t)Tcap * TILE * 4));
     w.iters = reinterpret_cast<int *>(take((size_t)T * TILE * 4));
-    w.fbe = reinterpret_cast<int *>(take((size_t)T * TILE * 4));
-    w.fraw = reinterpret_cast<int *>(take((size_t)T * TILE * 4));
-    w.fnz = reinterpret_cast<int *>(take((size_t)T * TILE * 4));
+    w.conv = reinterpret_cast<int *>(take((size_t)T * TILE * 4));
+    w.fcnt = reinterpret_cast<int *>(take((size_t)3 * T * TILE * 4));
+    w.fbe = w.fcnt ? w.fcnt : nullptr;
+    w.fraw = w.fcnt ? w.fcnt + (size_t)T * TILE : nullptr;
+    w.fnz = w.fcnt ? w.fcnt + (size_t)2 * T * TILE : nullptr;
     w.tcount = reinterpret_cast<int *>(take(2 * 4));
-    w.tlist = reinterpret_cast<int *>(take((size_t)2 * T * 4));
+    w.tlist = reinterpret_cast<int *>(take((size_t)2 * Tcap * 4));
     w.kdev = reinterpret_cast<int *>(take(4));
-    w.nlaunch = nullptr;  // set by the caller (a plan-owned counter that outlives the workspace)
+    w.work = reinterpret_cast<int *>(take(4 * 4));
+    w.ctl = reinterpret_cast<int *>(take(8 * 4));
+    w.csrc = reinterpret_cast<int *>(take((size_t)Tcap * 4));
+    w.ccnt = reinterpret_cast<int *>(take((size_t)Tcap * 4));
+    w.cmap = reinterpret_cast<int *>(take((size_t)Tcap * TILE * 4));
+    w.nlaunch = h->dev_launches;
+    if (total) *total = off;
     return w;
 }
 
-int64_t auto_chunk_tiles(ldpc_plan *h, bool loc16) {
-    size_t freeb = 0, total = 0;
-    cudaMemGetInfo(&freeb, &total);
-    size_t budget = std::min<size_t>(freeb / 2 + h->ws_bytes / 2, (size_t)32 << 30);
-    int64_t tiles = (int64_t)(budget / tile_bytes(h->g, loc16));
-    return std::max<int64_t>(1, std::min<int64_t>(tiles, 65535));
+size_t ws_bytes_for(const ldpc_plan *h, int T) {
+    size_t total = 0;
+    carve(nullptr, T, tile_capacity(h, T), h, &total);
+    return total;
 }
 
-int ensure_ws(ldpc_plan *h, int T, bool loc16) {
-    // size for the full per-array layout of T tiles
-    size_t need = 0;
-    {
-        const size_t m = h->g.m, n = h->g.n;
-        need = 2 * align256((size_t)T * n * TILE * 4) + align256((size_t)T * m * row_record_bytes(h->g, loc16)) +
-               align256((size_t)2 * T * 16) + align256((size_t)T * 16) + 4 * align256((size_t)T * TILE * 4) +
-               align256(8) + align256((size_t)2 * T * 4) + align256(4);
-    }
+int64_t auto_chunk_tiles(ldpc_plan *h) {
+    size_t freeb = 0, total = 0;
+    cudaMemGetInfo(&freeb, &total);
+    const size_t budget = std::min<size_t>(freeb / 2 + h->ws_bytes / 2, (size_t)64 << 30);
+    const size_t per = std::max<size_t>(1, ws_bytes_for(h, 1024) / 1024);  // bytes per chunk tile
+    const int64_t tiles = (int64_t)(budget / per);
+    return std::max<int64_t>(1, std::min<int64_t>(tiles, 32767));
+}
+
+int ensure_ws(ldpc_plan *h, int T) {
+    const size_t need = ws_bytes_for(h, T);
     if (need <= h->ws_bytes) return LDPC_OK;
     for (auto &ge : h->graphs) {  // graphs embed workspace pointers
         cudaGraphExecDestroy(ge.exec);
@@ -190,16 +198,18 @@ int check_async(ldpc_plan *h) {
     return LDPC_OK;
 }
 
-// kernels of a chunk graph outside the WHILE node: stage-in, check + bit node of body 1, loop_pre,
-// final syndrome, finalize, frame stats.  Each WHILE iteration adds 3 (counted by the loop kernels).
-constexpr int GRAPH_STATIC_LAUNCHES = 7;
+// kernels of a chunk graph outside the WHILE node: stage-in, body 1 (check node, bit node, compaction
+// plan + move), loop_pre, final syndrome, finalize, frame stats.  Each WHILE iteration adds
+// BODY_LAUNCHES (counted by the loop kernels on the device).
+constexpr int GRAPH_STATIC_LAUNCHES = 9;
 
 // One chunk as a CUDA graph: stage-in, body 1, then a conditional WHILE node whose body (check node,
-// bit node, loop step) repeats while a frame is still running and k <= L, then the final syndrome
-// pass and stage-out.  No host round trip and no launch for bodies after the last frame stopped.
+// bit node, compaction, loop step) repeats while a frame is still running and k <= L, then the final
+// syndrome pass and stage-out.  No host round trip and no launch for bodies after the last frame
+// stopped.
 template <typename Tail>
 int run_graph(ldpc_plan *h, const Graph &g, const StreamState &w, const float *llr, int64_t fc, int L, bool early,
-              bool literal, bool loc16, float *post, uint8_t *bits, int32_t *iters, uint8_t *conv, int64_t *stats,
+              bool literal, float *post, uint8_t *bits, int32_t *iters, uint8_t *conv, int64_t *stats,
               cudaStream_t st, Tail &&tail) {
     const void *key[8] = {llr, post, bits, iters, conv, stats, w.r, nullptr};
     for (auto &ge : h->graphs) {
@@ -223,8 +233,9 @@ int run_graph(ldpc_plan *h, const Graph &g, const StreamState &w, const float *l
     cudaError_t e = cudaStreamBeginCapture(c0, cudaStreamCaptureModeRelaxed);
     if (e != cudaSuccess) return status_of(e);
     launch_stage_in(g, w, llr, fc, c0);
-    launch_check_node(g, w, 1, true, early, literal, loc16, h->cfg, c0);
-    launch_bit_node(g, w, 1, early, literal, loc16, h->cfg, c0);
+    launch_check_node(g, w, 1, true, early, literal, h->cfg, c0);
+    launch_bit_node(g, w, 1, L, early, h->cfg, c0);
+    launch_compact(g, w, 1, h->cfg, c0);
     cudaStreamCaptureStatus cs;
     cudaGraph_t capg = nullptr;
     const cudaGraphNode_t *deps = nullptr;
@@ -246,8 +257,9 @@ int run_graph(ldpc_plan *h, const Graph &g, const StreamState &w, const float *l
         cudaGraph_t body = cp.conditional.phGraph_out[0];
         e = cudaStreamBeginCaptureToGraph(c1, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed);
         if (e == cudaSuccess) {
-            launch_check_node(g, w, 2, false, early, literal, loc16, h->cfg, c1, w.kdev);
-            launch_bit_node(g, w, 2, early, literal, loc16, h->cfg, c1, w.kdev);
+            launch_check_node(g, w, 2, false, early, literal, h->cfg, c1, w.kdev);
+            launch_bit_node(g, w, 2, L, early, h->cfg, c1, w.kdev);
+            launch_compact(g, w, 2, h->cfg, c1, w.kdev);
             launch_loop_step(w, L, handle, c1);
             cudaGraph_t out = nullptr;
             e = cudaStreamEndCapture(c1, &out);
@@ -295,56 +307,55 @@ int decode_stream(ldpc_plan *h, const float *llr, int64_t frames, int L, uint8_t
                   uint8_t *conv, int64_t *stats, cudaStream_t st) {
     const bool early = !(h->flags & LDPC_FLAG_NO_EARLY_STOP);
     const bool literal = (h->flags & LDPC_FLAG_SIGN_PAPER_LITERAL) != 0;
-    const bool loc16 = h->g.max_row_deg > 255;
     const Graph g = h->g.view();
-    int64_t cap_tiles = h->chunk_cap > 0 ? (h->chunk_cap + TILE - 1) / TILE : auto_chunk_tiles(h, loc16);
-    cap_tiles = std::min<int64_t>(cap_tiles, 65535);
-    const int64_t need_tiles = (frames + TILE - 1) / TILE;
-    const int T_max = (int)std::min<int64_t>(cap_tiles, need_tiles);
-    int rc = ensure_ws(h, T_max, loc16);
-    if (rc) return rc;
-    const int final_slot = (L + 1) & 1;
     if (!h->dev_launches) {
-        if (cudaMalloc(&h->dev_launches, sizeof(unsigned long long)) != cudaSuccess) {
+        if (cudaMalloc(&h->dev_launches, 4 * sizeof(unsigned long long)) != cudaSuccess) {
             cudaGetLastError();
             return LDPC_ERR_OOM;
         }
-        if (cudaMemsetAsync(h->dev_launches, 0, sizeof(unsigned long long), st) != cudaSuccess) return LDPC_ERR_CUDA;
+        if (cudaMemsetAsync(h->dev_launches, 0, 4 * sizeof(unsigned long long), st) != cudaSuccess)
+            return LDPC_ERR_CUDA;
     }
+    int64_t cap_tiles = h->chunk_cap > 0 ? (h->chunk_cap + TILE - 1) / TILE : auto_chunk_tiles(h);
+    cap_tiles = std::min<int64_t>(cap_tiles, 32767);
+    const int64_t need_tiles = (frames + TILE - 1) / TILE;
+    const int T_max = (int)std::min<int64_t>(cap_tiles, need_tiles);
+    int rc = ensure_ws(h, T_max);
+    if (rc) return rc;
+    const int final_slot = (L + 1) & 1;
     const bool graphs = h->use_graphs && !h->prof && L >= 2 && !(h->flags & LDPC_FLAG_NO_GRAPH);
     for (int64_t c0 = 0; c0 < frames; c0 += (int64_t)T_max * TILE) {
         const int64_t fc = std::min<int64_t>((int64_t)T_max * TILE, frames - c0);
         const int T = (int)((fc + TILE - 1) / TILE);
-        StreamState w = carve(h->ws, T, h->g, loc16);
-        w.nlaunch = h->dev_launches;
+        const StreamState w = carve(h->ws, T, tile_capacity(h, T), h, nullptr);
+        const float *sfin = L > 0 ? w.s : w.r;  // L = 0: the soft output is r itself
         const float *cl = llr + c0 * g.n;
         float *cp = post ? post + c0 * g.n : nullptr;
         uint8_t *cb = bits ? bits + c0 * g.n : nullptr;
         int32_t *ci = iters ? iters + c0 : nullptr;
         uint8_t *cc = conv ? conv + c0 : nullptr;
         auto tail = [&](cudaStream_t s2) {
-            int nl = launch_syndrome(g, w, final_slot, h->cfg, s2);
-            nl += launch_finalize(g, w, fc, cp, cb, s2);
-            nl += launch_frame_stats(g, w, fc, L, early, final_slot, ci, cc,
-                                     reinterpret_cast<unsigned long long *>(stats), s2);
+            int nl = launch_syndrome(g, w, final_slot, sfin, h->cfg, s2);
+            nl += launch_finalize(g, w, L, final_slot, sfin, cp, cb, s2);
+            nl += launch_frame_stats(w, fc, ci, cc, reinterpret_cast<unsigned long long *>(stats), s2);
             return nl;
         };
         if (graphs && h->use_graphs) {
-            rc = run_graph(h, g, w, cl, fc, L, early, literal, loc16, cp, cb, ci, cc, stats, st, tail);
+            rc = run_graph(h, g, w, cl, fc, L, early, literal, cp, cb, ci, cc, stats, st, tail);
             if (rc == LDPC_OK) continue;
             if (rc != LDPC_ERR_UNSUPPORTED) return rc;
         }
         launch(h, LDPC_K_STAGE_IN, st, [&] { return launch_stage_in(g, w, cl, fc, st); });
         for (int k = 1; k <= L; k++) {
             launch(h, LDPC_K_CHECK_NODE, st,
-                   [&] { return launch_check_node(g, w, k, k == 1, early, literal, loc16, h->cfg, st); });
-            launch(h, LDPC_K_BIT_NODE, st, [&] { return launch_bit_node(g, w, k, early, literal, loc16, h->cfg, st); });
+                   [&] { return launch_check_node(g, w, k, k == 1, early, literal, h->cfg, st); });
+            launch(h, LDPC_K_BIT_NODE, st, [&] { return launch_bit_node(g, w, k, L, early, h->cfg, st); });
+            launch(h, LDPC_K_COMPACT, st, [&] { return launch_compact(g, w, k, h->cfg, st); });
         }
-        launch(h, LDPC_K_SYNDROME, st, [&] { return launch_syndrome(g, w, final_slot, h->cfg, st); });
+        launch(h, LDPC_K_SYNDROME, st, [&] { return launch_syndrome(g, w, final_slot, sfin, h->cfg, st); });
         launch(h, LDPC_K_FINALIZE, st, [&] {
-            int nl = launch_finalize(g, w, fc, cp, cb, st);
-            nl += launch_frame_stats(g, w, fc, L, early, final_slot, ci, cc,
-                                     reinterpret_cast<unsigned long long *>(stats), st);
+            int nl = launch_finalize(g, w, L, final_slot, sfin, cp, cb, st);
+            nl += launch_frame_stats(w, fc, ci, cc, reinterpret_cast<unsigned long long *>(stats), st);
             return nl;
         });
         rc = check_async(h);
@@ -406,8 +417,11 @@ int finish_prepare(ldpc_plan *p, int rc, uint32_t flags, ldpc_handle_t *out) {
     p->launches = p->g.launches;
     cudaGetDevice(&p->device);
     p->rp = plan_resident(p->g, p->g.max_row_deg > 255, p->device);
-    if (const char *s = getenv("LDPC_ROWS_PER_CTA")) p->cfg.rows_per_cta = std::min(256, std::max(8, atoi(s)));
-    if (const char *s = getenv("LDPC_CN_UNROLL")) p->cfg.cn_unroll = std::max(0, atoi(s));
+    cudaDeviceGetAttribute(&p->cfg.sms, cudaDevAttrMultiProcessorCount, p->device);
+    if (p->cfg.sms <= 0) p->cfg.sms = 148;
+    // knobs for A/B measurements and the parity tests (every variant is bit-identical)
+    if (const char *s = getenv("LDPC_CN_GENERIC")) p->cfg.cn_generic = atoi(s) != 0;
+    if (const char *s = getenv("LDPC_NO_COMPACT")) p->cfg.compact = atoi(s) == 0;
     if (const char *s = getenv("LDPC_NO_GRAPHS")) p->use_graphs = atoi(s) == 0;
     *out = p;
     return LDPC_OK;
@@ -659,6 +673,23 @@ int ldpc_profile_reset(ldpc_handle_t h) {
         h->prof_ms[c] = 0.0;
     }
     return rc;
+}
+
+int ldpc_stream_counters(ldpc_handle_t h, int64_t *counters) {
+    if (!h || !counters) return LDPC_ERR_INVALID_ARG;
+    unsigned long long c[4] = {0, 0, 0, 0};
+    if (h->dev_launches) {
+        cudaError_t e = cudaDeviceSynchronize();
+        if (e == cudaSuccess) e = cudaMemcpy(c, h->dev_launches, sizeof(c), cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) {
+            h->poisoned = true;
+            return LDPC_ERR_CUDA;
+        }
+    }
+    counters[0] = (int64_t)c[1];
+    counters[1] = (int64_t)c[2];
+    counters[2] = (int64_t)c[3];
+    return LDPC_OK;
 }
 
 int64_t ldpc_launch_count(ldpc_handle_t h) {

@@ -205,12 +205,13 @@ def test_graph_loop_equals_plain_launches(cfg_name, frames):
             assert np.array_equal(a, b)
 
 
-@pytest.mark.parametrize("cu", [0, 1, 2])
-def test_stream_unroll_variants(monkeypatch, cu):
-    """Every check-node variant of the streaming schedule is bit-identical: LDPC_CN_UNROLL = 0 (one
-    register row buffer, rows of degree <= 8; the default) / 1 (generic, any degree) / 2 (two row
-    buffers)."""
-    monkeypatch.setenv("LDPC_CN_UNROLL", str(cu))
+@pytest.mark.parametrize("knob", ["default", "LDPC_CN_GENERIC", "LDPC_NO_COMPACT"])
+def test_stream_variants(monkeypatch, knob):
+    """Every kernel variant of the streaming schedule is bit-identical: the degree-specialised check node
+    (rows of degree <= 8, default) or the any-degree one (LDPC_CN_GENERIC=1); with or without the
+    compaction of sparse tiles (LDPC_NO_COMPACT=1)."""
+    if knob != "default":
+        monkeypatch.setenv(knob, "1")
     cfg = codes.CONFIGS["c2"]
     code = cfg["code"]()
     parts = [channel.bpsk_awgn(code.n, code.rate, e, cfg["seed"], p, 100, 300).numpy() for p, e in enumerate(cfg["ebn0"])]
@@ -220,6 +221,36 @@ def test_stream_unroll_variants(monkeypatch, cu):
     code3 = codes.random_small(37, 70, 2, 2, 9)  # irregular, rows of degree 2..
     llr3 = (np.random.default_rng(3).standard_normal((300, code3.n)) - 0.5).astype(np.float32)
     compare(code3, llr3, 12, h=handle(code3, FORCE_STREAM))
+
+
+@pytest.mark.parametrize("graph", [True, False])
+@pytest.mark.parametrize("T", [1, 3])
+def test_compaction_moves_frames_exactly(graph, T):
+    """Tiles whose running frames drop under half are compacted into fresh tiles: a batch that
+    interleaves easy (5 dB) and hard (1 dB) frames makes most tiles sparse after a few bodies.  Results equal
+    the oracle and the uncompacted decode bit for bit, and the handle reports frames actually moved."""
+    code = codes.regular(504, 1008, 3, 6, 1008)
+    F = 128 * 40 + 77  # ragged last tile
+    easy = channel.bpsk_awgn(code.n, code.rate, 5.0, 3, 0, 0, F).numpy()
+    hard = channel.bpsk_awgn(code.n, code.rate, 1.0, 3, 1, 0, F).numpy()
+    pick = (np.arange(F) % 5) == 0  # 20 % hard frames in every tile
+    llr = np.where(pick[:, None], hard, easy).astype(np.float32)
+    flags = FORCE_STREAM | (0 if graph else 16)
+    h = handle(code, flags)
+    got = compare(code, llr, 40, flags, h=h, check_every=T)
+    c = h.stream_counters()
+    assert c["compactions"] >= 1 and c["frames_moved"] > 0 and c["tiles_retired"] > c["compactions"]
+    import os
+
+    os.environ["LDPC_NO_COMPACT"] = "1"
+    try:
+        h2 = handle(code, flags)
+    finally:
+        del os.environ["LDPC_NO_COMPACT"]
+    ref = compare(code, llr, 40, flags, h=h2, check_every=T)
+    assert h2.stream_counters()["compactions"] == 0
+    for a_, b_ in zip(got, ref):
+        assert np.array_equal(a_, b_)
 
 
 @pytest.mark.parametrize("which", ["paper", "reg", "small"])
