@@ -42,7 +42,7 @@ namespace ldpc {
 
 namespace {
 
-constexpr unsigned FULL = 0xffffffffu;
+constexpr unsigned FULL_MASK = 0xffffffffu;
 
 __device__ __forceinline__ float comp(const float4 &a, int v) { return v == 0 ? a.x : v == 1 ? a.y : v == 2 ? a.z : a.w; }
 __device__ __forceinline__ unsigned comp(const uint4 &a, int v) { return v == 0 ? a.x : v == 1 ? a.y : v == 2 ? a.z : a.w; }
@@ -55,12 +55,22 @@ __device__ __forceinline__ float flip31(float mag, uint32_t bit31) {
     return __uint_as_float(__float_as_uint(mag) ^ (bit31 & 0x80000000u));
 }
 
+// CTA barrier reached by every thread, with the warp reconverged first (barrier.sync is .aligned: the
+// whole warp must execute it together; the per-lane branches before it need not reconverge on their own)
+__device__ __forceinline__ void cta_sync() {
+    __syncwarp();
+    __syncthreads();
+}
+
+// zeros of s and r are kept as -0 in the streaming schedule (reading A12: same slice and sign())
+__device__ __forceinline__ float zneg(float x) { return x == 0.f ? -0.0f : x; }
+
 // Take the next (tile, block) item of a persistent sweep from a work counter.  Two barriers: every
 // thread has finished the previous item (and read its index) before thread 0 overwrites s_item.
 __device__ __forceinline__ int next_item(int *ctr, int &s_item) {
-    __syncthreads();
+    cta_sync();
     if (threadIdx.x == 0) s_item = atomicAdd(ctr, 1);
-    __syncthreads();
+    cta_sync();
     return s_item;
 }
 
@@ -81,8 +91,8 @@ constexpr int BN_COLS = 16;   // columns per bit-node item (4 per warp)
 constexpr int CN_NW = CN_T / 32;
 
 // ------------------------------------------------------------------------------------------------
-// a2: stage-in.  llr [F][n] -> r [t][n][128] (canonical zeros: -0 -> +0, same slice and sign() under
-// reading A12, so that no s and no lambda is ever -0 and IEEE sign bits can be read directly), the
+// a2: stage-in.  llr [F][n] -> r [t][n][128] (zeros kept as -0: same slice and sign() under reading
+// A12; with every zero of r and s being -0, slice(s) = 0 iff the IEEE sign bit of s is set), the
 // per-slot frame index, per-tile flags, and the raw channel errors of every frame (r_j > 0) counted
 // where r is read anyway.  Body 1 reads r itself (s = r).
 // ------------------------------------------------------------------------------------------------
@@ -104,18 +114,21 @@ __global__ void __launch_bounds__(CTA) k_stage_in(const float *__restrict__ llr,
             const bool ok = f < frames && j < n;
             const float v = ok ? __ldg(llr + f * n + j) : -1.0f;
             tile[lane][fl] = v;
-            const int c = __popc(__ballot_sync(FULL, ok && v > 0.f));
+            const int c = __popc(__ballot_sync(FULL_MASK, ok && v > 0.f));
             if (lane == (fl >> 3)) raw += c;
         }
-        __syncthreads();
+        cta_sync();
         for (int jl = warp; jl < 32; jl += CTA / 32) {
             const int jj = j0 + jl;
             if (jj >= n) break;
             const size_t base = ((size_t)t * n + jj) * TILE;
 #pragma unroll
-            for (int q = 0; q < 4; q++) w.r[base + lane + 32 * q] = __fadd_rn(tile[jl][lane + 32 * q], 0.0f);
+            for (int q = 0; q < 4; q++) {
+                const float v = tile[jl][lane + 32 * q];
+                w.r[base + lane + 32 * q] = v == 0.f ? -0.0f : v;  // zeros kept as -0 (reading A12)
+            }
         }
-        __syncthreads();
+        cta_sync();
     }
     if (lane < 16 && raw) {
         const int64_t f = f0 + warp + 8 * lane;
@@ -180,41 +193,51 @@ __device__ __forceinline__ void cn_fetch(CnRow<CH> &R, int cj, const float *__re
     }
 #pragma unroll
     for (int u = 0; u < CH; u++) {
-        const int j = __shfl_sync(FULL, cj, u);
+        const int j = __shfl_sync(FULL_MASK, cj, u);
         R.sv[u] = ld4(Sl + (size_t)j * TILE);
     }
 }
 
-template <int CH, bool FIRST, bool EARLY>
+// FULL: the row has exactly CH edges (no per-edge guard).  Per frame-edge on the ALU pipe: the isloc
+// test and magnitude select (2), the sign flip (1), the decision parity (1, zeros of s are -0: slice(s)
+// = 0 iff the IEEE sign bit is set), first-strict-minimum tracking (FSETP, 3 FMNMX, SEL; reading A13)
+// and the new sign bit (one funnel shift).  lambda = (s - eta) + 0 runs on the otherwise idle FMA pipe
+// and makes every zero lambda +0, so its sign (sign(0) = +1) is its IEEE sign bit.
+template <int CH, bool FIRST, bool EARLY, bool FULL>
 __device__ __forceinline__ void cn_compute(const CnRow<CH> &R, unsigned char *__restrict__ Ri, int d, int literal,
                                            int lane, uint32_t (&u)[4]) {
     const float INF = __int_as_float(0x7f800000);
     const float om0[4] = {R.m0.x, R.m0.y, R.m0.z, R.m0.w}, om1[4] = {R.m1.x, R.m1.y, R.m1.z, R.m1.w};
     float nm0[4] = {INF, INF, INF, INF}, nm1[4] = {INF, INF, INF, INF};
     int nloc[4] = {0, 0, 0, 0};
-    uint32_t syn[4] = {0u, 0u, 0u, 0u}, sw = 0;  // sw: sign nibble of edge p at bits 4p..4p+3
+    uint32_t syn[4] = {0u, 0u, 0u, 0u}, sw = 0;  // sw: sign bits pushed in (p, v) order
 #pragma unroll
     for (int p = 0; p < CH; p++) {
-        if (p < d) {
+        if (FULL || p < d) {
             const uint32_t b = FIRST ? 0u : R.eb[p];
 #pragma unroll
             for (int v = 0; v < 4; v++) {
                 const float sj = comp(R.sv[p], v);
-                float x = sj;
-                if (!FIRST) {
+                float x;
+                if (FIRST) {
+                    x = __fadd_rn(sj, 0.0f);  // eta^prev = 0
+                } else {
                     const float mag = (b & (16u << v)) ? om1[v] : om0[v];  // Obs. 1 (+ row parity)
-                    x = sj - flip31(mag, b << (31 - v));                      // lambda_k - eta^prev_{i,k}
+                    x = __fadd_rn(__fsub_rn(sj, flip31(mag, b << (31 - v))), 0.0f);  // lambda - eta^prev
                 }
                 const float ax = fabsf(x);
                 const bool lt = ax < nm0[v];  // first strict minimum (A13)
                 nm1[v] = fminf(nm1[v], fmaxf(nm0[v], ax));
                 nm0[v] = fminf(nm0[v], ax);
                 nloc[v] = lt ? p : nloc[v];
-                if (EARLY) syn[v] ^= __float_as_uint(sj) - 1u;     // bit 31: slice(s_j) == 0
-                sw |= (__float_as_uint(x) >> 31) << (4 * p + v);  // sign(0) = +1: x is never -0
+                if (EARLY) syn[v] ^= __float_as_uint(sj);  // bit 31: slice(s_j) == 0
+                sw = __funnelshift_l(__float_as_uint(x), sw, 1);
             }
         }
     }
+    // bit 4p+v of sw = sign of lambda (edge p, slot 4l+v)
+    if (FULL) sw = CH == 8 ? __brev(sw) : __brev(sw) >> (32 - 4 * CH);
+    else sw = __brev(sw) >> (32 - 4 * d);
     // sign parity per slot (Obs. 2): XOR of bits v, v+4, ..., of sw, times (-1)^{d_i} (reading A1)
     uint32_t pw = sw ^ (sw >> 16);
     pw ^= pw >> 8;
@@ -228,18 +251,18 @@ __device__ __forceinline__ void cn_compute(const CnRow<CH> &R, unsigned char *__
     st4(reinterpret_cast<float *>(Ri) + 128 + 4 * lane,
         make_float4(__uint_as_float(__float_as_uint(nm1[0]) | s0), __uint_as_float(__float_as_uint(nm1[1]) | s1),
                     __uint_as_float(__float_as_uint(nm1[2]) | s2), __uint_as_float(__float_as_uint(nm1[3]) | s3)));
+    // edge bytes: sign nibble | isloc nibble << 4.  lm has bit 4p+v set iff min0Location of slot v is p;
+    // interleaving the nibbles of sw and lm gives the bytes of the even edges in ze, of the odd ones in zo
+    const uint32_t lm = (1u << (4 * nloc[0])) | (2u << (4 * nloc[1])) | (4u << (4 * nloc[2])) | (8u << (4 * nloc[3]));
+    const uint32_t ze = (sw & 0x0f0f0f0fu) | ((lm & 0x0f0f0f0fu) << 4);
+    const uint32_t zo = ((sw >> 4) & 0x0f0f0f0fu) | (lm & 0xf0f0f0f0u);
 #pragma unroll
-    for (int p = 0; p < CH; p++) {
-        if (p < d) {
-            const uint32_t il = (uint32_t)(nloc[0] == p) | ((uint32_t)(nloc[1] == p) << 1) |
-                                ((uint32_t)(nloc[2] == p) << 2) | ((uint32_t)(nloc[3] == p) << 3);
-            Ri[REC_EDGE0 + 32 * p + lane] = (unsigned char)(((sw >> (4 * p)) & 0xfu) | (il << 4));
-        }
-    }
+    for (int p = 0; p < CH; p++)
+        if (FULL || p < d) Ri[REC_EDGE0 + 32 * p + lane] = (unsigned char)(((p & 1) ? zo : ze) >> (8 * (p >> 1)));
     if (EARLY) {
         const uint32_t dp = (uint32_t)(d & 1);  // XOR_j b_j = d_i mod 2 xor XOR_j (1 - b_j)
 #pragma unroll
-        for (int v = 0; v < 4; v++) u[v] |= __ballot_sync(FULL, ((syn[v] >> 31) ^ dp) != 0u);
+        for (int v = 0; v < 4; v++) u[v] |= __ballot_sync(FULL_MASK, ((syn[v] >> 31) ^ dp) != 0u);
     }
 }
 
@@ -277,7 +300,7 @@ __global__ void __launch_bounds__(CN_T, CN_MINB) k_cn(Graph g, StreamState w, in
                 rb = __ldg(g.row_ptr + i0 + CN_NW * lane + 1);
             }
             auto cols_of = [&](int q) {  // lane p: column of edge p of row q (0 past the degree / the rows)
-                const int a = __shfl_sync(FULL, ra, q & 31), d = __shfl_sync(FULL, rb, q & 31) - a;
+                const int a = __shfl_sync(FULL_MASK, ra, q & 31), d = __shfl_sync(FULL_MASK, rb, q & 31) - a;
                 return (q < nr && lane < d) ? __ldg(g.col_idx + a + lane) : 0;
             };
             CnRow<CH> A;
@@ -286,9 +309,10 @@ __global__ void __launch_bounds__(CN_T, CN_MINB) k_cn(Graph g, StreamState w, in
                 const int i = i0 + CN_NW * q;
                 unsigned char *Ri = RB + (size_t)i * w.rs;
                 cn_fetch<CH, FIRST>(A, cj, Sl, Ri, lane);
-                const int d = __shfl_sync(FULL, rb, q) - __shfl_sync(FULL, ra, q);
+                const int d = __shfl_sync(FULL_MASK, rb, q) - __shfl_sync(FULL_MASK, ra, q);
                 cj = cols_of(q + 1);
-                cn_compute<CH, FIRST, EARLY>(A, Ri, d, literal, lane, u);
+                if (d == CH) cn_compute<CH, FIRST, EARLY, true>(A, Ri, d, literal, lane, u);
+                else cn_compute<CH, FIRST, EARLY, false>(A, Ri, d, literal, lane, u);
             }
         }
         if (EARLY) {
@@ -297,7 +321,7 @@ __global__ void __launch_bounds__(CN_T, CN_MINB) k_cn(Graph g, StreamState w, in
                 for (int v = 0; v < 4; v++)
                     if (u[v]) atomicOr(&s_u[v], u[v]);
             }
-            __syncthreads();
+            cta_sync();
             if (threadIdx.x < 4 && s_u[threadIdx.x])
                 atomicOr(w.unsat + ((size_t)(k & 1) * w.Tcap + t) * 4 + threadIdx.x, s_u[threadIdx.x]);
         }
@@ -353,7 +377,7 @@ __global__ void __launch_bounds__(CN_T, 2) k_cn_generic(Graph g, StreamState w, 
                 uint32_t eb[C8];
 #pragma unroll
                 for (int u8 = 0; u8 < C8; u8++) {
-                    const int j = __shfl_sync(FULL, cj, (p0 + u8) & 31);
+                    const int j = __shfl_sync(FULL_MASK, cj, (p0 + u8) & 31);
                     sv[u8] = ld4(Sl + (size_t)j * TILE);  // unconditional: edges past d_i read column 0
                     eb[u8] = FIRST ? 0u : Ri[REC_EDGE0 + 32 * (p0 + u8) + lane];
                 }
@@ -365,10 +389,12 @@ __global__ void __launch_bounds__(CN_T, 2) k_cn_generic(Graph g, StreamState w, 
 #pragma unroll
                         for (int v = 0; v < 4; v++) {
                             const float sj = comp(sv[u8], v);
-                            float x = sj;
-                            if (!FIRST) {
+                            float x;
+                            if (FIRST) {
+                                x = __fadd_rn(sj, 0.0f);
+                            } else {
                                 const float mag = (eb[u8] & (16u << v)) ? om1[v] : om0[v];
-                                x = sj - flip31(mag, eb[u8] << (31 - v));
+                                x = __fadd_rn(__fsub_rn(sj, flip31(mag, eb[u8] << (31 - v))), 0.0f);
                             }
                             const float ax = fabsf(x);
                             const bool lt = ax < nm0[v];
@@ -376,7 +402,7 @@ __global__ void __launch_bounds__(CN_T, 2) k_cn_generic(Graph g, StreamState w, 
                             nm0[v] = fminf(nm0[v], ax);
                             nloc[v] = lt ? p : nloc[v];
                             par[v] ^= __float_as_uint(x);
-                            if (EARLY) syn[v] ^= __float_as_uint(sj) - 1u;
+                            if (EARLY) syn[v] ^= __float_as_uint(sj);
                             nib |= (__float_as_uint(x) >> 31) << v;
                         }
                         Ri[REC_EDGE0 + 32 * p + lane] = (unsigned char)nib;  // sign nibble, isloc = 0
@@ -403,7 +429,7 @@ __global__ void __launch_bounds__(CN_T, 2) k_cn_generic(Graph g, StreamState w, 
             if (EARLY) {
                 const uint32_t dp = (uint32_t)(d & 1);
 #pragma unroll
-                for (int v = 0; v < 4; v++) u[v] |= __ballot_sync(FULL, ((syn[v] >> 31) ^ dp) != 0u);
+                for (int v = 0; v < 4; v++) u[v] |= __ballot_sync(FULL_MASK, ((syn[v] >> 31) ^ dp) != 0u);
             }
         }
         if (EARLY) {
@@ -412,7 +438,7 @@ __global__ void __launch_bounds__(CN_T, 2) k_cn_generic(Graph g, StreamState w, 
                 for (int v = 0; v < 4; v++)
                     if (u[v]) atomicOr(&s_u[v], u[v]);
             }
-            __syncthreads();
+            cta_sync();
             if (threadIdx.x < 4 && s_u[threadIdx.x])
                 atomicOr(w.unsat + ((size_t)(k & 1) * w.Tcap + t) * 4 + threadIdx.x, s_u[threadIdx.x]);
         }
@@ -428,6 +454,8 @@ __global__ void __launch_bounds__(CN_T, 2) k_cn_generic(Graph g, StreamState w, 
 // and the tile goes to the list of body k+1 -- or, when fewer than half of its slots still run and
 // at least two bodies remain, to the compaction sources.
 // ------------------------------------------------------------------------------------------------
+constexpr int BN_REC = 256;  // edge records of an item staged in shared memory (16 columns x up to 16)
+
 template <bool EARLY>
 __global__ void __launch_bounds__(BN_T, BN_MINB)
     k_bn(Graph g, StreamState w, int k, int L, const int *kdev, int check_every, int compact) {
@@ -435,6 +463,8 @@ __global__ void __launch_bounds__(BN_T, BN_MINB)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int Tc = w.Tcap;
     __shared__ int s_item;
+    __shared__ int2 s_rec[BN_REC];  // {row i, position p in N_i} of the item's edges, column-major
+    __shared__ int s_cp[BN_COLS + 1];
     const int cnt = w.tcount[k & 1];
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         w.work[WK_CN] = 0;  // next check-node sweep
@@ -450,17 +480,17 @@ __global__ void __launch_bounds__(BN_T, BN_MINB)
         if (it >= items) break;
         const int y = it / ncb, x = it - y * ncb;
         const int t = w.tlist[(size_t)(k & 1) * Tc + y];
-        uint4 act = make_uint4(FULL, FULL, FULL, FULL);
+        uint4 act = make_uint4(FULL_MASK, FULL_MASK, FULL_MASK, FULL_MASK);
         if (EARLY) {
             // the syndrome of k_cn(k) tests b^(k-1); it may stop frames only at a check point (k-1) % T == 0
             const bool check = ((k - 1) % check_every) == 0;
-            const uint4 ua = check ? ldu4(w.unsat + ((size_t)(k & 1) * Tc + t) * 4) : make_uint4(FULL, FULL, FULL, FULL);
+            const uint4 ua = check ? ldu4(w.unsat + ((size_t)(k & 1) * Tc + t) * 4) : make_uint4(FULL_MASK, FULL_MASK, FULL_MASK, FULL_MASK);
             const uint4 dw = ldu4(w.done + (size_t)t * 4);
             const uint4 newly = make_uint4(~ua.x & ~dw.x, ~ua.y & ~dw.y, ~ua.z & ~dw.z, ~ua.w & ~dw.w);
             act = make_uint4(ua.x & ~dw.x, ua.y & ~dw.y, ua.z & ~dw.z, ua.w & ~dw.w);
             // every thread has read `done` before the tile's bookkeeping item rewrites it (other items of
             // the tile may see either value: act is the same for both, since newly and ua are disjoint)
-            __syncthreads();
+            cta_sync();
             if (x == 0) {
                 const int tid = threadIdx.x;
                 if (tid < 4) {
@@ -494,17 +524,41 @@ __global__ void __launch_bounds__(BN_T, BN_MINB)
         const unsigned char *RB = w.rst + (size_t)t * m * w.rs;
         const float *__restrict__ Rl = w.r + (size_t)t * n * TILE + 4 * lane;
         float *__restrict__ Sl = w.s + (size_t)t * n * TILE + 4 * lane;
-        const int j1 = min(n, x * BN_COLS + BN_COLS);
-        for (int j = x * BN_COLS + warp; j < j1; j += BN_T / 32) {
-            const int c0 = __ldg(g.col_ptr + j), dv = __ldg(g.col_ptr + j + 1) - c0;
+        const int jb = x * BN_COLS, j1 = min(n, jb + BN_COLS);
+        // the item's edge records into shared memory: the edge loop below then waits on data loads only
+        const int cb = __ldg(g.col_ptr + jb), ne = __ldg(g.col_ptr + j1) - cb;
+        const bool staged = ne <= BN_REC;  // uniform
+        if (staged) {
+            for (int q = threadIdx.x; q < ne; q += BN_T) {
+                const int4 ed = __ldg(g.bn_edge + cb + q);
+                s_rec[q] = make_int2(ed.y, ed.z);
+            }
+            if (threadIdx.x <= j1 - jb) s_cp[threadIdx.x] = __ldg(g.col_ptr + jb + threadIdx.x) - cb;
+        }
+        cta_sync();
+        for (int j = jb + warp; j < j1; j += BN_T / 32) {
+            int c0, dv;
+            if (staged) {
+                c0 = s_cp[j - jb];
+                dv = s_cp[j - jb + 1] - c0;
+            } else {
+                c0 = __ldg(g.col_ptr + j) - cb;
+                dv = __ldg(g.col_ptr + j + 1) - cb - c0;
+            }
             const float4 rv = ld4(Rl + (size_t)j * TILE);
             float acc[4] = {0.f, 0.f, 0.f, 0.f};
             for (int q = 0; q < dv; q++) {
-                const int4 ed = __ldg(g.bn_edge + c0 + q);  // {e, i, p, -}, ascending i
-                const unsigned char *Ri = RB + (size_t)ed.y * w.rs;
+                int2 ed;  // {row i, position p}, ascending i
+                if (staged) {
+                    ed = s_rec[c0 + q];
+                } else {
+                    const int4 e4 = __ldg(g.bn_edge + cb + c0 + q);
+                    ed = make_int2(e4.y, e4.z);
+                }
+                const unsigned char *Ri = RB + (size_t)ed.x * w.rs;
                 const float4 m0 = ld4(reinterpret_cast<const float *>(Ri) + 4 * lane);
                 const float4 m1 = ld4(reinterpret_cast<const float *>(Ri) + 128 + 4 * lane);
-                const uint32_t b = Ri[REC_EDGE0 + 32 * ed.z + lane];
+                const uint32_t b = Ri[REC_EDGE0 + 32 * ed.y + lane];
 #pragma unroll
                 for (int v = 0; v < 4; v++) {
                     const float mag = (b & (16u << v)) ? comp(m1, v) : comp(m0, v);  // Obs. 1
@@ -512,16 +566,18 @@ __global__ void __launch_bounds__(BN_T, BN_MINB)
                 }
             }
             float *o = Sl + (size_t)j * TILE;
+            const float n0 = zneg(acc[0] + rv.x), n1 = zneg(acc[1] + rv.y), n2 = zneg(acc[2] + rv.z),
+                        n3 = zneg(acc[3] + rv.w);  // zeros of s kept as -0 (A12)
             if (mine == 0xFu) {
-                st4(o, make_float4(acc[0] + rv.x, acc[1] + rv.y, acc[2] + rv.z, acc[3] + rv.w));
+                st4(o, make_float4(n0, n1, n2, n3));
             } else if (k == 1) {  // body 1: frames that stopped at the pre-check keep s = r
-                st4(o, make_float4((mine & 1u) ? acc[0] + rv.x : rv.x, (mine & 2u) ? acc[1] + rv.y : rv.y,
-                                   (mine & 4u) ? acc[2] + rv.z : rv.z, (mine & 8u) ? acc[3] + rv.w : rv.w));
+                st4(o, make_float4((mine & 1u) ? n0 : rv.x, (mine & 2u) ? n1 : rv.y, (mine & 4u) ? n2 : rv.z,
+                                   (mine & 8u) ? n3 : rv.w));
             } else if (mine) {  // frozen frames keep their s
-                if (mine & 1u) o[0] = acc[0] + rv.x;
-                if (mine & 2u) o[1] = acc[1] + rv.y;
-                if (mine & 4u) o[2] = acc[2] + rv.z;
-                if (mine & 8u) o[3] = acc[3] + rv.w;
+                if (mine & 1u) o[0] = n0;
+                if (mine & 2u) o[1] = n1;
+                if (mine & 4u) o[2] = n2;
+                if (mine & 8u) o[3] = n3;
             }
         }
     }
@@ -549,7 +605,7 @@ __global__ void __launch_bounds__(1024) k_compact_plan(StreamState w, int k, con
     int sum = 0;
     for (int q = a; q < b; q++) sum += w.ccnt[q];
     s_part[tid] = sum;
-    __syncthreads();
+    cta_sync();
     if (tid == 0) {
         int run = 0;
         for (int q = 0; q < NT; q++) {
@@ -559,7 +615,7 @@ __global__ void __launch_bounds__(1024) k_compact_plan(StreamState w, int k, con
         }
         s_tot = run;
     }
-    __syncthreads();
+    cta_sync();
     const int R = s_tot, ndst = (R + TILE - 1) / TILE, base = w.ctl[CT_TNEXT];
     const int nxt = (k + 1) & 1;
     if (ndst >= nsrc || base + ndst > Tc) {  // nothing to gain (or no room): the sources keep running
@@ -582,10 +638,10 @@ __global__ void __launch_bounds__(1024) k_compact_plan(StreamState w, int k, con
             w.fid[(size_t)(base + dt) * TILE + ds] = w.fid[(size_t)t * TILE + sl];
             w.fid[(size_t)t * TILE + sl] = -1;  // moved: its outputs come from the fresh tile
         }
-        w.done[(size_t)t * 4 + 0] = FULL;
-        w.done[(size_t)t * 4 + 1] = FULL;
-        w.done[(size_t)t * 4 + 2] = FULL;
-        w.done[(size_t)t * 4 + 3] = FULL;
+        w.done[(size_t)t * 4 + 0] = FULL_MASK;
+        w.done[(size_t)t * 4 + 1] = FULL_MASK;
+        w.done[(size_t)t * 4 + 2] = FULL_MASK;
+        w.done[(size_t)t * 4 + 3] = FULL_MASK;
     }
     // fresh tiles: padding slots past R in the last one
     for (int q = tid; q < ndst * TILE; q += NT) {
@@ -639,7 +695,7 @@ __global__ void __launch_bounds__(MV_T) k_compact_move(Graph g, StreamState w) {
         if (it >= items) break;
         const int y = it / per, x = it - y * per;
         if (threadIdx.x < TILE) s_map[threadIdx.x] = w.cmap[(size_t)y * TILE + threadIdx.x];
-        __syncthreads();
+        cta_sync();
         const int T2 = base + y;
         int src[4];
 #pragma unroll
@@ -728,13 +784,13 @@ __global__ void __launch_bounds__(CTA) k_syndrome(Graph g, StreamState w, int sl
                        ((unsigned)(sv.w > 0.f) << 3);
             }
 #pragma unroll
-            for (int v = 0; v < 4; v++) u[v] |= __ballot_sync(FULL, (syn >> v) & 1u);
+            for (int v = 0; v < 4; v++) u[v] |= __ballot_sync(FULL_MASK, (syn >> v) & 1u);
         }
         if (lane == 0)
 #pragma unroll
             for (int v = 0; v < 4; v++)
                 if (u[v]) atomicOr(&s_u[v], u[v]);
-        __syncthreads();
+        cta_sync();
         if (threadIdx.x < 4 && s_u[threadIdx.x])
             atomicOr(w.unsat + ((size_t)slot * w.Tcap + t) * 4 + threadIdx.x, s_u[threadIdx.x]);
     }
@@ -765,7 +821,7 @@ __global__ void __launch_bounds__(CTA) k_finalize(StreamState w, int n, int L, i
             }
         }
     }
-    __syncthreads();
+    cta_sync();
     int be_acc = 0;  // lane q < 16 of warp w: slot w + 8q
     bool nz_acc = false;
     for (int sb = 0; sb < SI_SUB; sb++) {
@@ -778,7 +834,7 @@ __global__ void __launch_bounds__(CTA) k_finalize(StreamState w, int n, int L, i
 #pragma unroll
             for (int q = 0; q < 4; q++) ts[jl][lane + 32 * q] = sfin[base + lane + 32 * q];
         }
-        __syncthreads();
+        cta_sync();
         const int j = j0 + lane;
         const bool jv = j < n;
 #pragma unroll 4
@@ -792,14 +848,14 @@ __global__ void __launch_bounds__(CTA) k_finalize(StreamState w, int n, int L, i
                 if (post) post[(int64_t)f * n + j] = sv;
                 if (bits) bits[(int64_t)f * n + j] = (uint8_t)b;
             }
-            const int be = __popc(__ballot_sync(FULL, b));
-            const bool nz = __any_sync(FULL, jv && fabsf(sv) <= 1e-4f);
+            const int be = __popc(__ballot_sync(FULL_MASK, b));
+            const bool nz = __any_sync(FULL_MASK, jv && fabsf(sv) <= 1e-4f);
             if (lane == q) {
                 be_acc += be;
                 nz_acc = nz_acc || nz;
             }
         }
-        __syncthreads();  // the next sub-block overwrites ts
+        cta_sync();  // the next sub-block overwrites ts
     }
     if (lane < TILE / (CTA / 32)) {
         const int f = s_fid[warp + (CTA / 32) * lane];
@@ -816,7 +872,7 @@ __global__ void __launch_bounds__(CTA) k_frame_stats(StreamState w, int64_t fram
                                                      unsigned long long *__restrict__ stats) {
     __shared__ unsigned long long s_acc[8];
     if (threadIdx.x < 8) s_acc[threadIdx.x] = 0;
-    __syncthreads();
+    cta_sync();
     const int64_t f = blockIdx.x * (int64_t)CTA + threadIdx.x;
     unsigned long long c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (f < frames) {
@@ -837,10 +893,10 @@ __global__ void __launch_bounds__(CTA) k_frame_stats(StreamState w, int64_t fram
 #pragma unroll
         for (int q = 0; q < 8; q++) {
             unsigned long long x = c[q];
-            for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
+            for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(FULL_MASK, x, o);
             if ((threadIdx.x & 31) == 0 && x) atomicAdd(&s_acc[q], x);
         }
-        __syncthreads();
+        cta_sync();
         if (threadIdx.x < 8 && s_acc[threadIdx.x]) atomicAdd(stats + threadIdx.x, s_acc[threadIdx.x]);
     }
 }

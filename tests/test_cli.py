@@ -41,8 +41,24 @@ def test_decode_and_sweep(tmp_path):
     r = run("decode", "--matrix", str(h), "--llr", str(llr))
     assert r.returncode == 0 and r.stdout.strip() == "isCodeword=1 k=1 b=0000000000"  # worked example P4
     out = tmp_path / "s.csv"
-    r = run("sweep", "--matrix", str(h), "--snr", "1,3", "--frames", "2000", "--out", str(out))
+    r = run("sweep", "--matrix", str(h), "--snr", "1,3", "--frames", "2000", "--out", str(out), "--timings")
     assert r.returncode == 0, r.stderr
+    assert any(ln.startswith("resident ") for ln in r.stderr.splitlines()), r.stderr  # stage-timing table
     lines = out.read_text().splitlines()
     assert lines[0] == "snr_db,frames,raw_ber,decoded_ber,fer,avg_iterations,wall_seconds,throughput_bps"
     assert len(lines) == 3 and all(len(x.split(",")) == 8 for x in lines)
+
+
+def test_scaling_usage():
+    assert run("scaling", "--gpus", "0").returncode == 1
+
+
+@pytest.mark.gpu
+def test_scaling_one_gpu(tmp_path):
+    """scalingStudy on the GPUs this box has (1 here): one row per visible count, outcomes consistent."""
+    out = tmp_path / "sc.csv"
+    r = run("scaling", "--config", "c1", "--gpus", "1", "--steps", "1", "--warmup", "3", "--out", str(out))
+    assert r.returncode == 0, r.stderr
+    lines = out.read_text().splitlines()
+    assert lines[0] == "gpus,wall_seconds,throughput_bps,frames,sum_iterations,frame_errors,bit_errors"
+    assert len(lines) == 2 and lines[1].startswith("1,") and int(lines[1].split(",")[3]) == 10000

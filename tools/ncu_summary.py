@@ -38,7 +38,13 @@ for vals in raw[2:]:
             except ValueError:
                 pass
         if name in ("dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_sector_hit_rate.pct",
-                    "gpu__time_duration.sum"):
+                    "gpu__time_duration.sum", "lts__t_bytes.sum", "lts__t_sectors_srcunit_tex.sum",
+                    "lts__throughput.avg.pct_of_peak_sustained_elapsed", "sm__inst_executed.sum",
+                    "smsp__inst_executed.avg.per_cycle_active", "sm__cycles_elapsed.avg.per_second",
+                    "l1tex__t_bytes.sum", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+                    "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+                    "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+                    "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"):
             print(f"  {name:40s} {vals[h.index(name)]} {u[h.index(name)]}")
     tot = sum(x for x, _ in stalls) or 1
     print("  stalls:", ", ".join(f"{n} {x / tot * 100:.0f}%" for x, n in sorted(stalls, reverse=True)[:8]))
