@@ -81,10 +81,10 @@ __device__ __forceinline__ int next_item(int *ctr, int &s_item) {
 #define CN_MINB 3
 #endif
 #ifndef BN_T
-#define BN_T 128  // 128 threads x 12 CTAs per SM (48 warps): the bit node lives on loads in flight
+#define BN_T 128  // the bit node lives on loads in flight
 #endif
 #ifndef BN_MINB
-#define BN_MINB 12
+#define BN_MINB 8  // 8 x 128 threads with up to 64 registers: 32 warps, each with BN_G edges of loads in flight
 #endif
 constexpr int CN_ROWS = 128;  // rows per check-node item (16 per warp)
 constexpr int BN_COLS = 16;   // columns per bit-node item (4 per warp)
@@ -454,17 +454,18 @@ __global__ void __launch_bounds__(CN_T, 2) k_cn_generic(Graph g, StreamState w, 
 // and the tile goes to the list of body k+1 -- or, when fewer than half of its slots still run and
 // at least two bodies remain, to the compaction sources.
 // ------------------------------------------------------------------------------------------------
-constexpr int BN_REC = 256;  // edge records of an item staged in shared memory (16 columns x up to 16)
+#ifndef BN_G
+#define BN_G 4  // edges of a column whose loads are issued together
+#endif
 
+// Items are taken in a static stride (no work counter, no per-item barrier): the bit node is bound by
+// loads in flight, and its items cost the same.
 template <bool EARLY>
 __global__ void __launch_bounds__(BN_T, BN_MINB)
     k_bn(Graph g, StreamState w, int k, int L, const int *kdev, int check_every, int compact) {
     if (kdev) k = *kdev;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int Tc = w.Tcap;
-    __shared__ int s_item;
-    __shared__ int2 s_rec[BN_REC];  // {row i, position p in N_i} of the item's edges, column-major
-    __shared__ int s_cp[BN_COLS + 1];
     const int cnt = w.tcount[k & 1];
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         w.work[WK_CN] = 0;  // next check-node sweep
@@ -475,23 +476,22 @@ __global__ void __launch_bounds__(BN_T, BN_MINB)
     const int ncb = (n + BN_COLS - 1) / BN_COLS;
     const int items = cnt * ncb;
     const bool compact_ok = EARLY && compact && k + 2 <= L;
-    for (;;) {
-        const int it = next_item(w.work + WK_BN, s_item);
-        if (it >= items) break;
+    for (int it = blockIdx.x; it < items; it += gridDim.x) {
         const int y = it / ncb, x = it - y * ncb;
         const int t = w.tlist[(size_t)(k & 1) * Tc + y];
         uint4 act = make_uint4(FULL_MASK, FULL_MASK, FULL_MASK, FULL_MASK);
         if (EARLY) {
             // the syndrome of k_cn(k) tests b^(k-1); it may stop frames only at a check point (k-1) % T == 0
             const bool check = ((k - 1) % check_every) == 0;
-            const uint4 ua = check ? ldu4(w.unsat + ((size_t)(k & 1) * Tc + t) * 4) : make_uint4(FULL_MASK, FULL_MASK, FULL_MASK, FULL_MASK);
+            const uint4 ua = check ? ldu4(w.unsat + ((size_t)(k & 1) * Tc + t) * 4)
+                                   : make_uint4(FULL_MASK, FULL_MASK, FULL_MASK, FULL_MASK);
             const uint4 dw = ldu4(w.done + (size_t)t * 4);
             const uint4 newly = make_uint4(~ua.x & ~dw.x, ~ua.y & ~dw.y, ~ua.z & ~dw.z, ~ua.w & ~dw.w);
             act = make_uint4(ua.x & ~dw.x, ua.y & ~dw.y, ua.z & ~dw.z, ua.w & ~dw.w);
-            // every thread has read `done` before the tile's bookkeeping item rewrites it (other items of
-            // the tile may see either value: act is the same for both, since newly and ua are disjoint)
-            cta_sync();
-            if (x == 0) {
+            if (x == 0) {  // the tile's bookkeeping item (uniform in the CTA)
+                // every thread has read `done` before it is rewritten (other items of the tile may see either
+                // value: act is the same for both, since newly and ua are disjoint)
+                cta_sync();
                 const int tid = threadIdx.x;
                 if (tid < 4) {
                     w.done[(size_t)t * 4 + tid] = comp(dw, tid) | comp(newly, tid);
@@ -524,45 +524,33 @@ __global__ void __launch_bounds__(BN_T, BN_MINB)
         const unsigned char *RB = w.rst + (size_t)t * m * w.rs;
         const float *__restrict__ Rl = w.r + (size_t)t * n * TILE + 4 * lane;
         float *__restrict__ Sl = w.s + (size_t)t * n * TILE + 4 * lane;
-        const int jb = x * BN_COLS, j1 = min(n, jb + BN_COLS);
-        // the item's edge records into shared memory: the edge loop below then waits on data loads only
-        const int cb = __ldg(g.col_ptr + jb), ne = __ldg(g.col_ptr + j1) - cb;
-        const bool staged = ne <= BN_REC;  // uniform
-        if (staged) {
-            for (int q = threadIdx.x; q < ne; q += BN_T) {
-                const int4 ed = __ldg(g.bn_edge + cb + q);
-                s_rec[q] = make_int2(ed.y, ed.z);
-            }
-            if (threadIdx.x <= j1 - jb) s_cp[threadIdx.x] = __ldg(g.col_ptr + jb + threadIdx.x) - cb;
-        }
-        cta_sync();
-        for (int j = jb + warp; j < j1; j += BN_T / 32) {
-            int c0, dv;
-            if (staged) {
-                c0 = s_cp[j - jb];
-                dv = s_cp[j - jb + 1] - c0;
-            } else {
-                c0 = __ldg(g.col_ptr + j) - cb;
-                dv = __ldg(g.col_ptr + j + 1) - cb - c0;
-            }
+        const int j1 = min(n, x * BN_COLS + BN_COLS);
+        for (int j = x * BN_COLS + warp; j < j1; j += BN_T / 32) {
+            const int c0 = __ldg(g.col_ptr + j), dv = __ldg(g.col_ptr + j + 1) - c0;
             const float4 rv = ld4(Rl + (size_t)j * TILE);
             float acc[4] = {0.f, 0.f, 0.f, 0.f};
-            for (int q = 0; q < dv; q++) {
-                int2 ed;  // {row i, position p}, ascending i
-                if (staged) {
-                    ed = s_rec[c0 + q];
-                } else {
-                    const int4 e4 = __ldg(g.bn_edge + cb + c0 + q);
-                    ed = make_int2(e4.y, e4.z);
-                }
-                const unsigned char *Ri = RB + (size_t)ed.x * w.rs;
-                const float4 m0 = ld4(reinterpret_cast<const float *>(Ri) + 4 * lane);
-                const float4 m1 = ld4(reinterpret_cast<const float *>(Ri) + 128 + 4 * lane);
-                const uint32_t b = Ri[REC_EDGE0 + 32 * ed.y + lane];
+            for (int q0 = 0; q0 < dv; q0 += BN_G) {
+                // all loads of up to BN_G edges in flight together (past the column's last edge: its last edge
+                // again, not accumulated), then the sums in ascending row order from +0.0 (A14)
+                float4 m0[BN_G], m1[BN_G];
+                uint32_t b[BN_G];
 #pragma unroll
-                for (int v = 0; v < 4; v++) {
-                    const float mag = (b & (16u << v)) ? comp(m1, v) : comp(m0, v);  // Obs. 1
-                    acc[v] = acc[v] + flip31(mag, b << (31 - v));                    // ascending rows from +0.0 (A14)
+                for (int u = 0; u < BN_G; u++) {
+                    const int4 ed = __ldg(g.bn_edge + c0 + min(q0 + u, dv - 1));  // {e, i, p, -}, ascending i
+                    const unsigned char *Ri = RB + (size_t)ed.y * w.rs;
+                    m0[u] = ld4(reinterpret_cast<const float *>(Ri) + 4 * lane);
+                    m1[u] = ld4(reinterpret_cast<const float *>(Ri) + 128 + 4 * lane);
+                    b[u] = Ri[REC_EDGE0 + 32 * ed.z + lane];
+                }
+#pragma unroll
+                for (int u = 0; u < BN_G; u++) {
+                    if (q0 + u < dv) {
+#pragma unroll
+                        for (int v = 0; v < 4; v++) {
+                            const float mag = (b[u] & (16u << v)) ? comp(m1[u], v) : comp(m0[u], v);  // Obs. 1
+                            acc[v] = acc[v] + flip31(mag, b[u] << (31 - v));
+                        }
+                    }
                 }
             }
             float *o = Sl + (size_t)j * TILE;

@@ -9,6 +9,8 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_sort.cuh>
 
 #include "ldpc_internal.cuh"
 
@@ -17,7 +19,7 @@ namespace ldpc {
 namespace {
 
 __global__ void k_dense_count(const uint8_t *__restrict__ H, int m, int n, int *__restrict__ row_deg,
-                              int *__restrict__ err) {
+                              int *__restrict__ err, unsigned long long *__restrict__ total) {
     // one warp per row; lanes stride the columns (coalesced byte loads)
     int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (warp >= m) return;
@@ -34,6 +36,7 @@ __global__ void k_dense_count(const uint8_t *__restrict__ H, int m, int n, int *
     }
     if (lane == 0) {
         row_deg[warp] = cnt;
+        if (cnt) atomicAdd(total, (unsigned long long)cnt);  // E in 64 bits (a dense H may exceed 2^31 ones)
         if (bad) atomicOr(err, ERRB_NOT_BINARY);
     }
 }
@@ -75,22 +78,17 @@ __global__ void k_coo_fill(const int32_t *__restrict__ rows, const int32_t *__re
     col_idx[row_ptr[i] + slot] = cols[t];
 }
 
-// insertion sort of each segment (rows or columns); flags equal neighbours as duplicates
-__global__ void k_sort_segments(const int *__restrict__ ptr, int count, int *__restrict__ vals, int *__restrict__ err,
-                                int *__restrict__ max_len) {
-    int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= count) return;
-    int a = ptr[s], b = ptr[s + 1];
-    for (int x = a + 1; x < b; x++) {
-        int v = vals[x], y = x - 1;
-        while (y >= a && vals[y] > v) {
-            vals[y + 1] = vals[y];
-            y--;
-        }
-        vals[y + 1] = v;
-    }
+// after the segmented sort: equal neighbours inside a segment are duplicates; longest segment
+__global__ void k_seg_check(const int *__restrict__ ptr, int count, const int *__restrict__ vals,
+                            int *__restrict__ err, int *__restrict__ max_len) {
+    const int sgm = blockIdx.x * blockDim.x + threadIdx.x;
+    if (sgm >= count) return;
+    const int a = ptr[sgm], b = ptr[sgm + 1];
     for (int x = a + 1; x < b; x++)
-        if (vals[x] == vals[x - 1]) atomicOr(err, ERRB_DUPLICATE);
+        if (vals[x] == vals[x - 1]) {
+            atomicOr(err, ERRB_DUPLICATE);
+            break;
+        }
     atomicMax(max_len, b - a);
 }
 
@@ -129,40 +127,6 @@ __global__ void k_bn_edges(const int *__restrict__ col_edge, int E, const int *_
     out[q] = make_int4(e, i, edge_pos[e], d & 1);
 }
 
-// single-CTA exclusive scan: out[0] = 0, out[k+1] = sum(in[0..k]); count up to a few million
-__global__ void k_scan(const int *__restrict__ in, int count, int *__restrict__ out) {
-    __shared__ long long warp_sums[32];
-    int tid = threadIdx.x, nt = blockDim.x;
-    int per = (count + nt - 1) / nt;
-    int a = min(count, tid * per), b = min(count, a + per);
-    long long sum = 0;
-    for (int x = a; x < b; x++) sum += in[x];
-    // block exclusive scan of per-thread sums
-    long long incl = sum;
-    int lane = tid & 31, wid = tid >> 5;
-    for (int o = 1; o < 32; o <<= 1) {
-        long long y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-    }
-    if (lane == 31) warp_sums[wid] = incl;
-    __syncthreads();
-    if (wid == 0) {
-        long long w = (lane < (nt >> 5)) ? warp_sums[lane] : 0;
-        for (int o = 1; o < 32; o <<= 1) {
-            long long y = __shfl_up_sync(0xffffffffu, w, o);
-            if (lane >= o) w += y;
-        }
-        warp_sums[lane] = w;
-    }
-    __syncthreads();
-    long long run = incl - sum + (wid ? warp_sums[wid - 1] : 0);
-    if (tid == 0) out[0] = 0;
-    for (int x = a; x < b; x++) {
-        run += in[x];
-        out[x + 1] = (int)min(run, (long long)0x7fffffff);
-    }
-}
-
 int cuda_status(cudaError_t e) {
     if (e == cudaErrorMemoryAllocation) return LDPC_ERR_OOM;
     return e == cudaSuccess ? LDPC_OK : LDPC_ERR_CUDA;
@@ -184,11 +148,52 @@ struct Builder {
     HostGraph *hg;
     cudaStream_t st;
     int *row_deg = nullptr, *err = nullptr, *maxes = nullptr, *col_deg = nullptr, *cursor = nullptr,
-        *edge_row = nullptr, *edge_pos = nullptr;
+        *edge_row = nullptr, *edge_pos = nullptr, *keys_tmp = nullptr;
+    void *temp = nullptr;  // CUB scratch
+    size_t temp_bytes = 0;
     void scratch_free() {
         cudaFree(row_deg); cudaFree(err); cudaFree(maxes); cudaFree(col_deg); cudaFree(cursor);
-        cudaFree(edge_row); cudaFree(edge_pos);
-        row_deg = err = maxes = col_deg = cursor = edge_row = edge_pos = nullptr;
+        cudaFree(edge_row); cudaFree(edge_pos); cudaFree(keys_tmp); cudaFree(temp);
+        row_deg = err = maxes = col_deg = cursor = edge_row = edge_pos = keys_tmp = nullptr;
+        temp = nullptr;
+        temp_bytes = 0;
+    }
+    int need_temp(size_t bytes) {
+        if (bytes <= temp_bytes) return LDPC_OK;
+        cudaFree(temp);
+        temp = nullptr;
+        temp_bytes = 0;
+        CK(cudaMalloc(&temp, std::max<size_t>(bytes, 256)));
+        temp_bytes = std::max<size_t>(bytes, 256);
+        return LDPC_OK;
+    }
+    // out[0] = 0, out[k+1] = in[0] + ... + in[k]: a device-wide scan (any count)
+    int scan(const int *in, int count, int *out) {
+        CK(cudaMemsetAsync(out, 0, sizeof(int), st));
+        if (count == 0) return LDPC_OK;
+        size_t bytes = 0;
+        CK(cub::DeviceScan::InclusiveSum(nullptr, bytes, in, out + 1, count, st));
+        if (int rc = need_temp(bytes)) return rc;
+        CK(cub::DeviceScan::InclusiveSum(temp, bytes, in, out + 1, count, st));
+        hg->launches += 2;
+        return LDPC_OK;
+    }
+    // sort every segment [ptr[q], ptr[q+1]) of vals ascending (a segmented sort: any segment length), then
+    // flag repeated values and record the longest segment in *max_len
+    int sort_segments(int *vals, int E, const int *ptr, int count, int *max_len) {
+        if (E > 1) {
+            if (!keys_tmp) CK(cudaMalloc(&keys_tmp, sizeof(int) * (size_t)E));
+            size_t bytes = 0;
+            CK(cub::DeviceSegmentedSort::SortKeys(nullptr, bytes, vals, keys_tmp, E, count, ptr, ptr + 1, st));
+            if (int rc = need_temp(bytes)) return rc;
+            CK(cub::DeviceSegmentedSort::SortKeys(temp, bytes, vals, keys_tmp, E, count, ptr, ptr + 1, st));
+            CK(cudaMemcpyAsync(vals, keys_tmp, sizeof(int) * (size_t)E, cudaMemcpyDeviceToDevice, st));
+            hg->launches += 3;
+        }
+        k_seg_check<<<blocks(count, 256), 256, 0, st>>>(ptr, count, vals, err, max_len);
+        hg->launches += 1;
+        CK(cudaGetLastError());
+        return LDPC_OK;
     }
     void on_error() {
         scratch_free();
@@ -222,12 +227,14 @@ struct Builder {
         CK(cudaMemsetAsync(cursor, 0, sizeof(int) * std::max(m, n), st));
         k_rows_finish<<<blocks(m, 256), 256, 0, st>>>(hg->row_ptr, hg->col_idx, m, col_deg, edge_row, edge_pos, err,
                                                        maxes + 0);
-        k_scan<<<1, 1024, 0, st>>>(col_deg, n, hg->col_ptr);
+        hg->launches += 1;
+        if (int rc = scan(col_deg, n, hg->col_ptr)) return rc;
         k_col_fill<<<blocks(E, 256), 256, 0, st>>>(hg->col_idx, E, hg->col_ptr, cursor, hg->col_edge);
+        hg->launches += 1;
         // ascending edge id == ascending row, because the row CSR is row-major
-        k_sort_segments<<<blocks(n, 256), 256, 0, st>>>(hg->col_ptr, n, hg->col_edge, err, maxes + 1);
+        if (int rc = sort_segments(hg->col_edge, E, hg->col_ptr, n, maxes + 1)) return rc;
         k_bn_edges<<<blocks(E, 256), 256, 0, st>>>(hg->col_edge, E, edge_row, edge_pos, hg->row_ptr, hg->bn_edge);
-        hg->launches += 5;
+        hg->launches += 1;
         CK(cudaGetLastError());
         int h_max[2] = {0, 0};
         CK(cudaMemcpyAsync(h_max, maxes, sizeof(h_max), cudaMemcpyDeviceToHost, st));
@@ -260,15 +267,20 @@ int ingest_dense(const uint8_t *H, int m, int n, cudaStream_t st, HostGraph *hg)
     CK(cudaMalloc(&hg->row_ptr, sizeof(int) * (m + 1)));
     CK(cudaMemsetAsync(b.err, 0, sizeof(int), st));
     CK(cudaMemsetAsync(b.maxes, 0, sizeof(int) * 2, st));
-    k_dense_count<<<blocks((int64_t)m * 32, 256), 256, 0, st>>>(H, m, n, b.row_deg, b.err);
-    k_scan<<<1, 1024, 0, st>>>(b.row_deg, m, hg->row_ptr);
-    hg->launches += 2;
+    unsigned long long *total = nullptr;
+    CK(cudaMalloc(&total, sizeof(unsigned long long)));
+    CK(cudaMemsetAsync(total, 0, sizeof(unsigned long long), st));
+    k_dense_count<<<blocks((int64_t)m * 32, 256), 256, 0, st>>>(H, m, n, b.row_deg, b.err, total);
+    hg->launches += 1;
     CK(cudaGetLastError());
-    int E = 0;
-    CK(cudaMemcpyAsync(&E, hg->row_ptr + m, sizeof(int), cudaMemcpyDeviceToHost, st));
+    unsigned long long E64 = 0;
+    CK(cudaMemcpyAsync(&E64, total, sizeof(E64), cudaMemcpyDeviceToHost, st));
     int rc = b.read_err();  // synchronises; NOT_BINARY is reported before anything else is built
+    cudaFree(total);
     if (rc) return rc;
-    if (E == 0x7fffffff) return b.fail(LDPC_ERR_UNSUPPORTED);
+    if (E64 >= 0x7fffffffull) return b.fail(LDPC_ERR_UNSUPPORTED);
+    const int E = (int)E64;
+    if ((rc = b.scan(b.row_deg, m, hg->row_ptr))) return rc;
     hg->E = E;
     CK(cudaMalloc(&hg->col_idx, sizeof(int) * std::max(E, 1)));
     k_dense_fill<<<blocks((int64_t)m * 32, 256), 256, 0, st>>>(H, m, n, hg->row_ptr, hg->col_idx);
@@ -300,10 +312,10 @@ int ingest_coo(const int32_t *rows, const int32_t *cols, int64_t nnz, int m, int
     CK(cudaGetLastError());
     int rc = b.read_err();  // range errors first: the fill below indexes by row
     if (rc) return rc;
-    k_scan<<<1, 1024, 0, st>>>(b.row_deg, m, hg->row_ptr);
+    if ((rc = b.scan(b.row_deg, m, hg->row_ptr))) return rc;
     k_coo_fill<<<blocks(nnz, 256), 256, 0, st>>>(rows, cols, nnz, hg->row_ptr, b.cursor, hg->col_idx);
-    k_sort_segments<<<blocks(m, 256), 256, 0, st>>>(hg->row_ptr, m, hg->col_idx, b.err, b.maxes + 0);
-    hg->launches += 3;
+    hg->launches += 1;
+    if ((rc = b.sort_segments(hg->col_idx, (int)nnz, hg->row_ptr, m, b.maxes + 0))) return rc;
     CK(cudaGetLastError());
     cudaFree(b.cursor);
     b.cursor = nullptr;

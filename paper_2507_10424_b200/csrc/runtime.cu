@@ -117,14 +117,14 @@ int tile_capacity(const ldpc_plan *h, int T) { return h->cfg.compact ? 2 * T : T
 // flags, slot frame indices, compaction map; per chunk frame: k, isCodeword, three counters.
 StreamState carve(void *base, int T, int Tcap, const ldpc_plan *h, size_t *total) {
     const size_t m = h->g.m, n = h->g.n;
-    char *p0 = static_cast<char *>(base), *p = p0;
+    char *p0 = static_cast<char *>(base);
     size_t off = 0;
     auto take = [&](size_t bytes) {
         char *q = p0 ? p0 + off : nullptr;
         off += align256(bytes);
         return q;
     };
-    (void)p;
+
     StreamState w{};
     w.T = T;
     w.Tcap = Tcap;
