@@ -132,12 +132,15 @@ __device__ __forceinline__ void cn_rows(const float *__restrict__ s, float *mn0,
     float nm0[4] = {INF, INF, INF, INF}, nm1[4] = {INF, INF, INF, INF};
     int nloc[4] = {0xff, 0xff, 0xff, 0xff};
     uint32_t synw[4] = {0u, 0u, 0u, 0u};  // XOR of the sign bits of s over the row: bit 31 = XOR of (1 - b_j)
+    // new sign bits are pushed into wn by one funnel shift per slot-edge, in (p, v) order; a full word (8
+    // edges) is bit-reversed into the stored layout (bit 4(p%8)+v)
     uint32_t wo = valid ? sgw[0] : 0u, wn = 0u, pf = 0u;  // old / new sign word of the current 8 edges
     const int pe = DC > 0 ? DC : dmax;
     // DC > 0: every row has degree DC (regular code) -- the edge loop is fully unrolled
 #pragma unroll(DC > 0 ? DC : 2)
     for (int p = 0; p < pe; p++) {
         if ((DC == 0 || DC > 8) && p > 0 && (p & 7) == 0) {  // next sign word of the row
+            wn = __brev(wn);
             if (valid) sgw[((p >> 3) - 1) * LR] = wn;
             pf ^= wn;
             wn = 0u;
@@ -155,15 +158,21 @@ __device__ __forceinline__ void cn_rows(const float *__restrict__ s, float *mn0,
         for (int v = 0; v < 4; v++) {
             const int sh = 4 * (p & 7) + v;
             const float sj = f4c(sv, v);
-            const float x = sj - flip31(mg[v], wo << (31 - sh));  // lambda - eta^prev (Obs. 2 sign)
+            // lambda - eta^prev (Obs. 2 sign); + 0 makes a zero lambda +0 (s may be -0), so its IEEE sign bit is
+            // sign(0) = +1; the add runs on the otherwise idle FMA pipe
+            const float x = __fadd_rn(__fsub_rn(sj, flip31(mg[v], wo << (31 - sh))), 0.0f);
             const float ax = HAS ? (has ? fabsf(x) : INF) : fabsf(x);
             const bool lt = ax < nm0[v];  // first strict minimum (A13)
             nm1[v] = fminf(nm1[v], fmaxf(nm0[v], ax));
             nm0[v] = fminf(nm0[v], ax);
             nloc[v] = lt ? p : nloc[v];
-            if ((HAS ? has : true) && x < 0.f) wn |= 1u << sh;          // sign(0) = +1
+            wn = __funnelshift_l(HAS ? (has ? __float_as_uint(x) : 0u) : __float_as_uint(x), wn, 1);
             synw[v] ^= (HAS ? has : true) ? __float_as_uint(sj) : 0u;  // slice(s_j) = 0 iff sign bit
         }
+    }
+    {
+        const int pushed = 4 * (((pe - 1) & 7) + 1);  // slot-edges in the last word
+        wn = pushed == 32 ? __brev(wn) : __brev(wn) >> (32 - pushed);
     }
     if (valid) sgw[((pe - 1) >> 3) * LR] = wn;
     pf ^= wn;

@@ -84,10 +84,12 @@ __device__ __forceinline__ int next_item(int *ctr, int &s_item) {
 #define BN_T 128  // the bit node lives on loads in flight
 #endif
 #ifndef BN_MINB
-#define BN_MINB 8  // 8 x 128 threads with up to 64 registers: 32 warps, each with BN_G edges of loads in flight
+#define BN_MINB 12  // 12 x 128 threads (48 warps per SM)
 #endif
 constexpr int CN_ROWS = 128;  // rows per check-node item (16 per warp)
-constexpr int BN_COLS = 16;   // columns per bit-node item (4 per warp)
+#ifndef BN_COLS
+#define BN_COLS 16  // columns per bit-node item (4 per warp)
+#endif
 constexpr int CN_NW = CN_T / 32;
 
 // ------------------------------------------------------------------------------------------------
@@ -455,17 +457,23 @@ __global__ void __launch_bounds__(CN_T, 2) k_cn_generic(Graph g, StreamState w, 
 // at least two bodies remain, to the compaction sources.
 // ------------------------------------------------------------------------------------------------
 #ifndef BN_G
-#define BN_G 4  // edges of a column whose loads are issued together
+#define BN_G 1  // edges of a column whose loads are issued together (1 measured best: 2-5 cut occupancy)
+#endif
+#ifndef BN_CM1
+#define BN_CM1 1  // load min1 only if the edge is min0Location for one of the lane's frames (fewer L2 bytes)
 #endif
 
-// Items are taken in a static stride (no work counter, no per-item barrier): the bit node is bound by
-// loads in flight, and its items cost the same.
+#ifndef BN_DYN
+#define BN_DYN 1  // items from the work counter (keeps the tiles in flight together for L2 reuse)
+#endif
+
 template <bool EARLY>
 __global__ void __launch_bounds__(BN_T, BN_MINB)
     k_bn(Graph g, StreamState w, int k, int L, const int *kdev, int check_every, int compact) {
     if (kdev) k = *kdev;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int Tc = w.Tcap;
+    __shared__ int s_item;
     const int cnt = w.tcount[k & 1];
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         w.work[WK_CN] = 0;  // next check-node sweep
@@ -476,7 +484,9 @@ __global__ void __launch_bounds__(BN_T, BN_MINB)
     const int ncb = (n + BN_COLS - 1) / BN_COLS;
     const int items = cnt * ncb;
     const bool compact_ok = EARLY && compact && k + 2 <= L;
-    for (int it = blockIdx.x; it < items; it += gridDim.x) {
+    for (int it0 = blockIdx.x;; it0 += gridDim.x) {
+        const int it = BN_DYN ? next_item(w.work + WK_BN, s_item) : it0;
+        if (it >= items) break;
         const int y = it / ncb, x = it - y * ncb;
         const int t = w.tlist[(size_t)(k & 1) * Tc + y];
         uint4 act = make_uint4(FULL_MASK, FULL_MASK, FULL_MASK, FULL_MASK);
@@ -539,8 +549,9 @@ __global__ void __launch_bounds__(BN_T, BN_MINB)
                     const int4 ed = __ldg(g.bn_edge + c0 + min(q0 + u, dv - 1));  // {e, i, p, -}, ascending i
                     const unsigned char *Ri = RB + (size_t)ed.y * w.rs;
                     m0[u] = ld4(reinterpret_cast<const float *>(Ri) + 4 * lane);
-                    m1[u] = ld4(reinterpret_cast<const float *>(Ri) + 128 + 4 * lane);
                     b[u] = Ri[REC_EDGE0 + 32 * ed.z + lane];
+                    if (!BN_CM1 || (b[u] & 0xf0u)) m1[u] = ld4(reinterpret_cast<const float *>(Ri) + 128 + 4 * lane);
+                    else m1[u] = m0[u];
                 }
 #pragma unroll
                 for (int u = 0; u < BN_G; u++) {
