@@ -460,7 +460,7 @@ __global__ void __launch_bounds__(CN_T, 2) k_cn_generic(Graph g, StreamState w, 
 #define BN_G 1  // edges of a column whose loads are issued together (1 measured best: 2-5 cut occupancy)
 #endif
 #ifndef BN_CM1
-#define BN_CM1 1  // load min1 only if the edge is min0Location for one of the lane's frames (fewer L2 bytes)
+#define BN_CM1 0  // 1: load min1 only where the edge is a min0Location of the lane (fewer L2 bytes, measured slower)
 #endif
 
 #ifndef BN_DYN
