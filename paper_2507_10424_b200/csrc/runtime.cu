@@ -490,11 +490,11 @@ int ldpc_decode_host(ldpc_handle_t h, const float *llr, int64_t frames, int32_t 
     if (h->poisoned) return LDPC_ERR_CUDA;
     if (frames == 0) return LDPC_OK;
     const int64_t n = h->g.n;
-    // chunk of frames per pipeline stage: LDPC_HOST_CHUNK_MB of LLRs (default 384 MB: enough tiles per
-    // launch to fill the GPU in the streaming schedule, few kernel tails in the resident one, small
-    // enough to overlap copies and decode; measured e2e on C2-C4)
+    // chunk of frames per pipeline stage: LDPC_HOST_CHUNK_MB of LLRs (default 384 MB for the resident
+    // schedule -- few kernel tails, copies overlapped -- and 1 GB for the streaming one, whose chunks must
+    // hold enough tiles for compaction and a full sweep grid: 1482 frames of C4 per 384 MB were too few)
     const char *cm = getenv("LDPC_HOST_CHUNK_MB");
-    const int64_t chunk_mb = cm ? std::max(1, atoi(cm)) : 384;
+    const int64_t chunk_mb = cm ? std::max(1, atoi(cm)) : (use_resident(h) ? 384 : 1024);
     int64_t chunk = std::max<int64_t>(TILE, std::min<int64_t>(frames, (chunk_mb << 20) / (n * 4)));
     chunk = (chunk + TILE - 1) / TILE * TILE;
     const size_t per_frame = n * 4 + (bits_out ? n : 0) + (posterior_out ? n * 4 : 0) + 4 + 1;
