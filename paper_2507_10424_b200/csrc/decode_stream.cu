@@ -330,10 +330,12 @@ __global__ void __launch_bounds__(CN_T, CN_MINB) k_cn(Graph g, StreamState w, in
     }
 }
 
-// Rows of any degree: edges in chunks of 8 (one gather batch); each edge byte is written with its
-// sign nibble during the sweep, and the isloc bits are OR-ed into the (at most 4) min0Location
-// bytes of the lane afterwards (each lane owns byte `lane` of every edge block: no conflicts).
-template <bool FIRST, bool EARLY>
+// Rows of any degree: edges in chunks of 8 (one gather batch, all loads in flight together).  The sign
+// bits of a chunk are pushed into one word by a funnel shift per frame-edge and its edge bytes written at
+// the end of the chunk; NWK > 0 (rows of at most 8*NWK edges) keeps the chunk words in registers and
+// merges the isloc nibbles into the bytes of the min0Location edges at the end of the row; NWK = 0 (any
+// degree) ORs them into the bytes already written (each lane owns byte `lane` of every edge block).
+template <bool FIRST, bool EARLY, int NWK>
 __global__ void __launch_bounds__(CN_T, 2) k_cn_generic(Graph g, StreamState w, int k, int literal, const int *kdev) {
     if (kdev) k = *kdev;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -371,10 +373,15 @@ __global__ void __launch_bounds__(CN_T, 2) k_cn_generic(Graph g, StreamState w, 
             }
             float nm0[4] = {INF, INF, INF, INF}, nm1[4] = {INF, INF, INF, INF};
             int nloc[4] = {0, 0, 0, 0};
-            uint32_t par[4] = {0u, 0u, 0u, 0u}, syn[4] = {0u, 0u, 0u, 0u};
+            uint32_t syn[4] = {0u, 0u, 0u, 0u}, pf = 0u;
+            uint32_t cws[NWK > 0 ? NWK : 1];
             int cj = 0;
-            for (int p0 = 0; p0 < d; p0 += C8) {
+            // NWK > 0: the chunk loop is unrolled (chunk words stay in registers)
+#pragma unroll(NWK > 0 ? NWK : 1)
+            for (int p0 = 0; p0 < (NWK > 0 ? 8 * NWK : d); p0 += C8) {
+                if (NWK > 0 && p0 >= d) break;
                 if ((p0 & 31) == 0) cj = (lane < d - p0) ? __ldg(g.col_idx + a + p0 + lane) : 0;
+                const bool full = p0 + C8 <= d;  // warp-uniform
                 float4 sv[C8];
                 uint32_t eb[C8];
 #pragma unroll
@@ -383,11 +390,11 @@ __global__ void __launch_bounds__(CN_T, 2) k_cn_generic(Graph g, StreamState w, 
                     sv[u8] = ld4(Sl + (size_t)j * TILE);  // unconditional: edges past d_i read column 0
                     eb[u8] = FIRST ? 0u : Ri[REC_EDGE0 + 32 * (p0 + u8) + lane];
                 }
+                uint32_t cw = 0;
 #pragma unroll
                 for (int u8 = 0; u8 < C8; u8++) {
                     const int p = p0 + u8;
-                    if (p < d) {
-                        uint32_t nib = 0;
+                    if (full || p < d) {
 #pragma unroll
                         for (int v = 0; v < 4; v++) {
                             const float sj = comp(sv[u8], v);
@@ -399,35 +406,69 @@ __global__ void __launch_bounds__(CN_T, 2) k_cn_generic(Graph g, StreamState w, 
                                 x = __fadd_rn(__fsub_rn(sj, flip31(mag, eb[u8] << (31 - v))), 0.0f);
                             }
                             const float ax = fabsf(x);
-                            const bool lt = ax < nm0[v];
+                            const bool lt = ax < nm0[v];  // first strict minimum (A13)
                             nm1[v] = fminf(nm1[v], fmaxf(nm0[v], ax));
                             nm0[v] = fminf(nm0[v], ax);
                             nloc[v] = lt ? p : nloc[v];
-                            par[v] ^= __float_as_uint(x);
                             if (EARLY) syn[v] ^= __float_as_uint(sj);
-                            nib |= (__float_as_uint(x) >> 31) << v;
+                            cw = __funnelshift_l(__float_as_uint(x), cw, 1);
                         }
-                        Ri[REC_EDGE0 + 32 * p + lane] = (unsigned char)nib;  // sign nibble, isloc = 0
                     }
                 }
-            }
-            // isloc bits into the min0Location bytes of this lane (same thread wrote them: ordered)
+                const int pushed = full ? 32 : 4 * (d - p0);
+                cw = pushed == 32 ? __brev(cw) : __brev(cw) >> (32 - pushed);  // bit 4u+v: edge p0+u, slot 4l+v
+                pf ^= cw;
+                if (NWK > 0) {
 #pragma unroll
-            for (int v = 0; v < 4; v++) {
-                unsigned char *bp = Ri + REC_EDGE0 + 32 * nloc[v] + lane;
-                *bp = (unsigned char)(*bp | (16u << v));
-            }
-            const uint32_t c31 = ((uint32_t)(d & 1) & (uint32_t)(!literal)) << 31;
-            float4 o0, o1;
-            uint32_t sb[4];
+                    for (int q = 0; q < (NWK > 0 ? NWK : 1); q++)
+                        if (q == (p0 >> 3)) cws[q] = cw;
+                } else {
+                    const uint32_t ze = cw & 0x0f0f0f0fu, zo = (cw >> 4) & 0x0f0f0f0fu;
 #pragma unroll
-            for (int v = 0; v < 4; v++) sb[v] = (par[v] & 0x80000000u) ^ c31;
-            o0 = make_float4(__uint_as_float(__float_as_uint(nm0[0]) | sb[0]), __uint_as_float(__float_as_uint(nm0[1]) | sb[1]),
-                             __uint_as_float(__float_as_uint(nm0[2]) | sb[2]), __uint_as_float(__float_as_uint(nm0[3]) | sb[3]));
-            o1 = make_float4(__uint_as_float(__float_as_uint(nm1[0]) | sb[0]), __uint_as_float(__float_as_uint(nm1[1]) | sb[1]),
-                             __uint_as_float(__float_as_uint(nm1[2]) | sb[2]), __uint_as_float(__float_as_uint(nm1[3]) | sb[3]));
-            st4(reinterpret_cast<float *>(Ri) + 4 * lane, o0);
-            st4(reinterpret_cast<float *>(Ri) + 128 + 4 * lane, o1);
+                    for (int u8 = 0; u8 < C8; u8++)
+                        if (full || p0 + u8 < d)
+                            Ri[REC_EDGE0 + 32 * (p0 + u8) + lane] = (unsigned char)(((u8 & 1) ? zo : ze) >> (8 * (u8 >> 1)));
+                }
+            }
+            if (NWK > 0) {  // edge bytes with their isloc nibbles, chunk by chunk
+#pragma unroll
+                for (int q = 0; q < (NWK > 0 ? NWK : 1); q++) {
+                    if (8 * q < d) {
+                        uint32_t lm = 0;
+#pragma unroll
+                        for (int v = 0; v < 4; v++) {
+                            const int r = nloc[v] - 8 * q;
+                            lm |= (r >= 0 && r < 8) ? (1u << (4 * r + v)) : 0u;
+                        }
+                        const uint32_t ze = (cws[q] & 0x0f0f0f0fu) | ((lm & 0x0f0f0f0fu) << 4);
+                        const uint32_t zo = ((cws[q] >> 4) & 0x0f0f0f0fu) | (lm & 0xf0f0f0f0u);
+#pragma unroll
+                        for (int u8 = 0; u8 < C8; u8++)
+                            if (8 * q + u8 < d)
+                                Ri[REC_EDGE0 + 32 * (8 * q + u8) + lane] =
+                                    (unsigned char)(((u8 & 1) ? zo : ze) >> (8 * (u8 >> 1)));
+                    }
+                }
+            } else {  // isloc bits into the min0Location bytes of this lane (same thread wrote them: ordered)
+#pragma unroll
+                for (int v = 0; v < 4; v++) {
+                    unsigned char *bp = Ri + REC_EDGE0 + 32 * nloc[v] + lane;
+                    *bp = (unsigned char)(*bp | (16u << v));
+                }
+            }
+            // sign parity per slot (Obs. 2): XOR of bits v, v+4, ... of the chunk words, times (-1)^{d_i} (A1)
+            uint32_t pw = pf ^ (pf >> 16);
+            pw ^= pw >> 8;
+            pw ^= pw >> 4;
+            pw ^= ((uint32_t)(d & 1) & (uint32_t)(!literal)) ? 0xfu : 0u;
+            const uint32_t sb[4] = {pw << 31, (pw << 30) & 0x80000000u, (pw << 29) & 0x80000000u,
+                                    (pw << 28) & 0x80000000u};
+            st4(reinterpret_cast<float *>(Ri) + 4 * lane,
+                make_float4(__uint_as_float(__float_as_uint(nm0[0]) | sb[0]), __uint_as_float(__float_as_uint(nm0[1]) | sb[1]),
+                            __uint_as_float(__float_as_uint(nm0[2]) | sb[2]), __uint_as_float(__float_as_uint(nm0[3]) | sb[3])));
+            st4(reinterpret_cast<float *>(Ri) + 128 + 4 * lane,
+                make_float4(__uint_as_float(__float_as_uint(nm1[0]) | sb[0]), __uint_as_float(__float_as_uint(nm1[1]) | sb[1]),
+                            __uint_as_float(__float_as_uint(nm1[2]) | sb[2]), __uint_as_float(__float_as_uint(nm1[3]) | sb[3])));
             if (EARLY) {
                 const uint32_t dp = (uint32_t)(d & 1);
 #pragma unroll
@@ -931,8 +972,12 @@ void cn_launch(const Graph &g, const StreamState &w, int k, int lit, const Strea
         else if (g.dmax <= 6) k_cn<6, F, EA><<<grid, CN_T, 0, st>>>(g, w, k, lit, kdev);
         else if (g.dmax == 7) k_cn<7, F, EA><<<grid, CN_T, 0, st>>>(g, w, k, lit, kdev);
         else k_cn<8, F, EA><<<grid, CN_T, 0, st>>>(g, w, k, lit, kdev);
+    } else if (g.dmax <= 16) {
+        k_cn_generic<F, EA, 2><<<gridg, CN_T, 0, st>>>(g, w, k, lit, kdev);
+    } else if (g.dmax <= 32) {
+        k_cn_generic<F, EA, 4><<<gridg, CN_T, 0, st>>>(g, w, k, lit, kdev);
     } else {
-        k_cn_generic<F, EA><<<gridg, CN_T, 0, st>>>(g, w, k, lit, kdev);
+        k_cn_generic<F, EA, 0><<<gridg, CN_T, 0, st>>>(g, w, k, lit, kdev);
     }
 }
 
