@@ -361,8 +361,28 @@ __global__ void __launch_bounds__(CN_T, 2) k_cn_generic(Graph g, StreamState w, 
         const float *__restrict__ Sl = (FIRST ? w.r : w.s) + (size_t)t * n * TILE + 4 * lane;
         unsigned char *RB = w.rst + (size_t)t * m * w.rs;
         uint32_t u[4] = {0u, 0u, 0u, 0u};
-        for (int i = x * CN_ROWS + warp; i < min(m, x * CN_ROWS + CN_ROWS); i += CN_NW) {
-            const int a = __ldg(g.row_ptr + i), d = __ldg(g.row_ptr + i + 1) - a;
+        // the warp's rows i0 + 8q: their row pointers in lanes q (one load), and the first 32 column
+        // indices of the next row fetched while the current row is processed
+        const int i0 = x * CN_ROWS + warp, i1 = min(m, x * CN_ROWS + CN_ROWS);
+        const int nr = i0 < i1 ? (i1 - i0 + CN_NW - 1) / CN_NW : 0;
+        int ra = 0, rb = 0;
+        if (lane < nr) {
+            ra = __ldg(g.row_ptr + i0 + CN_NW * lane);
+            rb = __ldg(g.row_ptr + i0 + CN_NW * lane + 1);
+        }
+        int cj_next = 0;
+        if (nr > 0) {
+            const int a0 = __shfl_sync(FULL_MASK, ra, 0), d0 = __shfl_sync(FULL_MASK, rb, 0) - a0;
+            cj_next = lane < d0 ? __ldg(g.col_idx + a0 + lane) : 0;
+        }
+        for (int q = 0; q < nr; q++) {
+            const int i = i0 + CN_NW * q;
+            const int a = __shfl_sync(FULL_MASK, ra, q), d = __shfl_sync(FULL_MASK, rb, q) - a;
+            const int cj_row = cj_next;
+            {
+                const int an = __shfl_sync(FULL_MASK, ra, (q + 1) & 31), dn = __shfl_sync(FULL_MASK, rb, (q + 1) & 31) - an;
+                cj_next = (q + 1 < nr && lane < dn) ? __ldg(g.col_idx + an + lane) : 0;
+            }
             unsigned char *Ri = RB + (size_t)i * w.rs;
             float om0[4] = {0.f, 0.f, 0.f, 0.f}, om1[4] = {0.f, 0.f, 0.f, 0.f};
             if (!FIRST) {
@@ -375,12 +395,12 @@ __global__ void __launch_bounds__(CN_T, 2) k_cn_generic(Graph g, StreamState w, 
             int nloc[4] = {0, 0, 0, 0};
             uint32_t syn[4] = {0u, 0u, 0u, 0u}, pf = 0u;
             uint32_t cws[NWK > 0 ? NWK : 1];
-            int cj = 0;
+            int cj = cj_row;
             // NWK > 0: the chunk loop is unrolled (chunk words stay in registers)
 #pragma unroll(NWK > 0 ? NWK : 1)
             for (int p0 = 0; p0 < (NWK > 0 ? 8 * NWK : d); p0 += C8) {
                 if (NWK > 0 && p0 >= d) break;
-                if ((p0 & 31) == 0) cj = (lane < d - p0) ? __ldg(g.col_idx + a + p0 + lane) : 0;
+                if (p0 > 0 && (p0 & 31) == 0) cj = (lane < d - p0) ? __ldg(g.col_idx + a + p0 + lane) : 0;
                 const bool full = p0 + C8 <= d;  // warp-uniform
                 float4 sv[C8];
                 uint32_t eb[C8];
