@@ -509,6 +509,211 @@ __global__ void __launch_bounds__(CN_T, 2) k_cn_generic(Graph g, StreamState w, 
 }
 
 // ------------------------------------------------------------------------------------------------
+// Check node with the row's loads staged by the TMA engine (cp.async.bulk, SASS UBLKCP): each warp owns
+// a ring of CNB_R row buffers in shared memory; for a row, the lane of edge p issues one 512-byte bulk
+// copy of s_j for the tile's 128 slots and lane 0 one copy of the row record (min0, min1, edge blocks),
+// all completing on the buffer's mbarrier.  While a row is computed from shared memory, the next
+// CNB_R - 1 rows are in flight, and no register holds a load across the latency.  Rows of degree <= 32.
+// ------------------------------------------------------------------------------------------------
+#ifndef CNB_W
+#define CNB_W 4  // warps per CTA
+#endif
+#ifndef CNB_R
+#define CNB_R 3  // row buffers per warp
+#endif
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(phase)
+            : "memory");
+    } while (!done);
+}
+
+template <bool FIRST, bool EARLY, int NWK>
+__global__ void __launch_bounds__(CNB_W * 32, 1)
+    k_cn_bulk(Graph g, StreamState w, int k, int literal, const int *kdev, int slot_bytes) {
+    if (kdev) k = *kdev;
+    extern __shared__ __align__(128) unsigned char cnb_smem[];
+    __shared__ __align__(8) uint64_t bars[CNB_W][CNB_R];
+    __shared__ uint32_t s_u[4];
+    __shared__ int s_item;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int cnt = w.tcount[k & 1];
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        w.tcount[(k + 1) & 1] = 0;
+        w.work[WK_BN] = 0;
+        w.ctl[CT_NSRC] = 0;
+    }
+    if (lane == 0) {
+        for (int r = 0; r < CNB_R; r++) mbar_init(&bars[warp][r], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    unsigned char *ring = cnb_smem + (size_t)warp * CNB_R * slot_bytes;
+    uint32_t phases = 0;  // bit r: parity of the next completion of buffer r
+    const int m = g.m, n = g.n;
+    const int nrb = (m + CN_ROWS - 1) / CN_ROWS;
+    const int items = cnt * nrb;
+    const float INF = __int_as_float(0x7f800000);
+    for (;;) {
+        if (EARLY && threadIdx.x < 4) s_u[threadIdx.x] = 0;
+        const int it = next_item(w.work + WK_CN, s_item);
+        if (it >= items) break;
+        const int y = it / nrb, x = it - y * nrb;
+        const int t = w.tlist[(size_t)(k & 1) * w.Tcap + y];
+        const float *__restrict__ Sb = (FIRST ? w.r : w.s) + (size_t)t * n * TILE;
+        unsigned char *RB = w.rst + (size_t)t * m * w.rs;
+        const int i0 = x * CN_ROWS + warp, i1 = min(m, x * CN_ROWS + CN_ROWS);
+        const int nr = i0 < i1 ? (i1 - i0 + CNB_W - 1) / CNB_W : 0;  // rows of this warp (<= 32)
+        int ra = 0, rb = 0;
+        if (lane < nr) {
+            ra = __ldg(g.row_ptr + i0 + CNB_W * lane);
+            rb = __ldg(g.row_ptr + i0 + CNB_W * lane + 1);
+        }
+        // issue the loads of the warp's row q into buffer q % CNB_R
+        auto issue = [&](int q) {
+            const int a = __shfl_sync(FULL_MASK, ra, q), d = __shfl_sync(FULL_MASK, rb, q) - a;
+            const int r = q % CNB_R;
+            unsigned char *buf = ring + (size_t)r * slot_bytes;
+            const int cj = lane < d ? __ldg(g.col_idx + a + lane) : 0;
+            if (lane == 0) {
+                // the buffer was last read by this warp's generic-proxy loads: order them before the copies
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_expect_tx(&bars[warp][r], (uint32_t)(d * 512 + (FIRST ? 0 : REC_EDGE0 + 32 * d)));
+            }
+            __syncwarp();
+            if (lane < d) bulk_g2s(buf + 512 * lane, Sb + (size_t)cj * TILE, 512u, &bars[warp][r]);
+            if (!FIRST && lane == 0)
+                bulk_g2s(buf + 512 * d, RB + (size_t)(i0 + CNB_W * q) * w.rs, (uint32_t)(REC_EDGE0 + 32 * d),
+                         &bars[warp][r]);
+        };
+        for (int q = 0; q < CNB_R - 1 && q < nr; q++) issue(q);
+        uint32_t u[4] = {0u, 0u, 0u, 0u};
+        for (int q = 0; q < nr; q++) {
+            if (q + CNB_R - 1 < nr) issue(q + CNB_R - 1);
+            const int r = q % CNB_R;
+            const int a = __shfl_sync(FULL_MASK, ra, q), d = __shfl_sync(FULL_MASK, rb, q) - a;
+            (void)a;
+            mbar_wait(&bars[warp][r], (phases >> r) & 1u);
+            phases ^= 1u << r;
+            const unsigned char *buf = ring + (size_t)r * slot_bytes;
+            const unsigned char *rec = buf + 512 * d;  // the staged row record
+            unsigned char *Ri = RB + (size_t)(i0 + CNB_W * q) * w.rs;
+            float om0[4] = {0.f, 0.f, 0.f, 0.f}, om1[4] = {0.f, 0.f, 0.f, 0.f};
+            if (!FIRST) {
+                const float4 A = *reinterpret_cast<const float4 *>(rec + 16 * lane);
+                const float4 B = *reinterpret_cast<const float4 *>(rec + 512 + 16 * lane);
+                om0[0] = A.x; om0[1] = A.y; om0[2] = A.z; om0[3] = A.w;
+                om1[0] = B.x; om1[1] = B.y; om1[2] = B.z; om1[3] = B.w;
+            }
+            float nm0[4] = {INF, INF, INF, INF}, nm1[4] = {INF, INF, INF, INF};
+            int nloc[4] = {0, 0, 0, 0};
+            uint32_t syn[4] = {0u, 0u, 0u, 0u}, pf = 0u;
+            uint32_t cws[NWK];
+#pragma unroll
+            for (int c = 0; c < NWK; c++) {
+                const int p0 = 8 * c;
+                if (p0 >= d) break;
+                const bool full = p0 + 8 <= d;
+                uint32_t cw = 0;
+#pragma unroll
+                for (int u8 = 0; u8 < 8; u8++) {
+                    const int p = p0 + u8;
+                    if (full || p < d) {
+                        const float4 sv = *reinterpret_cast<const float4 *>(buf + 512 * p + 16 * lane);
+                        const uint32_t eb = FIRST ? 0u : rec[REC_EDGE0 + 32 * p + lane];
+#pragma unroll
+                        for (int v = 0; v < 4; v++) {
+                            const float sj = comp(sv, v);
+                            float xv;
+                            if (FIRST) {
+                                xv = __fadd_rn(sj, 0.0f);
+                            } else {
+                                const float mag = (eb & (16u << v)) ? om1[v] : om0[v];
+                                xv = __fadd_rn(__fsub_rn(sj, flip31(mag, eb << (31 - v))), 0.0f);
+                            }
+                            const float ax = fabsf(xv);
+                            const bool lt = ax < nm0[v];  // first strict minimum (A13)
+                            nm1[v] = fminf(nm1[v], fmaxf(nm0[v], ax));
+                            nm0[v] = fminf(nm0[v], ax);
+                            nloc[v] = lt ? p : nloc[v];
+                            if (EARLY) syn[v] ^= __float_as_uint(sj);
+                            cw = __funnelshift_l(__float_as_uint(xv), cw, 1);
+                        }
+                    }
+                }
+                const int pushed = full ? 32 : 4 * (d - p0);
+                cw = pushed == 32 ? __brev(cw) : __brev(cw) >> (32 - pushed);
+                pf ^= cw;
+                cws[c] = cw;
+            }
+#pragma unroll
+            for (int c = 0; c < NWK; c++) {
+                if (8 * c < d) {
+                    uint32_t lm = 0;
+#pragma unroll
+                    for (int v = 0; v < 4; v++) {
+                        const int rr = nloc[v] - 8 * c;
+                        lm |= (rr >= 0 && rr < 8) ? (1u << (4 * rr + v)) : 0u;
+                    }
+                    const uint32_t ze = (cws[c] & 0x0f0f0f0fu) | ((lm & 0x0f0f0f0fu) << 4);
+                    const uint32_t zo = ((cws[c] >> 4) & 0x0f0f0f0fu) | (lm & 0xf0f0f0f0u);
+#pragma unroll
+                    for (int u8 = 0; u8 < 8; u8++)
+                        if (8 * c + u8 < d)
+                            Ri[REC_EDGE0 + 32 * (8 * c + u8) + lane] = (unsigned char)(((u8 & 1) ? zo : ze) >> (8 * (u8 >> 1)));
+                }
+            }
+            uint32_t pw = pf ^ (pf >> 16);
+            pw ^= pw >> 8;
+            pw ^= pw >> 4;
+            pw ^= ((uint32_t)(d & 1) & (uint32_t)(!literal)) ? 0xfu : 0u;
+            const uint32_t sb[4] = {pw << 31, (pw << 30) & 0x80000000u, (pw << 29) & 0x80000000u,
+                                    (pw << 28) & 0x80000000u};
+            st4(reinterpret_cast<float *>(Ri) + 4 * lane,
+                make_float4(__uint_as_float(__float_as_uint(nm0[0]) | sb[0]), __uint_as_float(__float_as_uint(nm0[1]) | sb[1]),
+                            __uint_as_float(__float_as_uint(nm0[2]) | sb[2]), __uint_as_float(__float_as_uint(nm0[3]) | sb[3])));
+            st4(reinterpret_cast<float *>(Ri) + 128 + 4 * lane,
+                make_float4(__uint_as_float(__float_as_uint(nm1[0]) | sb[0]), __uint_as_float(__float_as_uint(nm1[1]) | sb[1]),
+                            __uint_as_float(__float_as_uint(nm1[2]) | sb[2]), __uint_as_float(__float_as_uint(nm1[3]) | sb[3])));
+            if (EARLY) {
+                const uint32_t dp = (uint32_t)(d & 1);
+#pragma unroll
+                for (int v = 0; v < 4; v++) u[v] |= __ballot_sync(FULL_MASK, ((syn[v] >> 31) ^ dp) != 0u);
+            }
+            __syncwarp();  // every lane has read the buffer before it is refilled
+        }
+        if (EARLY) {
+            if (lane == 0) {
+#pragma unroll
+                for (int v = 0; v < 4; v++)
+                    if (u[v]) atomicOr(&s_u[v], u[v]);
+            }
+            cta_sync();
+            if (threadIdx.x < 4 && s_u[threadIdx.x])
+                atomicOr(w.unsat + ((size_t)(k & 1) * w.Tcap + t) * 4 + threadIdx.x, s_u[threadIdx.x]);
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
 // a5/a6: bit-node sweep of loop body k; stops frames whose b^(k-1) satisfied every check.
 // Item = 16 columns of one tile; a warp walks each of its columns' edges one at a time (broadcast edge
 // record, then three loads: min0, min1 -- 512 B each per warp -- and the lane's edge byte), with few
@@ -983,11 +1188,35 @@ __global__ void k_loop_step(StreamState w, int L, cudaGraphConditionalHandle h) 
 
 inline dim3 grid2(int64_t x, int y) { return dim3((unsigned)std::max<int64_t>(1, x), (unsigned)y); }
 
+// shared memory of one CTA of the bulk-staged check node (CNB_W warps x CNB_R row buffers), 0 if the
+// rows are too long for it
+size_t cn_bulk_smem(int dmax) {
+    if (dmax > 32) return 0;
+    const int ecap = dmax <= 8 ? 8 : dmax <= 16 ? 16 : 32;
+    const size_t slot = ((size_t)512 * ecap + REC_EDGE0 + 32 * ecap + 127) / 128 * 128;
+    return slot * CNB_W * CNB_R;
+}
+
+template <bool F, bool EA, int NWK>
+void cnb_launch(const Graph &g, const StreamState &w, int k, int lit, const StreamLaunch &cfg, cudaStream_t st,
+                const int *kdev) {
+    const size_t smem = cn_bulk_smem(g.dmax);
+    const int slot = (int)(smem / (CNB_W * CNB_R));
+    int per_sm = cfg.smem_per_sm > 0 ? (int)(cfg.smem_per_sm / (smem + 2048)) : 1;
+    per_sm = std::max(1, std::min(per_sm, 8));
+    cudaFuncSetAttribute(k_cn_bulk<F, EA, NWK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_cn_bulk<F, EA, NWK><<<cfg.sms * per_sm, CNB_W * 32, smem, st>>>(g, w, k, lit, kdev, slot);
+}
+
 template <bool F, bool EA>
 void cn_launch(const Graph &g, const StreamState &w, int k, int lit, const StreamLaunch &cfg, cudaStream_t st,
                const int *kdev) {
     const dim3 grid(cfg.sms * CN_MINB), gridg(cfg.sms * 2);
-    if (!cfg.cn_generic && g.dmax <= 8) {
+    if (cfg.cn_bulk && g.dmax <= 32) {
+        if (g.dmax <= 8) cnb_launch<F, EA, 1>(g, w, k, lit, cfg, st, kdev);
+        else if (g.dmax <= 16) cnb_launch<F, EA, 2>(g, w, k, lit, cfg, st, kdev);
+        else cnb_launch<F, EA, 4>(g, w, k, lit, cfg, st, kdev);
+    } else if (!cfg.cn_generic && g.dmax <= 8) {
         if (g.dmax <= 4) k_cn<4, F, EA><<<grid, CN_T, 0, st>>>(g, w, k, lit, kdev);
         else if (g.dmax <= 6) k_cn<6, F, EA><<<grid, CN_T, 0, st>>>(g, w, k, lit, kdev);
         else if (g.dmax == 7) k_cn<7, F, EA><<<grid, CN_T, 0, st>>>(g, w, k, lit, kdev);

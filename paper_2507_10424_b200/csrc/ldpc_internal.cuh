@@ -87,6 +87,8 @@ struct HostGraph {  // device allocations owned by the plan
 struct StreamLaunch {
     int sms = 148;          // persistent sweep grids are multiples of the SM count
     bool cn_generic = false;  // force the any-degree check-node kernel (tests)
+    bool cn_bulk = false;     // check node with cp.async.bulk row staging (rows of degree <= 32)
+    size_t smem_per_sm = 0;   // shared memory per SM (bytes), for the bulk kernel's grid
     bool compact = true;    // f1: compaction of tiles with fewer than half of their frames running
     int check_every = 1;    // codeword test after body k when k % T == 0 (and after body L)
 };

@@ -420,7 +420,13 @@ int finish_prepare(ldpc_plan *p, int rc, uint32_t flags, ldpc_handle_t *out) {
     cudaDeviceGetAttribute(&p->cfg.sms, cudaDevAttrMultiProcessorCount, p->device);
     if (p->cfg.sms <= 0) p->cfg.sms = 148;
     // knobs for A/B measurements and the parity tests (every variant is bit-identical)
+    {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerMultiprocessor, p->device);
+        p->cfg.smem_per_sm = (size_t)v;
+    }
     if (const char *s = getenv("LDPC_CN_GENERIC")) p->cfg.cn_generic = atoi(s) != 0;
+    if (const char *s = getenv("LDPC_CN_BULK")) p->cfg.cn_bulk = atoi(s) != 0;
     if (const char *s = getenv("LDPC_NO_COMPACT")) p->cfg.compact = atoi(s) == 0;
     if (const char *s = getenv("LDPC_NO_GRAPHS")) p->use_graphs = atoi(s) == 0;
     *out = p;

@@ -205,11 +205,11 @@ def test_graph_loop_equals_plain_launches(cfg_name, frames):
             assert np.array_equal(a, b)
 
 
-@pytest.mark.parametrize("knob", ["default", "LDPC_CN_GENERIC", "LDPC_NO_COMPACT"])
+@pytest.mark.parametrize("knob", ["default", "LDPC_CN_GENERIC", "LDPC_CN_BULK", "LDPC_NO_COMPACT"])
 def test_stream_variants(monkeypatch, knob):
     """Every kernel variant of the streaming schedule is bit-identical: the degree-specialised check node
-    (rows of degree <= 8, default) or the any-degree one (LDPC_CN_GENERIC=1); with or without the
-    compaction of sparse tiles (LDPC_NO_COMPACT=1)."""
+    (rows of degree <= 8, default), the any-degree one (LDPC_CN_GENERIC=1) or the one whose rows are staged
+    by cp.async.bulk (LDPC_CN_BULK=1); with or without the compaction of sparse tiles (LDPC_NO_COMPACT=1)."""
     if knob != "default":
         monkeypatch.setenv(knob, "1")
     cfg = codes.CONFIGS["c2"]
