@@ -360,6 +360,7 @@ def run_ours(args):
     for j in jobs:
         j["stats"].zero_()
     launches0 = sum(j["h"].launch_count for j in jobs)  # synchronises (device-side loop counters)
+    sc0 = [j["h"].stream_counters() for j in jobs] if sched == "stream" else None
     barrier(world)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -372,6 +373,7 @@ def run_ours(args):
     barrier(world)
     ms_local = e0.elapsed_time(e1)
     launches = sum(j["h"].launch_count for j in jobs) - launches0
+    sc1 = [j["h"].stream_counters() for j in jobs] if sched == "stream" else None
     ms = reduce_max(ms_local, world, dev)
     tot_stats = reduce_sum_(sum(j["stats"] for j in jobs).clone(), world).cpu().numpy()
 
@@ -413,6 +415,18 @@ def run_ours(args):
     hbm, sm_mhz, peak_src = peaks()
     roof = roofline(args, sched, prof, prof_step_ms, cn_b, bn_b, io_b, cu_sum, bu_sum, hbm, sm_mhz, peak_src, ms_local,
                     args.steps)
+    if roof is not None and sc0 is not None:
+        # live frames per swept slot: frame-bodies the method needs / (tile-bodies swept x 128 slots)
+        d = {k: sum(b[k] - a[k] for a, b in zip(sc0, sc1)) / args.steps for k in sc0[0]}
+        fe_cn = cu_sum / cl[0].nnz if len(cl) == 1 else None
+        fe_bn = bu_sum / cl[0].nnz if len(cl) == 1 else None
+        roof["occupancy"] = {
+            "check_node": round(fe_cn / (128 * d["cn_tile_bodies"]), 4) if fe_cn and d["cn_tile_bodies"] else None,
+            "bit_node": round(fe_bn / (128 * d["bn_tile_bodies"]), 4) if fe_bn and d["bn_tile_bodies"] else None,
+            "frames_moved_per_step": d["frames_moved"], "compactions_per_step": d["compactions"],
+            "what": "frame-bodies the method needs / (tile-bodies the sweep processed x 128 slots), per timed step; "
+                    "the rest is slots of stopped frames swept with their tile (compaction bounds it to < 1/2 "
+                    "per tile)"}
     value = float(reduce_sum_(torch.tensor([Fr * len(cl) * n], dtype=torch.float64, device=dev), world).item())
     value = value * args.steps / (ms / 1e3) / 1e9
 

@@ -186,12 +186,13 @@ LDPC_API int ldpc_profile_reset(ldpc_handle_t h);
 LDPC_API int64_t ldpc_launch_count(ldpc_handle_t h);
 
 /*
- * Compaction activity of the streaming schedule since the handle was created (tiles with
- * fewer than half of their frames running have those frames moved into fresh dense tiles):
- * counters[0] frames moved, [1] compactions, [2] source tiles retired.  Host output; synchronises the
- * device.  Errors: INVALID_ARG, CUDA.
+ * Work counters of the streaming schedule since the handle was created (tiles with fewer
+ * than half of their frames running have those frames moved into fresh dense tiles): counters[0] frames
+ * moved, [1] compactions, [2] source tiles retired, [3] tile-bodies swept by the check node (tiles of 128
+ * slots x loop bodies), [4] tile-bodies swept by the bit node.  Host output; synchronises the device.
+ * Errors: INVALID_ARG, CUDA.
  */
-LDPC_API int ldpc_stream_counters(ldpc_handle_t h, int64_t *counters /* [3] */);
+LDPC_API int ldpc_stream_counters(ldpc_handle_t h, int64_t *counters /* [5] */);
 
 LDPC_API void ldpc_destroy(ldpc_handle_t h);
 LDPC_API const char *ldpc_status_string(int code);

@@ -233,11 +233,13 @@ class Handle:
             _check(self._lib.ldpc_profile_reset(self._h), "ldpc_profile_reset")
 
     def stream_counters(self) -> dict:
-        """Compaction activity of the streaming schedule (frames moved, compactions, tiles retired)."""
-        c = (ctypes.c_int64 * 3)()
+        """Work counters of the streaming schedule: compaction activity (frames moved, compactions, tiles
+        retired) and the tile-bodies each sweep processed (128 slots each)."""
+        c = (ctypes.c_int64 * 5)()
         with torch.cuda.device(self.device):
             _check(self._lib.ldpc_stream_counters(self._h, c), "ldpc_stream_counters")
-        return {"frames_moved": int(c[0]), "compactions": int(c[1]), "tiles_retired": int(c[2])}
+        return {"frames_moved": int(c[0]), "compactions": int(c[1]), "tiles_retired": int(c[2]),
+                "cn_tile_bodies": int(c[3]), "bn_tile_bodies": int(c[4])}
 
     @property
     def launch_count(self) -> int:

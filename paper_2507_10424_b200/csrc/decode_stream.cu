@@ -280,6 +280,7 @@ __global__ void __launch_bounds__(CN_T, CN_MINB) k_cn(Graph g, StreamState w, in
         w.tcount[(k + 1) & 1] = 0;  // rebuilt by k_bn of body k
         w.work[WK_BN] = 0;
         w.ctl[CT_NSRC] = 0;
+        if (w.nlaunch) w.nlaunch[4] += (unsigned long long)cnt;  // tile-bodies swept by the check node
     }
     const int m = g.m, n = g.n;
     const int nrb = (m + CN_ROWS - 1) / CN_ROWS;
@@ -346,6 +347,7 @@ __global__ void __launch_bounds__(CN_T, 2) k_cn_generic(Graph g, StreamState w, 
         w.tcount[(k + 1) & 1] = 0;
         w.work[WK_BN] = 0;
         w.ctl[CT_NSRC] = 0;
+        if (w.nlaunch) w.nlaunch[4] += (unsigned long long)cnt;
     }
     const int m = g.m, n = g.n;
     const int nrb = (m + CN_ROWS - 1) / CN_ROWS;
@@ -560,6 +562,7 @@ __global__ void __launch_bounds__(CNB_W * 32, 1)
         w.tcount[(k + 1) & 1] = 0;
         w.work[WK_BN] = 0;
         w.ctl[CT_NSRC] = 0;
+        if (w.nlaunch) w.nlaunch[4] += (unsigned long long)cnt;
     }
     if (lane == 0) {
         for (int r = 0; r < CNB_R; r++) mbar_init(&bars[warp][r], 1);
@@ -745,6 +748,7 @@ __global__ void __launch_bounds__(BN_T, BN_MINB)
         w.work[WK_CN] = 0;  // next check-node sweep
         w.work[WK_MOVE] = 0;
         w.work[WK_SYN] = 0;
+        if (w.nlaunch) w.nlaunch[5] += (unsigned long long)cnt;  // tile-bodies swept by the bit node
     }
     const int m = g.m, n = g.n;
     const int ncb = (n + BN_COLS - 1) / BN_COLS;

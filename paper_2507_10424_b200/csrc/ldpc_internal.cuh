@@ -65,8 +65,9 @@ struct StreamState {
     int *work;    // [4]
     int *ctl;     // [8]
     int *csrc, *ccnt, *cmap;
-    unsigned long long *nlaunch;  // [4] handle counters: [0] graph-loop launches, [1] frames moved by
-                                  // compaction, [2] compactions, [3] tiles retired by them; or null
+    unsigned long long *nlaunch;  // [8] handle counters: [0] graph-loop launches, [1] frames moved by
+                                  // compaction, [2] compactions, [3] tiles retired by them, [4] / [5]
+                                  // tile-bodies swept by the check / bit node; or null
 };
 
 // ---- ingest (ingest.cu) ----

@@ -309,11 +309,11 @@ int decode_stream(ldpc_plan *h, const float *llr, int64_t frames, int L, uint8_t
     const bool literal = (h->flags & LDPC_FLAG_SIGN_PAPER_LITERAL) != 0;
     const Graph g = h->g.view();
     if (!h->dev_launches) {
-        if (cudaMalloc(&h->dev_launches, 4 * sizeof(unsigned long long)) != cudaSuccess) {
+        if (cudaMalloc(&h->dev_launches, 8 * sizeof(unsigned long long)) != cudaSuccess) {
             cudaGetLastError();
             return LDPC_ERR_OOM;
         }
-        if (cudaMemsetAsync(h->dev_launches, 0, 4 * sizeof(unsigned long long), st) != cudaSuccess)
+        if (cudaMemsetAsync(h->dev_launches, 0, 8 * sizeof(unsigned long long), st) != cudaSuccess)
             return LDPC_ERR_CUDA;
     }
     int64_t cap_tiles = h->chunk_cap > 0 ? (h->chunk_cap + TILE - 1) / TILE : auto_chunk_tiles(h);
@@ -683,7 +683,7 @@ int ldpc_profile_reset(ldpc_handle_t h) {
 
 int ldpc_stream_counters(ldpc_handle_t h, int64_t *counters) {
     if (!h || !counters) return LDPC_ERR_INVALID_ARG;
-    unsigned long long c[4] = {0, 0, 0, 0};
+    unsigned long long c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (h->dev_launches) {
         cudaError_t e = cudaDeviceSynchronize();
         if (e == cudaSuccess) e = cudaMemcpy(c, h->dev_launches, sizeof(c), cudaMemcpyDeviceToHost);
@@ -692,9 +692,7 @@ int ldpc_stream_counters(ldpc_handle_t h, int64_t *counters) {
             return LDPC_ERR_CUDA;
         }
     }
-    counters[0] = (int64_t)c[1];
-    counters[1] = (int64_t)c[2];
-    counters[2] = (int64_t)c[3];
+    for (int q = 0; q < 5; q++) counters[q] = (int64_t)c[q + 1];
     return LDPC_OK;
 }
 
