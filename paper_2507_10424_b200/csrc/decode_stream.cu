@@ -80,6 +80,9 @@ __device__ __forceinline__ int next_item(int *ctr, int &s_item) {
 #ifndef CN_MINB
 #define CN_MINB 3
 #endif
+#ifndef CN_SMEMU
+#define CN_SMEMU 0  // 1: syndrome ballots OR-ed into shared memory per row instead of per-item registers
+#endif
 #ifndef BN_T
 #define BN_T 128  // the bit node lives on loads in flight
 #endif
@@ -207,7 +210,7 @@ __device__ __forceinline__ void cn_fetch(CnRow<CH> &R, int cj, const float *__re
 // and makes every zero lambda +0, so its sign (sign(0) = +1) is its IEEE sign bit.
 template <int CH, bool FIRST, bool EARLY, bool FULL>
 __device__ __forceinline__ void cn_compute(const CnRow<CH> &R, unsigned char *__restrict__ Ri, int d, int literal,
-                                           int lane, uint32_t (&u)[4]) {
+                                           int lane, uint32_t (&u)[4], uint32_t *su) {
     const float INF = __int_as_float(0x7f800000);
     const float om0[4] = {R.m0.x, R.m0.y, R.m0.z, R.m0.w}, om1[4] = {R.m1.x, R.m1.y, R.m1.z, R.m1.w};
     float nm0[4] = {INF, INF, INF, INF}, nm1[4] = {INF, INF, INF, INF};
@@ -264,7 +267,14 @@ __device__ __forceinline__ void cn_compute(const CnRow<CH> &R, unsigned char *__
     if (EARLY) {
         const uint32_t dp = (uint32_t)(d & 1);  // XOR_j b_j = d_i mod 2 xor XOR_j (1 - b_j)
 #pragma unroll
-        for (int v = 0; v < 4; v++) u[v] |= __ballot_sync(FULL_MASK, ((syn[v] >> 31) ^ dp) != 0u);
+        for (int v = 0; v < 4; v++) {
+            const uint32_t bv = __ballot_sync(FULL_MASK, ((syn[v] >> 31) ^ dp) != 0u);
+            if (CN_SMEMU) {  // straight into the CTA's words (4 registers fewer across the row loop)
+                if (lane == 0 && bv) atomicOr(su + v, bv);
+            } else {
+                u[v] |= bv;
+            }
+        }
     }
 }
 
@@ -314,8 +324,8 @@ __global__ void __launch_bounds__(CN_T, CN_MINB) k_cn(Graph g, StreamState w, in
                 cn_fetch<CH, FIRST>(A, cj, Sl, Ri, lane);
                 const int d = __shfl_sync(FULL_MASK, rb, q) - __shfl_sync(FULL_MASK, ra, q);
                 cj = cols_of(q + 1);
-                if (d == CH) cn_compute<CH, FIRST, EARLY, true>(A, Ri, d, literal, lane, u);
-                else cn_compute<CH, FIRST, EARLY, false>(A, Ri, d, literal, lane, u);
+                if (d == CH) cn_compute<CH, FIRST, EARLY, true>(A, Ri, d, literal, lane, u, s_u);
+                else cn_compute<CH, FIRST, EARLY, false>(A, Ri, d, literal, lane, u, s_u);
             }
         }
         if (EARLY) {
