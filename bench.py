@@ -575,6 +575,17 @@ def run_e2e(jobs, L, args, world, dev):
             h.decode_host(hl, L, posterior=False, stats=st, out=o)
 
     step()  # warm (pipeline buffers, graphs)
+    # the host link alone: one pinned H2D copy of the step's LLRs (what e2e cannot beat when the decode is faster)
+    j0 = jobs[0]
+    scratch = torch.empty_like(j0["llr"])
+    torch.cuda.synchronize()
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    c0.record()
+    scratch.copy_(hosts[0][1], non_blocking=True)
+    c1.record()
+    torch.cuda.synchronize()
+    h2d_gbs = hosts[0][1].numel() * 4 / (c0.elapsed_time(c1) / 1e3) / 1e9
+    del scratch
     barrier(world)
     torch.cuda.synchronize()
     steps = max(1, min(args.steps, 3))
@@ -588,6 +599,8 @@ def run_e2e(jobs, L, args, world, dev):
     bits = float(world) * F * n * steps
     return {"value": round(bits / secs / 1e9, 4), "unit": "Gbit/s", "steps": steps,
             "h2d_bytes_per_step": int(F * n * 4), "d2h_bytes_per_step": int(F * n + F * 4 + F),
+            "host_link_h2d_gbs": round(h2d_gbs, 1),
+            "copy_bound_gbps": round(float(world) * F * n / (F * n * 4 / (h2d_gbs * 1e9)) / 1e9, 3),
             "api": "ldpc_decode_host over the step's batch (pinned host buffers; chunked H2D / decode / D2H "
                    "overlap; returns b, k, isCodeword and the counters)"}
 

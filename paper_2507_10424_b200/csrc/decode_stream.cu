@@ -80,6 +80,12 @@ __device__ __forceinline__ int next_item(int *ctr, int &s_item) {
 #ifndef CN_MINB
 #define CN_MINB 3
 #endif
+#ifndef CN_PF
+#define CN_PF 0  // 1: prefetch the next row's gathers and state into L1 while the current row is computed
+#endif
+#ifndef CNG_PF
+#define CNG_PF 0  // 1: any-degree check node prefetches the next chunk's gathers into L1
+#endif
 #ifndef CN_SMEMU
 #define CN_SMEMU 0  // 1: syndrome ballots OR-ed into shared memory per row instead of per-item registers
 #endif
@@ -186,6 +192,20 @@ struct CnRow {
     float4 m0, m1;
     uint32_t eb[CH];
 };
+
+__device__ __forceinline__ void pf_l1(const void *p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+
+// L1 prefetch of a row's loads (no registers held across the latency): its CH gathers and its state
+template <int CH, bool FIRST>
+__device__ __forceinline__ void cn_prefetch(int cj, const float *__restrict__ Sl, const unsigned char *__restrict__ Ri,
+                                            int lane) {
+    if (!FIRST) {
+        pf_l1(reinterpret_cast<const float *>(Ri) + 4 * lane);
+        pf_l1(reinterpret_cast<const float *>(Ri) + 128 + 4 * lane);
+    }
+#pragma unroll
+    for (int u = 0; u < CH; u++) pf_l1(Sl + (size_t)__shfl_sync(FULL_MASK, cj, u) * TILE);
+}
 
 template <int CH, bool FIRST>
 __device__ __forceinline__ void cn_fetch(CnRow<CH> &R, int cj, const float *__restrict__ Sl,
@@ -324,6 +344,7 @@ __global__ void __launch_bounds__(CN_T, CN_MINB) k_cn(Graph g, StreamState w, in
                 cn_fetch<CH, FIRST>(A, cj, Sl, Ri, lane);
                 const int d = __shfl_sync(FULL_MASK, rb, q) - __shfl_sync(FULL_MASK, ra, q);
                 cj = cols_of(q + 1);
+                if (CN_PF && q + 1 < nr) cn_prefetch<CH, FIRST>(cj, Sl, RB + (size_t)(i + CN_NW) * w.rs, lane);
                 if (d == CH) cn_compute<CH, FIRST, EARLY, true>(A, Ri, d, literal, lane, u, s_u);
                 else cn_compute<CH, FIRST, EARLY, false>(A, Ri, d, literal, lane, u, s_u);
             }
@@ -421,6 +442,15 @@ __global__ void __launch_bounds__(CN_T, 2) k_cn_generic(Graph g, StreamState w, 
                     const int j = __shfl_sync(FULL_MASK, cj, (p0 + u8) & 31);
                     sv[u8] = ld4(Sl + (size_t)j * TILE);  // unconditional: edges past d_i read column 0
                     eb[u8] = FIRST ? 0u : Ri[REC_EDGE0 + 32 * (p0 + u8) + lane];
+                }
+                if (CNG_PF) {  // the next chunk's gathers into L1 while this chunk is computed
+                    if (p0 + C8 < d && ((p0 + C8) & 31) != 0) {
+#pragma unroll
+                        for (int u8 = 0; u8 < C8; u8++) pf_l1(Sl + (size_t)__shfl_sync(FULL_MASK, cj, (p0 + C8 + u8) & 31) * TILE);
+                    } else if (p0 + C8 >= d && q + 1 < nr) {  // last chunk: the next row's first chunk
+#pragma unroll
+                        for (int u8 = 0; u8 < C8; u8++) pf_l1(Sl + (size_t)__shfl_sync(FULL_MASK, cj_next, u8) * TILE);
+                    }
                 }
                 uint32_t cw = 0;
 #pragma unroll

@@ -480,3 +480,58 @@ def test_compute_sanitizer_clean():
                            timeout=900, env=dict(os.environ, **env))
         assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
         assert "0 errors" in r.stdout or "0 hazards" in r.stdout or "0 error" in r.stdout, r.stdout[-2000:]
+
+
+def test_binding_validates_buffers():
+    """The binding refuses buffers whose shape, dtype, contiguity or device would make the C-ABI read or write
+    out of bounds (llr [F, n], out fields [F, n] / [F], stats int64[8])."""
+    P = ldpc()
+    code = codes.regular(60, 120, 3, 6, 5)
+    h = handle(code)
+    llr = torch.zeros((10, 120), dtype=torch.float32, device="cuda")
+    with pytest.raises(ValueError):
+        h.decode(torch.zeros((10, 121), dtype=torch.float32, device="cuda"), 5)
+    with pytest.raises(ValueError):
+        h.decode(llr.double(), 5)
+    with pytest.raises(ValueError):
+        h.decode(torch.zeros((120, 10), dtype=torch.float32, device="cuda").t(), 5)
+    bad = P.DecodeResult(torch.empty((9, 120), dtype=torch.uint8, device="cuda"), None, None, None)
+    with pytest.raises(ValueError):
+        h.decode(llr, 5, out=bad)
+    bad = P.DecodeResult(None, torch.empty(10, dtype=torch.int64, device="cuda"), None, None)
+    with pytest.raises(ValueError):
+        h.decode(llr, 5, out=bad)
+    bad = P.DecodeResult(None, None, None, torch.empty((10, 120), dtype=torch.float32))
+    with pytest.raises(ValueError):
+        h.decode(llr, 5, out=bad)  # posterior on the host for a device decode
+    with pytest.raises(ValueError):
+        h.decode(llr, 5, stats=torch.zeros(7, dtype=torch.int64, device="cuda"))
+    with pytest.raises(ValueError):
+        h.decode_host(torch.zeros((10, 119), dtype=torch.float32), 5)
+    with pytest.raises(ValueError):
+        h.decode_host(torch.zeros((10, 120), dtype=torch.float32), 5,
+                      out=P.DecodeResult(torch.empty((10, 120), dtype=torch.uint8, device="cuda"), None, None, None))
+    out = h.decode(llr, 5)  # and the valid call still works
+    torch.cuda.synchronize()
+    assert out.bits.shape == (10, 120)
+
+
+def test_stream_counters_and_launch_count():
+    """ldpc_launch_count includes the loop bodies the graph's conditional node ran (counted on the device):
+    a graph decode and a plain-launch decode of the same frames count the same kernels per body; the
+    tile-body counters equal the tiles x bodies swept."""
+    code = codes.regular(504, 1008, 3, 6, 1008)
+    llr = channel.bpsk_awgn(code.n, code.rate, 1.0, 3, 0, 0, 128 * 6).numpy()  # 6 tiles, every frame runs L
+    L = 12
+    counts = {}
+    for flags in (FORCE_STREAM, FORCE_STREAM | 16):
+        h = handle(code, flags | NOES)
+        l0 = h.launch_count
+        gpu_decode(h, llr, L)
+        counts[flags] = h.launch_count - l0
+        c = h.stream_counters()
+        assert c["cn_tile_bodies"] == 6 * L and c["bn_tile_bodies"] == 6 * L, c
+    # plain launches: stage-in, L x (check node, bit node, compaction plan + move), syndrome, finalize, stats
+    assert counts[FORCE_STREAM | 16] == 1 + 4 * L + 3
+    # graph: the same kernels plus the loop-control kernels (pre + one step per body after the first)
+    assert counts[FORCE_STREAM] == 1 + 4 * L + 3 + 1 + (L - 1)
