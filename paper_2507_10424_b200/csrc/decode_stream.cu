@@ -84,7 +84,7 @@ __device__ __forceinline__ int next_item(int *ctr, int &s_item) {
 #define CN_PF 0  // 1: prefetch the next row's gathers and state into L1 while the current row is computed
 #endif
 #ifndef CNG_PF
-#define CNG_PF 0  // 1: any-degree check node prefetches the next chunk's gathers into L1
+#define CNG_PF 1  // any-degree check node: the next chunk's gathers prefetched into L1 (C6: -8 %)
 #endif
 #ifndef CN_SMEMU
 #define CN_SMEMU 0  // 1: syndrome ballots OR-ed into shared memory per row instead of per-item registers
