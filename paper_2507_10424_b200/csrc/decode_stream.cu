@@ -50,6 +50,48 @@ __device__ __forceinline__ float4 ld4(const float *p) { return *reinterpret_cast
 __device__ __forceinline__ void st4(float *p, float4 v) { *reinterpret_cast<float4 *>(p) = v; }
 __device__ __forceinline__ uint4 ldu4(const uint32_t *p) { return *reinterpret_cast<const uint4 *>(p); }
 
+// L2 eviction priorities (createpolicy + .L2::cache_hint; the policy sits in the load's uniform descriptor,
+// no per-access cost).  Bit 0: data read or written once per sweep (r, s stores, the check node's row
+// records) is marked evict_first; bit 1: data gathered several times per sweep (s in the check node, row
+// records in the bit node) evict_last, so a tile's gathered working set stays in L2 while it is swept.
+// Measured (8192 frames, every frame running): bit node C4 -2.5 %, C3 equal; check node C3 +1.5 %
+// (so the check node keeps plain loads).
+#ifndef L2H_CN
+#define L2H_CN 0
+#endif
+#ifndef L2H_BN
+#define L2H_BN 3
+#endif
+__device__ __forceinline__ uint64_t pol_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t pol_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+template <int BIT, int L2H>
+__device__ __forceinline__ float4 ldh4(const float *p, uint64_t pol) {
+    if (!(L2H & BIT)) return *reinterpret_cast<const float4 *>(p);
+    float4 v;
+    asm volatile("ld.global.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+template <int BIT, int L2H>
+__device__ __forceinline__ void sth4(float *p, float4 v, uint64_t pol) {
+    if (!(L2H & BIT)) {
+        *reinterpret_cast<float4 *>(p) = v;
+        return;
+    }
+    asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
+                 "f"(v.w), "l"(pol)
+                 : "memory");
+}
+
 // the sign of a magnitude picked by Obs. 1 flipped by one stored sign bit (already moved to bit 31)
 __device__ __forceinline__ float flip31(float mag, uint32_t bit31) {
     return __uint_as_float(__float_as_uint(mag) ^ (bit31 & 0x80000000u));
@@ -209,17 +251,17 @@ __device__ __forceinline__ void cn_prefetch(int cj, const float *__restrict__ Sl
 
 template <int CH, bool FIRST>
 __device__ __forceinline__ void cn_fetch(CnRow<CH> &R, int cj, const float *__restrict__ Sl,
-                                         const unsigned char *__restrict__ Ri, int lane) {
+                                         const unsigned char *__restrict__ Ri, int lane, uint64_t pf, uint64_t pl) {
     if (!FIRST) {
-        R.m0 = ld4(reinterpret_cast<const float *>(Ri) + 4 * lane);
-        R.m1 = ld4(reinterpret_cast<const float *>(Ri) + 128 + 4 * lane);
+        R.m0 = ldh4<1, L2H_CN>(reinterpret_cast<const float *>(Ri) + 4 * lane, pf);
+        R.m1 = ldh4<1, L2H_CN>(reinterpret_cast<const float *>(Ri) + 128 + 4 * lane, pf);
 #pragma unroll
         for (int p = 0; p < CH; p++) R.eb[p] = Ri[REC_EDGE0 + 32 * p + lane];
     }
 #pragma unroll
     for (int u = 0; u < CH; u++) {
         const int j = __shfl_sync(FULL_MASK, cj, u);
-        R.sv[u] = ld4(Sl + (size_t)j * TILE);
+        R.sv[u] = ldh4<2, L2H_CN>(Sl + (size_t)j * TILE, pl);
     }
 }
 
@@ -230,7 +272,7 @@ __device__ __forceinline__ void cn_fetch(CnRow<CH> &R, int cj, const float *__re
 // and makes every zero lambda +0, so its sign (sign(0) = +1) is its IEEE sign bit.
 template <int CH, bool FIRST, bool EARLY, bool FULL>
 __device__ __forceinline__ void cn_compute(const CnRow<CH> &R, unsigned char *__restrict__ Ri, int d, int literal,
-                                           int lane, uint32_t (&u)[4], uint32_t *su) {
+                                           int lane, uint32_t (&u)[4], uint32_t *su, uint64_t pf) {
     const float INF = __int_as_float(0x7f800000);
     const float om0[4] = {R.m0.x, R.m0.y, R.m0.z, R.m0.w}, om1[4] = {R.m1.x, R.m1.y, R.m1.z, R.m1.w};
     float nm0[4] = {INF, INF, INF, INF}, nm1[4] = {INF, INF, INF, INF};
@@ -270,12 +312,14 @@ __device__ __forceinline__ void cn_compute(const CnRow<CH> &R, unsigned char *__
     pw ^= ((uint32_t)(d & 1) & (uint32_t)(!literal)) ? 0xfu : 0u;
     const uint32_t s0 = pw << 31, s1 = (pw << 30) & 0x80000000u, s2 = (pw << 29) & 0x80000000u,
                    s3 = (pw << 28) & 0x80000000u;
-    st4(reinterpret_cast<float *>(Ri) + 4 * lane,
-        make_float4(__uint_as_float(__float_as_uint(nm0[0]) | s0), __uint_as_float(__float_as_uint(nm0[1]) | s1),
-                    __uint_as_float(__float_as_uint(nm0[2]) | s2), __uint_as_float(__float_as_uint(nm0[3]) | s3)));
-    st4(reinterpret_cast<float *>(Ri) + 128 + 4 * lane,
-        make_float4(__uint_as_float(__float_as_uint(nm1[0]) | s0), __uint_as_float(__float_as_uint(nm1[1]) | s1),
-                    __uint_as_float(__float_as_uint(nm1[2]) | s2), __uint_as_float(__float_as_uint(nm1[3]) | s3)));
+    sth4<1, L2H_CN>(reinterpret_cast<float *>(Ri) + 4 * lane,
+            make_float4(__uint_as_float(__float_as_uint(nm0[0]) | s0), __uint_as_float(__float_as_uint(nm0[1]) | s1),
+                        __uint_as_float(__float_as_uint(nm0[2]) | s2), __uint_as_float(__float_as_uint(nm0[3]) | s3)),
+            pf);
+    sth4<1, L2H_CN>(reinterpret_cast<float *>(Ri) + 128 + 4 * lane,
+            make_float4(__uint_as_float(__float_as_uint(nm1[0]) | s0), __uint_as_float(__float_as_uint(nm1[1]) | s1),
+                        __uint_as_float(__float_as_uint(nm1[2]) | s2), __uint_as_float(__float_as_uint(nm1[3]) | s3)),
+            pf);
     // edge bytes: sign nibble | isloc nibble << 4.  lm has bit 4p+v set iff min0Location of slot v is p;
     // interleaving the nibbles of sw and lm gives the bytes of the even edges in ze, of the odd ones in zo
     const uint32_t lm = (1u << (4 * nloc[0])) | (2u << (4 * nloc[1])) | (4u << (4 * nloc[2])) | (8u << (4 * nloc[3]));
@@ -315,6 +359,7 @@ __global__ void __launch_bounds__(CN_T, CN_MINB) k_cn(Graph g, StreamState w, in
     const int m = g.m, n = g.n;
     const int nrb = (m + CN_ROWS - 1) / CN_ROWS;
     const int items = cnt * nrb;
+    const uint64_t pf = (L2H_CN & 1) ? pol_first() : 0, pl = (L2H_CN & 2) ? pol_last() : 0;
     for (;;) {
         if (EARLY && threadIdx.x < 4) s_u[threadIdx.x] = 0;
         const int it = next_item(w.work + WK_CN, s_item);
@@ -341,12 +386,12 @@ __global__ void __launch_bounds__(CN_T, CN_MINB) k_cn(Graph g, StreamState w, in
             for (int q = 0; q < nr; q++) {
                 const int i = i0 + CN_NW * q;
                 unsigned char *Ri = RB + (size_t)i * w.rs;
-                cn_fetch<CH, FIRST>(A, cj, Sl, Ri, lane);
+                cn_fetch<CH, FIRST>(A, cj, Sl, Ri, lane, pf, pl);
                 const int d = __shfl_sync(FULL_MASK, rb, q) - __shfl_sync(FULL_MASK, ra, q);
                 cj = cols_of(q + 1);
                 if (CN_PF && q + 1 < nr) cn_prefetch<CH, FIRST>(cj, Sl, RB + (size_t)(i + CN_NW) * w.rs, lane);
-                if (d == CH) cn_compute<CH, FIRST, EARLY, true>(A, Ri, d, literal, lane, u, s_u);
-                else cn_compute<CH, FIRST, EARLY, false>(A, Ri, d, literal, lane, u, s_u);
+                if (d == CH) cn_compute<CH, FIRST, EARLY, true>(A, Ri, d, literal, lane, u, s_u, pf);
+                else cn_compute<CH, FIRST, EARLY, false>(A, Ri, d, literal, lane, u, s_u, pf);
             }
         }
         if (EARLY) {
@@ -772,6 +817,23 @@ __global__ void __launch_bounds__(CNB_W * 32, 1)
 #define BN_CM1 0  // 1: load min1 only where the edge is a min0Location of the lane (fewer L2 bytes, measured slower)
 #endif
 
+#ifndef BN_PF
+// how the bit node finds an edge's row record (A/B, 8192 frames, every frame running, C3 / C4 ms per 20 / 10 bodies):
+// 3 = per-edge offset records (Graph::bn_off, 32-byte units; one IMAD.WIDE per address, 37 instead of 42
+//     instructions per warp-edge): 14.57 / 30.82 against 15.27 / 32.15 for 0 = the {e, i, p} records;
+// 1 = the next column's edge list prefetched into lanes: slower (fewer warps or spills);
+// 2 = the next edge's record loaded one edge ahead: equal to 0.
+#define BN_PF 3
+#endif
+
+#ifndef BN_U2
+#define BN_U2 0  // BN_PF 3: two edges of a column per step (more loads in flight, more registers)
+#endif
+
+#ifndef BN_RVLATE
+#define BN_RVLATE 0  // 1: r of the column loaded after its edges (4 registers fewer across the edge loop)
+#endif
+
 #ifndef BN_DYN
 #define BN_DYN 1  // items from the work counter (keeps the tiles in flight together for L2 reuse)
 #endif
@@ -794,6 +856,7 @@ __global__ void __launch_bounds__(BN_T, BN_MINB)
     const int ncb = (n + BN_COLS - 1) / BN_COLS;
     const int items = cnt * ncb;
     const bool compact_ok = EARLY && compact && k + 2 <= L;
+    const uint64_t pf = (L2H_BN & 1) ? pol_first() : 0, pl = (L2H_BN & 2) ? pol_last() : 0;
     for (int it0 = blockIdx.x;; it0 += gridDim.x) {
         const int it = BN_DYN ? next_item(w.work + WK_BN, s_item) : it0;
         if (it >= items) break;
@@ -842,12 +905,130 @@ __global__ void __launch_bounds__(BN_T, BN_MINB)
         const unsigned mine = ((act.x >> lane) & 1u) | (((act.y >> lane) & 1u) << 1) | (((act.z >> lane) & 1u) << 2) |
                               (((act.w >> lane) & 1u) << 3);
         const unsigned char *RB = w.rst + (size_t)t * m * w.rs;
-        const float *__restrict__ Rl = w.r + (size_t)t * n * TILE + 4 * lane;
-        float *__restrict__ Sl = w.s + (size_t)t * n * TILE + 4 * lane;
+        const size_t tb = (size_t)t * n * TILE + 4 * lane;  // r and s of the tile (one offset, two bases)
         const int j1 = min(n, x * BN_COLS + BN_COLS);
+#if BN_PF == 1
+        // The edge list of the warp's next column is loaded into lanes (lane p: row and in-row position of
+        // edge p) while the current column runs, so every row-state gather of an edge is issued without
+        // waiting for its edge record (the round-2 profile: 22 % of the stalls sat on that dependent load).
+        const int jb = x * BN_COLS;
+        const int cpv = (lane <= BN_COLS && jb + lane <= n) ? __ldg(g.col_ptr + jb + lane) : 0;
+        const int nq = jb + warp < j1 ? (j1 - jb - warp + BN_T / 32 - 1) / (BN_T / 32) : 0;
+        auto col_edges = [&](int q, int &dv) {
+            const int c = warp + (BN_T / 32) * q;
+            const int c0 = __shfl_sync(FULL_MASK, cpv, c & 31);
+            dv = q < nq ? __shfl_sync(FULL_MASK, cpv, (c + 1) & 31) - c0 : 0;
+            int2 e = make_int2(0, 0);
+            if (lane < dv) {  // {e, i, p, -} of edge `lane` (ascending i): only i and p are loaded
+                const int *ed = reinterpret_cast<const int *>(g.bn_edge + c0 + lane);
+                e = make_int2(__ldg(ed + 1), __ldg(ed + 2));
+            }
+            return e;
+        };
+        int dvn;
+        int2 en = col_edges(0, dvn);
+        for (int q = 0; q < nq; q++) {
+            const int j = jb + warp + (BN_T / 32) * q;
+            const int dv = dvn;
+            int2 ec = en;
+            en = col_edges(q + 1, dvn);
+#if !BN_RVLATE
+            const float4 rv = ldh4<1, L2H_BN>(w.r + tb + (size_t)j * TILE, pf);
+#endif
+            float acc[4] = {0.f, 0.f, 0.f, 0.f};
+            for (int e0 = 0; e0 < dv; e0 += 32) {
+                if (e0 > 0) {  // columns of degree > 32: the next 32 edges
+                    ec = make_int2(0, 0);
+                    const int c0 = __shfl_sync(FULL_MASK, cpv, j - jb);
+                    if (lane < dv - e0) {
+                        const int *ed = reinterpret_cast<const int *>(g.bn_edge + c0 + e0 + lane);
+                        ec = make_int2(__ldg(ed + 1), __ldg(ed + 2));
+                    }
+                }
+                const int ne = min(32, dv - e0);
+#pragma unroll 1
+                for (int u = 0; u < ne; u++) {  // ascending row order from +0.0 (A14)
+                    const unsigned char *Ri = RB + (size_t)__shfl_sync(FULL_MASK, ec.x, u) * w.rs;
+                    const float4 m0 = ldh4<2, L2H_BN>(reinterpret_cast<const float *>(Ri) + 4 * lane, pl);
+                    const float4 m1 = ldh4<2, L2H_BN>(reinterpret_cast<const float *>(Ri) + 128 + 4 * lane, pl);
+                    const uint32_t b = Ri[REC_EDGE0 + 32 * __shfl_sync(FULL_MASK, ec.y, u) + lane];
+#pragma unroll
+                    for (int v = 0; v < 4; v++) {
+                        const float mag = (b & (16u << v)) ? comp(m1, v) : comp(m0, v);  // Obs. 1
+                        acc[v] = acc[v] + flip31(mag, b << (31 - v));
+                    }
+                }
+            }
+#elif BN_PF == 3
+        // per-edge offset records (Graph::bn_off, 32-byte units): one IMAD.WIDE per gather address, the
+        // record pointer advanced by 8 bytes per edge
+        const unsigned char *RBm = RB + 16 * lane, *RBb = RB + lane;
         for (int j = x * BN_COLS + warp; j < j1; j += BN_T / 32) {
             const int c0 = __ldg(g.col_ptr + j), dv = __ldg(g.col_ptr + j + 1) - c0;
-            const float4 rv = ld4(Rl + (size_t)j * TILE);
+            const float4 rv = ldh4<1, L2H_BN>(w.r + tb + (size_t)j * TILE, pf);
+            float acc[4] = {0.f, 0.f, 0.f, 0.f};
+            const int2 *op = g.bn_off + c0;  // ascending i (A14)
+            int q = 0;
+#if BN_U2
+            for (; q + 1 < dv; q += 2, op += 2) {  // two edges' gathers in flight, summed in order
+                const int2 o0 = __ldg(op), o1 = __ldg(op + 1);
+                const float *Ra = reinterpret_cast<const float *>(RBm + ((size_t)(unsigned)o0.x << 5));
+                const float *Rb = reinterpret_cast<const float *>(RBm + ((size_t)(unsigned)o1.x << 5));
+                const float4 a0 = ldh4<2, L2H_BN>(Ra, pl), a1 = ldh4<2, L2H_BN>(Ra + 128, pl);
+                const float4 b0 = ldh4<2, L2H_BN>(Rb, pl), b1 = ldh4<2, L2H_BN>(Rb + 128, pl);
+                const uint32_t ba = RBb[(size_t)(unsigned)o0.y << 5], bb = RBb[(size_t)(unsigned)o1.y << 5];
+#pragma unroll
+                for (int v = 0; v < 4; v++) {
+                    acc[v] = acc[v] + flip31((ba & (16u << v)) ? comp(a1, v) : comp(a0, v), ba << (31 - v));
+                    acc[v] = acc[v] + flip31((bb & (16u << v)) ? comp(b1, v) : comp(b0, v), bb << (31 - v));
+                }
+            }
+#endif
+#pragma unroll 1
+            for (; q < dv; q++, op++) {
+                const int2 o = __ldg(op);
+                const float *Rm = reinterpret_cast<const float *>(RBm + ((size_t)(unsigned)o.x << 5));
+                const float4 m0 = ldh4<2, L2H_BN>(Rm, pl);
+                const float4 m1 = ldh4<2, L2H_BN>(Rm + 128, pl);
+                const uint32_t b = RBb[(size_t)(unsigned)o.y << 5];
+#pragma unroll
+                for (int v = 0; v < 4; v++) {
+                    const float mag = (b & (16u << v)) ? comp(m1, v) : comp(m0, v);  // Obs. 1
+                    acc[v] = acc[v] + flip31(mag, b << (31 - v));
+                }
+            }
+#elif BN_PF == 2
+        // one edge ahead: the record of edge q+1 is loaded after the row-state gathers of edge q
+        for (int j = x * BN_COLS + warp; j < j1; j += BN_T / 32) {
+            const int c0 = __ldg(g.col_ptr + j), dv = __ldg(g.col_ptr + j + 1) - c0;
+            const float4 rv = ldh4<1, L2H_BN>(w.r + tb + (size_t)j * TILE, pf);
+            float acc[4] = {0.f, 0.f, 0.f, 0.f};
+            const int *edp = reinterpret_cast<const int *>(g.bn_edge + c0);  // {e, i, p, -}, ascending i
+            int ni = 0, np = 0;
+            if (dv > 0) {
+                ni = __ldg(edp + 1);
+                np = __ldg(edp + 2);
+            }
+#pragma unroll 1
+            for (int q = 0; q < dv; q++) {
+                const unsigned char *Ri = RB + (size_t)ni * w.rs;
+                const float4 m0 = ldh4<2, L2H_BN>(reinterpret_cast<const float *>(Ri) + 4 * lane, pl);
+                const float4 m1 = ldh4<2, L2H_BN>(reinterpret_cast<const float *>(Ri) + 128 + 4 * lane, pl);
+                const uint32_t b = Ri[REC_EDGE0 + 32 * np + lane];
+                if (q + 1 < dv) {
+                    ni = __ldg(edp + 4 * (q + 1) + 1);
+                    np = __ldg(edp + 4 * (q + 1) + 2);
+                }
+#pragma unroll
+                for (int v = 0; v < 4; v++) {
+                    const float mag = (b & (16u << v)) ? comp(m1, v) : comp(m0, v);  // Obs. 1
+                    acc[v] = acc[v] + flip31(mag, b << (31 - v));
+                }
+            }
+#else
+        for (int j = x * BN_COLS + warp; j < j1; j += BN_T / 32) {
+            const int c0 = __ldg(g.col_ptr + j), dv = __ldg(g.col_ptr + j + 1) - c0;
+            const float4 rv = ldh4<1, L2H_BN>(w.r + tb + (size_t)j * TILE, pf);
             float acc[4] = {0.f, 0.f, 0.f, 0.f};
             for (int q0 = 0; q0 < dv; q0 += BN_G) {
                 // all loads of up to BN_G edges in flight together (past the column's last edge: its last edge
@@ -858,10 +1039,15 @@ __global__ void __launch_bounds__(BN_T, BN_MINB)
                 for (int u = 0; u < BN_G; u++) {
                     const int4 ed = __ldg(g.bn_edge + c0 + min(q0 + u, dv - 1));  // {e, i, p, -}, ascending i
                     const unsigned char *Ri = RB + (size_t)ed.y * w.rs;
-                    m0[u] = ld4(reinterpret_cast<const float *>(Ri) + 4 * lane);
+                    m0[u] = ldh4<2, L2H_BN>(reinterpret_cast<const float *>(Ri) + 4 * lane, pl);
+#ifdef BN_XP  // timing experiments only (wrong results): 1 = no min1 gather, 2 = no edge-byte gather
+                    b[u] = BN_XP == 2 ? (uint32_t)(ed.z * 0x11) : Ri[REC_EDGE0 + 32 * ed.z + lane];
+                    m1[u] = BN_XP == 1 ? m0[u] : ldh4<2, L2H_BN>(reinterpret_cast<const float *>(Ri) + 128 + 4 * lane, pl);
+#else
                     b[u] = Ri[REC_EDGE0 + 32 * ed.z + lane];
-                    if (!BN_CM1 || (b[u] & 0xf0u)) m1[u] = ld4(reinterpret_cast<const float *>(Ri) + 128 + 4 * lane);
+                    if (!BN_CM1 || (b[u] & 0xf0u)) m1[u] = ldh4<2, L2H_BN>(reinterpret_cast<const float *>(Ri) + 128 + 4 * lane, pl);
                     else m1[u] = m0[u];
+#endif
                 }
 #pragma unroll
                 for (int u = 0; u < BN_G; u++) {
@@ -874,11 +1060,15 @@ __global__ void __launch_bounds__(BN_T, BN_MINB)
                     }
                 }
             }
-            float *o = Sl + (size_t)j * TILE;
+#endif
+#if BN_PF == 1 && BN_RVLATE
+            const float4 rv = ldh4<1, L2H_BN>(w.r + tb + (size_t)j * TILE, pf);
+#endif
+            float *o = w.s + tb + (size_t)j * TILE;
             const float n0 = zneg(acc[0] + rv.x), n1 = zneg(acc[1] + rv.y), n2 = zneg(acc[2] + rv.z),
                         n3 = zneg(acc[3] + rv.w);  // zeros of s kept as -0 (A12)
             if (mine == 0xFu) {
-                st4(o, make_float4(n0, n1, n2, n3));
+                sth4<1, L2H_BN>(o, make_float4(n0, n1, n2, n3), pf);
             } else if (k == 1) {  // body 1: frames that stopped at the pre-check keep s = r
                 st4(o, make_float4((mine & 1u) ? n0 : rv.x, (mine & 2u) ? n1 : rv.y, (mine & 4u) ? n2 : rv.z,
                                    (mine & 8u) ? n3 : rv.w));
@@ -890,6 +1080,13 @@ __global__ void __launch_bounds__(BN_T, BN_MINB)
             }
         }
     }
+}
+
+__global__ void k_bn_offsets(const int4 *__restrict__ bn_edge, int E, int rs32, int2 *__restrict__ out) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= E) return;
+    const int4 ed = bn_edge[q];  // {e, i, p, d_i & 1}
+    out[q] = make_int2(ed.y * rs32, ed.y * rs32 + REC_EDGE0 / 32 + ed.z);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -1279,6 +1476,11 @@ void cn_launch(const Graph &g, const StreamState &w, int k, int lit, const Strea
 int edge_capacity(int dmax, bool generic) {
     if (!generic && dmax <= 8) return dmax <= 4 ? 4 : dmax <= 6 ? 6 : dmax == 7 ? 7 : 8;
     return (dmax + 7) / 8 * 8;
+}
+
+int launch_bn_offsets(const Graph &g, int rs, int2 *out, cudaStream_t st) {
+    k_bn_offsets<<<(g.E + 255) / 256, 256, 0, st>>>(g.bn_edge, g.E, rs / 32, out);
+    return 1;
 }
 
 int launch_stage_in(const Graph &g, const StreamState &w, const float *llr, int64_t frames, cudaStream_t st) {

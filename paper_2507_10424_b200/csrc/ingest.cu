@@ -251,9 +251,10 @@ struct Builder {
 }  // namespace
 
 void HostGraph::free_all() {
-    cudaFree(row_ptr); cudaFree(col_idx); cudaFree(col_ptr); cudaFree(col_edge); cudaFree(bn_edge);
+    cudaFree(row_ptr); cudaFree(col_idx); cudaFree(col_ptr); cudaFree(col_edge); cudaFree(bn_edge); cudaFree(bn_off);
     row_ptr = col_idx = col_ptr = col_edge = nullptr;
     bn_edge = nullptr;
+    bn_off = nullptr;
 }
 
 int ingest_dense(const uint8_t *H, int m, int n, cudaStream_t st, HostGraph *hg) {

@@ -23,6 +23,8 @@ struct Graph {
     const int *col_idx;  // [E]     ascending within a row
     const int *col_ptr;  // [n+1]   M_j = bn_edge[col_ptr[j] .. col_ptr[j+1])
     const int4 *bn_edge; // [E]     {edge id e (row-list position), row i, position p in N_i, d_i & 1}
+    const int2 *bn_off;  // [E]     streaming bit node, same order: {i * rs / 32, (i * rs + REC_EDGE0 + 32 p) / 32}
+                         //         (row record and edge block of the edge, in 32-byte units inside a tile)
     int wr;              // sign words per row and lane in the streaming layout: ceil(max row degree / 8)
     int dmax;            // max row degree
     int dvmax;           // max column degree
@@ -79,8 +81,11 @@ struct HostGraph {  // device allocations owned by the plan
     int m = 0, n = 0, E = 0, max_row_deg = 0, max_col_deg = 0;
     int *row_ptr = nullptr, *col_idx = nullptr, *col_ptr = nullptr, *col_edge = nullptr;
     int4 *bn_edge = nullptr;
+    int2 *bn_off = nullptr;  // filled at prepare once the row-record size is known (launch_bn_offsets)
     int64_t launches = 0;
-    Graph view() const { return Graph{m, n, E, row_ptr, col_idx, col_ptr, bn_edge, (max_row_deg + 7) / 8, max_row_deg, max_col_deg}; }
+    Graph view() const {
+        return Graph{m, n, E, row_ptr, col_idx, col_ptr, bn_edge, bn_off, (max_row_deg + 7) / 8, max_row_deg, max_col_deg};
+    }
     void free_all();
 };
 
@@ -96,6 +101,8 @@ struct StreamLaunch {
 // edge blocks per row record for a maximum row degree (the check-node instance reads CH of them)
 int edge_capacity(int dmax, bool generic);
 // Launch helpers; each returns the number of kernels launched.
+// the streaming bit node's per-edge record offsets for row records of rs bytes (rs % 32 == 0)
+int launch_bn_offsets(const Graph &g, int rs, int2 *out, cudaStream_t st);
 int launch_stage_in(const Graph &g, const StreamState &w, const float *llr, int64_t frames, cudaStream_t st);
 int launch_check_node(const Graph &g, const StreamState &w, int k, bool first, bool early, bool literal,
                       const StreamLaunch &cfg, cudaStream_t st, const int *kdev = nullptr);

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cstdlib>
 #include <cstring>
 #include <new>
@@ -407,7 +408,7 @@ void mark_last(ldpc_plan *h, cudaStream_t st) {
     h->last_recorded = cudaEventRecord(h->last, st) == cudaSuccess;
 }
 
-int finish_prepare(ldpc_plan *p, int rc, uint32_t flags, ldpc_handle_t *out) {
+int finish_prepare(ldpc_plan *p, int rc, uint32_t flags, ldpc_handle_t *out, cudaStream_t st) {
     if (rc != LDPC_OK) {
         p->g.free_all();
         delete p;
@@ -429,6 +430,25 @@ int finish_prepare(ldpc_plan *p, int rc, uint32_t flags, ldpc_handle_t *out) {
     if (const char *s = getenv("LDPC_CN_BULK")) p->cfg.cn_bulk = atoi(s) != 0;
     if (const char *s = getenv("LDPC_NO_COMPACT")) p->cfg.compact = atoi(s) == 0;
     if (const char *s = getenv("LDPC_NO_GRAPHS")) p->use_graphs = atoi(s) == 0;
+    // the streaming bit node's edge records need the row-record size (in 32-byte units: fits int32 for any
+    // workspace that fits the device)
+    if (p->g.E > 0) {
+        const int rs = row_record_bytes(p);
+        if ((int64_t)p->g.m * (rs / 32) >= INT32_MAX ||
+            cudaMalloc(&p->g.bn_off, sizeof(int2) * (size_t)p->g.E) != cudaSuccess) {
+            cudaGetLastError();
+            p->g.free_all();
+            delete p;
+            return LDPC_ERR_OOM;
+        }
+        p->launches += launch_bn_offsets(p->g.view(), rs, p->g.bn_off, st);
+        if (cudaStreamSynchronize(st) != cudaSuccess) {
+            cudaGetLastError();
+            p->g.free_all();
+            delete p;
+            return LDPC_ERR_CUDA;
+        }
+    }
     *out = p;
     return LDPC_OK;
 }
@@ -460,7 +480,7 @@ int ldpc_prepare_dense(const uint8_t *H, int32_t m, int32_t n, uint32_t flags, l
     ldpc_plan *p = new (std::nothrow) ldpc_plan;
     if (!p) return LDPC_ERR_OOM;
     int rc = ingest_dense(H, m, n, static_cast<cudaStream_t>(stream), &p->g);
-    return finish_prepare(p, rc, flags, out);
+    return finish_prepare(p, rc, flags, out, static_cast<cudaStream_t>(stream));
 }
 
 int ldpc_prepare_coo(const int32_t *rows, const int32_t *cols, int64_t nnz, int32_t m, int32_t n, uint32_t flags,
@@ -469,7 +489,7 @@ int ldpc_prepare_coo(const int32_t *rows, const int32_t *cols, int64_t nnz, int3
     ldpc_plan *p = new (std::nothrow) ldpc_plan;
     if (!p) return LDPC_ERR_OOM;
     int rc = ingest_coo(rows, cols, nnz, m, n, static_cast<cudaStream_t>(stream), &p->g);
-    return finish_prepare(p, rc, flags, out);
+    return finish_prepare(p, rc, flags, out, static_cast<cudaStream_t>(stream));
 }
 
 int ldpc_decode(ldpc_handle_t h, const float *llr, int64_t frames, int32_t max_iter, uint8_t *bits_out,
