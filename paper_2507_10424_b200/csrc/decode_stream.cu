@@ -92,6 +92,17 @@ __device__ __forceinline__ void sth4(float *p, float4 v, uint64_t pol) {
                  : "memory");
 }
 
+// min(a, b, c) in one FMNMX3 (sm_100)
+__device__ __forceinline__ float fmin3f(float a, float b, float c) {
+    float d;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+
+#ifndef CN_PAIR
+#define CN_PAIR 1  // check node: edges in pairs (FMNMX3 second-minimum update, 3-input parity XOR)
+#endif
+
 // the sign of a magnitude picked by Obs. 1 flipped by one stored sign bit (already moved to bit 31)
 __device__ __forceinline__ float flip31(float mag, uint32_t bit31) {
     return __uint_as_float(__float_as_uint(mag) ^ (bit31 & 0x80000000u));
@@ -278,6 +289,51 @@ __device__ __forceinline__ void cn_compute(const CnRow<CH> &R, unsigned char *__
     float nm0[4] = {INF, INF, INF, INF}, nm1[4] = {INF, INF, INF, INF};
     int nloc[4] = {0, 0, 0, 0};
     uint32_t syn[4] = {0u, 0u, 0u, 0u}, sw = 0;  // sw: sign bits pushed in (p, v) order
+#if CN_PAIR
+    // Edges in pairs (p, p+1): the pair's smaller and larger |lambda| (s, t) update the row state with
+    //   nm0' = min(nm0, s), nm1' = min3(nm1, max(nm0, s), t) (FMNMX3), loc' = s < nm0 ? (t-edge < s-edge ?
+    //   p+1 : p) : loc -- the same first strict minimum (A13) and second minimum as the edge-by-edge update,
+    // in 9 instead of 10 ALU operations per pair and slot; the decision parity takes both edges in one
+    // 3-input XOR.  An edge past d_i enters as |lambda| = +inf and parity 0 (it changes nothing).
+#pragma unroll
+    for (int p = 0; p < CH; p += 2) {
+        const bool va = FULL || p < d, vb = p + 1 < CH && (FULL || p + 1 < d);
+        if (!va) continue;
+        const uint32_t ba = FIRST ? 0u : R.eb[p], bb = (FIRST || p + 1 >= CH) ? 0u : R.eb[p + 1];
+        float xa[4], xb[4];
+#pragma unroll
+        for (int v = 0; v < 4; v++) {
+            const float sa = comp(R.sv[p], v);
+            const float sb = p + 1 < CH ? comp(R.sv[p + 1], v) : 0.f;
+            if (FIRST) {
+                xa[v] = __fadd_rn(sa, 0.0f);  // eta^prev = 0
+                xb[v] = __fadd_rn(sb, 0.0f);
+            } else {
+                const float ma = (ba & (16u << v)) ? om1[v] : om0[v];  // Obs. 1 (+ row parity)
+                const float mb = (bb & (16u << v)) ? om1[v] : om0[v];
+                xa[v] = __fadd_rn(__fsub_rn(sa, flip31(ma, ba << (31 - v))), 0.0f);  // lambda - eta^prev
+                xb[v] = __fadd_rn(__fsub_rn(sb, flip31(mb, bb << (31 - v))), 0.0f);
+            }
+            if (EARLY) syn[v] ^= __float_as_uint(sa) ^ (vb ? __float_as_uint(sb) : 0u);  // bit 31: slice(s_j) == 0
+        }
+#pragma unroll
+        for (int v = 0; v < 4; v++) sw = __funnelshift_l(__float_as_uint(xa[v]), sw, 1);
+        if (vb) {
+#pragma unroll
+            for (int v = 0; v < 4; v++) sw = __funnelshift_l(__float_as_uint(xb[v]), sw, 1);
+        }
+#pragma unroll
+        for (int v = 0; v < 4; v++) {
+            const float a = fabsf(xa[v]), b = vb ? fabsf(xb[v]) : INF;
+            const float sm = fminf(a, b), tm = fmaxf(a, b);
+            const int lp = b < a ? p + 1 : p;
+            const bool lt = sm < nm0[v];
+            nm1[v] = fmin3f(nm1[v], fmaxf(nm0[v], sm), tm);
+            nm0[v] = fminf(nm0[v], sm);
+            nloc[v] = lt ? lp : nloc[v];
+        }
+    }
+#else
 #pragma unroll
     for (int p = 0; p < CH; p++) {
         if (FULL || p < d) {
@@ -302,6 +358,7 @@ __device__ __forceinline__ void cn_compute(const CnRow<CH> &R, unsigned char *__
             }
         }
     }
+#endif
     // bit 4p+v of sw = sign of lambda (edge p, slot 4l+v)
     if (FULL) sw = CH == 8 ? __brev(sw) : __brev(sw) >> (32 - 4 * CH);
     else sw = __brev(sw) >> (32 - 4 * d);
@@ -822,7 +879,9 @@ __global__ void __launch_bounds__(CNB_W * 32, 1)
 // 3 = per-edge offset records (Graph::bn_off, 32-byte units; one IMAD.WIDE per address, 37 instead of 42
 //     instructions per warp-edge): 14.57 / 30.82 against 15.27 / 32.15 for 0 = the {e, i, p} records;
 // 1 = the next column's edge list prefetched into lanes: slower (fewer warps or spills);
-// 2 = the next edge's record loaded one edge ahead: equal to 0.
+// 2 = the next edge's record loaded one edge ahead: equal to 0;
+// (measured and removed: row state staged through shared memory with cp.async, 3-8 edges in flight per
+//  warp, parity-green but 40-55 % slower.)
 #define BN_PF 3
 #endif
 
@@ -837,6 +896,26 @@ __global__ void __launch_bounds__(CNB_W * 32, 1)
 #ifndef BN_DYN
 #define BN_DYN 1  // items from the work counter (keeps the tiles in flight together for L2 reuse)
 #endif
+
+// s of one column for this lane's 4 slots: new values for the running frames, r for frames stopped at
+// the pre-check (body 1), untouched for frozen frames; zeros kept as -0 (A12)
+__device__ __forceinline__ void bn_store(float *o, const float (&acc)[4], float4 rv, unsigned mine, int k,
+                                         uint64_t pf) {
+    const float n0 = zneg(acc[0] + rv.x), n1 = zneg(acc[1] + rv.y), n2 = zneg(acc[2] + rv.z),
+                n3 = zneg(acc[3] + rv.w);
+    if (mine == 0xFu) {
+        sth4<1, L2H_BN>(o, make_float4(n0, n1, n2, n3), pf);
+    } else if (k == 1) {  // body 1: frames that stopped at the pre-check keep s = r
+        st4(o, make_float4((mine & 1u) ? n0 : rv.x, (mine & 2u) ? n1 : rv.y, (mine & 4u) ? n2 : rv.z,
+                           (mine & 8u) ? n3 : rv.w));
+    } else if (mine) {  // frozen frames keep their s
+        if (mine & 1u) o[0] = n0;
+        if (mine & 2u) o[1] = n1;
+        if (mine & 4u) o[2] = n2;
+        if (mine & 8u) o[3] = n3;
+    }
+}
+
 
 template <bool EARLY>
 __global__ void __launch_bounds__(BN_T, BN_MINB)
@@ -1064,20 +1143,7 @@ __global__ void __launch_bounds__(BN_T, BN_MINB)
 #if BN_PF == 1 && BN_RVLATE
             const float4 rv = ldh4<1, L2H_BN>(w.r + tb + (size_t)j * TILE, pf);
 #endif
-            float *o = w.s + tb + (size_t)j * TILE;
-            const float n0 = zneg(acc[0] + rv.x), n1 = zneg(acc[1] + rv.y), n2 = zneg(acc[2] + rv.z),
-                        n3 = zneg(acc[3] + rv.w);  // zeros of s kept as -0 (A12)
-            if (mine == 0xFu) {
-                sth4<1, L2H_BN>(o, make_float4(n0, n1, n2, n3), pf);
-            } else if (k == 1) {  // body 1: frames that stopped at the pre-check keep s = r
-                st4(o, make_float4((mine & 1u) ? n0 : rv.x, (mine & 2u) ? n1 : rv.y, (mine & 4u) ? n2 : rv.z,
-                                   (mine & 8u) ? n3 : rv.w));
-            } else if (mine) {  // frozen frames keep their s
-                if (mine & 1u) o[0] = n0;
-                if (mine & 2u) o[1] = n1;
-                if (mine & 4u) o[2] = n2;
-                if (mine & 8u) o[3] = n3;
-            }
+            bn_store(w.s + tb + (size_t)j * TILE, acc, rv, mine, k, pf);
         }
     }
 }
