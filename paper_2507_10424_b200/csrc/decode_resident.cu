@@ -103,6 +103,17 @@ __device__ __forceinline__ void f4s(float4 &a, int v, float x) {
 // lambda = s - (+-0) has the magnitude and sign() of s, s being -0 rather than +0 for zero).
 // sgw: this lane's sign words of row i (sgw[q * LR] = edges 8q..8q+7): read as eta^prev's signs and
 // overwritten with the new ones (each lane owns its words: no ballot, no synchronisation).
+#ifndef RES_PAIR
+#define RES_PAIR 1  // check-node pass: edges in pairs (see cn_rows)
+#endif
+
+// min(a, b, c) in one FMNMX3 (sm_100)
+__device__ __forceinline__ float fmin3f(float a, float b, float c) {
+    float d;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+
 __device__ __forceinline__ float flip31(float mag, uint32_t bit31) {
     return __uint_as_float(__float_as_uint(mag) ^ (bit31 & 0x80000000u));
 }
@@ -136,6 +147,59 @@ __device__ __forceinline__ void cn_rows(const float *__restrict__ s, float *mn0,
     // edges) is bit-reversed into the stored layout (bit 4(p%8)+v)
     uint32_t wo = valid ? sgw[0] : 0u, wn = 0u, pf = 0u;  // old / new sign word of the current 8 edges
     const int pe = DC > 0 ? DC : dmax;
+#if RES_PAIR
+    // Edges in pairs (p, p+1; p even, so a pair never straddles a sign word): the pair's smaller and
+    // larger |lambda| (sm, tm) update the row state with nm0' = min(nm0, sm), nm1' = min3(nm1, max(nm0, sm),
+    // tm) (FMNMX3) and loc' = sm < nm0 ? (b < a ? p+1 : p) : loc -- the same first strict minimum (A13)
+    // and second minimum as the edge-by-edge update in fewer ALU operations; the decision parity takes
+    // both edges in one 3-input XOR.  An absent edge enters as |lambda| = +inf, sign bit 0, parity 0.
+#pragma unroll(DC > 0 ? (DC + 1) / 2 : 1)
+    for (int p = 0; p < pe; p += 2) {
+        if ((DC == 0 || DC > 8) && p > 0 && (p & 7) == 0) {  // next sign word of the row
+            wn = __brev(wn);
+            if (valid) sgw[((p >> 3) - 1) * LR] = wn;
+            pf ^= wn;
+            wn = 0u;
+            wo = valid ? sgw[(p >> 3) * LR] : 0u;
+        }
+        const bool inb = p + 1 < pe;
+        const bool ha = HAS ? (p < d) : true, hb = inb && (HAS ? (p + 1 < d) : true);
+        const int ja = ha ? col[ra + p] : 0, jb = hb ? col[ra + p + 1] : 0;
+        const uint32_t ppa = (uint32_t)p * 0x01010101u, ppb = (uint32_t)(p + 1) * 0x01010101u;
+        const float4 sva = *reinterpret_cast<const float4 *>(s + ja * S + q0);
+        const float4 svb = *reinterpret_cast<const float4 *>(s + jb * S + q0);
+        const uint32_t la = olc ^ ppa, lb = olc ^ ppb;
+        const float mga[4] = {(la & 0xffu) ? om0.x : om1.x, (la & 0xff00u) ? om0.y : om1.y,
+                              (la & 0xff0000u) ? om0.z : om1.z, (la & 0xff000000u) ? om0.w : om1.w};  // Obs. 1
+        const float mgb[4] = {(lb & 0xffu) ? om0.x : om1.x, (lb & 0xff00u) ? om0.y : om1.y,
+                              (lb & 0xff0000u) ? om0.z : om1.z, (lb & 0xff000000u) ? om0.w : om1.w};
+        float xa[4], xb[4];
+#pragma unroll
+        for (int v = 0; v < 4; v++) {
+            const int sha = 4 * (p & 7) + v, shb = 4 * ((p + 1) & 7) + v;
+            const float sa = f4c(sva, v), sb = f4c(svb, v);
+            xa[v] = __fadd_rn(__fsub_rn(sa, flip31(mga[v], wo << (31 - sha))), 0.0f);
+            xb[v] = __fadd_rn(__fsub_rn(sb, flip31(mgb[v], wo << (31 - shb))), 0.0f);
+            synw[v] ^= (ha ? __float_as_uint(sa) : 0u) ^ (hb ? __float_as_uint(sb) : 0u);  // slice(s_j) = 0 iff sign bit
+        }
+#pragma unroll
+        for (int v = 0; v < 4; v++) wn = __funnelshift_l(ha ? __float_as_uint(xa[v]) : 0u, wn, 1);
+        if (inb) {
+#pragma unroll
+            for (int v = 0; v < 4; v++) wn = __funnelshift_l(hb ? __float_as_uint(xb[v]) : 0u, wn, 1);
+        }
+#pragma unroll
+        for (int v = 0; v < 4; v++) {
+            const float a = ha ? fabsf(xa[v]) : INF, b = hb ? fabsf(xb[v]) : INF;
+            const float sm = fminf(a, b), tm = fmaxf(a, b);
+            const int lp = b < a ? p + 1 : p;
+            const bool lt = sm < nm0[v];
+            nm1[v] = fmin3f(nm1[v], fmaxf(nm0[v], sm), tm);
+            nm0[v] = fminf(nm0[v], sm);
+            nloc[v] = lt ? lp : nloc[v];
+        }
+    }
+#else
     // DC > 0: every row has degree DC (regular code) -- the edge loop is fully unrolled
 #pragma unroll(DC > 0 ? DC : 2)
     for (int p = 0; p < pe; p++) {
@@ -170,6 +234,7 @@ __device__ __forceinline__ void cn_rows(const float *__restrict__ s, float *mn0,
             synw[v] ^= (HAS ? has : true) ? __float_as_uint(sj) : 0u;  // slice(s_j) = 0 iff sign bit
         }
     }
+#endif
     {
         const int pushed = 4 * (((pe - 1) & 7) + 1);  // slot-edges in the last word
         wn = pushed == 32 ? __brev(wn) : __brev(wn) >> (32 - pushed);
