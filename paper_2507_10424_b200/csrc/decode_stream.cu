@@ -555,6 +555,46 @@ __global__ void __launch_bounds__(CN_T, 2) k_cn_generic(Graph g, StreamState w, 
                     }
                 }
                 uint32_t cw = 0;
+#if CN_PAIR
+#pragma unroll
+                for (int u8 = 0; u8 < C8; u8 += 2) {  // edge pairs, as in cn_compute
+                    const int p = p0 + u8;
+                    const bool va = full || p < d, vb = full || p + 1 < d;
+                    if (va) {
+                        float xa[4], xb[4];
+#pragma unroll
+                        for (int v = 0; v < 4; v++) {
+                            const float sa = comp(sv[u8], v), sb = comp(sv[u8 + 1], v);
+                            if (FIRST) {
+                                xa[v] = __fadd_rn(sa, 0.0f);
+                                xb[v] = __fadd_rn(sb, 0.0f);
+                            } else {
+                                const float ma = (eb[u8] & (16u << v)) ? om1[v] : om0[v];
+                                const float mb = (eb[u8 + 1] & (16u << v)) ? om1[v] : om0[v];
+                                xa[v] = __fadd_rn(__fsub_rn(sa, flip31(ma, eb[u8] << (31 - v))), 0.0f);
+                                xb[v] = __fadd_rn(__fsub_rn(sb, flip31(mb, eb[u8 + 1] << (31 - v))), 0.0f);
+                            }
+                            if (EARLY) syn[v] ^= __float_as_uint(sa) ^ (vb ? __float_as_uint(sb) : 0u);
+                        }
+#pragma unroll
+                        for (int v = 0; v < 4; v++) cw = __funnelshift_l(__float_as_uint(xa[v]), cw, 1);
+                        if (vb) {
+#pragma unroll
+                            for (int v = 0; v < 4; v++) cw = __funnelshift_l(__float_as_uint(xb[v]), cw, 1);
+                        }
+#pragma unroll
+                        for (int v = 0; v < 4; v++) {
+                            const float a = fabsf(xa[v]), b = vb ? fabsf(xb[v]) : INF;
+                            const float sm = fminf(a, b), tm = fmaxf(a, b);
+                            const int lp = b < a ? p + 1 : p;
+                            const bool lt = sm < nm0[v];
+                            nm1[v] = fmin3f(nm1[v], fmaxf(nm0[v], sm), tm);
+                            nm0[v] = fminf(nm0[v], sm);
+                            nloc[v] = lt ? lp : nloc[v];
+                        }
+                    }
+                }
+#else
 #pragma unroll
                 for (int u8 = 0; u8 < C8; u8++) {
                     const int p = p0 + u8;
@@ -579,6 +619,7 @@ __global__ void __launch_bounds__(CN_T, 2) k_cn_generic(Graph g, StreamState w, 
                         }
                     }
                 }
+#endif
                 const int pushed = full ? 32 : 4 * (d - p0);
                 cw = pushed == 32 ? __brev(cw) : __brev(cw) >> (32 - pushed);  // bit 4u+v: edge p0+u, slot 4l+v
                 pf ^= cw;
