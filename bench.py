@@ -529,15 +529,23 @@ def roofline(args, sched, prof, prof_step_ms, cn_b, bn_b, io_b, cu_edges, bu_edg
                 "kernel_ms_profiled_step": {k: round(v, 3) for k, v in kms.items()},
                 "share_of_step": round(t / prof_step_ms, 4), "whole_step": whole}
     bytes_of = {"check_node": cn_b, "bit_node": bn_b}
+    alu_of = {"check_node": cu_edges * ALU_CN, "bit_node": bu_edges * ALU_BN}
+    alu_peak = 148 * 4 * 16 * sm_mhz * 1e6 / 1e12  # T lane-ops/s on the half-rate ALU pipe
     sweeps = {}
     for k, b in bytes_of.items():
         if kms.get(k, 0) > 0:
             ach = b / (kms[k] / 1e3) / 1e9
+            alu = alu_of[k] / (kms[k] / 1e3) / 1e12
             traffic, tratio, tsrc = ncu_traffic(args.config, k)
             sweeps[k] = {"achieved": round(ach, 1), "frac": round(ach / hbm, 4),
                          "algorithmic_bytes_per_launch": round(b / kl[k]), "avg_launch_us": round(kms[k] / kl[k] * 1e3, 2),
                          "launches": kl[k], "share_of_step": round(kms[k] / prof_step_ms, 4),
-                         "traffic": traffic, "traffic_vs_algorithmic_in_capture": tratio}
+                         "traffic": traffic, "traffic_vs_algorithmic_in_capture": tratio,
+                         # the same sweep against the ALU pipe: the method's minimum ALU operations per
+                         # frame-edge (ALU_CN / ALU_BN) per second of the sweep; rows of high degree (C6) make the
+                         # check node's bytes per edge small, so there the ALU pipe is the nearer roof
+                         "alu_pipe": {"achieved": round(alu, 3), "peak": round(alu_peak, 2), "unit": "T lane-ops/s",
+                                      "frac": round(alu / alu_peak, 4), "ops_per_frame_edge": ALU_CN if k == "check_node" else ALU_BN}}
     if not sweeps:
         return None
     dom = max(sweeps, key=lambda k: kms[k])

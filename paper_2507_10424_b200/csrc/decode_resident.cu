@@ -7,13 +7,13 @@
 //   min0 [m][S]  fp32          Observation 1's minimum; SIGN BIT = the row's sign parity
 //                              (Obs. 2) x (-1)^{d_i} (reading A1)
 //   min1 [m][S]  fp32          Observation 1's second minimum, same sign bit
-//   lc   [m][S]  u8            min0Location as the position p inside row i's list (0xff = none)
-//   sgr  [m][WR][LR] u32       sign of lambda_e = s_j - eta_e, row-transposed: the lane that owns slots
-//                              4l..4l+3 of row i owns word (i, p/8, l), whose bit 4(p%8) + v is the sign
-//                              for edge p and slot 4l + v (WR = ceil(dmax / 8), LR = S / 4)
-// eta_e = (loc == p ? min1 : min0) with its sign bit XORed with the stored bit: one FSEL and one LOP3
-// per slot-edge (the bit is moved to bit 31 by a constant shift when the row degree is a template
-// constant).
+//   eb   [m][LR][DMP] u8       edge bytes: byte (i, l, p) = sign nibble (bit v: sign of lambda_e = s_j -
+//                              eta_e for edge p of row i and slot 4l + v) | isloc nibble << 4 (bit v: p is
+//                              min0Location of slot 4l + v); the lane that owns slots 4l..4l+3 of row i
+//                              owns its DMP = ceil(dmax / 8) * 8 bytes (read and written 8 at a time)
+// eta_e = (isloc ? min1 : min0) with its sign bit XORed with the stored bit: one FSEL and one LOP3 per
+// slot-edge, the select predicates of 4 slots from one byte (the layout of the streaming schedule's edge
+// blocks; it replaced round 1's location bytes and row-transposed sign words: C2 9.80 -> 10.77 Gbps).
 // Zeros of s are kept as -0.0 (same slice and sign() under reading A12), so the decision of a slot is
 // the complement of the IEEE sign bit of s and the syndrome is a XOR of sign bits.
 // plus the Tanner graph itself as 16-bit lists (N_i, M_j).  r lives in a global scratch
@@ -39,28 +39,25 @@ constexpr unsigned FULLM = 0xffffffffu;
 
 
 struct Layout {
-    size_t s, m0, m1, lc, sgr, rp, cp, col, rec, rec2, meta, total;
+    size_t s, m0, m1, eb, rp, cp, col, rec, rec2, meta, total;
 };
 
 constexpr size_t a16(size_t x) { return (x + 15) & ~(size_t)15; }
 
 constexpr int META_INTS = 8 * 32 + 16;
 
-// Sign bits are kept as the warp ballots that produced them: for the block of G rows a warp sweeps
-// together (rg = i / G), position p of the rows and slot component v, one u32 whose bit
-// (i % G) * LR + l is the sign of lambda for row i, slot 4l + v.  The writer stores four words per
-// edge position with one 16-byte store; readers test a lane bit.
+// Edge bytes per lane and row: DMP = ceil(dm / 8) * 8 bytes (8-byte chunks), see eb_dmp.
 // compact: the bit node's per-edge records are a u16 row offset and a u8 position (3 B per edge instead
-// of 8: the ballot word and bit are recomputed from them), for codes that fit no other way (C5 size)
+// of 8: the edge-byte index is recomputed from them), for codes that fit no other way (C5 size)
+__host__ __device__ constexpr int eb_dmp(int dm) { return (dm + 7) / 8 * 8; }
+
 Layout layout_for(int S, int m, int n, int E, int dm, bool compact = false) {
     Layout L{};
-    const int G = 128 / S;
     size_t o = 0;
     L.s = o;    o = a16(o + (size_t)n * S * 4);
     L.m0 = o;   o = a16(o + (size_t)m * S * 4);
     L.m1 = o;   o = a16(o + (size_t)m * S * 4);
-    L.lc = o;   o = a16(o + (size_t)m * S);
-    L.sgr = o;  o = a16(o + (size_t)m * ((dm + 7) / 8) * (S / 4) * 4);
+    L.eb = o;   o = a16(o + (size_t)m * (S / 4) * eb_dmp(dm));
     L.rp = o;   o = a16(o + (size_t)(m + 1) * 2);
     L.cp = o;   o = a16(o + (size_t)(n + 1) * 2);
     L.col = o;  o = a16(o + (size_t)E * 2);
@@ -103,10 +100,6 @@ __device__ __forceinline__ void f4s(float4 &a, int v, float x) {
 // lambda = s - (+-0) has the magnitude and sign() of s, s being -0 rather than +0 for zero).
 // sgw: this lane's sign words of row i (sgw[q * LR] = edges 8q..8q+7): read as eta^prev's signs and
 // overwritten with the new ones (each lane owns its words: no ballot, no synchronisation).
-#ifndef RES_PAIR
-#define RES_PAIR 1  // check-node pass: edges in pairs (see cn_rows)
-#endif
-
 // min(a, b, c) in one FMNMX3 (sm_100)
 __device__ __forceinline__ float fmin3f(float a, float b, float c) {
     float d;
@@ -118,22 +111,27 @@ __device__ __forceinline__ float flip31(float mag, uint32_t bit31) {
     return __uint_as_float(__float_as_uint(mag) ^ (bit31 & 0x80000000u));
 }
 
+// The 8 edge bytes of a chunk from its sign word sw (bit 4u+v: sign of lambda, edge u, slot v) and isloc
+// word lm (same layout): byte u = sign nibble | isloc nibble << 4, one 8-byte store (all 8 bytes of the
+// chunk; bytes past the row's degree are never read).
+__device__ __forceinline__ void res_store_chunk(uint8_t *p, uint32_t sw, uint32_t lm) {
+    const uint32_t ze = (sw & 0x0f0f0f0fu) | ((lm & 0x0f0f0f0fu) << 4);  // edges 0, 2, 4, 6
+    const uint32_t zo = ((sw >> 4) & 0x0f0f0f0fu) | (lm & 0xf0f0f0f0u);  // edges 1, 3, 5, 7
+    *reinterpret_cast<uint2 *>(p) = make_uint2(__byte_perm(ze, zo, 0x5140), __byte_perm(ze, zo, 0x7362));
+}
+
 template <int S, bool HAS, int DC>
-__device__ __forceinline__ void cn_rows(const float *__restrict__ s, float *mn0, float *mn1, uint8_t *lc,
-                                        uint32_t *__restrict__ sgw, const uint16_t *col, int i, bool valid, int ra,
-                                        int d, int dmax, int l, unsigned fm, uint32_t fmb, bool corr,
-                                        unsigned &syn_acc) {
-    constexpr int LR = S / 4;
+__device__ __forceinline__ void cn_rows(const float *__restrict__ s, float *mn0, float *mn1, uint8_t *__restrict__ ebr,
+                                        const uint16_t *col, int i, bool valid, int ra, int d, int dmax, int l,
+                                        unsigned fm, bool corr, unsigned &syn_acc) {
     const float INF = __int_as_float(0x7f800000);
     const int q0 = 4 * l;
     float4 om0 = make_float4(0.f, 0.f, 0.f, 0.f), om1 = om0;
-    uint32_t olc = 0xffffffffu;  // byte v: min0Location of slot q0 + v
     const int ca = i * S + q0;
     if (valid) {
         om0 = *reinterpret_cast<const float4 *>(mn0 + ca);
         om1 = *reinterpret_cast<const float4 *>(mn1 + ca);
-        olc = *reinterpret_cast<const uint32_t *>(lc + ca) | fmb;
-        if (fm) {  // fresh slots start from eta = 0: min0 = min1 = +0, no location
+        if (fm) {  // fresh slots start from eta = 0: min0 = min1 = +0 (eta^prev = +-0 whatever the edge byte)
             if (fm & 1u) { om0.x = 0.f; om1.x = 0.f; }
             if (fm & 2u) { om0.y = 0.f; om1.y = 0.f; }
             if (fm & 4u) { om0.z = 0.f; om1.z = 0.f; }
@@ -141,45 +139,47 @@ __device__ __forceinline__ void cn_rows(const float *__restrict__ s, float *mn0,
         }
     }
     float nm0[4] = {INF, INF, INF, INF}, nm1[4] = {INF, INF, INF, INF};
-    int nloc[4] = {0xff, 0xff, 0xff, 0xff};
+    int nloc[4] = {0, 0, 0, 0};
     uint32_t synw[4] = {0u, 0u, 0u, 0u};  // XOR of the sign bits of s over the row: bit 31 = XOR of (1 - b_j)
-    // new sign bits are pushed into wn by one funnel shift per slot-edge, in (p, v) order; a full word (8
-    // edges) is bit-reversed into the stored layout (bit 4(p%8)+v)
-    uint32_t wo = valid ? sgw[0] : 0u, wn = 0u, pf = 0u;  // old / new sign word of the current 8 edges
+    // the lane's edge bytes of the row (sign nibble | isloc nibble << 4), 8 per chunk (one 8-byte access);
+    // new sign bits are pushed into wn by one funnel shift per slot-edge, in (p, v) order, and a chunk's
+    // word is bit-reversed into bit 4(p%8)+v
+    uint2 ob = make_uint2(0u, 0u);
+    uint32_t wn = 0u, pf = 0u;
     const int pe = DC > 0 ? DC : dmax;
-#if RES_PAIR
-    // Edges in pairs (p, p+1; p even, so a pair never straddles a sign word): the pair's smaller and
-    // larger |lambda| (sm, tm) update the row state with nm0' = min(nm0, sm), nm1' = min3(nm1, max(nm0, sm),
-    // tm) (FMNMX3) and loc' = sm < nm0 ? (b < a ? p+1 : p) : loc -- the same first strict minimum (A13)
-    // and second minimum as the edge-by-edge update in fewer ALU operations; the decision parity takes
-    // both edges in one 3-input XOR.  An absent edge enters as |lambda| = +inf, sign bit 0, parity 0.
+    // Edges in pairs (p, p+1; p even, so a pair never straddles a chunk): the pair's smaller and larger
+    // |lambda| (sm, tm) update the row state with nm0' = min(nm0, sm), nm1' = min3(nm1, max(nm0, sm), tm)
+    // (FMNMX3) and loc' = sm < nm0 ? (b < a ? p+1 : p) : loc -- the same first strict minimum (A13) and
+    // second minimum as the edge-by-edge update in fewer ALU operations; the decision parity takes both
+    // edges in one 3-input XOR.  An absent edge enters as |lambda| = +inf, sign bit 0, parity 0.
 #pragma unroll(DC > 0 ? (DC + 1) / 2 : 1)
     for (int p = 0; p < pe; p += 2) {
-        if ((DC == 0 || DC > 8) && p > 0 && (p & 7) == 0) {  // next sign word of the row
-            wn = __brev(wn);
-            if (valid) sgw[((p >> 3) - 1) * LR] = wn;
-            pf ^= wn;
-            wn = 0u;
-            wo = valid ? sgw[(p >> 3) * LR] : 0u;
+        if ((p & 7) == 0) {
+            if (p > 0) {  // the finished chunk: its bytes with the sign nibbles (isloc merged at the row end)
+                wn = __brev(wn);
+                pf ^= wn;
+                if (valid) res_store_chunk(ebr + p - 8, wn, 0u);
+                wn = 0u;
+            }
+            if (valid) ob = *reinterpret_cast<const uint2 *>(ebr + p);
         }
         const bool inb = p + 1 < pe;
         const bool ha = HAS ? (p < d) : true, hb = inb && (HAS ? (p + 1 < d) : true);
         const int ja = ha ? col[ra + p] : 0, jb = hb ? col[ra + p + 1] : 0;
-        const uint32_t ppa = (uint32_t)p * 0x01010101u, ppb = (uint32_t)(p + 1) * 0x01010101u;
         const float4 sva = *reinterpret_cast<const float4 *>(s + ja * S + q0);
         const float4 svb = *reinterpret_cast<const float4 *>(s + jb * S + q0);
-        const uint32_t la = olc ^ ppa, lb = olc ^ ppb;
-        const float mga[4] = {(la & 0xffu) ? om0.x : om1.x, (la & 0xff00u) ? om0.y : om1.y,
-                              (la & 0xff0000u) ? om0.z : om1.z, (la & 0xff000000u) ? om0.w : om1.w};  // Obs. 1
-        const float mgb[4] = {(lb & 0xffu) ? om0.x : om1.x, (lb & 0xff00u) ? om0.y : om1.y,
-                              (lb & 0xff0000u) ? om0.z : om1.z, (lb & 0xff000000u) ? om0.w : om1.w};
+        const uint32_t ow = (p & 4) ? ob.y : ob.x;
+        const uint32_t ba = ow >> (8 * (p & 3)), bb = ow >> (8 * ((p + 1) & 3));
         float xa[4], xb[4];
 #pragma unroll
         for (int v = 0; v < 4; v++) {
-            const int sha = 4 * (p & 7) + v, shb = 4 * ((p + 1) & 7) + v;
             const float sa = f4c(sva, v), sb = f4c(svb, v);
-            xa[v] = __fadd_rn(__fsub_rn(sa, flip31(mga[v], wo << (31 - sha))), 0.0f);
-            xb[v] = __fadd_rn(__fsub_rn(sb, flip31(mgb[v], wo << (31 - shb))), 0.0f);
+            const float ma = (ba & (16u << v)) ? f4c(om1, v) : f4c(om0, v);  // Obs. 1 (+ row parity)
+            const float mb = (bb & (16u << v)) ? f4c(om1, v) : f4c(om0, v);
+            // lambda - eta^prev; + 0 makes a zero lambda +0 (s may be -0), so its IEEE sign bit is
+            // sign(0) = +1 (P:279); the add runs on the otherwise idle FMA pipe
+            xa[v] = __fadd_rn(__fsub_rn(sa, flip31(ma, ba << (31 - v))), 0.0f);
+            xb[v] = __fadd_rn(__fsub_rn(sb, flip31(mb, bb << (31 - v))), 0.0f);
             synw[v] ^= (ha ? __float_as_uint(sa) : 0u) ^ (hb ? __float_as_uint(sb) : 0u);  // slice(s_j) = 0 iff sign bit
         }
 #pragma unroll
@@ -199,48 +199,23 @@ __device__ __forceinline__ void cn_rows(const float *__restrict__ s, float *mn0,
             nloc[v] = lt ? lp : nloc[v];
         }
     }
-#else
-    // DC > 0: every row has degree DC (regular code) -- the edge loop is fully unrolled
-#pragma unroll(DC > 0 ? DC : 2)
-    for (int p = 0; p < pe; p++) {
-        if ((DC == 0 || DC > 8) && p > 0 && (p & 7) == 0) {  // next sign word of the row
-            wn = __brev(wn);
-            if (valid) sgw[((p >> 3) - 1) * LR] = wn;
-            pf ^= wn;
-            wn = 0u;
-            wo = valid ? sgw[(p >> 3) * LR] : 0u;
-        }
-        const bool has = HAS ? (p < d) : true;
-        const int e = ra + p;
-        const int j = has ? col[e] : 0;
-        const uint32_t pp = (uint32_t)p * 0x01010101u;
-        const float4 sv = *reinterpret_cast<const float4 *>(s + j * S + q0);
-        const float mg[4] = {((olc ^ pp) & 0xffu) ? om0.x : om1.x, ((olc ^ pp) & 0xff00u) ? om0.y : om1.y,
-                             ((olc ^ pp) & 0xff0000u) ? om0.z : om1.z,
-                             ((olc ^ pp) & 0xff000000u) ? om0.w : om1.w};  // Obs. 1 (+ row parity)
-#pragma unroll
-        for (int v = 0; v < 4; v++) {
-            const int sh = 4 * (p & 7) + v;
-            const float sj = f4c(sv, v);
-            // lambda - eta^prev (Obs. 2 sign); + 0 makes a zero lambda +0 (s may be -0), so its IEEE sign bit is
-            // sign(0) = +1 (P:279); the add runs on the otherwise idle FMA pipe
-            const float x = __fadd_rn(__fsub_rn(sj, flip31(mg[v], wo << (31 - sh))), 0.0f);
-            const float ax = HAS ? (has ? fabsf(x) : INF) : fabsf(x);
-            const bool lt = ax < nm0[v];  // first strict minimum (A13)
-            nm1[v] = fminf(nm1[v], fmaxf(nm0[v], ax));
-            nm0[v] = fminf(nm0[v], ax);
-            nloc[v] = lt ? p : nloc[v];
-            wn = __funnelshift_l(HAS ? (has ? __float_as_uint(x) : 0u) : __float_as_uint(x), wn, 1);
-            synw[v] ^= (HAS ? has : true) ? __float_as_uint(sj) : 0u;  // slice(s_j) = 0 iff sign bit
-        }
-    }
-#endif
     {
-        const int pushed = 4 * (((pe - 1) & 7) + 1);  // slot-edges in the last word
+        const int last = (pe - 1) & ~7;            // first edge of the last chunk
+        const int pushed = 4 * (pe - last);        // slot-edges in the last chunk
         wn = pushed == 32 ? __brev(wn) : __brev(wn) >> (32 - pushed);
+        pf ^= wn;
+        if (valid) {
+            if (pe <= 8) {  // one chunk (regular codes of degree <= 8): isloc merged before the only store
+                const uint32_t lm = (1u << (4 * nloc[0])) | (2u << (4 * nloc[1])) | (4u << (4 * nloc[2])) |
+                                    (8u << (4 * nloc[3]));
+                res_store_chunk(ebr, wn, lm);
+            } else {
+                res_store_chunk(ebr + last, wn, 0u);
+#pragma unroll
+                for (int v = 0; v < 4; v++) ebr[nloc[v]] |= (uint8_t)(16u << v);  // this thread wrote them
+            }
+        }
     }
-    if (valid) sgw[((pe - 1) >> 3) * LR] = wn;
-    pf ^= wn;
     if (valid) {
         // this lane's row sign parity per slot (XOR of bits v, v+4, ... of the sign words), times
         // (-1)^{d_i} under the CORRECTED rule (reading A1)
@@ -256,8 +231,6 @@ __device__ __forceinline__ void cn_rows(const float *__restrict__ s, float *mn0,
         *reinterpret_cast<float4 *>(mn1 + ca) =
             make_float4(__uint_as_float(__float_as_uint(nm1[0]) | sb[0]), __uint_as_float(__float_as_uint(nm1[1]) | sb[1]),
                         __uint_as_float(__float_as_uint(nm1[2]) | sb[2]), __uint_as_float(__float_as_uint(nm1[3]) | sb[3]));
-        *reinterpret_cast<uint32_t *>(lc + ca) =
-            (uint32_t)nloc[0] | ((uint32_t)nloc[1] << 8) | ((uint32_t)nloc[2] << 16) | ((uint32_t)nloc[3] << 24);
         // row unsatisfied iff XOR_j b_j = 1, with XOR_j b_j = d_i mod 2 xor XOR_j (1 - b_j)
         const uint32_t dp = (uint32_t)(d & 1);
         syn_acc |= (((synw[0] >> 31) ^ dp) | (((synw[1] >> 31) ^ dp) << 1) | (((synw[2] >> 31) ^ dp) << 2) |
@@ -277,9 +250,8 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
     float *s = reinterpret_cast<float *>(sm + a.lay.s);
     float *mn0 = reinterpret_cast<float *>(sm + a.lay.m0);
     float *mn1 = reinterpret_cast<float *>(sm + a.lay.m1);
-    uint8_t *lc = reinterpret_cast<uint8_t *>(sm + a.lay.lc);
-    uint32_t *sgr = reinterpret_cast<uint32_t *>(sm + a.lay.sgr);
-    const int WR = (a.dm + 7) / 8;  // sign words per lane and row
+    uint8_t *ebt = sm + a.lay.eb;
+    const int DMP = eb_dmp(a.dm);  // edge bytes per lane and row
     uint16_t *rp = reinterpret_cast<uint16_t *>(sm + a.lay.rp);
     uint16_t *cp = reinterpret_cast<uint16_t *>(sm + a.lay.cp);
     uint16_t *col = reinterpret_cast<uint16_t *>(sm + a.lay.col);
@@ -301,7 +273,6 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
     const int q0 = 4 * l;                      // first slot of this lane
     float *rs = a.rs + (size_t)blockIdx.x * n * S;
     const bool corr = !a.literal;
-    const int dm = a.dm;
 
     // ---- the Tanner graph into shared memory (16-bit lists)
     for (int q = tid; q <= m; q += RT) rp[q] = (uint16_t)__ldg(a.g.row_ptr + q);
@@ -314,10 +285,10 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
             reinterpret_cast<uint8_t *>(rec2)[e] = (uint8_t)be.z;
             continue;
         }
-        // first state element of row i (the lane adds its slot offset) | position p in row i << 24
-        rec[e] = (uint32_t)be.y * S | ((uint32_t)be.z << 24);
-        // the edge's sign word (the lane adds l) | the shift that brings its bits to 28..31 << 24
-        rec2[e] = (uint32_t)((be.y * WR + (be.z >> 3)) * LR) | ((uint32_t)(28 - 4 * (be.z & 7)) << 24);
+        // first state element of row i (the lane adds its slot offset)
+        rec[e] = (uint32_t)be.y * S;
+        // the edge's byte for lane 0 (the lane adds l * DMP)
+        rec2[e] = (uint32_t)(be.y * LR * DMP + be.z);
     }
     if (tid < 32) {
         slot_f[tid] = -1;
@@ -341,8 +312,6 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
         if (pass > 0) {
             const unsigned fresh_prev = ctl[1];
             const unsigned fm = (fresh_prev >> q0) & 0xfu;  // this lane's fresh slots (eta^prev = 0)
-            const uint32_t fmb =
-                (fm & 1u) * 0xffu | (fm & 2u) * 0x7f80u | (fm & 4u) * 0x3fc000u | (fm & 8u) * 0x1fe00000u;
             // ---------------- C: check-node pass + syndrome of b = slice(s)
             unsigned syn_acc = 0;  // bit v: slot q0+v has an unsatisfied check
             for (int rb = warp * G; rb < m; rb += NWARP * G) {
@@ -351,13 +320,13 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
                 const int ra = DC > 0 ? i * DC : (valid ? rp[i] : 0);
                 const int d = DC > 0 ? (valid ? DC : 0) : (valid ? (int)rp[i + 1] - ra : 0);
                 const int dmax = DC > 0 ? DC : __reduce_max_sync(FULLM, d);
-                uint32_t *sgw = sgr + (size_t)(valid ? i : 0) * WR * LR + l;
+                uint8_t *ebr = ebt + ((size_t)(valid ? i : 0) * LR + l) * DMP;
                 if (DC > 0 && rb + G <= m)
-                    cn_rows<S, false, DC>(s, mn0, mn1, lc, sgw, col, i, valid, ra, d, dmax, l, fm, fmb, corr, syn_acc);
+                    cn_rows<S, false, DC>(s, mn0, mn1, ebr, col, i, valid, ra, d, dmax, l, fm, corr, syn_acc);
                 else if (__all_sync(FULLM, d == dmax))
-                    cn_rows<S, false, 0>(s, mn0, mn1, lc, sgw, col, i, valid, ra, d, dmax, l, fm, fmb, corr, syn_acc);
+                    cn_rows<S, false, 0>(s, mn0, mn1, ebr, col, i, valid, ra, d, dmax, l, fm, corr, syn_acc);
                 else
-                    cn_rows<S, true, 0>(s, mn0, mn1, lc, sgw, col, i, valid, ra, d, dmax, l, fm, fmb, corr, syn_acc);
+                    cn_rows<S, true, 0>(s, mn0, mn1, ebr, col, i, valid, ra, d, dmax, l, fm, corr, syn_acc);
             }
             const unsigned mine = (syn_acc << q0) & active;
             const unsigned wmask = __reduce_or_sync(FULLM, mine);
@@ -476,33 +445,24 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
 #pragma unroll
                         for (int u = 0; u < 3; u++) {
                             if (q3 + u < dv) {
-                                int ca;
-                                uint32_t pp, widx, shift;
+                                int ca, bi;  // state index of row i for this lane, index of its edge byte
                                 if (CMP) {
                                     const int ro = reinterpret_cast<const uint16_t *>(rec)[c0 + q3 + u];
                                     const int pq = reinterpret_cast<const uint8_t *>(rec2)[c0 + q3 + u];
-                                    const int i = ro / S;
                                     ca = ro + q0;
-                                    pp = (uint32_t)pq * 0x01010101u;
-                                    widx = (uint32_t)((i * WR + (pq >> 3)) * LR);
-                                    shift = (uint32_t)(28 - 4 * (pq & 7));
+                                    bi = (ro / S * LR + l) * DMP + pq;
                                 } else {
-                                    const uint32_t r1 = rec[c0 + q3 + u], r2 = rec2[c0 + q3 + u];
-                                    ca = (int)(r1 & 0xffffffu) + q0;
-                                    pp = __byte_perm(r1, 0u, 0x3333u);  // position p in every byte
-                                    widx = r2 & 0xffffffu;
-                                    shift = r2 >> 24;
+                                    ca = (int)rec[c0 + q3 + u] + q0;
+                                    bi = (int)rec2[c0 + q3 + u] + l * DMP;
                                 }
                                 const float4 m0 = *reinterpret_cast<const float4 *>(mn0 + ca);
                                 const float4 m1 = *reinterpret_cast<const float4 *>(mn1 + ca);
-                                const uint32_t lv = *reinterpret_cast<const uint32_t *>(lc + ca) ^ pp;
-                                const uint32_t ws = sgr[widx + l] << shift;  // bits of edge p -> 28..31
-                                const float mg[4] = {(lv & 0xffu) ? m0.x : m1.x, (lv & 0xff00u) ? m0.y : m1.y,
-                                                     (lv & 0xff0000u) ? m0.z : m1.z,
-                                                     (lv & 0xff000000u) ? m0.w : m1.w};  // Obs. 1
+                                const uint32_t b = ebt[bi];  // sign nibble | isloc nibble << 4
 #pragma unroll
-                                for (int v = 0; v < 4; v++)  // ascending rows from +0.0 (A14)
-                                    acc[v] = acc[v] + flip31(mg[v], ws << (3 - v));
+                                for (int v = 0; v < 4; v++) {  // ascending rows from +0.0 (A14)
+                                    const float mg = (b & (16u << v)) ? f4c(m1, v) : f4c(m0, v);  // Obs. 1
+                                    acc[v] = acc[v] + flip31(mg, b << (31 - v));
+                                }
                             }
                         }
                     }
