@@ -35,15 +35,21 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return SO
     objs = []
     logs = []
-    for src in sources():
+    procs = []
+    for src in sources():  # one nvcc per translation unit, all in parallel
         obj = os.path.join(CSRC, os.path.basename(src)[:-3] + ".o")
         cmd = [NVCC] + ARCH + FLAGS + ["-c", src, "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        logs.append(r.stdout + r.stderr)
-        if r.returncode != 0:
-            sys.stderr.write(r.stdout + r.stderr)
-            raise RuntimeError(f"nvcc failed on {src}")
+        procs.append((src, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
+    failed = None
+    for src, obj, pr in procs:
+        out, _ = pr.communicate()
+        logs.append(out)
+        if pr.returncode != 0:
+            sys.stderr.write(out)
+            failed = failed or src
         objs.append(obj)
+    if failed:
+        raise RuntimeError(f"nvcc failed on {failed}")
     tmp = SO + ".tmp"
     # cudart is linked statically (nvcc default), so the .so only needs the driver at run time
     cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs

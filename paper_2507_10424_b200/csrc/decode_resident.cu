@@ -75,6 +75,7 @@ struct ResArgs {
     int L, T, early, literal, dm;
     int dc, dv;  // > 0: every row has degree dc and every column degree dv (regular code)
     int compact;  // bit-node records in the compact form (see layout_for)
+    int any_degree;  // force the any-degree check-node instance (tests)
     float *post;
     uint8_t *bits;
     int32_t *iters;
@@ -146,6 +147,7 @@ __device__ __forceinline__ void cn_rows(const float *__restrict__ s, float *mn0,
     // word is bit-reversed into bit 4(p%8)+v
     uint2 ob = make_uint2(0u, 0u);
     uint32_t wn = 0u, pf = 0u;
+    // DC > 0: the warp's rows have at most DC edges, DC of them without HAS (unrolled); DC == 0: any degree
     const int pe = DC > 0 ? DC : dmax;
     // Edges in pairs (p, p+1; p even, so a pair never straddles a chunk): the pair's smaller and larger
     // |lambda| (sm, tm) update the row state with nm0' = min(nm0, sm), nm1' = min3(nm1, max(nm0, sm), tm)
@@ -205,7 +207,7 @@ __device__ __forceinline__ void cn_rows(const float *__restrict__ s, float *mn0,
         wn = pushed == 32 ? __brev(wn) : __brev(wn) >> (32 - pushed);
         pf ^= wn;
         if (valid) {
-            if (pe <= 8) {  // one chunk (regular codes of degree <= 8): isloc merged before the only store
+            if ((DC > 0 && DC <= 8) || pe <= 8) {  // one chunk (regular codes of degree <= 8): isloc merged before the only store
                 const uint32_t lm = (1u << (4 * nloc[0])) | (2u << (4 * nloc[1])) | (4u << (4 * nloc[2])) |
                                     (8u << (4 * nloc[3]));
                 res_store_chunk(ebr, wn, lm);
@@ -321,12 +323,29 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
                 const int d = DC > 0 ? (valid ? DC : 0) : (valid ? (int)rp[i + 1] - ra : 0);
                 const int dmax = DC > 0 ? DC : __reduce_max_sync(FULLM, d);
                 uint8_t *ebr = ebt + ((size_t)(valid ? i : 0) * LR + l) * DMP;
-                if (DC > 0 && rb + G <= m)
-                    cn_rows<S, false, DC>(s, mn0, mn1, ebr, col, i, valid, ra, d, dmax, l, fm, corr, syn_acc);
-                else if (__all_sync(FULLM, d == dmax))
-                    cn_rows<S, false, 0>(s, mn0, mn1, ebr, col, i, valid, ra, d, dmax, l, fm, corr, syn_acc);
-                else
-                    cn_rows<S, true, 0>(s, mn0, mn1, ebr, col, i, valid, ra, d, dmax, l, fm, corr, syn_acc);
+#define CN_ROWS_(H, K) cn_rows<S, H, K>(s, mn0, mn1, ebr, col, i, valid, ra, d, dmax, l, fm, corr, syn_acc)
+                if (DC > 0 && rb + G <= m) {
+                    CN_ROWS_(false, (DC > 0 ? DC : 1));
+                } else if (DC < 0) {
+                    // rows of degree <= 8, any code: an instance per largest degree of the warp's rows (a
+                    // run-time value), unrolled, with per-edge guards only where the warp's degrees differ
+                    const bool eq = __all_sync(FULLM, d == dmax);
+                    switch (dmax) {
+                        case 2: if (eq) CN_ROWS_(false, 2); else CN_ROWS_(true, 2); break;
+                        case 3: if (eq) CN_ROWS_(false, 3); else CN_ROWS_(true, 3); break;
+                        case 4: if (eq) CN_ROWS_(false, 4); else CN_ROWS_(true, 4); break;
+                        case 5: if (eq) CN_ROWS_(false, 5); else CN_ROWS_(true, 5); break;
+                        case 6: if (eq) CN_ROWS_(false, 6); else CN_ROWS_(true, 6); break;
+                        case 7: if (eq) CN_ROWS_(false, 7); else CN_ROWS_(true, 7); break;
+                        case 8: if (eq) CN_ROWS_(false, 8); else CN_ROWS_(true, 8); break;
+                        default: CN_ROWS_(true, 0); break;
+                    }
+                } else if (__all_sync(FULLM, d == dmax)) {
+                    CN_ROWS_(false, 0);
+                } else {
+                    CN_ROWS_(true, 0);
+                }
+#undef CN_ROWS_
             }
             const unsigned mine = (syn_acc << q0) & active;
             const unsigned wmask = __reduce_or_sync(FULLM, mine);
@@ -543,6 +562,12 @@ void launch_c(const ResArgs &args, int ctas, size_t smem, cudaStream_t st) {
         k_resident<S, RT, 6, 3, CMP><<<ctas, RT, smem, st>>>(args);
         return;
     }
+    // rows of degree <= 8 (most codes): the check-node pass unrolled over at most 4 edge pairs
+    if (args.dm <= 8 && !args.any_degree) {
+        cudaFuncSetAttribute(k_resident<S, RT, -8, 0, CMP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_resident<S, RT, -8, 0, CMP><<<ctas, RT, smem, st>>>(args);
+        return;
+    }
     cudaFuncSetAttribute(k_resident<S, RT, 0, 0, CMP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_resident<S, RT, 0, 0, CMP><<<ctas, RT, smem, st>>>(args);
 }
@@ -639,7 +664,13 @@ int launch_resident(const Graph &g, const ResidentPlan &rp, const float *llr, in
     a.dm = rp.dm;
     a.dc = rp.regular ? rp.dm : 0;
     a.dv = rp.regular ? rp.dv : 0;
-    if (getenv("LDPC_RES_GENERIC")) a.dc = a.dv = 0;
+    // LDPC_RES_GENERIC=1: no regular-code instance (rows of degree <= 8 still take the bounded-degree one);
+    // =2: the any-degree instance
+    a.any_degree = 0;
+    if (const char *e = getenv("LDPC_RES_GENERIC")) {
+        a.dc = a.dv = 0;
+        a.any_degree = atoi(e) >= 2;
+    }
     a.compact = rp.compact ? 1 : 0;
     a.lay = layout_for(rp.slots, g.m, g.n, g.E, rp.dm, rp.compact);
     cudaMemsetAsync(work_counter, 0, sizeof(int), st);

@@ -318,15 +318,17 @@ def test_randomised_shapes_flags_and_check_points(case):
         compare(code, llr, L, flags | sched, h=h, check_every=T)
 
 
-def test_resident_generic_equals_regular_instance(monkeypatch):
-    """The degree-specialised resident kernel for regular (3,6) codes and the generic one agree
-    (LDPC_RES_GENERIC=1 forces the generic instance), and both match the oracle."""
+@pytest.mark.parametrize("generic", ["1", "2"])
+def test_resident_generic_equals_regular_instance(monkeypatch, generic):
+    """The degree-specialised resident kernel for regular (3,6) codes and the generic ones agree
+    (LDPC_RES_GENERIC=1: the instance for rows of degree <= 8; =2: the any-degree instance), and all
+    match the oracle."""
     cfg = codes.CONFIGS["c2"]
     code = cfg["code"]()
     parts = [channel.bpsk_awgn(code.n, code.rate, e, cfg["seed"], p, 500, 300).numpy() for p, e in enumerate(cfg["ebn0"])]
     llr = np.concatenate(parts)
     ref = compare(code, llr, cfg["max_iter"], FORCE_RESIDENT, h=handle(code, FORCE_RESIDENT))
-    monkeypatch.setenv("LDPC_RES_GENERIC", "1")
+    monkeypatch.setenv("LDPC_RES_GENERIC", generic)
     got = compare(code, llr, cfg["max_iter"], FORCE_RESIDENT, h=handle(code, FORCE_RESIDENT))
     for a, b in zip(ref, got):
         assert np.array_equal(a, b)
