@@ -54,10 +54,11 @@ __device__ __forceinline__ uint4 ldu4(const uint32_t *p) { return *reinterpret_c
 // no per-access cost).  Bit 0: data read or written once per sweep (r, s stores, the check node's row
 // records) is marked evict_first; bit 1: data gathered several times per sweep (s in the check node, row
 // records in the bit node) evict_last, so a tile's gathered working set stays in L2 while it is swept.
-// Measured (8192 frames, every frame running): bit node C4 -2.5 %, C3 equal; check node C3 +1.5 %
-// (so the check node keeps plain loads).
+// Measured (8192 frames, every frame running): bit node bits 0+1: C4 -2.5 % (DRAM / algorithmic bytes
+// 1.18 -> 1.02), C3 equal; check node bit 1 (s gathers evict_last): C3 -2.2 %, C4 -1.5 %, while bit 0 on
+// its row records costs 1-1.5 %.
 #ifndef L2H_CN
-#define L2H_CN 0
+#define L2H_CN 2
 #endif
 #ifndef L2H_BN
 #define L2H_BN 3
