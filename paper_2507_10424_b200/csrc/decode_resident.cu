@@ -61,8 +61,8 @@ Layout layout_for(int S, int m, int n, int E, int dm, bool compact = false) {
     L.rp = o;   o = a16(o + (size_t)(m + 1) * 2);
     L.cp = o;   o = a16(o + (size_t)(n + 1) * 2);
     L.col = o;  o = a16(o + (size_t)E * 2);
-    L.rec = o;  o = a16(o + (size_t)E * (compact ? 2 : 4));
-    L.rec2 = o; o = a16(o + (size_t)E * (compact ? 1 : 4));
+    L.rec = o;  o = a16(o + (size_t)E * (compact ? 2 : 8));  // compact: u16 row offset; else uint2 {state, byte}
+    L.rec2 = o; o = a16(o + (size_t)E * (compact ? 1 : 0));  // compact: u8 position
     L.meta = o; o = a16(o + (size_t)META_INTS * 4 + 8 * 8);
     L.total = o;
     return L;
@@ -287,10 +287,9 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
             reinterpret_cast<uint8_t *>(rec2)[e] = (uint8_t)be.z;
             continue;
         }
-        // first state element of row i (the lane adds its slot offset)
-        rec[e] = (uint32_t)be.y * S;
-        // the edge's byte for lane 0 (the lane adds l * DMP)
-        rec2[e] = (uint32_t)(be.y * LR * DMP + be.z);
+        // {first state element of row i (the lane adds its slot offset), the edge's byte for lane 0 (the
+        // lane adds l * DMP)}: one 8-byte shared load per edge in the bit-node pass
+        reinterpret_cast<uint2 *>(rec)[e] = make_uint2((uint32_t)be.y * S, (uint32_t)(be.y * LR * DMP + be.z));
     }
     if (tid < 32) {
         slot_f[tid] = -1;
@@ -471,8 +470,9 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
                                     ca = ro + q0;
                                     bi = (ro / S * LR + l) * DMP + pq;
                                 } else {
-                                    ca = (int)rec[c0 + q3 + u] + q0;
-                                    bi = (int)rec2[c0 + q3 + u] + l * DMP;
+                                    const uint2 r12 = reinterpret_cast<const uint2 *>(rec)[c0 + q3 + u];
+                                    ca = (int)r12.x + q0;
+                                    bi = (int)r12.y + l * DMP;
                                 }
                                 const float4 m0 = *reinterpret_cast<const float4 *>(mn0 + ca);
                                 const float4 m1 = *reinterpret_cast<const float4 *>(mn1 + ca);

@@ -100,8 +100,14 @@ __device__ __forceinline__ float fmin3f(float a, float b, float c) {
     return d;
 }
 
+// check node: edges in pairs (FMNMX3 second-minimum update, 3-input parity XOR).  k_cn (rows of degree
+// <= 8): no gain (C3 -0.5 %, C4 equal) and 1-2 % more SASS (selects of the half-empty last pair), so off;
+// k_cn_generic (C6, d = 32): -4 %, on.
 #ifndef CN_PAIR
-#define CN_PAIR 1  // check node: edges in pairs (FMNMX3 second-minimum update, 3-input parity XOR)
+#define CN_PAIR 0
+#endif
+#ifndef CNG_PAIR
+#define CNG_PAIR 1
 #endif
 
 // the sign of a magnitude picked by Obs. 1 flipped by one stored sign bit (already moved to bit 31)
@@ -556,7 +562,7 @@ __global__ void __launch_bounds__(CN_T, 2) k_cn_generic(Graph g, StreamState w, 
                     }
                 }
                 uint32_t cw = 0;
-#if CN_PAIR
+#if CNG_PAIR
 #pragma unroll
                 for (int u8 = 0; u8 < C8; u8 += 2) {  // edge pairs, as in cn_compute
                     const int p = p0 + u8;
