@@ -110,6 +110,37 @@ __device__ __forceinline__ float fmin3f(float a, float b, float c) {
 #define CNG_PAIR 1
 #endif
 
+// 256-bit (8 x fp32) global accesses (LDG.E.ENL2.256 / STG.E.ENL2.256 on sm_100), with an optional L2 policy
+struct f8 {
+    float v[8];
+};
+template <int L2H>
+__device__ __forceinline__ f8 ld8h(const float *p, uint64_t pol) {
+    f8 r;
+    if (L2H)
+        asm volatile("ld.global.L2::cache_hint.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+                     : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]), "=f"(r.v[5]),
+                       "=f"(r.v[6]), "=f"(r.v[7])
+                     : "l"(p), "l"(pol));
+    else
+        asm volatile("ld.global.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]), "=f"(r.v[5]),
+                       "=f"(r.v[6]), "=f"(r.v[7])
+                     : "l"(p));
+    return r;
+}
+template <int L2H>
+__device__ __forceinline__ void st8h(float *p, const f8 &r, uint64_t pol) {
+    if (L2H)
+        asm volatile("st.global.L2::cache_hint.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8}, %9;" ::"l"(p), "f"(r.v[0]),
+                     "f"(r.v[1]), "f"(r.v[2]), "f"(r.v[3]), "f"(r.v[4]), "f"(r.v[5]), "f"(r.v[6]), "f"(r.v[7]), "l"(pol)
+                     : "memory");
+    else
+        asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(r.v[0]), "f"(r.v[1]),
+                     "f"(r.v[2]), "f"(r.v[3]), "f"(r.v[4]), "f"(r.v[5]), "f"(r.v[6]), "f"(r.v[7])
+                     : "memory");
+}
+
 // the sign of a magnitude picked by Obs. 1 flipped by one stored sign bit (already moved to bit 31)
 __device__ __forceinline__ float flip31(float mag, uint32_t bit31) {
     return __uint_as_float(__float_as_uint(mag) ^ (bit31 & 0x80000000u));
@@ -915,30 +946,19 @@ __global__ void __launch_bounds__(CNB_W * 32, 1)
 // and the tile goes to the list of body k+1 -- or, when fewer than half of its slots still run and
 // at least two bodies remain, to the compaction sources.
 // ------------------------------------------------------------------------------------------------
-#ifndef BN_G
-#define BN_G 1  // edges of a column whose loads are issued together (1 measured best: 2-5 cut occupancy)
-#endif
-#ifndef BN_CM1
-#define BN_CM1 0  // 1: load min1 only where the edge is a min0Location of the lane (fewer L2 bytes, measured slower)
-#endif
-
-#ifndef BN_PF
-// how the bit node finds an edge's row record (A/B, 8192 frames, every frame running, C3 / C4 ms per 20 / 10 bodies):
-// 3 = per-edge offset records (Graph::bn_off, 32-byte units; one IMAD.WIDE per address, 37 instead of 42
-//     instructions per warp-edge): 14.57 / 30.82 against 15.27 / 32.15 for 0 = the {e, i, p} records;
-// 1 = the next column's edge list prefetched into lanes: slower (fewer warps or spills);
-// 2 = the next edge's record loaded one edge ahead: equal to 0;
-// (measured and removed: row state staged through shared memory with cp.async, 3-8 edges in flight per
-//  warp, parity-green but 40-55 % slower.)
-#define BN_PF 3
-#endif
-
-#ifndef BN_U2
-#define BN_U2 0  // BN_PF 3: two edges of a column per step (more loads in flight, more registers)
-#endif
-
-#ifndef BN_RVLATE
-#define BN_RVLATE 0  // 1: r of the column loaded after its edges (4 registers fewer across the edge loop)
+// How the bit node gathers (A/B, 8192 frames at the lowest Eb/N0, every frame running, early stop off;
+// C3 / C4 ms per 20 / 10 bodies):
+//   BN_V8 = 1  256-bit accesses, half-warps on separate columns, 8 slots per lane, 12 CTAs x 128 threads:
+//              12.74 / 27.39 (C6 3.27 against 3.96);
+//   BN_V8 = 0  float4 accesses, 4 slots per lane, per-edge offset records (Graph::bn_off, 32-byte units;
+//              one IMAD.WIDE per address): 14.57 / 30.82 (round-1 {e, i, p} records: 15.27 / 32.15).
+// Measured and removed: the next column's edge list prefetched into lanes (slower: fewer warps or
+// spills), the next edge's record loaded one edge ahead (equal), two edges per step (equal), loads of
+// 2-5 edges together (0-15 % slower), min1 loaded only where the edge is a min0Location (25 % slower),
+// row state staged through shared memory with cp.async 3-8 edges deep per warp (40-55 % slower),
+// 256-bit accesses at 8 / 10 / 14 / 16 CTAs per SM (slower than 12).
+#ifndef BN_V8
+#define BN_V8 1
 #endif
 
 #ifndef BN_DYN
@@ -1034,59 +1054,61 @@ __global__ void __launch_bounds__(BN_T, BN_MINB)
         const unsigned char *RB = w.rst + (size_t)t * m * w.rs;
         const size_t tb = (size_t)t * n * TILE + 4 * lane;  // r and s of the tile (one offset, two bases)
         const int j1 = min(n, x * BN_COLS + BN_COLS);
-#if BN_PF == 1
-        // The edge list of the warp's next column is loaded into lanes (lane p: row and in-row position of
-        // edge p) while the current column runs, so every row-state gather of an edge is issued without
-        // waiting for its edge record (the round-2 profile: 22 % of the stalls sat on that dependent load).
-        const int jb = x * BN_COLS;
-        const int cpv = (lane <= BN_COLS && jb + lane <= n) ? __ldg(g.col_ptr + jb + lane) : 0;
-        const int nq = jb + warp < j1 ? (j1 - jb - warp + BN_T / 32 - 1) / (BN_T / 32) : 0;
-        auto col_edges = [&](int q, int &dv) {
-            const int c = warp + (BN_T / 32) * q;
-            const int c0 = __shfl_sync(FULL_MASK, cpv, c & 31);
-            dv = q < nq ? __shfl_sync(FULL_MASK, cpv, (c + 1) & 31) - c0 : 0;
-            int2 e = make_int2(0, 0);
-            if (lane < dv) {  // {e, i, p, -} of edge `lane` (ascending i): only i and p are loaded
-                const int *ed = reinterpret_cast<const int *>(g.bn_edge + c0 + lane);
-                e = make_int2(__ldg(ed + 1), __ldg(ed + 2));
-            }
-            return e;
-        };
-        int dvn;
-        int2 en = col_edges(0, dvn);
-        for (int q = 0; q < nq; q++) {
-            const int j = jb + warp + (BN_T / 32) * q;
-            const int dv = dvn;
-            int2 ec = en;
-            en = col_edges(q + 1, dvn);
-#if !BN_RVLATE
-            const float4 rv = ldh4<1, L2H_BN>(w.r + tb + (size_t)j * TILE, pf);
-#endif
-            float acc[4] = {0.f, 0.f, 0.f, 0.f};
-            for (int e0 = 0; e0 < dv; e0 += 32) {
-                if (e0 > 0) {  // columns of degree > 32: the next 32 edges
-                    ec = make_int2(0, 0);
-                    const int c0 = __shfl_sync(FULL_MASK, cpv, j - jb);
-                    if (lane < dv - e0) {
-                        const int *ed = reinterpret_cast<const int *>(g.bn_edge + c0 + e0 + lane);
-                        ec = make_int2(__ldg(ed + 1), __ldg(ed + 2));
-                    }
-                }
-                const int ne = min(32, dv - e0);
+#if BN_V8
+        // 256-bit accesses: half-warp h (lanes 16h..16h+15) sweeps its own columns, half-lane hl owns the 8
+        // slots 8hl..8hl+7 (32 contiguous bytes of min0, of min1, of r and of s; its two edge-block bytes in
+        // one 16-bit load).  One warp instruction moves two edges' worth of row state for 128 slots, so a
+        // warp keeps twice the bytes in flight with half the load instructions per edge.
+        {
+            const int hw = (warp << 1) | (lane >> 4), hl = lane & 15;
+            // slot 8hl + v of the tile = old lane 2hl + (v >> 2), component v & 3: bit v of mine8
+            const unsigned mine8 = ((act.x >> (2 * hl)) & 1u) | (((act.y >> (2 * hl)) & 1u) << 1) |
+                                   (((act.z >> (2 * hl)) & 1u) << 2) | (((act.w >> (2 * hl)) & 1u) << 3) |
+                                   (((act.x >> (2 * hl + 1)) & 1u) << 4) | (((act.y >> (2 * hl + 1)) & 1u) << 5) |
+                                   (((act.z >> (2 * hl + 1)) & 1u) << 6) | (((act.w >> (2 * hl + 1)) & 1u) << 7);
+            const unsigned char *RBm = RB + 32 * hl, *RBb = RB + 2 * hl;
+            const size_t tb8 = (size_t)t * n * TILE + 8 * hl;
+            constexpr int NHW = BN_T / 16;  // half-warps per CTA
+            for (int jb = x * BN_COLS; jb < j1; jb += NHW) {  // warp-uniform trip count
+                const int j = jb + hw;
+                const bool colok = j < j1;
+                const int c0 = colok ? __ldg(g.col_ptr + j) : 0, dv = colok ? __ldg(g.col_ptr + j + 1) - c0 : 0;
+                float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                const int2 *op = g.bn_off + c0;  // ascending i (A14)
 #pragma unroll 1
-                for (int u = 0; u < ne; u++) {  // ascending row order from +0.0 (A14)
-                    const unsigned char *Ri = RB + (size_t)__shfl_sync(FULL_MASK, ec.x, u) * w.rs;
-                    const float4 m0 = ldh4<2, L2H_BN>(reinterpret_cast<const float *>(Ri) + 4 * lane, pl);
-                    const float4 m1 = ldh4<2, L2H_BN>(reinterpret_cast<const float *>(Ri) + 128 + 4 * lane, pl);
-                    const uint32_t b = Ri[REC_EDGE0 + 32 * __shfl_sync(FULL_MASK, ec.y, u) + lane];
+                for (int q = 0; q < dv; q++, op++) {
+                    const int2 o = __ldg(op);
+                    const float *Rm = reinterpret_cast<const float *>(RBm + ((size_t)(unsigned)o.x << 5));
+                    const f8 m0 = ld8h<L2H_BN>(Rm, pl), m1 = ld8h<L2H_BN>(Rm + 128, pl);
+                    const uint32_t b = *reinterpret_cast<const uint16_t *>(RBb + ((size_t)(unsigned)o.y << 5));
 #pragma unroll
-                    for (int v = 0; v < 4; v++) {
-                        const float mag = (b & (16u << v)) ? comp(m1, v) : comp(m0, v);  // Obs. 1
-                        acc[v] = acc[v] + flip31(mag, b << (31 - v));
+                    for (int v = 0; v < 8; v++) {
+                        const int sb = v < 4 ? v : v + 4;  // sign bit of slot v; its isloc bit is sb + 4
+                        const float mag = (b & (16u << sb)) ? m1.v[v] : m0.v[v];  // Obs. 1
+                        acc[v] = acc[v] + flip31(mag, b << (31 - sb));
+                    }
+                }
+                if (colok) {
+                    float *o8 = w.s + tb8 + (size_t)j * TILE;
+                    const f8 rv = ld8h<L2H_BN>(w.r + tb8 + (size_t)j * TILE, pf);
+                    f8 nv;
+#pragma unroll
+                    for (int v = 0; v < 8; v++) nv.v[v] = zneg(acc[v] + rv.v[v]);  // zeros of s kept as -0 (A12)
+                    if (mine8 == 0xFFu) {
+                        st8h<L2H_BN>(o8, nv, pf);
+                    } else if (k == 1) {  // body 1: frames that stopped at the pre-check keep s = r
+#pragma unroll
+                        for (int v = 0; v < 8; v++) nv.v[v] = ((mine8 >> v) & 1u) ? nv.v[v] : rv.v[v];
+                        st8h<0>(o8, nv, pf);
+                    } else if (mine8) {  // frozen frames keep their s
+#pragma unroll
+                        for (int v = 0; v < 8; v++)
+                            if ((mine8 >> v) & 1u) o8[v] = nv.v[v];
                     }
                 }
             }
-#elif BN_PF == 3
+        }
+#else  // float4 accesses, per-edge offset records
         // per-edge offset records (Graph::bn_off, 32-byte units): one IMAD.WIDE per gather address, the
         // record pointer advanced by 8 bytes per edge
         const unsigned char *RBm = RB + 16 * lane, *RBb = RB + lane;
@@ -1096,21 +1118,6 @@ __global__ void __launch_bounds__(BN_T, BN_MINB)
             float acc[4] = {0.f, 0.f, 0.f, 0.f};
             const int2 *op = g.bn_off + c0;  // ascending i (A14)
             int q = 0;
-#if BN_U2
-            for (; q + 1 < dv; q += 2, op += 2) {  // two edges' gathers in flight, summed in order
-                const int2 o0 = __ldg(op), o1 = __ldg(op + 1);
-                const float *Ra = reinterpret_cast<const float *>(RBm + ((size_t)(unsigned)o0.x << 5));
-                const float *Rb = reinterpret_cast<const float *>(RBm + ((size_t)(unsigned)o1.x << 5));
-                const float4 a0 = ldh4<2, L2H_BN>(Ra, pl), a1 = ldh4<2, L2H_BN>(Ra + 128, pl);
-                const float4 b0 = ldh4<2, L2H_BN>(Rb, pl), b1 = ldh4<2, L2H_BN>(Rb + 128, pl);
-                const uint32_t ba = RBb[(size_t)(unsigned)o0.y << 5], bb = RBb[(size_t)(unsigned)o1.y << 5];
-#pragma unroll
-                for (int v = 0; v < 4; v++) {
-                    acc[v] = acc[v] + flip31((ba & (16u << v)) ? comp(a1, v) : comp(a0, v), ba << (31 - v));
-                    acc[v] = acc[v] + flip31((bb & (16u << v)) ? comp(b1, v) : comp(b0, v), bb << (31 - v));
-                }
-            }
-#endif
 #pragma unroll 1
             for (; q < dv; q++, op++) {
                 const int2 o = __ldg(op);
@@ -1124,75 +1131,11 @@ __global__ void __launch_bounds__(BN_T, BN_MINB)
                     acc[v] = acc[v] + flip31(mag, b << (31 - v));
                 }
             }
-#elif BN_PF == 2
-        // one edge ahead: the record of edge q+1 is loaded after the row-state gathers of edge q
-        for (int j = x * BN_COLS + warp; j < j1; j += BN_T / 32) {
-            const int c0 = __ldg(g.col_ptr + j), dv = __ldg(g.col_ptr + j + 1) - c0;
-            const float4 rv = ldh4<1, L2H_BN>(w.r + tb + (size_t)j * TILE, pf);
-            float acc[4] = {0.f, 0.f, 0.f, 0.f};
-            const int *edp = reinterpret_cast<const int *>(g.bn_edge + c0);  // {e, i, p, -}, ascending i
-            int ni = 0, np = 0;
-            if (dv > 0) {
-                ni = __ldg(edp + 1);
-                np = __ldg(edp + 2);
-            }
-#pragma unroll 1
-            for (int q = 0; q < dv; q++) {
-                const unsigned char *Ri = RB + (size_t)ni * w.rs;
-                const float4 m0 = ldh4<2, L2H_BN>(reinterpret_cast<const float *>(Ri) + 4 * lane, pl);
-                const float4 m1 = ldh4<2, L2H_BN>(reinterpret_cast<const float *>(Ri) + 128 + 4 * lane, pl);
-                const uint32_t b = Ri[REC_EDGE0 + 32 * np + lane];
-                if (q + 1 < dv) {
-                    ni = __ldg(edp + 4 * (q + 1) + 1);
-                    np = __ldg(edp + 4 * (q + 1) + 2);
-                }
-#pragma unroll
-                for (int v = 0; v < 4; v++) {
-                    const float mag = (b & (16u << v)) ? comp(m1, v) : comp(m0, v);  // Obs. 1
-                    acc[v] = acc[v] + flip31(mag, b << (31 - v));
-                }
-            }
-#else
-        for (int j = x * BN_COLS + warp; j < j1; j += BN_T / 32) {
-            const int c0 = __ldg(g.col_ptr + j), dv = __ldg(g.col_ptr + j + 1) - c0;
-            const float4 rv = ldh4<1, L2H_BN>(w.r + tb + (size_t)j * TILE, pf);
-            float acc[4] = {0.f, 0.f, 0.f, 0.f};
-            for (int q0 = 0; q0 < dv; q0 += BN_G) {
-                // all loads of up to BN_G edges in flight together (past the column's last edge: its last edge
-                // again, not accumulated), then the sums in ascending row order from +0.0 (A14)
-                float4 m0[BN_G], m1[BN_G];
-                uint32_t b[BN_G];
-#pragma unroll
-                for (int u = 0; u < BN_G; u++) {
-                    const int4 ed = __ldg(g.bn_edge + c0 + min(q0 + u, dv - 1));  // {e, i, p, -}, ascending i
-                    const unsigned char *Ri = RB + (size_t)ed.y * w.rs;
-                    m0[u] = ldh4<2, L2H_BN>(reinterpret_cast<const float *>(Ri) + 4 * lane, pl);
-#ifdef BN_XP  // timing experiments only (wrong results): 1 = no min1 gather, 2 = no edge-byte gather
-                    b[u] = BN_XP == 2 ? (uint32_t)(ed.z * 0x11) : Ri[REC_EDGE0 + 32 * ed.z + lane];
-                    m1[u] = BN_XP == 1 ? m0[u] : ldh4<2, L2H_BN>(reinterpret_cast<const float *>(Ri) + 128 + 4 * lane, pl);
-#else
-                    b[u] = Ri[REC_EDGE0 + 32 * ed.z + lane];
-                    if (!BN_CM1 || (b[u] & 0xf0u)) m1[u] = ldh4<2, L2H_BN>(reinterpret_cast<const float *>(Ri) + 128 + 4 * lane, pl);
-                    else m1[u] = m0[u];
 #endif
-                }
-#pragma unroll
-                for (int u = 0; u < BN_G; u++) {
-                    if (q0 + u < dv) {
-#pragma unroll
-                        for (int v = 0; v < 4; v++) {
-                            const float mag = (b[u] & (16u << v)) ? comp(m1[u], v) : comp(m0[u], v);  // Obs. 1
-                            acc[v] = acc[v] + flip31(mag, b[u] << (31 - v));
-                        }
-                    }
-                }
-            }
-#endif
-#if BN_PF == 1 && BN_RVLATE
-            const float4 rv = ldh4<1, L2H_BN>(w.r + tb + (size_t)j * TILE, pf);
-#endif
+#if !BN_V8
             bn_store(w.s + tb + (size_t)j * TILE, acc, rv, mine, k, pf);
         }
+#endif
     }
 }
 
