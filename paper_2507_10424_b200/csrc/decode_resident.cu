@@ -28,6 +28,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "ldpc_internal.cuh"
 
@@ -51,8 +52,9 @@ constexpr int META_INTS = 8 * 32 + 16;
 // of 8: the edge-byte index is recomputed from them), for codes that fit no other way (C5 size)
 __host__ __device__ constexpr int eb_dmp(int dm) { return (dm + 7) / 8 * 8; }
 
-Layout layout_for(int S, int m, int n, int E, int dm, bool compact = false) {
+Layout layout_for(int S, int m, int n, int E, int dm, bool compact = false, bool gg = false) {
     Layout L{};
+    if (gg) E = 0;  // global-graph mode: the edge lists stay in global memory (L2)
     size_t o = 0;
     L.s = o;    o = a16(o + (size_t)n * S * 4);
     L.m0 = o;   o = a16(o + (size_t)m * S * 4);
@@ -75,6 +77,7 @@ struct ResArgs {
     int L, T, early, literal, dm;
     int dc, dv;  // > 0: every row has degree dc and every column degree dv (regular code)
     int compact;  // bit-node records in the compact form (see layout_for)
+    int gg;       // Tanner-graph edge lists read from global memory
     int any_degree;  // force the any-degree check-node instance (tests)
     float *post;
     uint8_t *bits;
@@ -101,6 +104,11 @@ __device__ __forceinline__ void f4s(float4 &a, int v, float x) {
 // lambda = s - (+-0) has the magnitude and sign() of s, s being -0 rather than +0 for zero).
 // sgw: this lane's sign words of row i (sgw[q * LR] = edges 8q..8q+7): read as eta^prev's signs and
 // overwritten with the new ones (each lane owns its words: no ballot, no synchronisation).
+#ifndef RES_ANY_UNROLL
+#define RES_ANY_UNROLL 1  // edge pairs per unrolled step of the any-degree check-node pass (4: 1 % slower)
+#endif
+constexpr int kAnyUnroll = RES_ANY_UNROLL;  // (#pragma unroll does not expand macros)
+
 // min(a, b, c) in one FMNMX3 (sm_100)
 __device__ __forceinline__ float fmin3f(float a, float b, float c) {
     float d;
@@ -121,9 +129,12 @@ __device__ __forceinline__ void res_store_chunk(uint8_t *p, uint32_t sw, uint32_
     *reinterpret_cast<uint2 *>(p) = make_uint2(__byte_perm(ze, zo, 0x5140), __byte_perm(ze, zo, 0x7362));
 }
 
-template <int S, bool HAS, int DC>
+__device__ __forceinline__ int colat(const uint16_t *c, int e) { return c[e]; }
+__device__ __forceinline__ int colat(const int *c, int e) { return __ldg(c + e); }
+
+template <int S, bool HAS, int DC, typename CT>
 __device__ __forceinline__ void cn_rows(const float *__restrict__ s, float *mn0, float *mn1, uint8_t *__restrict__ ebr,
-                                        const uint16_t *col, int i, bool valid, int ra, int d, int dmax, int l,
+                                        const CT *col, int i, bool valid, int ra, int d, int dmax, int l,
                                         unsigned fm, bool corr, unsigned &syn_acc) {
     const float INF = __int_as_float(0x7f800000);
     const int q0 = 4 * l;
@@ -154,7 +165,7 @@ __device__ __forceinline__ void cn_rows(const float *__restrict__ s, float *mn0,
     // (FMNMX3) and loc' = sm < nm0 ? (b < a ? p+1 : p) : loc -- the same first strict minimum (A13) and
     // second minimum as the edge-by-edge update in fewer ALU operations; the decision parity takes both
     // edges in one 3-input XOR.  An absent edge enters as |lambda| = +inf, sign bit 0, parity 0.
-#pragma unroll(DC > 0 ? (DC + 1) / 2 : 1)
+#pragma unroll(DC > 0 ? (DC + 1) / 2 : kAnyUnroll)
     for (int p = 0; p < pe; p += 2) {
         if ((p & 7) == 0) {
             if (p > 0) {  // the finished chunk: its bytes with the sign nibbles (isloc merged at the row end)
@@ -167,7 +178,7 @@ __device__ __forceinline__ void cn_rows(const float *__restrict__ s, float *mn0,
         }
         const bool inb = p + 1 < pe;
         const bool ha = HAS ? (p < d) : true, hb = inb && (HAS ? (p + 1 < d) : true);
-        const int ja = ha ? col[ra + p] : 0, jb = hb ? col[ra + p + 1] : 0;
+        const int ja = ha ? colat(col, ra + p) : 0, jb = hb ? colat(col, ra + p + 1) : 0;
         const float4 sva = *reinterpret_cast<const float4 *>(s + ja * S + q0);
         const float4 svb = *reinterpret_cast<const float4 *>(s + jb * S + q0);
         const uint32_t ow = (p & 4) ? ob.y : ob.x;
@@ -242,7 +253,7 @@ __device__ __forceinline__ void cn_rows(const float *__restrict__ s, float *mn0,
 
 // Lane layout: a lane owns 4 consecutive slots (float4) of one row or column; LR = S/4 lanes cover a
 // row, G = 32/LR rows per warp.  Bit of slot q = 4*l + v inside an S-bit sign word: v*LR + l.
-template <int S, int RT, int DC, int DV, bool CMP>
+template <int S, int RT, int DC, int DV, bool CMP, bool GG = false>
 __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 2) : RT == 384 ? 2 : 1) k_resident(ResArgs a) {
     constexpr int NWARP = RT / 32;
     constexpr int LR = S / 4;
@@ -257,6 +268,10 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
     uint16_t *rp = reinterpret_cast<uint16_t *>(sm + a.lay.rp);
     uint16_t *cp = reinterpret_cast<uint16_t *>(sm + a.lay.cp);
     uint16_t *col = reinterpret_cast<uint16_t *>(sm + a.lay.col);
+    // the check-node pass's column lists: shared memory, or (GG) the ingested int32 lists in global memory
+    const typename std::conditional<GG, int, uint16_t>::type *colp;
+    if constexpr (GG) colp = a.g.col_idx;
+    else colp = col;
     uint32_t *rec = reinterpret_cast<uint32_t *>(sm + a.lay.rec);
     uint32_t *rec2 = reinterpret_cast<uint32_t *>(sm + a.lay.rec2);
     int *meta = reinterpret_cast<int *>(sm + a.lay.meta);
@@ -279,7 +294,7 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
     // ---- the Tanner graph into shared memory (16-bit lists)
     for (int q = tid; q <= m; q += RT) rp[q] = (uint16_t)__ldg(a.g.row_ptr + q);
     for (int q = tid; q <= n; q += RT) cp[q] = (uint16_t)__ldg(a.g.col_ptr + q);
-    for (int e = tid; e < E; e += RT) {
+    for (int e = tid; e < (GG ? 0 : E); e += RT) {
         col[e] = (uint16_t)__ldg(a.g.col_idx + e);
         const int4 be = __ldg(a.g.bn_edge + e);  // {edge id, row, pos, parity}
         if (CMP) {  // u16 row offset, u8 position
@@ -322,7 +337,7 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
                 const int d = DC > 0 ? (valid ? DC : 0) : (valid ? (int)rp[i + 1] - ra : 0);
                 const int dmax = DC > 0 ? DC : __reduce_max_sync(FULLM, d);
                 uint8_t *ebr = ebt + ((size_t)(valid ? i : 0) * LR + l) * DMP;
-#define CN_ROWS_(H, K) cn_rows<S, H, K>(s, mn0, mn1, ebr, col, i, valid, ra, d, dmax, l, fm, corr, syn_acc)
+#define CN_ROWS_(H, K) cn_rows<S, H, K>(s, mn0, mn1, ebr, colp, i, valid, ra, d, dmax, l, fm, corr, syn_acc)
                 if (DC > 0 && rb + G <= m) {
                     CN_ROWS_(false, (DC > 0 ? DC : 1));
                 } else if (DC < 0) {
@@ -464,7 +479,11 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
                         for (int u = 0; u < 3; u++) {
                             if (q3 + u < dv) {
                                 int ca, bi;  // state index of row i for this lane, index of its edge byte
-                                if (CMP) {
+                                if (GG) {  // {e, i, p, -} from global memory (L2)
+                                    const int4 be = __ldg(a.g.bn_edge + c0 + q3 + u);
+                                    ca = be.y * S + q0;
+                                    bi = (be.y * LR + l) * DMP + be.z;
+                                } else if (CMP) {
                                     const int ro = reinterpret_cast<const uint16_t *>(rec)[c0 + q3 + u];
                                     const int pq = reinterpret_cast<const uint8_t *>(rec2)[c0 + q3 + u];
                                     ca = ro + q0;
@@ -572,8 +591,24 @@ void launch_c(const ResArgs &args, int ctas, size_t smem, cudaStream_t st) {
     k_resident<S, RT, 0, 0, CMP><<<ctas, RT, smem, st>>>(args);
 }
 
+// global-graph mode (codes whose per-slot state fills shared memory, C6 size): S <= 8, 512 threads
+template <int S>
+void launch_gg(const ResArgs &args, int ctas, size_t smem, cudaStream_t st) {
+    if (args.dm <= 8 && !args.any_degree) {
+        cudaFuncSetAttribute(k_resident<S, 512, -8, 0, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_resident<S, 512, -8, 0, false, true><<<ctas, 512, smem, st>>>(args);
+        return;
+    }
+    cudaFuncSetAttribute(k_resident<S, 512, 0, 0, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_resident<S, 512, 0, 0, false, true><<<ctas, 512, smem, st>>>(args);
+}
+
 template <int S, int RT>
 void launch_s(const ResArgs &args, int ctas, size_t smem, cudaStream_t st) {
+    if (args.gg) {  // the planner only picks the global-graph mode with S <= 8 and 512 threads
+        if constexpr (S <= 8 && RT == 512) launch_gg<S>(args, ctas, smem, st);
+        return;
+    }
     if (args.compact) {  // the planner only picks compact records with S <= 8 and 256 / 512 threads
         if constexpr (S <= 8 && (RT == 256 || RT == 512)) launch_c<S, RT, true>(args, ctas, smem, st);
         return;
@@ -638,6 +673,30 @@ ResidentPlan plan_resident(const HostGraph &g, bool loc16, int device) {
             break;
         }
     }
+    // Optional: the per-slot state alone in shared memory, the edge lists read from global memory
+    // (L2-resident; C6: 1022 x 8176, d_c = 32, S = 4 in one 512-thread CTA per SM).  Measured slower than
+    // the streaming schedule on C6 (1.62 against 2.46 Gbps: 4 frames per SM and L2 latency on every edge
+    // list), so only LDPC_RES_GG=1 selects it (tests, A/B); parity-green.
+    const char *gge = getenv("LDPC_RES_GG");
+    const bool gg_force = gge && atoi(gge) == 1;
+    if (gg_force) rp = ResidentPlan{};
+    if (!rp.ok && gg_force) {
+        for (int S : {8, 4}) {
+            if (force_s && S != force_s) continue;
+            const Layout L = layout_for(S, g.m, g.n, g.E, dm, false, true);
+            if (L.total > (size_t)cap) continue;
+            rp.ok = true;
+            rp.global_graph = true;
+            rp.slots = S;
+            rp.dm = dm;
+            rp.dv = g.max_col_deg;
+            rp.regular = false;
+            rp.smem = L.total;
+            rp.threads = 512;
+            rp.ctas = sms;
+            break;
+        }
+    }
     return rp;
 }
 
@@ -672,7 +731,8 @@ int launch_resident(const Graph &g, const ResidentPlan &rp, const float *llr, in
         a.any_degree = atoi(e) >= 2;
     }
     a.compact = rp.compact ? 1 : 0;
-    a.lay = layout_for(rp.slots, g.m, g.n, g.E, rp.dm, rp.compact);
+    a.gg = rp.global_graph ? 1 : 0;
+    a.lay = layout_for(rp.slots, g.m, g.n, g.E, rp.dm, rp.compact, rp.global_graph);
     cudaMemsetAsync(work_counter, 0, sizeof(int), st);
     switch (rp.slots) {
         case 32: launch_t<32>(a, rp.threads, rp.ctas, rp.smem, st); break;

@@ -130,6 +130,7 @@ struct ResidentPlan {
     int dv = 0;          // max column degree
     bool regular = false;  // every row has degree dm and every column degree dv
     bool compact = false;  // compact bit-node records (larger codes, see layout_for)
+    bool global_graph = false;  // Tanner-graph lists read from global memory (state only in shared memory)
 };
 ResidentPlan plan_resident(const HostGraph &g, bool loc16, int device);
 size_t resident_scratch_bytes(const HostGraph &g, const ResidentPlan &rp);  // work counter + r scratch

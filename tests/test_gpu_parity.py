@@ -427,14 +427,35 @@ def test_c4_full_size_sampled():
     _sampled_full_size("c4", 12)
 
 
-def test_c6_paper_shaped_qc():
+@pytest.mark.parametrize("mode", ["default", "global_graph"])
+def test_c6_paper_shaped_qc(monkeypatch, mode):
     """C6: the paper's benchmark shape (QC 1022 x 8176, row degree 32; max 60 iterations, codeword
-    test every 6, SNR 3.0-3.6 dB) -- every frame of a reduced batch, plus a full-size sample."""
+    test every 6, SNR 3.0-3.6 dB) -- every frame of a reduced batch, with the default schedule
+    (streaming) and the resident one with the edge lists in global memory (LDPC_RES_GG=1)."""
     cfg = codes.CONFIGS["c6"]
     code = cfg["code"]()
     parts = [channel.bpsk_awgn(code.n, code.rate, e, cfg["seed"], p, 0, 150).numpy() for p, e in enumerate(cfg["ebn0"])]
-    compare(code, np.concatenate(parts), cfg["max_iter"], check_every=cfg["check_every"],
-            h=handle(code, 0, coo=True))
+    if mode == "global_graph":
+        monkeypatch.setenv("LDPC_RES_GG", "1")
+    h = handle(code, 0, coo=True)
+    assert h.schedule == ("resident" if mode == "global_graph" else "stream")
+    compare(code, np.concatenate(parts), cfg["max_iter"], check_every=cfg["check_every"], h=h)
+
+
+@pytest.mark.parametrize("generic", ["0", "2"])
+def test_resident_global_graph_mode(monkeypatch, generic):
+    """The resident schedule with the edge lists read from global memory (LDPC_RES_GG=1 forces it; the
+    bounded-degree and the any-degree instances) matches the oracle on the C2 code and on an irregular code."""
+    monkeypatch.setenv("LDPC_RES_GG", "1")
+    if generic != "0":
+        monkeypatch.setenv("LDPC_RES_GENERIC", generic)
+    cfg = codes.CONFIGS["c2"]
+    code = cfg["code"]()
+    parts = [channel.bpsk_awgn(code.n, code.rate, e, cfg["seed"], p, 100, 200).numpy() for p, e in enumerate(cfg["ebn0"])]
+    compare(code, np.concatenate(parts), cfg["max_iter"], FORCE_RESIDENT, h=handle(code, FORCE_RESIDENT))
+    code = codes.random_small(300, 700, 21, dmin=2, dmax=12)  # odd and even row degrees up to 12
+    llr = channel.bpsk_awgn(code.n, code.rate, 2.0, 5, 0, 0, 900).numpy()
+    compare(code, llr, 25, FORCE_RESIDENT, h=handle(code, FORCE_RESIDENT))
 
 
 def test_c5_sixteen_handles():
