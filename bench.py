@@ -352,7 +352,7 @@ def run_ours(args):
 
     # several codes (C5): their decodes alternate over `--code-streams` side streams, so one code's tail
     # (its last frames, when most persistent CTAs have exited) overlaps the next code's start
-    nside = max(1, args.code_streams) if len(jobs) > 1 else 0
+    nside = args.code_streams if len(jobs) > 1 and args.code_streams > 1 else 0
     side = [torch.cuda.Stream(device=dev) for _ in range(nside)]
 
     def step(sequential=False):
