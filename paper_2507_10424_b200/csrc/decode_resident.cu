@@ -454,6 +454,17 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
                 const int j = cb + sub;
                 if (j >= n || !(cm | fk | fw)) continue;
                 float *sp = s + j * S + q0;
+                // global loads first (r of the continuing slots, the channel values of the new frames), so
+                // their latency overlaps the outputs and the bit-node pass below (ncu: the staging and the
+                // final add were waiting on them)
+                float4 rj = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (cm) rj = *reinterpret_cast<const float4 *>(rs + (size_t)j * S + q0);
+                float xs[4] = {0.f, 0.f, 0.f, 0.f};
+                if (fw) {
+#pragma unroll
+                    for (int v = 0; v < 4; v++)
+                        if ((fw >> v) & 1u) xs[v] = __ldg(a.llr + fr[v] + j);
+                }
                 // the old s is needed unless all four slots continue (their s is overwritten)
                 float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
                 if (cm != 0xfu) o = *reinterpret_cast<const float4 *>(sp);
@@ -471,7 +482,6 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
                     }
                 }
                 if (cm) {
-                    const float4 rj = *reinterpret_cast<const float4 *>(rs + (size_t)j * S + q0);
                     const int c0 = DV > 0 ? j * DV : cp[j], dv = DV > 0 ? DV : (int)cp[j + 1] - c0;
                     float acc[4] = {0.f, 0.f, 0.f, 0.f};
                     for (int q3 = 0; q3 < dv; q3 += 3) {  // chunks of 3 edges: no remainder loop for d_v = 3
@@ -514,7 +524,7 @@ __global__ void __launch_bounds__(RT, RT == 128 ? 4 : RT == 256 ? (S == 4 ? 3 : 
 #pragma unroll
                     for (int v = 0; v < 4; v++) {
                         if ((fw >> v) & 1u) {
-                            const float x = __ldg(a.llr + fr[v] + j);
+                            const float x = xs[v];
                             f4s(o, v, x == 0.f ? -0.f : x);  // zeros of s are kept as -0 (A12)
                             rs[(size_t)j * S + q0 + v] = x;
                             raw[v] += x > 0.f;
