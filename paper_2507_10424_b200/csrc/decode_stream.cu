@@ -109,6 +109,11 @@ __device__ __forceinline__ float fmin3f(float a, float b, float c) {
 #ifndef CNG_PAIR
 #define CNG_PAIR 1
 #endif
+// check node (k_cn): min0 / min1 by a pair tournament after all of a row's lambdas, min0Location as the
+// edges that attain min0 (see cn_compute); 0: first-strict-minimum tracking edge by edge
+#ifndef CN_TREE
+#define CN_TREE 1
+#endif
 
 // 256-bit (8 x fp32) global accesses (LDG.E.ENL2.256 / STG.E.ENL2.256 on sm_100), with an optional L2 policy
 struct f8 {
@@ -371,6 +376,57 @@ __device__ __forceinline__ void cn_compute(const CnRow<CH> &R, unsigned char *__
             nloc[v] = lt ? lp : nloc[v];
         }
     }
+#elif CN_TREE
+    // Every lambda of the row first, then min0 / min1 by a pair tournament and min0Location as the edges
+    // whose |lambda| equals min0.  The tournament keeps (lo, hi) = the two smallest |lambda| seen: a pair
+    // (a, b) enters as (min, max) and merges by lo' = min(lo, l2), hi' = min3(hi, h2, max(lo, l2)) -- 2.1
+    // FMNMX per slot-edge for CH = 7 instead of FSETP + 3 FMNMX + SEL.  isloc_p = (|lambda_p| == min0)
+    // marks every edge of a tie; under a tie min1 = min0 (same value, same sign bit), so eta_e =
+    // (isloc ? min1 : min0) is the same value as with the first strict minimum only (reading A13).  Its
+    // bit is the complement of the sign bit of min0 - |lambda_p| (exact, +0 iff equal; an FMA-pipe
+    // FADD), pushed like the sign bits.  Edges past d_i enter as |lambda| = +inf (never a minimum, never
+    // a location); their pushed sign bits are masked off.
+    float ax[CH][4];
+    uint32_t iw = 0;
+#pragma unroll
+    for (int p = 0; p < CH; p++) {
+        const bool va = FULL || p < d;
+        const uint32_t b = FIRST ? 0u : R.eb[p];
+#pragma unroll
+        for (int v = 0; v < 4; v++) {
+            const float sj = comp(R.sv[p], v);
+            float x;
+            if (FIRST) {
+                x = __fadd_rn(sj, 0.0f);  // eta^prev = 0
+            } else {
+                const float mag = (b & (16u << v)) ? om1[v] : om0[v];  // Obs. 1 (+ row parity)
+                x = __fadd_rn(__fsub_rn(sj, flip31(mag, b << (31 - v))), 0.0f);  // lambda - eta^prev
+            }
+            ax[p][v] = va ? fabsf(x) : INF;
+            sw = __funnelshift_l(__float_as_uint(x), sw, 1);
+            if (EARLY) syn[v] ^= va ? __float_as_uint(sj) : 0u;  // bit 31: slice(s_j) == 0
+        }
+    }
+#pragma unroll
+    for (int v = 0; v < 4; v++) {
+        float lo = fminf(ax[0][v], ax[1][v]), hi = fmaxf(ax[0][v], ax[1][v]);
+#pragma unroll
+        for (int p = 2; p + 1 < CH; p += 2) {
+            const float l2 = fminf(ax[p][v], ax[p + 1][v]), h2 = fmaxf(ax[p][v], ax[p + 1][v]);
+            hi = fmin3f(hi, h2, fmaxf(lo, l2));
+            lo = fminf(lo, l2);
+        }
+        if (CH & 1) {
+            hi = fminf(hi, fmaxf(lo, ax[CH - 1][v]));
+            lo = fminf(lo, ax[CH - 1][v]);
+        }
+        nm0[v] = lo;
+        nm1[v] = hi;
+    }
+#pragma unroll
+    for (int p = 0; p < CH; p++)
+#pragma unroll
+        for (int v = 0; v < 4; v++) iw = __funnelshift_l(__float_as_uint(__fsub_rn(nm0[v], ax[p][v])), iw, 1);
 #else
 #pragma unroll
     for (int p = 0; p < CH; p++) {
@@ -398,8 +454,14 @@ __device__ __forceinline__ void cn_compute(const CnRow<CH> &R, unsigned char *__
     }
 #endif
     // bit 4p+v of sw = sign of lambda (edge p, slot 4l+v)
+#if CN_TREE && !CN_PAIR
+    sw = CH == 8 ? __brev(sw) : __brev(sw) >> (32 - 4 * CH);
+    if (!FULL) sw &= (1u << (4 * d)) - 1u;  // d < CH <= 8
+    const uint32_t lm = CH == 8 ? __brev(~iw) : __brev(~iw) >> (32 - 4 * CH);  // bit 4p+v: isloc
+#else
     if (FULL) sw = CH == 8 ? __brev(sw) : __brev(sw) >> (32 - 4 * CH);
     else sw = __brev(sw) >> (32 - 4 * d);
+#endif
     // sign parity per slot (Obs. 2): XOR of bits v, v+4, ..., of sw, times (-1)^{d_i} (reading A1)
     uint32_t pw = sw ^ (sw >> 16);
     pw ^= pw >> 8;
@@ -417,7 +479,9 @@ __device__ __forceinline__ void cn_compute(const CnRow<CH> &R, unsigned char *__
             pf);
     // edge bytes: sign nibble | isloc nibble << 4.  lm has bit 4p+v set iff min0Location of slot v is p;
     // interleaving the nibbles of sw and lm gives the bytes of the even edges in ze, of the odd ones in zo
+#if !CN_TREE || CN_PAIR
     const uint32_t lm = (1u << (4 * nloc[0])) | (2u << (4 * nloc[1])) | (4u << (4 * nloc[2])) | (8u << (4 * nloc[3]));
+#endif
     const uint32_t ze = (sw & 0x0f0f0f0fu) | ((lm & 0x0f0f0f0fu) << 4);
     const uint32_t zo = ((sw >> 4) & 0x0f0f0f0fu) | (lm & 0xf0f0f0f0u);
 #pragma unroll
