@@ -108,6 +108,9 @@ __device__ __forceinline__ void f4s(float4 &a, int v, float x) {
 #define RES_ANY_UNROLL 1  // edge pairs per unrolled step of the any-degree check-node pass (4: 1 % slower)
 #endif
 constexpr int kAnyUnroll = RES_ANY_UNROLL;  // (#pragma unroll does not expand macros)
+#ifndef RES_TREE
+#define RES_TREE 1  // rows of <= 8 edges: pair tournament after all lambdas, isloc = (|lambda| == min0)
+#endif
 
 // min(a, b, c) in one FMNMX3 (sm_100)
 __device__ __forceinline__ float fmin3f(float a, float b, float c) {
@@ -165,67 +168,120 @@ __device__ __forceinline__ void cn_rows(const float *__restrict__ s, float *mn0,
     // (FMNMX3) and loc' = sm < nm0 ? (b < a ? p+1 : p) : loc -- the same first strict minimum (A13) and
     // second minimum as the edge-by-edge update in fewer ALU operations; the decision parity takes both
     // edges in one 3-input XOR.  An absent edge enters as |lambda| = +inf, sign bit 0, parity 0.
-#pragma unroll(DC > 0 ? (DC + 1) / 2 : kAnyUnroll)
-    for (int p = 0; p < pe; p += 2) {
-        if ((p & 7) == 0) {
-            if (p > 0) {  // the finished chunk: its bytes with the sign nibbles (isloc merged at the row end)
-                wn = __brev(wn);
-                pf ^= wn;
-                if (valid) res_store_chunk(ebr + p - 8, wn, 0u);
-                wn = 0u;
+#if RES_TREE
+    if constexpr (DC > 0 && DC <= 8) {
+        // One chunk (rows of at most 8 edges): every lambda of the row first, then min0 / min1 by a pair
+        // tournament and the min0Location bits as the edges whose |lambda| equals min0 (every edge of a
+        // tie: under a tie min1 = min0, same value and sign bit, so eta_e is the same; reading A13) -- the
+        // check node of the streaming schedule (decode_stream.cu, cn_compute) in the resident layout.
+        if (valid) ob = *reinterpret_cast<const uint2 *>(ebr);
+        float ax[DC][4];
+        uint32_t iw = 0u;
+#pragma unroll
+        for (int p = 0; p < DC; p++) {
+            const bool hp = HAS ? (p < d) : true;
+            const int j = hp ? colat(col, ra + p) : 0;
+            const float4 sv = *reinterpret_cast<const float4 *>(s + j * S + q0);
+            const uint32_t b = ((p & 4) ? ob.y : ob.x) >> (8 * (p & 3));
+#pragma unroll
+            for (int v = 0; v < 4; v++) {
+                const float sj = f4c(sv, v);
+                const float mg = (b & (16u << v)) ? f4c(om1, v) : f4c(om0, v);  // Obs. 1 (+ row parity)
+                const float x = __fadd_rn(__fsub_rn(sj, flip31(mg, b << (31 - v))), 0.0f);  // lambda, zero -> +0
+                ax[p][v] = hp ? fabsf(x) : INF;
+                wn = __funnelshift_l(hp ? __float_as_uint(x) : 0u, wn, 1);
+                synw[v] ^= hp ? __float_as_uint(sj) : 0u;  // slice(s_j) = 0 iff sign bit
             }
-            if (valid) ob = *reinterpret_cast<const uint2 *>(ebr + p);
-        }
-        const bool inb = p + 1 < pe;
-        const bool ha = HAS ? (p < d) : true, hb = inb && (HAS ? (p + 1 < d) : true);
-        const int ja = ha ? colat(col, ra + p) : 0, jb = hb ? colat(col, ra + p + 1) : 0;
-        const float4 sva = *reinterpret_cast<const float4 *>(s + ja * S + q0);
-        const float4 svb = *reinterpret_cast<const float4 *>(s + jb * S + q0);
-        const uint32_t ow = (p & 4) ? ob.y : ob.x;
-        const uint32_t ba = ow >> (8 * (p & 3)), bb = ow >> (8 * ((p + 1) & 3));
-        float xa[4], xb[4];
-#pragma unroll
-        for (int v = 0; v < 4; v++) {
-            const float sa = f4c(sva, v), sb = f4c(svb, v);
-            const float ma = (ba & (16u << v)) ? f4c(om1, v) : f4c(om0, v);  // Obs. 1 (+ row parity)
-            const float mb = (bb & (16u << v)) ? f4c(om1, v) : f4c(om0, v);
-            // lambda - eta^prev; + 0 makes a zero lambda +0 (s may be -0), so its IEEE sign bit is
-            // sign(0) = +1; the add runs on the otherwise idle FMA pipe
-            xa[v] = __fadd_rn(__fsub_rn(sa, flip31(ma, ba << (31 - v))), 0.0f);
-            xb[v] = __fadd_rn(__fsub_rn(sb, flip31(mb, bb << (31 - v))), 0.0f);
-            synw[v] ^= (ha ? __float_as_uint(sa) : 0u) ^ (hb ? __float_as_uint(sb) : 0u);  // slice(s_j) = 0 iff sign bit
-        }
-#pragma unroll
-        for (int v = 0; v < 4; v++) wn = __funnelshift_l(ha ? __float_as_uint(xa[v]) : 0u, wn, 1);
-        if (inb) {
-#pragma unroll
-            for (int v = 0; v < 4; v++) wn = __funnelshift_l(hb ? __float_as_uint(xb[v]) : 0u, wn, 1);
         }
 #pragma unroll
         for (int v = 0; v < 4; v++) {
-            const float a = ha ? fabsf(xa[v]) : INF, b = hb ? fabsf(xb[v]) : INF;
-            const float sm = fminf(a, b), tm = fmaxf(a, b);
-            const int lp = b < a ? p + 1 : p;
-            const bool lt = sm < nm0[v];
-            nm1[v] = fmin3f(nm1[v], fmaxf(nm0[v], sm), tm);
-            nm0[v] = fminf(nm0[v], sm);
-            nloc[v] = lt ? lp : nloc[v];
+            float lo = fminf(ax[0][v], ax[1][v]), hi = fmaxf(ax[0][v], ax[1][v]);
+#pragma unroll
+            for (int p = 2; p + 1 < DC; p += 2) {
+                const float l2 = fminf(ax[p][v], ax[p + 1][v]), h2 = fmaxf(ax[p][v], ax[p + 1][v]);
+                hi = fmin3f(hi, h2, fmaxf(lo, l2));
+                lo = fminf(lo, l2);
+            }
+            if (DC & 1) {
+                hi = fminf(hi, fmaxf(lo, ax[DC - 1][v]));
+                lo = fminf(lo, ax[DC - 1][v]);
+            }
+            nm0[v] = lo;
+            nm1[v] = hi;
         }
-    }
+#pragma unroll
+        for (int p = 0; p < DC; p++)
+#pragma unroll
+            for (int v = 0; v < 4; v++) iw = __funnelshift_l(__float_as_uint(__fsub_rn(nm0[v], ax[p][v])), iw, 1);
+        wn = DC == 8 ? __brev(wn) : __brev(wn) >> (32 - 4 * DC);
+        pf = wn;
+        const uint32_t lm = DC == 8 ? __brev(~iw) : __brev(~iw) >> (32 - 4 * DC);  // bit 4p+v: isloc
+        if (valid) res_store_chunk(ebr, wn, lm);
+    } else
+#endif
     {
-        const int last = (pe - 1) & ~7;            // first edge of the last chunk
-        const int pushed = 4 * (pe - last);        // slot-edges in the last chunk
-        wn = pushed == 32 ? __brev(wn) : __brev(wn) >> (32 - pushed);
-        pf ^= wn;
-        if (valid) {
-            if ((DC > 0 && DC <= 8) || pe <= 8) {  // one chunk (regular codes of degree <= 8): isloc merged before the only store
-                const uint32_t lm = (1u << (4 * nloc[0])) | (2u << (4 * nloc[1])) | (4u << (4 * nloc[2])) |
-                                    (8u << (4 * nloc[3]));
-                res_store_chunk(ebr, wn, lm);
-            } else {
-                res_store_chunk(ebr + last, wn, 0u);
+#pragma unroll(DC > 0 ? (DC + 1) / 2 : kAnyUnroll)
+        for (int p = 0; p < pe; p += 2) {
+            if ((p & 7) == 0) {
+                if (p > 0) {  // the finished chunk: its bytes with the sign nibbles (isloc merged at the row end)
+                    wn = __brev(wn);
+                    pf ^= wn;
+                    if (valid) res_store_chunk(ebr + p - 8, wn, 0u);
+                    wn = 0u;
+                }
+                if (valid) ob = *reinterpret_cast<const uint2 *>(ebr + p);
+            }
+            const bool inb = p + 1 < pe;
+            const bool ha = HAS ? (p < d) : true, hb = inb && (HAS ? (p + 1 < d) : true);
+            const int ja = ha ? colat(col, ra + p) : 0, jb = hb ? colat(col, ra + p + 1) : 0;
+            const float4 sva = *reinterpret_cast<const float4 *>(s + ja * S + q0);
+            const float4 svb = *reinterpret_cast<const float4 *>(s + jb * S + q0);
+            const uint32_t ow = (p & 4) ? ob.y : ob.x;
+            const uint32_t ba = ow >> (8 * (p & 3)), bb = ow >> (8 * ((p + 1) & 3));
+            float xa[4], xb[4];
 #pragma unroll
-                for (int v = 0; v < 4; v++) ebr[nloc[v]] |= (uint8_t)(16u << v);  // this thread wrote them
+            for (int v = 0; v < 4; v++) {
+                const float sa = f4c(sva, v), sb = f4c(svb, v);
+                const float ma = (ba & (16u << v)) ? f4c(om1, v) : f4c(om0, v);  // Obs. 1 (+ row parity)
+                const float mb = (bb & (16u << v)) ? f4c(om1, v) : f4c(om0, v);
+                // lambda - eta^prev; + 0 makes a zero lambda +0 (s may be -0), so its IEEE sign bit is
+                // sign(0) = +1; the add runs on the otherwise idle FMA pipe
+                xa[v] = __fadd_rn(__fsub_rn(sa, flip31(ma, ba << (31 - v))), 0.0f);
+                xb[v] = __fadd_rn(__fsub_rn(sb, flip31(mb, bb << (31 - v))), 0.0f);
+                synw[v] ^= (ha ? __float_as_uint(sa) : 0u) ^ (hb ? __float_as_uint(sb) : 0u);  // slice(s_j) = 0 iff sign bit
+            }
+#pragma unroll
+            for (int v = 0; v < 4; v++) wn = __funnelshift_l(ha ? __float_as_uint(xa[v]) : 0u, wn, 1);
+            if (inb) {
+#pragma unroll
+                for (int v = 0; v < 4; v++) wn = __funnelshift_l(hb ? __float_as_uint(xb[v]) : 0u, wn, 1);
+            }
+#pragma unroll
+            for (int v = 0; v < 4; v++) {
+                const float a = ha ? fabsf(xa[v]) : INF, b = hb ? fabsf(xb[v]) : INF;
+                const float sm = fminf(a, b), tm = fmaxf(a, b);
+                const int lp = b < a ? p + 1 : p;
+                const bool lt = sm < nm0[v];
+                nm1[v] = fmin3f(nm1[v], fmaxf(nm0[v], sm), tm);
+                nm0[v] = fminf(nm0[v], sm);
+                nloc[v] = lt ? lp : nloc[v];
+            }
+        }
+        {
+            const int last = (pe - 1) & ~7;            // first edge of the last chunk
+            const int pushed = 4 * (pe - last);        // slot-edges in the last chunk
+            wn = pushed == 32 ? __brev(wn) : __brev(wn) >> (32 - pushed);
+            pf ^= wn;
+            if (valid) {
+                if ((DC > 0 && DC <= 8) || pe <= 8) {  // one chunk (regular codes of degree <= 8): isloc merged before the only store
+                    const uint32_t lm = (1u << (4 * nloc[0])) | (2u << (4 * nloc[1])) | (4u << (4 * nloc[2])) |
+                                        (8u << (4 * nloc[3]));
+                    res_store_chunk(ebr, wn, lm);
+                } else {
+                    res_store_chunk(ebr + last, wn, 0u);
+#pragma unroll
+                    for (int v = 0; v < 4; v++) ebr[nloc[v]] |= (uint8_t)(16u << v);  // this thread wrote them
+                }
             }
         }
     }
