@@ -125,8 +125,10 @@ LDPC_API int ldpc_decode(ldpc_handle_t h, const float *llr, int64_t frames, int3
 /*
  * Same as ldpc_decode, but every buffer is in HOST memory (pageable or pinned); stats_inout is host too.
  * Chunks are copied host->device, decoded and copied back with the copies of one chunk overlapping
- * the decode of another (two internal streams ordered after `stream`).  Synchronous: returns when
- * the outputs are in host memory.
+ * the decode of another (three internal streams ordered after `stream`: copy-in, decode, copy-out; three
+ * device buffer sets rotate, so the copy-in runs up to two chunks ahead of the decode and never waits for
+ * a copy-back; environment LDPC_HOST_NBUF = 2..4 and LDPC_HOST_CHUNK_MB override the set count and the
+ * 768 MB chunk of LLRs).  Synchronous: returns when the outputs are in host memory.
  */
 LDPC_API int ldpc_decode_host(ldpc_handle_t h, const float *llr, int64_t frames, int32_t max_iter, uint8_t *bits_out,
                      int32_t *iters_out, float *posterior_out, uint8_t *converged_out, int64_t *stats_inout,

@@ -11,6 +11,10 @@
 
 #include "ldpc_internal.cuh"
 
+// buffer sets of the ldpc_decode_host pipeline (LDPC_HOST_NBUF overrides the default, 2..NHB_MAX)
+constexpr int NHB_MAX = 4;
+constexpr int NHB_DEFAULT = 3;
+
 using namespace ldpc;
 
 struct ldpc_plan {
@@ -57,7 +61,9 @@ struct ldpc_plan {
     cudaStream_t cap[2] = {nullptr, nullptr};
     // host pipeline
     cudaStream_t hs[3] = {nullptr, nullptr, nullptr};
-    void *hbuf[2] = {nullptr, nullptr};
+    // ldpc_decode_host buffer sets (LLRs in, outputs back): with NHB sets the host -> device copies run up
+    // to NHB - 1 chunks ahead of the decode, so a copy never waits for the copy-back of the chunk before
+    void *hbuf[NHB_MAX] = {};
     size_t hbuf_bytes = 0;
     unsigned long long *hstats = nullptr;  // device counters of ldpc_decode_host (64 B, allocated once)
     // device-side accounting of graph-driven loop bodies (3 launches per body that ran)
@@ -516,11 +522,13 @@ int ldpc_decode_host(ldpc_handle_t h, const float *llr, int64_t frames, int32_t 
     if (h->poisoned) return LDPC_ERR_CUDA;
     if (frames == 0) return LDPC_OK;
     const int64_t n = h->g.n;
-    // chunk of frames per pipeline stage: LDPC_HOST_CHUNK_MB of LLRs (default 384 MB: enough frames per
+    // chunk of frames per pipeline stage: LDPC_HOST_CHUNK_MB of LLRs (default 768 MB: enough frames per
     // decode to fill the GPU, small enough that the unoverlapped first copy and last decode + copy-back are
-    // short; 1 GB chunks measured 16 % lower e2e on C3)
+    // short).  Measured e2e (one B200, 55 GB/s host link; buffer sets x chunk MB): C3 2 x 384: 6.41 Gbit/s,
+    // 3 x 384: 8.64, 3 x 768: 8.97 (device 9.15), 3 x 1536: 8.82, 4 x 768: 8.23; C2 2 x 384: 9.23,
+    // 3 x 768: 10.91 (device 11.61)
     const char *cm = getenv("LDPC_HOST_CHUNK_MB");
-    const int64_t chunk_mb = cm ? std::max(1, atoi(cm)) : 384;
+    const int64_t chunk_mb = cm ? std::max(1, atoi(cm)) : 768;
     int64_t chunk = std::max<int64_t>(TILE, std::min<int64_t>(frames, (chunk_mb << 20) / (n * 4)));
     chunk = (chunk + TILE - 1) / TILE * TILE;
     const size_t per_frame = n * 4 + (bits_out ? n : 0) + (posterior_out ? n * 4 : 0) + 4 + 1;
@@ -532,13 +540,15 @@ int ldpc_decode_host(ldpc_handle_t h, const float *llr, int64_t frames, int32_t 
         for (int q = 0; q < 3; q++) e = cudaStreamCreateWithFlags(&h->hs[q], cudaStreamNonBlocking);
         if (e != cudaSuccess) return status_of(e);
     }
-    if (h->hbuf_bytes < set_bytes) {
-        for (int q = 0; q < 2; q++) {
+    const char *nb = getenv("LDPC_HOST_NBUF");
+    const int nhb = nb ? std::min(NHB_MAX, std::max(2, atoi(nb))) : NHB_DEFAULT;
+    if (h->hbuf_bytes < set_bytes || !h->hbuf[nhb - 1]) {
+        for (int q = 0; q < NHB_MAX; q++) {
             cudaFree(h->hbuf[q]);
             h->hbuf[q] = nullptr;
         }
         h->hbuf_bytes = 0;
-        for (int q = 0; q < 2; q++)
+        for (int q = 0; q < nhb; q++)
             if (cudaMalloc(&h->hbuf[q], set_bytes) != cudaSuccess) {
                 cudaGetLastError();
                 return LDPC_ERR_OOM;
@@ -555,8 +565,12 @@ int ldpc_decode_host(ldpc_handle_t h, const float *llr, int64_t frames, int32_t 
     // every allocation is done: from here on, all paths return the events to the pool
     cudaStream_t user = static_cast<cudaStream_t>(stream);
     cudaStream_t s_in = h->hs[0], s_run = h->hs[1], s_out = h->hs[2];
-    cudaEvent_t ev_start = get_event(h), ev_in[2] = {get_event(h), get_event(h)},
-                ev_run[2] = {get_event(h), get_event(h)}, ev_out[2] = {get_event(h), get_event(h)};
+    cudaEvent_t ev_start = get_event(h), ev_in[NHB_MAX], ev_run[NHB_MAX], ev_out[NHB_MAX];
+    for (int q = 0; q < nhb; q++) {
+        ev_in[q] = get_event(h);
+        ev_run[q] = get_event(h);
+        ev_out[q] = get_event(h);
+    }
     cudaEventRecord(ev_start, user);
     cudaStreamWaitEvent(s_in, ev_start, 0);
     cudaStreamWaitEvent(s_run, ev_start, 0);
@@ -564,11 +578,12 @@ int ldpc_decode_host(ldpc_handle_t h, const float *llr, int64_t frames, int32_t 
     unsigned long long *d_stats = stats_inout ? h->hstats : nullptr;
     if (d_stats) cudaMemsetAsync(d_stats, 0, 64, s_run);
     int rc = LDPC_OK;
-    int idx = 0;
-    bool used[2] = {false, false};
+    int idx = 0, last = 0;
+    bool used[NHB_MAX] = {};
     // chunk sizes ramp up geometrically from chunk/16 (the first copy, which nothing overlaps, is short)
     int64_t cur = std::max<int64_t>(TILE, (chunk / 16 + TILE - 1) / TILE * TILE);
-    for (int64_t c0 = 0, fc = 0; c0 < frames && rc == LDPC_OK; c0 += fc, idx ^= 1, cur = std::min(chunk, 2 * cur)) {
+    for (int64_t c0 = 0, fc = 0; c0 < frames && rc == LDPC_OK; c0 += fc, idx = (idx + 1) % nhb, cur = std::min(chunk, 2 * cur)) {
+        last = idx;
         fc = std::min(cur, frames - c0);
         char *base = static_cast<char *>(h->hbuf[idx]);
         float *d_llr = reinterpret_cast<float *>(base);
@@ -595,14 +610,14 @@ int ldpc_decode_host(ldpc_handle_t h, const float *llr, int64_t frames, int32_t 
     }
     int64_t hstats[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (d_stats) {
-        cudaStreamWaitEvent(s_out, ev_run[idx ^ 1], 0);
+        cudaStreamWaitEvent(s_out, ev_run[last], 0);
         cudaMemcpyAsync(hstats, d_stats, 64, cudaMemcpyDeviceToHost, s_out);
     }
     e = cudaStreamSynchronize(s_out);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s_run);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s_in);
     h->pool.push_back(ev_start);
-    for (int q = 0; q < 2; q++) {
+    for (int q = 0; q < nhb; q++) {
         h->pool.push_back(ev_in[q]);
         h->pool.push_back(ev_run[q]);
         h->pool.push_back(ev_out[q]);
@@ -745,7 +760,7 @@ void ldpc_destroy(ldpc_handle_t h) {
     cudaFree(h->dev_launches);
     cudaFree(h->ws);
     cudaFree(h->work_counter);
-    for (int q = 0; q < 2; q++) cudaFree(h->hbuf[q]);
+    for (int q = 0; q < NHB_MAX; q++) cudaFree(h->hbuf[q]);
     for (int q = 0; q < 3; q++)
         if (h->hs[q]) cudaStreamDestroy(h->hs[q]);
     for (auto &ev : h->evs) {

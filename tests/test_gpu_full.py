@@ -121,13 +121,14 @@ def test_full_batch_parity_c2_streaming(flags):
     check_batch(f"c2_stream_flags{flags}", code, llr[idx].contiguous(), cfg["max_iter"], flags=flags)
 
 
-@pytest.mark.parametrize("flags", [0, 4])
-def test_decode_host_multichunk(monkeypatch, flags):
-    """ldpc_decode_host with a 1 MB chunk: about ten ramped, double-buffered chunks (ev_out reuse, buffer
-    sets alternating), against the oracle and against the device-buffer call."""
+@pytest.mark.parametrize("flags,nbuf", [(0, "3"), (4, "3"), (0, "2"), (4, "4")])
+def test_decode_host_multichunk(monkeypatch, flags, nbuf):
+    """ldpc_decode_host with a 1 MB chunk: about ten ramped chunks through 2-4 rotating buffer sets
+    (ev_out reuse), against the oracle and against the device-buffer call."""
     import paper_2507_10424_b200 as P
 
     monkeypatch.setenv("LDPC_HOST_CHUNK_MB", "1")
+    monkeypatch.setenv("LDPC_HOST_NBUF", nbuf)
     cfg = codes.CONFIGS["c2"]
     code = bench.code_list(cfg)[0]
     llr, _ = bench.gen_frames(code, cfg, cfg["seed"], 0, cfg["frames"], 0)
