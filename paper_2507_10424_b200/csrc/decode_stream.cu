@@ -38,6 +38,8 @@
 
 #include "ldpc_internal.cuh"
 
+#include <type_traits>
+
 namespace ldpc {
 
 namespace {
@@ -113,6 +115,9 @@ __device__ __forceinline__ float fmin3f(float a, float b, float c) {
 // edges that attain min0 (see cn_compute); 0: first-strict-minimum tracking edge by edge
 #ifndef CN_TREE
 #define CN_TREE 1
+#endif
+#ifndef CNG_TREE
+#define CNG_TREE 1  // the same for each 8-edge chunk of k_cn_generic (rows of at most 8 NWK edges)
 #endif
 
 // 256-bit (8 x fp32) global accesses (LDG.E.ENL2.256 / STG.E.ENL2.256 on sm_100), with an optional L2 policy
@@ -632,6 +637,10 @@ __global__ void __launch_bounds__(CN_T, 2) k_cn_generic(Graph g, StreamState w, 
             int nloc[4] = {0, 0, 0, 0};
             uint32_t syn[4] = {0u, 0u, 0u, 0u}, pf = 0u;
             uint32_t cws[NWK > 0 ? NWK : 1];
+#if CNG_TREE
+            float clo[NWK > 0 ? NWK : 1][4];  // chunk minima per slot
+            uint32_t cls[NWK > 0 ? NWK : 1];  // chunk isloc candidates (bit 4u+v)
+#endif
             int cj = cj_row;
             // NWK > 0: the chunk loop is unrolled (chunk words stay in registers)
 #pragma unroll(NWK > 0 ? NWK : 1)
@@ -657,6 +666,68 @@ __global__ void __launch_bounds__(CN_T, 2) k_cn_generic(Graph g, StreamState w, 
                     }
                 }
                 uint32_t cw = 0;
+#if CNG_TREE
+                if constexpr (NWK > 0) {
+                    // the chunk's lambdas first, then its two smallest |lambda| by a pair tournament (as in
+                    // cn_compute) merged into the row's (nm0, nm1), and the chunk's candidate isloc bits: the
+                    // edges whose |lambda| equals the chunk minimum.  At the row end a chunk keeps them for the
+                    // slots whose row minimum is its minimum (every edge of a tie: same eta, reading A13).
+                    // Full chunks (warp-uniform) take a guard-free copy of the body.
+                    auto chunk = [&](auto fullc) {
+                        constexpr bool FC = decltype(fullc)::value;
+                        float ax[C8][4], lo[4];
+                        uint32_t iwc = 0u;
+#pragma unroll
+                        for (int u8 = 0; u8 < C8; u8++) {
+                            const bool va = FC || p0 + u8 < d;
+#pragma unroll
+                            for (int v = 0; v < 4; v++) {
+                                const float sj = comp(sv[u8], v);
+                                float x;
+                                if (FIRST) {
+                                    x = __fadd_rn(sj, 0.0f);
+                                } else {
+                                    const float mag = (eb[u8] & (16u << v)) ? om1[v] : om0[v];
+                                    x = __fadd_rn(__fsub_rn(sj, flip31(mag, eb[u8] << (31 - v))), 0.0f);
+                                }
+                                ax[u8][v] = va ? fabsf(x) : INF;
+                                cw = __funnelshift_l(__float_as_uint(x), cw, 1);
+                                if (EARLY) syn[v] ^= va ? __float_as_uint(sj) : 0u;
+                            }
+                        }
+#pragma unroll
+                        for (int v = 0; v < 4; v++) {
+                            float l = fminf(ax[0][v], ax[1][v]), h = fmaxf(ax[0][v], ax[1][v]);
+#pragma unroll
+                            for (int u8 = 2; u8 < C8; u8 += 2) {
+                                const float l2 = fminf(ax[u8][v], ax[u8 + 1][v]), h2 = fmaxf(ax[u8][v], ax[u8 + 1][v]);
+                                h = fmin3f(h, h2, fmaxf(l, l2));
+                                l = fminf(l, l2);
+                            }
+                            nm1[v] = fmin3f(nm1[v], h, fmaxf(nm0[v], l));
+                            nm0[v] = fminf(nm0[v], l);
+                            lo[v] = l;
+                        }
+#pragma unroll
+                        for (int u8 = 0; u8 < C8; u8++)
+#pragma unroll
+                            for (int v = 0; v < 4; v++)
+                                iwc = __funnelshift_l(__float_as_uint(__fsub_rn(lo[v], ax[u8][v])), iwc, 1);
+#pragma unroll
+                        for (int q = 0; q < (NWK > 0 ? NWK : 1); q++)
+                            if (q == (p0 >> 3)) {
+                                cls[q] = __brev(~iwc);  // bit 4u+v: |lambda| = chunk minimum
+#pragma unroll
+                                for (int v = 0; v < 4; v++) clo[q][v] = lo[v];
+                            }
+                        cw = __brev(cw);
+                        if (!FC) cw &= (1u << (4 * (d - p0))) - 1u;
+                    };
+                    if (full) chunk(std::true_type{});
+                    else chunk(std::false_type{});
+                } else
+#endif
+                {
 #if CNG_PAIR
 #pragma unroll
                 for (int u8 = 0; u8 < C8; u8 += 2) {  // edge pairs, as in cn_compute
@@ -724,6 +795,7 @@ __global__ void __launch_bounds__(CN_T, 2) k_cn_generic(Graph g, StreamState w, 
 #endif
                 const int pushed = full ? 32 : 4 * (d - p0);
                 cw = pushed == 32 ? __brev(cw) : __brev(cw) >> (32 - pushed);  // bit 4u+v: edge p0+u, slot 4l+v
+                }
                 pf ^= cw;
                 if (NWK > 0) {
 #pragma unroll
@@ -742,11 +814,17 @@ __global__ void __launch_bounds__(CN_T, 2) k_cn_generic(Graph g, StreamState w, 
                 for (int q = 0; q < (NWK > 0 ? NWK : 1); q++) {
                     if (8 * q < d) {
                         uint32_t lm = 0;
+#if CNG_TREE
+#pragma unroll
+                        for (int v = 0; v < 4; v++) lm |= clo[q][v] == nm0[v] ? (0x11111111u << v) : 0u;
+                        lm &= cls[q];
+#else
 #pragma unroll
                         for (int v = 0; v < 4; v++) {
                             const int r = nloc[v] - 8 * q;
                             lm |= (r >= 0 && r < 8) ? (1u << (4 * r + v)) : 0u;
                         }
+#endif
                         const uint32_t ze = (cws[q] & 0x0f0f0f0fu) | ((lm & 0x0f0f0f0fu) << 4);
                         const uint32_t zo = ((cws[q] >> 4) & 0x0f0f0f0fu) | (lm & 0xf0f0f0f0u);
 #pragma unroll
