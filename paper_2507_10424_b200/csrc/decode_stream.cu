@@ -184,6 +184,9 @@ __device__ __forceinline__ int next_item(int *ctr, int &s_item) {
 #ifndef CN_PF
 #define CN_PF 0  // 1: prefetch the next row's gathers and state into L1 while the current row is computed
 #endif
+#ifndef CNG_MINB
+#define CNG_MINB 2  // any-degree check node: CTAs of CN_T threads per SM (2: 128 registers)
+#endif
 #ifndef CNG_PF
 #define CNG_PF 1  // any-degree check node: the next chunk's gathers prefetched into L1 (C6: -8 %)
 #endif
@@ -577,7 +580,7 @@ __global__ void __launch_bounds__(CN_T, CN_MINB) k_cn(Graph g, StreamState w, in
 // merges the isloc nibbles into the bytes of the min0Location edges at the end of the row; NWK = 0 (any
 // degree) ORs them into the bytes already written (each lane owns byte `lane` of every edge block).
 template <bool FIRST, bool EARLY, int NWK>
-__global__ void __launch_bounds__(CN_T, 2) k_cn_generic(Graph g, StreamState w, int k, int literal, const int *kdev) {
+__global__ void __launch_bounds__(CN_T, CNG_MINB) k_cn_generic(Graph g, StreamState w, int k, int literal, const int *kdev) {
     if (kdev) k = *kdev;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     __shared__ uint32_t s_u[4];
