@@ -1105,6 +1105,9 @@ __global__ void __launch_bounds__(CNB_W * 32, 1)
 #ifndef BN_V8
 #define BN_V8 1
 #endif
+#ifndef COMPACT_PCT
+#define COMPACT_PCT 50  // a tile with fewer than this percentage of its slots running becomes a compaction source
+#endif
 
 #ifndef BN_DYN
 #define BN_DYN 1  // items from the work counter (keeps the tiles in flight together for L2 reuse)
@@ -1179,7 +1182,7 @@ __global__ void __launch_bounds__(BN_T, BN_MINB)
                 }
                 if (tid == 0) {
                     const int run = __popc(act.x) + __popc(act.y) + __popc(act.z) + __popc(act.w);
-                    if (run > 0 && compact_ok && 2 * run < TILE) {  // compaction source
+                    if (run > 0 && compact_ok && 100 * run < COMPACT_PCT * TILE) {  // compaction source
                         const int pos = atomicAdd(w.ctl + CT_NSRC, 1);
                         w.csrc[pos] = t;
                         w.ccnt[pos] = run;
