@@ -90,7 +90,6 @@ struct ResArgs {
 };
 
 __device__ __forceinline__ float f4c(const float4 &a, int v) { return v == 0 ? a.x : v == 1 ? a.y : v == 2 ? a.z : a.w; }
-__device__ __forceinline__ uint32_t f4c(const uint4 &a, int v) { return v == 0 ? a.x : v == 1 ? a.y : v == 2 ? a.z : a.w; }
 __device__ __forceinline__ void f4s(float4 &a, int v, float x) {
     if (v == 0) a.x = x;
     else if (v == 1) a.y = x;

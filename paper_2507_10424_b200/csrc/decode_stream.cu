@@ -338,7 +338,9 @@ __device__ __forceinline__ void cn_compute(const CnRow<CH> &R, unsigned char *__
     const float INF = __int_as_float(0x7f800000);
     const float om0[4] = {R.m0.x, R.m0.y, R.m0.z, R.m0.w}, om1[4] = {R.m1.x, R.m1.y, R.m1.z, R.m1.w};
     float nm0[4] = {INF, INF, INF, INF}, nm1[4] = {INF, INF, INF, INF};
+#if !CN_TREE || CN_PAIR
     int nloc[4] = {0, 0, 0, 0};
+#endif
     uint32_t syn[4] = {0u, 0u, 0u, 0u}, sw = 0;  // sw: sign bits pushed in (p, v) order
 #if CN_PAIR
     // Edges in pairs (p, p+1): the pair's smaller and larger |lambda| (s, t) update the row state with
@@ -1113,6 +1115,7 @@ __global__ void __launch_bounds__(CNB_W * 32, 1)
 #define BN_DYN 1  // items from the work counter (keeps the tiles in flight together for L2 reuse)
 #endif
 
+#if !BN_V8
 // s of one column for this lane's 4 slots: new values for the running frames, r for frames stopped at
 // the pre-check (body 1), untouched for frozen frames; zeros kept as -0 (A12)
 __device__ __forceinline__ void bn_store(float *o, const float (&acc)[4], float4 rv, unsigned mine, int k,
@@ -1131,6 +1134,7 @@ __device__ __forceinline__ void bn_store(float *o, const float (&acc)[4], float4
         if (mine & 8u) o[3] = n3;
     }
 }
+#endif
 
 
 template <bool EARLY>
@@ -1197,10 +1201,12 @@ __global__ void __launch_bounds__(BN_T, BN_MINB)
             const int pos = atomicAdd(w.tcount + ((k + 1) & 1), 1);
             w.tlist[(size_t)((k + 1) & 1) * Tc + pos] = t;
         }
+        const unsigned char *RB = w.rst + (size_t)t * m * w.rs;
+#if !BN_V8
         const unsigned mine = ((act.x >> lane) & 1u) | (((act.y >> lane) & 1u) << 1) | (((act.z >> lane) & 1u) << 2) |
                               (((act.w >> lane) & 1u) << 3);
-        const unsigned char *RB = w.rst + (size_t)t * m * w.rs;
         const size_t tb = (size_t)t * n * TILE + 4 * lane;  // r and s of the tile (one offset, two bases)
+#endif
         const int j1 = min(n, x * BN_COLS + BN_COLS);
 #if BN_V8
         // 256-bit accesses: half-warp h (lanes 16h..16h+15) sweeps its own columns, half-lane hl owns the 8
