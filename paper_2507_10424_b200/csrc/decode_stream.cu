@@ -199,7 +199,17 @@ __device__ __forceinline__ int next_item(int *ctr, int &s_item) {
 #ifndef BN_MINB
 #define BN_MINB 12  // 12 x 128 threads (48 warps per SM)
 #endif
-constexpr int CN_ROWS = 128;  // rows per check-node item (16 per warp)
+#ifndef CN_ROWS_N
+#define CN_ROWS_N 128
+#endif
+constexpr int CN_ROWS = CN_ROWS_N;  // rows per check-node item (16 per warp; at most 32 per warp)
+// rows per item of the any-degree check node: 64 (8 per warp) -- C6 (1022 rows of degree 32) check node
+// -14.7 % against 128 (8192 frames, every frame running: twice the items, shorter tail); 64 and 256 rows
+// per item in k_cn measured equal or 1-7 % slower (C3, C4)
+#ifndef CNG_ROWS_N
+#define CNG_ROWS_N 64
+#endif
+constexpr int CNG_ROWS = CNG_ROWS_N;
 #ifndef BN_COLS
 #define BN_COLS 16  // columns per bit-node item (4 per warp)
 #endif
@@ -595,7 +605,7 @@ __global__ void __launch_bounds__(CN_T, CNG_MINB) k_cn_generic(Graph g, StreamSt
         if (w.nlaunch) w.nlaunch[4] += (unsigned long long)cnt;
     }
     const int m = g.m, n = g.n;
-    const int nrb = (m + CN_ROWS - 1) / CN_ROWS;
+    const int nrb = (m + CNG_ROWS - 1) / CNG_ROWS;
     const int items = cnt * nrb;
     const float INF = __int_as_float(0x7f800000);
     constexpr int C8 = 8;
@@ -610,7 +620,7 @@ __global__ void __launch_bounds__(CN_T, CNG_MINB) k_cn_generic(Graph g, StreamSt
         uint32_t u[4] = {0u, 0u, 0u, 0u};
         // the warp's rows i0 + 8q: their row pointers in lanes q (one load), and the first 32 column
         // indices of the next row fetched while the current row is processed
-        const int i0 = x * CN_ROWS + warp, i1 = min(m, x * CN_ROWS + CN_ROWS);
+        const int i0 = x * CNG_ROWS + warp, i1 = min(m, x * CNG_ROWS + CNG_ROWS);
         const int nr = i0 < i1 ? (i1 - i0 + CN_NW - 1) / CN_NW : 0;
         int ra = 0, rb = 0;
         if (lane < nr) {
@@ -1663,7 +1673,7 @@ void cnb_launch(const Graph &g, const StreamState &w, int k, int lit, const Stre
 template <bool F, bool EA>
 void cn_launch(const Graph &g, const StreamState &w, int k, int lit, const StreamLaunch &cfg, cudaStream_t st,
                const int *kdev) {
-    const dim3 grid(cfg.sms * CN_MINB), gridg(cfg.sms * 2);
+    const dim3 grid(cfg.sms * CN_MINB), gridg(cfg.sms * CNG_MINB);
     if (cfg.cn_bulk && g.dmax <= 32) {
         if (g.dmax <= 8) cnb_launch<F, EA, 1>(g, w, k, lit, cfg, st, kdev);
         else if (g.dmax <= 16) cnb_launch<F, EA, 2>(g, w, k, lit, cfg, st, kdev);
